@@ -1,0 +1,131 @@
+/* factorla_b200.h — C ABI of the B200 factorized linear-algebra library.
+ *
+ * The reference (factorla, /root/reference/pkg/src/factorla) is pure Python over
+ * NumPy/SciPy/OpenBLAS and has no FFI layer of its own. The hot path
+ * sits behind its operator functions in rewrite.py and the ML drivers in ml.py; each
+ * entry point below replaces the native calls one of those functions makes, and the
+ * Python package paper_1612_07448_b200 binds them through ctypes exactly where the
+ * reference calls NumPy/SciPy/BLAS (see INTEGRATION.md for the binding).
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless stated; matrices are row-major float64,
+ *    FK columns int32 (0-based targets after remapping), sizes int64.
+ *  - Every compute entry point is stream-ordered on `stream`, performs no host
+ *    synchronisation and is CUDA-graph capturable. Scratch memory comes from the
+ *    caller's workspace (`ws`, `ws_bytes`); query the size with the *_workspace_bytes
+ *    function. The library never frees caller memory.
+ *  - Return value: FB_OK or an FB_ERR_* code; fb_last_error() gives the message
+ *    (thread-local). The Python layer maps codes to the reference's exception classes
+ *    (exceptions.py: ShapeError, DataError, NumericError).
+ */
+#ifndef FACTORLA_B200_H
+#define FACTORLA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* fb_stream_t; /* == cudaStream_t */
+
+#define FB_ABI_VERSION 1
+#define FB_MAX_PARTS 4
+
+enum {
+  FB_OK = 0,
+  FB_ERR_ARG = 1,     /* bad argument (null pointer, unsupported size) -> ValueError */
+  FB_ERR_SHAPE = 2,   /* non-conforming operands -> ShapeError */
+  FB_ERR_CUDA = 3,    /* CUDA runtime / launch failure -> RuntimeError */
+  FB_ERR_DATA = 4,    /* bad keys -> DataError */
+  FB_ERR_NUMERIC = 5, /* numeric failure -> NumericError */
+  FB_ERR_NCCL = 6
+};
+
+/* One attribute block (K_i, R_i) of a normalized matrix (normmat.py:47-130). */
+typedef struct fb_part {
+  const int32_t* fk;    /* n_s targets into rows of r (IndicatorMatrix.target, indicator.py:35) */
+  const double* r;      /* n_r x d_r row-major attribute table (unreferenced rows dropped) */
+  int64_t n_r;
+  int32_t d_r;
+  const double* counts; /* optional cached colSums(K) as f64 (indicator.py:61-66); may be NULL */
+} fb_part;
+
+/* Untransposed PK-FK / star normalized matrix T = [S, K_1 R_1, ..., K_q R_q]. */
+typedef struct fb_normalized {
+  const double* s; /* n_s x d_s row-major entity table (d_s may be 0) */
+  int64_t n_s;
+  int32_t d_s;
+  int32_t q;       /* number of attribute blocks, 0..FB_MAX_PARTS */
+  fb_part part[FB_MAX_PARTS];
+} fb_normalized;
+
+/* ---- library ---------------------------------------------------------------- */
+int fb_abi_version(void);
+const char* fb_last_error(void);
+/* Select the device and cache its SM count. */
+int fb_init(int device);
+/* Number of kernels this library has launched in this process (instrumentation). */
+uint64_t fb_launch_count(void);
+
+/* ---- construction (normmat.py:182-237, indicator.py:61-66) --------------------- */
+/* counts_full[j] = #{i : key[i] == j+1}; *first_bad = smallest i with key outside
+ * [1, n_r] or UINT64_MAX (device scalar). Replaces _check_keys' validation. */
+int fb_key_check(const int64_t* key, int64_t n, int64_t n_r, int32_t* counts_full,
+                 unsigned long long* first_bad, fb_stream_t stream);
+size_t fb_key_remap_workspace_bytes(int64_t n_r);
+/* _remap_part (normmat.py:168-179): lookup[j] = rank of j among used keys or -1,
+ * *n_used (device), target[i] = lookup[key[i]-1], used_idx[l] = j, counts_kept[l]. */
+int fb_key_remap(const int64_t* key, int64_t n, int64_t n_r, const int32_t* counts_full,
+                 int32_t* lookup, int32_t* n_used, int32_t* target, int64_t* used_idx,
+                 int32_t* counts_kept, void* ws, size_t ws_bytes, fb_stream_t stream);
+/* bincount of 0-based targets (IndicatorMatrix.counts). */
+int fb_fk_counts(const int32_t* fk, int64_t n, int32_t* counts, int64_t n_r, fb_stream_t stream);
+/* out[r,:] = in[idx[r],:]  (ndarray.take(axis=0)); idx int64. */
+int fb_gather_rows(const double* in, int64_t ld_in, const int64_t* idx, int64_t nrows, int32_t d,
+                   double* out, int64_t ld_out, fb_stream_t stream);
+int fb_gather_rows_i32(const double* in, int64_t ld_in, const int32_t* idx, int64_t nrows,
+                       int32_t d, double* out, int64_t ld_out, fb_stream_t stream);
+int fb_i32_to_f64(const int32_t* in, double* out, int64_t n, fb_stream_t stream);
+
+/* ---- operators (rewrite.py) ------------------------------------------------------ */
+/* LMM T·X (rewrite.py:172-191). x: d x d_x row-major, d = d_s + sum d_r; out: n_s x d_x. */
+size_t fb_lmm_workspace_bytes(const fb_normalized* nm, int32_t d_x);
+int fb_lmm(const fb_normalized* nm, const double* x, int32_t d_x, double* out, void* ws,
+           size_t ws_bytes, fb_stream_t stream);
+
+/* rowSums(T) (rewrite.py:118-128): out n_s x 1. */
+size_t fb_row_sums_workspace_bytes(const fb_normalized* nm);
+int fb_row_sums(const fb_normalized* nm, double* out, void* ws, size_t ws_bytes,
+                fb_stream_t stream);
+
+/* Weighted transposed product out(j, c) = sum_i w(i, j) T(i, c), j < n_w, c < d, with
+ * w(i, j) = w[i*w_rs + j*w_cs] and out(j, c) = out[j*o_js + c*o_cs]. Covers
+ *   rmm X·T (rewrite.py:194-212):          w = X^T  (w_rs = 1,   w_cs = n_s)
+ *   lmm on T.T, i.e. T^T·X (rewrite.py:182-183): w = X (w_rs = n_w, w_cs = 1)
+ * The X·K halves are FK scatter-adds (indicator.py:130-141) fused into the S pass. */
+size_t fb_wt_workspace_bytes(const fb_normalized* nm, int32_t n_w);
+int fb_wt(const fb_normalized* nm, const double* w, int32_t n_w, int64_t w_rs, int64_t w_cs,
+          double* out, int64_t o_js, int64_t o_cs, void* ws, size_t ws_bytes, fb_stream_t stream);
+
+/* colSums(T) (rewrite.py:131-149): out 1 x d. Uses part.counts when given. */
+size_t fb_col_sums_workspace_bytes(const fb_normalized* nm);
+int fb_col_sums(const fb_normalized* nm, double* out, void* ws, size_t ws_bytes,
+                fb_stream_t stream);
+/* sum(T) (rewrite.py:152-165): out[0] (device scalar). */
+int fb_sum_all(const fb_normalized* nm, double* out, void* ws, size_t ws_bytes,
+               fb_stream_t stream);
+
+/* Element-wise scalar op / function on one factor matrix (kernel.py:219-300).
+ * op: 0 add 1 radd 2 sub 3 rsub 4 mul 5 rmul 6 div 7 rdiv 8 pow 9 rpow
+ * fn: 0 exp 1 log 2 square 3 sqrt 4 abs 5 negative 6 log1p 7 expm1 8 sin 9 cos 10 tanh
+ *     11 sigmoid 12 reciprocal 13 identity */
+int fb_scalar_map(const double* in, double* out, int64_t n, int32_t op, double x,
+                  fb_stream_t stream);
+int fb_unary_map(const double* in, double* out, int64_t n, int32_t fn, fb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FACTORLA_B200_H */

@@ -1,0 +1,148 @@
+"""Generate golden vectors from the LIVE reference package (build container only).
+
+Run here, where /root/reference exists:
+
+    PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden.py
+
+It imports ``factorla`` from /root/reference/pkg/src, builds small seeded PK-FK / star /
+skewed fixtures (including unreferenced attribute rows and a zero-width S), runs every
+in-scope operator and driver through the reference's own public API, and writes
+``tests/golden/<fixture>.npz`` (inputs + outputs + the reference's op counters). The GPU
+box never reads /root/reference; tests read only these committed files.
+"""
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
+
+
+def _fixtures():
+    rng = np.random.default_rng(20161224)
+    fx = {}
+    # SPEC fixture F1
+    fx["f1"] = dict(s=np.array([[1.0, 2], [3, 4], [5, 6]]), parts=[(np.array([1, 2, 1]), np.array([[10.0, 20], [30, 40]]))])
+    # SPEC fixture F3, star q=2
+    fx["f3"] = dict(
+        s=np.array([[1.0], [2], [3]]),
+        parts=[(np.array([1, 2, 1]), np.array([[10.0], [20]])), (np.array([2, 1, 2]), np.array([[100.0], [200]]))],
+    )
+    # random PK-FK, N(0,1), R rows 3, 11, 29 never referenced
+    n_s, n_r = 257, 31
+    keys = rng.integers(1, n_r + 1, size=n_s)
+    keys[np.isin(keys, [3, 11, 29])] = 1
+    fx["pkfk_normal"] = dict(s=rng.standard_normal((n_s, 5)), parts=[(keys, rng.standard_normal((n_r, 7)))])
+    # star with two FKs, N(0,1)
+    n_s = 301
+    fx["star_normal"] = dict(
+        s=rng.standard_normal((n_s, 4)),
+        parts=[
+            (rng.integers(1, 21, size=n_s), rng.standard_normal((20, 3))),
+            (rng.integers(1, 53, size=n_s), rng.standard_normal((52, 6))),
+        ],
+    )
+    # Zipf(1.2)-skewed FK over U[0,1) tables (non-negative, for GNMF)
+    n_s, n_r = 503, 40
+    p = np.arange(1, n_r + 1, dtype=np.float64) ** -1.2
+    p /= p.sum()
+    zk = np.searchsorted(np.cumsum(p), rng.random(n_s), side="right") + 1
+    zk = np.minimum(zk, n_r)
+    fx["zipf_uniform"] = dict(s=rng.random((n_s, 3)), parts=[(zk, rng.random((n_r, 9)))])
+    # wide-ish U[0,1) PK-FK (crossprod / linreg)
+    n_s, n_r = 400, 25
+    fx["pkfk_uniform"] = dict(s=rng.random((n_s, 12)), parts=[(rng.integers(1, n_r + 1, size=n_s), rng.random((n_r, 18)))])
+    # zero-width entity table (SPEC.md DESIGN DECISIONS: d_S = 0 is legal)
+    n_s, n_r = 64, 9
+    fx["zero_width_s"] = dict(s=np.zeros((n_s, 0)), parts=[(rng.integers(1, n_r + 1, size=n_s), rng.standard_normal((n_r, 4)))])
+    return fx
+
+
+def main():
+    sys.path.insert(0, REF)
+    os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    import factorla
+    from factorla import kernel, ml, normmat, rewrite
+
+    os.makedirs(OUT, exist_ok=True)
+    rng = np.random.default_rng(7)
+    for name, f in _fixtures().items():
+        s, parts = f["s"], f["parts"]
+        if len(parts) == 1:
+            nm = normmat.build_pkfk(s, parts[0][0], parts[0][1])
+        else:
+            nm = normmat.build_star(s, parts)
+        n, d = nm.shape
+        rec = {"s": s, "q": np.array(len(parts))}
+        for i, (k, r) in enumerate(parts):
+            rec[f"key{i}"] = np.asarray(k, dtype=np.int64)
+            rec[f"r{i}"] = r
+            e, rk = nm.blocks[i + 1]
+            rec[f"target{i}"] = e.target
+            rec[f"used{i}"] = nm.source_rows[i + 1]
+            rec[f"counts{i}"] = e.counts
+            rec[f"rkept{i}"] = rk
+        rec["materialize"] = normmat.materialize(nm)
+        x1 = rng.standard_normal((d, 1))
+        x3 = rng.standard_normal((d, 3))
+        p2 = rng.standard_normal((n, 2))
+        xr = rng.standard_normal((2, n))
+        xt = rng.standard_normal((3, d))
+        rec.update(x1=x1, x3=x3, p2=p2, xr=xr, xt=xt)
+        c = kernel.OpCounter()
+        rec["lmm_x1"] = rewrite.lmm(nm, x1, c)
+        rec["cnt_lmm_x1"] = np.array([c.multiplies, c.additions])
+        rec["lmm_x3"] = rewrite.lmm(nm, x3)
+        c = kernel.OpCounter()
+        rec["tmm_p2"] = rewrite.lmm(nm.T, p2, c)
+        rec["cnt_tmm_p2"] = np.array([c.multiplies, c.additions])
+        c = kernel.OpCounter()
+        rec["rmm_xr"] = rewrite.rmm(xr, nm, c)
+        rec["cnt_rmm_xr"] = np.array([c.multiplies, c.additions])
+        rec["rmm_t_xt"] = rewrite.rmm(xt, nm.T)
+        c = kernel.OpCounter()
+        rec["row_sums"] = rewrite.row_sums(nm, c)
+        rec["cnt_row_sums"] = np.array([c.multiplies, c.additions])
+        c = kernel.OpCounter()
+        rec["col_sums"] = rewrite.col_sums(nm, c)
+        rec["cnt_col_sums"] = np.array([c.multiplies, c.additions])
+        c = kernel.OpCounter()
+        rec["sum_all"] = np.array(rewrite.sum_all(nm, c))
+        rec["cnt_sum_all"] = np.array([c.multiplies, c.additions])
+        rec["row_sums_t"] = rewrite.row_sums(nm.T)
+        rec["col_sums_t"] = rewrite.col_sums(nm.T)
+        for op, x in (("mul", 2.0), ("add", 3.0), ("rsub", 1.5), ("div", 4.0), ("pow", 2.0)):
+            c = kernel.OpCounter()
+            rec[f"scalar_{op}"] = normmat.materialize(rewrite.scalar_op(nm, x, op, c))
+            rec[f"cnt_scalar_{op}"] = np.array([c.multiplies, c.additions])
+        rec["fn_exp"] = normmat.materialize(rewrite.scalar_fn(nm, np.exp))
+        rec["fn_square"] = normmat.materialize(rewrite.scalar_fn(nm, np.square))
+        if s.shape[1] > 0:
+            c = kernel.OpCounter()
+            rec["crossprod"] = rewrite.crossprod(nm, counter=c)
+            rec["cnt_crossprod"] = np.array([c.multiplies, c.additions])
+            w_true = rng.standard_normal((d, 1))
+            t = normmat.materialize(nm)
+            y_lin = t @ w_true + 0.01 * rng.standard_normal((n, 1))
+            out = ml.linreg_normal(nm, y_lin)
+            rec.update(y_lin=y_lin, linreg_w=out.weights, linreg_obj=np.array(out.objective))
+            cfg = ml.TrainConfig(iterations=5, step_size=1e-3, k=3, r=2, rng_seed=3)
+            y_log = np.where(t @ w_true >= 0, 1.0, -1.0)
+            out = ml.logistic_gd(nm, y_log, cfg)
+            rec.update(y_log=y_log, logreg_w=out.weights, logreg_obj=np.array(out.objective))
+            out = ml.linreg_gd(nm, y_lin, cfg)
+            rec.update(linreg_gd_w=out.weights, linreg_gd_obj=np.array(out.objective))
+            out = ml.kmeans(nm, cfg)
+            rec.update(kmeans_c=out.centroids, kmeans_obj=np.array(out.objective))
+            if float(min(s.min(), min(r.min() for _, r in parts))) >= 0:
+                out = ml.gnmf(nm, cfg)
+                rec.update(gnmf_w=out.factors[0], gnmf_h=out.factors[1], gnmf_obj=np.array(out.objective))
+        path = os.path.join(OUT, f"{name}.npz")
+        np.savez_compressed(path, **{k: np.asarray(v) for k, v in rec.items()})
+        print("wrote", path, os.path.getsize(path), "bytes", "factorla", getattr(factorla, "__version__", "?"))
+
+
+if __name__ == "__main__":
+    main()

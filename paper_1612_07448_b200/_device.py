@@ -1,0 +1,75 @@
+"""Device plumbing: operand coercion, stream handles and per-stream workspaces.
+
+PyTorch owns device memory and streams; it is the plumbing under the C ABI, never
+the arithmetic. ``as_matrix`` mirrors ``kernel.as_matrix`` (kernel.py:73-88): inputs
+become 2-D float64 row-major matrices (a 1-D vector becomes a single column), but on
+the current CUDA device.
+"""
+
+import numpy as np
+import torch
+
+from .exceptions import ExtensionMissingError, ShapeError
+
+
+def device():
+    if not torch.cuda.is_available():
+        raise ExtensionMissingError("no CUDA device: the factorized operators run only on sm_100a")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t):
+    return t.data_ptr() if t is not None and t.numel() > 0 else None
+
+
+def is_host(a):
+    return not (isinstance(a, torch.Tensor) and a.is_cuda)
+
+
+def as_matrix(a, dtype=torch.float64):
+    """2-D contiguous float64 CUDA tensor (kernel.as_matrix semantics)."""
+    if isinstance(a, torch.Tensor):
+        t = a
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64)))
+    if t.dim() == 1:
+        t = t.reshape(-1, 1)
+    if t.dim() != 2:
+        raise ShapeError(f"expected a 2-D matrix, got ndim={t.dim()}")
+    return t.to(device=device(), dtype=dtype, non_blocking=True).contiguous()
+
+
+def as_vector_i64(a):
+    if isinstance(a, torch.Tensor):
+        t = a.reshape(-1)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(a).reshape(-1)))
+    return t.to(device=device(), non_blocking=True)
+
+
+def to_like(t, like_host):
+    """Return ``t`` as a NumPy array when the caller handed us host data."""
+    if like_host:
+        return t.cpu().numpy()
+    return t
+
+
+_ws = {}
+
+
+def workspace(nbytes):
+    """A scratch buffer reused across calls on the same (device, stream).
+
+    Calls on one stream execute in order, so one buffer per stream is race-free.
+    """
+    key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
+    buf = _ws.get(key)
+    need = max(int(nbytes), 256)
+    if buf is None or buf.numel() < need:
+        buf = torch.empty(need + (need >> 2), dtype=torch.uint8, device=device())
+        _ws[key] = buf
+    return buf

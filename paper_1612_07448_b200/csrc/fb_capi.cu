@@ -1,0 +1,373 @@
+// fb_capi.cu — extern "C" entry points declared in include/factorla_b200.h.
+//
+// Validation (shapes, nulls, supported sizes) happens here, before any launch, and
+// failures come back as FB_ERR_* codes with a thread-local message; the Python layer
+// maps them onto the reference's exception classes (exceptions.py).
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "factorla_b200.h"
+#include "fb_kernels.cuh"
+
+namespace fb {
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace fb
+
+namespace {
+
+thread_local char g_err[512] = "";
+int g_num_sms = 148;
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return FB_OK;
+  if (e == cudaErrorNotSupported) return fail(FB_ERR_ARG, "%s: unsupported size", what);
+  return fail(FB_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+inline cudaStream_t cs(fb_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// Carves a caller workspace; returns nullptr when it runs out.
+struct Carver {
+  char* p;
+  size_t left;
+  template <class T>
+  T* take(size_t count) {
+    size_t b = align256(count * sizeof(T));
+    if (b > left) return nullptr;
+    T* r = reinterpret_cast<T*>(p);
+    p += b;
+    left -= b;
+    return r;
+  }
+};
+
+int check_nm(const fb_normalized* nm) {
+  if (!nm) return fail(FB_ERR_ARG, "normalized matrix is NULL");
+  if (nm->q < 0 || nm->q > FB_MAX_PARTS)
+    return fail(FB_ERR_ARG, "q=%d attribute blocks outside [0, %d]", nm->q, FB_MAX_PARTS);
+  if (nm->n_s < 0 || nm->d_s < 0) return fail(FB_ERR_SHAPE, "negative entity shape");
+  if (nm->d_s > 0 && !nm->s && nm->n_s > 0) return fail(FB_ERR_ARG, "S is NULL");
+  for (int i = 0; i < nm->q; ++i) {
+    const fb_part& p = nm->part[i];
+    if (p.n_r < 1 || p.d_r < 0) return fail(FB_ERR_SHAPE, "part %d: bad shape %lldx%d", i, (long long)p.n_r, p.d_r);
+    if ((!p.fk && nm->n_s > 0) || (!p.r && p.d_r > 0)) return fail(FB_ERR_ARG, "part %d: NULL pointer", i);
+  }
+  return FB_OK;
+}
+
+int64_t total_cols(const fb_normalized* nm) {
+  int64_t d = nm->d_s;
+  for (int i = 0; i < nm->q; ++i) d += nm->part[i].d_r;
+  return d;
+}
+
+int64_t max_width(const fb_normalized* nm) {
+  int64_t d = nm->d_s;
+  for (int i = 0; i < nm->q; ++i) d = nm->part[i].d_r > d ? nm->part[i].d_r : d;
+  return d;
+}
+
+// Column chunk widths the templated kernels are instantiated for.
+int chunk_width(int rem) {
+  if (rem >= 16) return 16;
+  static const int ok[] = {12, 10, 8, 7, 6, 5, 4, 3, 2, 1};
+  if (rem == 16 || rem == 12 || rem == 10 || rem <= 8) return rem;
+  for (int w : ok)
+    if (w <= rem) return w;
+  return 1;
+}
+
+__global__ void fill_kernel(double* p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void sum_vector_kernel(const double* v, int64_t n, double* out) {
+  // single warp, fixed order per lane then a fixed shuffle tree: deterministic
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 32) s += v[i];
+  s = fb::warp_sum(s);
+  if (threadIdx.x == 0) *out = s;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fb_abi_version(void) { return FB_ABI_VERSION; }
+const char* fb_last_error(void) { return g_err; }
+uint64_t fb_launch_count(void) { return fb::g_launches.load(); }
+
+int fb_init(int device) {
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+  int sms = 0;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
+  g_num_sms = sms;
+  return FB_OK;
+}
+
+// ------------------------------------------------------------------ construction
+int fb_key_check(const int64_t* key, int64_t n, int64_t n_r, int32_t* counts_full,
+                 unsigned long long* first_bad, fb_stream_t stream) {
+  if (n < 0 || n_r < 1) return fail(FB_ERR_SHAPE, "key_check: n=%lld n_r=%lld", (long long)n, (long long)n_r);
+  if ((n > 0 && !key) || !counts_full || !first_bad) return fail(FB_ERR_ARG, "key_check: NULL pointer");
+  return cuda_status(fb::launch_key_check_hist(key, n, n_r, counts_full, first_bad, cs(stream), g_num_sms),
+                     "key_check");
+}
+
+size_t fb_key_remap_workspace_bytes(int64_t n_r) {
+  return align256(fb::used_scan_ws_ints(n_r) * sizeof(int32_t)) + 256;
+}
+
+int fb_key_remap(const int64_t* key, int64_t n, int64_t n_r, const int32_t* counts_full,
+                 int32_t* lookup, int32_t* n_used, int32_t* target, int64_t* used_idx,
+                 int32_t* counts_kept, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  if (ws_bytes < fb_key_remap_workspace_bytes(n_r) || !ws) return fail(FB_ERR_ARG, "key_remap: workspace too small");
+  cudaError_t e = fb::launch_used_scan(counts_full, n_r, lookup, n_used, static_cast<int32_t*>(ws), cs(stream), g_num_sms);
+  if (e != cudaSuccess) return cuda_status(e, "used_scan");
+  return cuda_status(fb::launch_remap(key, n, lookup, counts_full, n_r, target, used_idx, counts_kept, cs(stream), g_num_sms),
+                     "remap");
+}
+
+int fb_fk_counts(const int32_t* fk, int64_t n, int32_t* counts, int64_t n_r, fb_stream_t stream) {
+  if ((n > 0 && !fk) || !counts) return fail(FB_ERR_ARG, "fk_counts: NULL pointer");
+  return cuda_status(fb::launch_fk_hist(fk, n, counts, n_r, cs(stream), g_num_sms), "fk_counts");
+}
+
+int fb_gather_rows(const double* in, int64_t ld_in, const int64_t* idx, int64_t nrows, int32_t d,
+                   double* out, int64_t ld_out, fb_stream_t stream) {
+  return cuda_status(fb::launch_gather_rows(in, ld_in, idx, nullptr, nrows, d, out, ld_out, cs(stream), g_num_sms),
+                     "gather_rows");
+}
+
+int fb_gather_rows_i32(const double* in, int64_t ld_in, const int32_t* idx, int64_t nrows, int32_t d,
+                       double* out, int64_t ld_out, fb_stream_t stream) {
+  return cuda_status(fb::launch_gather_rows(in, ld_in, nullptr, idx, nrows, d, out, ld_out, cs(stream), g_num_sms),
+                     "gather_rows_i32");
+}
+
+int fb_i32_to_f64(const int32_t* in, double* out, int64_t n, fb_stream_t stream) {
+  return cuda_status(fb::launch_i32_to_f64(in, out, n, cs(stream), g_num_sms), "i32_to_f64");
+}
+
+// ------------------------------------------------------------------ LMM / rowSums
+size_t fb_lmm_workspace_bytes(const fb_normalized* nm, int32_t d_x) {
+  if (!nm) return 0;
+  int w = d_x < 16 ? d_x : 16;
+  size_t b = 0;
+  for (int i = 0; i < nm->q; ++i) b += align256(static_cast<size_t>(nm->part[i].n_r) * w * sizeof(double));
+  return b + 256;
+}
+
+int fb_lmm(const fb_normalized* nm, const double* x, int32_t d_x, double* out, void* ws,
+           size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (d_x < 1) return fail(FB_ERR_SHAPE, "lmm: d_x=%d", d_x);
+  if (!x || (!out && nm->n_s > 0)) return fail(FB_ERR_ARG, "lmm: NULL pointer");
+  if (ws_bytes < fb_lmm_workspace_bytes(nm, d_x)) return fail(FB_ERR_ARG, "lmm: workspace too small");
+  if (max_width(nm) > 256) return fail(FB_ERR_ARG, "lmm: factor widths above 256 are not supported");
+  for (int c0 = 0; c0 < d_x;) {
+    const int w = chunk_width(d_x - c0);
+    Carver cv{static_cast<char*>(ws), ws_bytes};
+    const int32_t* fks[FB_MAX_PARTS];
+    const double* zs[FB_MAX_PARTS];
+    int64_t off = nm->d_s;
+    for (int i = 0; i < nm->q; ++i) {
+      const fb_part& p = nm->part[i];
+      double* z = cv.take<double>(static_cast<size_t>(p.n_r) * w);
+      // z_i = R_i · X[off:off+d_r, c0:c0+w]   (rewrite.py:187)
+      cudaError_t e = fb::launch_lmm_rows(p.r, p.n_r, p.d_r, x + off * d_x + c0, w, d_x, 0, nullptr,
+                                          nullptr, z, w, cs(stream), g_num_sms);
+      if (e != cudaSuccess) return cuda_status(e, "lmm(z)");
+      fks[i] = p.fk;
+      zs[i] = z;
+      off += p.d_r;
+    }
+    // out = S · X[0:d_s, c0:c0+w] + Σ z_i[fk_i]   (rewrite.py:186-190)
+    cudaError_t e = fb::launch_lmm_rows(nm->s, nm->n_s, nm->d_s, x + c0, w, d_x, nm->q, fks, zs,
+                                        out + c0, d_x, cs(stream), g_num_sms);
+    if (e != cudaSuccess) return cuda_status(e, "lmm(S)");
+    c0 += w;
+  }
+  return FB_OK;
+}
+
+size_t fb_row_sums_workspace_bytes(const fb_normalized* nm) {
+  if (!nm) return 0;
+  return fb_lmm_workspace_bytes(nm, 1) + align256(static_cast<size_t>(total_cols(nm) + 1) * sizeof(double));
+}
+
+int fb_row_sums(const fb_normalized* nm, double* out, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (ws_bytes < fb_row_sums_workspace_bytes(nm)) return fail(FB_ERR_ARG, "row_sums: workspace too small");
+  const int64_t d = total_cols(nm);
+  double* ones = static_cast<double*>(ws);
+  const size_t ob = align256(static_cast<size_t>(d + 1) * sizeof(double));
+  fill_kernel<<<1, 256, 0, cs(stream)>>>(ones, d + 1, 1.0);
+  FB_LAUNCHED();
+  // rowSums(T) = S·1 + Σ K_i·(R_i·1): the LMM pass with X = ones (kernel.py:174-182)
+  return fb_lmm(nm, ones, 1, out, static_cast<char*>(ws) + ob, ws_bytes - ob, stream);
+}
+
+// ------------------------------------------------------------------ Wᵀ·T family
+size_t fb_wt_workspace_bytes(const fb_normalized* nm, int32_t n_w) {
+  if (!nm) return 0;
+  const int w = n_w < 16 ? n_w : 16;
+  size_t b = 0;
+  for (int i = 0; i < nm->q; ++i) b += align256(static_cast<size_t>(nm->part[i].n_r) * w * sizeof(double));
+  b += align256(fb::colreduce_workspace_doubles(0, static_cast<int>(max_width(nm)), w, g_num_sms) * sizeof(double));
+  b += 256;  // counter
+  return b;
+}
+
+static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_t w_rs, int64_t w_cs,
+                   const double* const* part_weights, double* out, int64_t o_js, int64_t o_cs, void* ws,
+                   size_t ws_bytes, fb_stream_t stream) {
+  // part_weights != nullptr: colSums mode — S pass with implicit ones, R_i pass with counts_i.
+  for (int j0 = 0; j0 < n_w;) {
+    const int nx = chunk_width(n_w - j0);
+    Carver cv{static_cast<char*>(ws), ws_bytes};
+    double* bins[FB_MAX_PARTS] = {};
+    if (!part_weights)
+      for (int i = 0; i < nm->q; ++i) bins[i] = cv.take<double>(static_cast<size_t>(nm->part[i].n_r) * nx);
+    double* partials = cv.take<double>(fb::colreduce_workspace_doubles(0, static_cast<int>(max_width(nm)), nx, g_num_sms));
+    unsigned int* counter = cv.take<unsigned int>(1);
+    if (!partials || !counter) return fail(FB_ERR_ARG, "wt: workspace too small");
+
+    fb::ColReduce c{};
+    c.a = nm->s;
+    c.n = nm->n_s;
+    c.d = nm->d_s;
+    c.nx = nx;
+    c.w = w ? w + j0 * w_cs : nullptr;
+    c.w_rs = w_rs;
+    c.w_cs = w_cs;
+    c.nfk = part_weights ? 0 : nm->q;
+    for (int i = 0; i < c.nfk; ++i) {
+      c.fk[i] = nm->part[i].fk;
+      c.bins[i] = bins[i];
+      c.nbins[i] = nm->part[i].n_r;
+    }
+    c.out = out + j0 * o_js;
+    c.o_js = o_js;
+    c.o_cs = o_cs;
+    c.partials = partials;
+    c.counter = counter;
+    cudaError_t e = fb::launch_colreduce(c, cs(stream), g_num_sms);
+    if (e != cudaSuccess) return cuda_status(e, "wt(S)");
+    int64_t off = nm->d_s;
+    for (int i = 0; i < nm->q; ++i) {
+      const fb_part& p = nm->part[i];
+      fb::ColReduce r{};
+      r.a = p.r;
+      r.n = p.n_r;
+      r.d = p.d_r;
+      r.nx = nx;
+      r.w = part_weights ? part_weights[i] : bins[i];
+      r.w_rs = nx;
+      r.w_cs = 1;
+      r.nfk = 0;
+      r.out = out + j0 * o_js + off * o_cs;
+      r.o_js = o_js;
+      r.o_cs = o_cs;
+      r.partials = partials;
+      r.counter = counter;
+      e = fb::launch_colreduce(r, cs(stream), g_num_sms);
+      if (e != cudaSuccess) return cuda_status(e, "wt(R)");
+      off += p.d_r;
+    }
+    j0 += nx;
+  }
+  return FB_OK;
+}
+
+int fb_wt(const fb_normalized* nm, const double* w, int32_t n_w, int64_t w_rs, int64_t w_cs, double* out,
+          int64_t o_js, int64_t o_cs, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (n_w < 1) return fail(FB_ERR_SHAPE, "wt: n_w=%d", n_w);
+  if ((!w && nm->n_s > 0) || !out) return fail(FB_ERR_ARG, "wt: NULL pointer");
+  if (max_width(nm) > 256) return fail(FB_ERR_ARG, "wt: factor widths above 256 are not supported");
+  if (ws_bytes < fb_wt_workspace_bytes(nm, n_w)) return fail(FB_ERR_ARG, "wt: workspace too small");
+  return wt_impl(nm, w, n_w, w_rs, w_cs, nullptr, out, o_js, o_cs, ws, ws_bytes, stream);
+}
+
+size_t fb_col_sums_workspace_bytes(const fb_normalized* nm) {
+  if (!nm) return 0;
+  size_t b = fb_wt_workspace_bytes(nm, 1);
+  for (int i = 0; i < nm->q; ++i) b += align256(static_cast<size_t>(nm->part[i].n_r) * sizeof(double));
+  return b + align256(static_cast<size_t>(total_cols(nm)) * sizeof(double));
+}
+
+int fb_col_sums(const fb_normalized* nm, double* out, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (max_width(nm) > 256) return fail(FB_ERR_ARG, "col_sums: factor widths above 256 are not supported");
+  if (ws_bytes < fb_col_sums_workspace_bytes(nm)) return fail(FB_ERR_ARG, "col_sums: workspace too small");
+  // colSums(T) = [1ᵀS, colSums(K_i)·R_i]  (rewrite.py:131-149); counts are cached per
+  // indicator (indicator.py:61-66) — derive them here only when the caller has none.
+  Carver cv{static_cast<char*>(ws), ws_bytes};
+  const double* cnt[FB_MAX_PARTS] = {};
+  for (int i = 0; i < nm->q; ++i) {
+    const fb_part& p = nm->part[i];
+    if (p.counts) {
+      cnt[i] = p.counts;
+    } else {
+      double* c = cv.take<double>(static_cast<size_t>(p.n_r));
+      int32_t* ci = reinterpret_cast<int32_t*>(cv.take<double>(static_cast<size_t>(p.n_r)));
+      cudaError_t e = fb::launch_fk_hist(p.fk, nm->n_s, ci, p.n_r, cs(stream), g_num_sms);
+      if (e == cudaSuccess) e = fb::launch_i32_to_f64(ci, c, p.n_r, cs(stream), g_num_sms);
+      if (e != cudaSuccess) return cuda_status(e, "col_sums(counts)");
+      cnt[i] = c;
+    }
+  }
+  return wt_impl(nm, nullptr, 1, 1, 1, cnt, out, 0, 1, cv.p, cv.left, stream);
+}
+
+int fb_sum_all(const fb_normalized* nm, double* out, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  const int64_t d = total_cols(nm);
+  const size_t vb = align256(static_cast<size_t>(d > 0 ? d : 1) * sizeof(double));
+  if (ws_bytes < vb + fb_col_sums_workspace_bytes(nm)) return fail(FB_ERR_ARG, "sum_all: workspace too small");
+  double* v = static_cast<double*>(ws);
+  // sum(T) = sum(S) + colSums(K)·rowSums(R) (rewrite.py:152-165) = Σ_c colSums(T)_c
+  st = fb_col_sums(nm, v, static_cast<char*>(ws) + vb, ws_bytes - vb, stream);
+  if (st) return st;
+  sum_vector_kernel<<<1, 32, 0, cs(stream)>>>(v, d, out);
+  FB_LAUNCHED();
+  return cuda_status(cudaGetLastError(), "sum_all");
+}
+
+// ------------------------------------------------------------------ element-wise
+int fb_scalar_map(const double* in, double* out, int64_t n, int32_t op, double x, fb_stream_t stream) {
+  if (op < 0 || op > 9) return fail(FB_ERR_ARG, "scalar_map: unknown op %d", op);
+  if (op == fb::kDiv && x == 0.0) return fail(FB_ERR_NUMERIC, "division by zero scalar");
+  if (n > 0 && (!in || !out)) return fail(FB_ERR_ARG, "scalar_map: NULL pointer");
+  return cuda_status(fb::launch_scalar_map(in, out, n, op, x, cs(stream), g_num_sms), "scalar_map");
+}
+
+int fb_unary_map(const double* in, double* out, int64_t n, int32_t fn, fb_stream_t stream) {
+  if (fn < 0 || fn > 13) return fail(FB_ERR_ARG, "unary_map: unknown function %d", fn);
+  if (n > 0 && (!in || !out)) return fail(FB_ERR_ARG, "unary_map: NULL pointer");
+  return cuda_status(fb::launch_unary_map(in, out, n, fn, cs(stream), g_num_sms), "unary_map");
+}
+
+}  // extern "C"

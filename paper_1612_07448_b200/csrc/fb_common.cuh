@@ -1,0 +1,131 @@
+// fb_common.cuh — shared device helpers for the factorized-LA kernels (sm_100a).
+//
+// PTX wrappers for the Blackwell async-copy path used by every streaming kernel:
+// 1-D bulk copies (cp.async.bulk, SASS UBLKCP) global->shared completing on an
+// mbarrier transaction count, plus warp reductions, the FP64 tensor-core MMA
+// (mma.sync m8n8k4 f64 -> SASS DMMA; tcgen05 has no f64 kind) and status plumbing
+// shared by the C-ABI in fb_capi.cu.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define FB_DEV __device__ __forceinline__
+
+namespace fb {
+
+constexpr int kNumSMs = 148;  // B200; the host side re-queries it at runtime
+
+// ---------------------------------------------------------------- mbarrier / bulk copy
+FB_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+FB_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+FB_DEV void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
+FB_DEV void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+FB_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+FB_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+FB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "FB_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra FB_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// global -> shared bulk copy; dst/src 16-byte aligned, bytes a multiple of 16.
+FB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Same, with an L2 evict-first policy: streamed factor tiles are read exactly once.
+FB_DEV void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+FB_DEV uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+
+FB_DEV uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+
+// Streaming 128-bit global loads that skip L1 allocation.
+FB_DEV double2 ld_stream_d2(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p));
+  return r;
+}
+
+// ---------------------------------------------------------------- warp helpers
+FB_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+FB_DEV int lane_id() { return threadIdx.x & 31; }
+
+// ---------------------------------------------------------------- FP64 tensor core
+// D(8x8) += A(8x4, row) * B(4x8, col). Fragment ownership (lane l, g = l>>2, t = l&3):
+//   a = A[g][t], b = B[t][g], c0/c1 = C[g][2t], C[g][2t+1].
+FB_DEV void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------- launch accounting
+// Every kernel launch in the library goes through FB_LAUNCHED() so fb_launch_count()
+// can report how many of our kernels ran (bench.py's gpu_launches).
+void count_launch();
+#define FB_LAUNCHED() ::fb::count_launch()
+
+// ---------------------------------------------------------------- launch geometry
+inline int grid_for(int64_t work_items, int per_cta, int ctas_per_sm, int num_sms) {
+  int64_t need = (work_items + per_cta - 1) / per_cta;
+  int64_t cap = static_cast<int64_t>(num_sms) * ctas_per_sm;
+  if (need < 1) need = 1;
+  return static_cast<int>(need < cap ? need : cap);
+}
+
+}  // namespace fb

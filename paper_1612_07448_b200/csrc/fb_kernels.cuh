@@ -1,0 +1,66 @@
+// fb_kernels.cuh — internal launcher declarations shared by the .cu files and the C-ABI.
+#pragma once
+#include "fb_stream.cuh"
+
+namespace fb {
+
+constexpr int kMaxParts = 4;  // attribute tables per star schema handled in one pass
+
+// fb_lmm.cu ------------------------------------------------------------------------
+// out[i, 0:dx] (ld ldo) = a[i, :] · x (d × dx, ld ldx) + Σ_q z_q[fk_q[i], 0:dx]
+cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, int dx, int64_t ldx,
+                            int nfk,
+                            const int32_t* const* fk, const double* const* z, double* out,
+                            int64_t ldo, cudaStream_t st, int num_sms);
+
+// fb_reduce.cu ---------------------------------------------------------------------
+struct ColReduce {
+  const double* a;  // rows streamed: n × d row-major
+  int64_t n;
+  int d;
+  int nx;           // weight columns (1 with w == nullptr means all-ones weights)
+  const double* w;  // w(i, j) = w[i*w_rs + j*w_cs]
+  int64_t w_rs, w_cs;
+  int nfk;                         // fused Kᵀ scatter of the same weights
+  const int32_t* fk[kMaxParts];    // (original row order; warp-aggregated atomics)
+  double* bins[kMaxParts];         // n_R,q × nx row-major, zeroed by the launcher
+  int64_t nbins[kMaxParts];
+  double* out;                     // out(j, c) = out[j*o_js + c*o_cs]
+  int64_t o_js, o_cs;
+  double* partials;                // workspace: grid × nx × d
+  unsigned int* counter;           // workspace: one zeroed word
+};
+size_t colreduce_workspace_doubles(int64_t n, int d, int nx, int num_sms);
+cudaError_t launch_colreduce(const ColReduce& c, cudaStream_t st, int num_sms);
+
+// fb_elementwise.cu ------------------------------------------------------------------
+enum ScalarOp : int {
+  kAdd = 0, kRadd, kSub, kRsub, kMul, kRmul, kDiv, kRdiv, kPow, kRpow
+};
+enum UnaryFn : int {
+  kExp = 0, kLog, kSquare, kSqrt, kAbs, kNeg, kLog1p, kExpm1, kSin, kCos, kTanh, kSigmoid,
+  kReciprocal, kIdentity
+};
+cudaError_t launch_scalar_map(const double* in, double* out, int64_t n, int op, double x,
+                              cudaStream_t st, int num_sms);
+cudaError_t launch_unary_map(const double* in, double* out, int64_t n, int fn, cudaStream_t st,
+                             int num_sms);
+
+// fb_build.cu ------------------------------------------------------------------------
+cudaError_t launch_key_check_hist(const int64_t* key, int64_t n, int64_t n_r, int32_t* counts,
+                                  unsigned long long* first_bad, cudaStream_t st, int num_sms);
+cudaError_t launch_used_scan(const int32_t* counts, int64_t n_r, int32_t* lookup,
+                             int32_t* n_used, int32_t* block_ws, cudaStream_t st, int num_sms);
+size_t used_scan_ws_ints(int64_t n_r);
+cudaError_t launch_remap(const int64_t* key, int64_t n, const int32_t* lookup,
+                         const int32_t* counts, int64_t n_r, int32_t* target, int64_t* used_idx,
+                         int32_t* counts_kept, cudaStream_t st, int num_sms);
+cudaError_t launch_fk_hist(const int32_t* fk, int64_t n, int32_t* counts, int64_t nbins,
+                           cudaStream_t st, int num_sms);
+cudaError_t launch_gather_rows(const double* in, int64_t ld_in, const int64_t* idx64,
+                               const int32_t* idx32, int64_t nrows, int d, double* out,
+                               int64_t ld_out, cudaStream_t st, int num_sms);
+cudaError_t launch_i32_to_f64(const int32_t* in, double* out, int64_t n, cudaStream_t st,
+                              int num_sms);
+
+}  // namespace fb

@@ -1,0 +1,257 @@
+// fb_reduce.cu — weighted column reductions Wᵀ·F with a fused Kᵀ scatter.
+//
+// Replaces, in one streaming pass over a factor matrix F (n × d):
+//   * X·S in rmm (rewrite.py:207-209 -> kernel.matmul, kernel.py:103-129),
+//   * colSums(S) and counts·R in col_sums (rewrite.py:131-149; kernel.py:185-193),
+//   * binsᵀ·R, the (X·K)·R half of rmm,
+//   * and, fused into the S pass, the X·K scatter-add of right_compress
+//     (indicator.py:130-141, SciPy csc_matvec in the reference).
+// out(j, c) = Σ_i w(i, j) · F(i, c).  Each CTA reduces a contiguous row range into
+// registers (threads <-> columns), folds its row groups in shared memory, writes one
+// partial, and the last CTA to finish sums the partials in CTA order, so the result
+// is deterministic for a fixed grid. The scatter uses warp-aggregated atomics
+// (__match_any_sync groups equal keys before one RED per group).
+#include "fb_kernels.cuh"
+
+namespace fb {
+
+// weight access modes for the staged tile
+enum WMode : int { kWOnes = 0, kWInterleaved = 1, kWColumns = 2, kWGlobal = 3 };
+
+struct ColRedDev {
+  ColReduce c;
+  int wmode;
+  int w_stream0;  // first stream index holding weights
+  int fk_stream0;
+};
+
+template <int NX>
+FB_DEV double wval(const ColRedDev& p, const TileRing& ring, const StreamSet& ss, int stage,
+                   int64_t row0, int r, int j) {
+  switch (p.wmode) {
+    case kWOnes:
+      return 1.0;
+    case kWInterleaved:
+      return reinterpret_cast<const double*>(ring.stage_ptr(stage, ss, p.w_stream0))[r * NX + j];
+    case kWColumns:
+      return reinterpret_cast<const double*>(ring.stage_ptr(stage, ss, p.w_stream0 + j))[r];
+    default:
+      return p.c.w[(row0 + r) * p.c.w_rs + j * p.c.w_cs];
+  }
+}
+
+// Warp-aggregated scatter-add of vals[0:NX] into bins[key*NX + j].
+template <int NX>
+FB_DEV void scatter_add(double* bins, int key, const double (&vals)[NX], bool active) {
+  const unsigned full = 0xffffffffu;
+  const int lane = lane_id();
+  // inactive lanes use a key no active lane can have
+  const int k = active ? key : -1 - lane;
+  const unsigned peers = __match_any_sync(full, k);
+  const int leader = __ffs(peers) - 1;
+  double acc[NX];
+#pragma unroll
+  for (int j = 0; j < NX; ++j) acc[j] = vals[j];
+  unsigned rem = (lane == leader) ? (peers & ~(1u << lane)) : 0u;
+  while (__any_sync(full, rem != 0)) {
+    const int src = rem ? (__ffs(rem) - 1) : lane;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      const double t = __shfl_sync(full, vals[j], src);
+      if (rem) acc[j] += t;
+    }
+    if (rem) rem &= rem - 1;
+  }
+  if (active && lane == leader) {
+    double* b = bins + static_cast<int64_t>(key) * NX;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) atomicAdd(b + j, acc[j]);
+  }
+}
+
+template <int NX>
+__global__ void __launch_bounds__(256) colreduce_kernel(ColRedDev p, StreamSet ss, int stages,
+                                                        int tile_rows) {
+  extern __shared__ __align__(128) char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  char* buf = smem + 128;
+  const int d = p.c.d;
+
+  TileRing ring;
+  ring.buf = buf;
+  ring.bar = bars;
+  ring.stages = stages;
+  ring.tile_rows = tile_rows;
+  ring.n_rows = p.c.n;
+  ring.policy = policy_evict_first();
+  const int64_t ntiles = (p.c.n + tile_rows - 1) / tile_rows;
+  cta_tile_range(ntiles, ring.tile_begin, ring.tile_end);
+  ring.start(ss);
+
+  const int groups = d > 0 ? static_cast<int>(blockDim.x) / d : 0;
+  const int col = d > 0 ? static_cast<int>(threadIdx.x) % d : 0;
+  const int grp = d > 0 ? static_cast<int>(threadIdx.x) / d : 0;
+  const bool colthread = grp < groups;
+
+  double acc[NX];
+#pragma unroll
+  for (int j = 0; j < NX; ++j) acc[j] = 0.0;
+
+  for (int64_t k = 0; k < ring.tile_end - ring.tile_begin; ++k) {
+    const int stage = ring.acquire(ss, k);
+    const int64_t tile = ring.tile_begin + k;
+    const int rows = ring.rows_of(tile);
+    const int64_t r0 = tile * tile_rows;
+    if (colthread) {
+      const double* A = reinterpret_cast<const double*>(ring.stage_ptr(stage, ss, 0));
+      for (int r = grp; r < rows; r += groups) {
+        const double a = A[static_cast<size_t>(r) * d + col];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) acc[j] = fma(wval<NX>(p, ring, ss, stage, r0, r, j), a, acc[j]);
+      }
+    }
+    // fused Kᵀ scatter of the same weights (row-per-thread)
+    for (int q = 0; q < p.c.nfk; ++q) {
+      const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, p.fk_stream0 + q));
+      for (int rb = 0; rb < rows; rb += blockDim.x) {
+        const int r = rb + threadIdx.x;
+        const bool live = r < rows;
+        double v[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) v[j] = live ? wval<NX>(p, ring, ss, stage, r0, r, j) : 0.0;
+        scatter_add<NX>(p.c.bins[q], live ? fkt[r] : 0, v, live);
+      }
+    }
+    ring.release(ss, k);
+  }
+
+  // fold row groups: red[g][j][c]
+  double* red = reinterpret_cast<double*>(buf);  // ring buffers are free now
+  if (colthread) {
+#pragma unroll
+    for (int j = 0; j < NX; ++j) red[(static_cast<size_t>(grp) * NX + j) * d + col] = acc[j];
+  }
+  __syncthreads();
+  double* part = p.c.partials + static_cast<size_t>(blockIdx.x) * NX * d;
+  for (int e = threadIdx.x; e < NX * d; e += blockDim.x) {
+    double s = 0.0;
+    for (int g = 0; g < groups; ++g) s += red[static_cast<size_t>(g) * NX * d + e];
+    part[e] = s;
+  }
+  // last CTA sums the partials in CTA order
+  __threadfence();
+  __shared__ unsigned int ticket;
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(p.c.counter, 1u);
+  __syncthreads();
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  for (int e = threadIdx.x; e < NX * d; e += blockDim.x) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b)
+      s += __ldcg(p.c.partials + static_cast<size_t>(b) * NX * d + e);
+    const int j = e / d, c = e % d;
+    p.c.out[j * p.c.o_js + c * p.c.o_cs] = s;
+  }
+  if (threadIdx.x == 0) *p.c.counter = 0u;  // ready for the next launch
+}
+
+// ------------------------------------------------------------------ host side
+static int colred_tile_rows(int d) {
+  // ~32 KB of factor rows per stage, a multiple of 4 rows, at least 32
+  int rows = d > 0 ? (32 * 1024) / (d * 8) : 256;
+  if (rows > 512) rows = 512;
+  if (rows < 32) rows = 32;
+  return rows & ~3;
+}
+
+size_t colreduce_workspace_doubles(int64_t n, int d, int nx, int num_sms) {
+  (void)n;
+  return static_cast<size_t>(num_sms) * 2 * static_cast<size_t>(nx) * (d > 0 ? d : 1);
+}
+
+template <int NX>
+static cudaError_t launch_colreduce_nx(const ColReduce& c, cudaStream_t st, int num_sms) {
+  ColRedDev p{};
+  p.c = c;
+  const int tile_rows = colred_tile_rows(c.d);
+  StreamSet ss{};
+  int ns = 0;
+  ss.base[ns] = reinterpret_cast<const char*>(c.a);
+  ss.row_bytes[ns++] = static_cast<uint32_t>(c.d) * 8u;
+  if (c.w == nullptr) {
+    p.wmode = kWOnes;
+  } else if (c.w_cs == 1 && c.w_rs == NX) {
+    p.wmode = kWInterleaved;
+    p.w_stream0 = ns;
+    ss.base[ns] = reinterpret_cast<const char*>(c.w);
+    ss.row_bytes[ns++] = NX * 8u;
+  } else if (NX + 1 < kMaxStreams && c.w_rs == 1 && NX + 1 + c.nfk <= kMaxStreams) {
+    p.wmode = kWColumns;
+    p.w_stream0 = ns;
+    if constexpr (NX + 1 < kMaxStreams) {
+      for (int j = 0; j < NX; ++j) {
+        ss.base[ns] = reinterpret_cast<const char*>(c.w + j * c.w_cs);
+        ss.row_bytes[ns++] = 8u;
+      }
+    }
+  } else {
+    p.wmode = kWGlobal;
+  }
+  p.fk_stream0 = ns;
+  for (int q = 0; q < c.nfk; ++q) {
+    ss.base[ns] = reinterpret_cast<const char*>(c.fk[q]);
+    ss.row_bytes[ns++] = 4u;
+  }
+  ss.count = ns;
+  stream_layout(ss, tile_rows);
+  const int threads = 256;
+  const size_t red_bytes = static_cast<size_t>(threads) * NX * 8 * (c.d > 0 ? 1 : 1);
+  int stages = 3;
+  size_t smem = 128 + static_cast<size_t>(stages) * ss.stage_bytes;
+  if (smem < 128 + red_bytes + 1024) smem = 128 + red_bytes + 1024;
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  auto kern = colreduce_kernel<NX>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int per_sm = static_cast<int>((227 * 1024) / (smem + 1024));
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 2) per_sm = 2;
+  const int64_t ntiles = (c.n + tile_rows - 1) / tile_rows;
+  const int grid = grid_for(ntiles, 1, per_sm, num_sms);
+  for (int q = 0; q < c.nfk; ++q) {
+    e = cudaMemsetAsync(c.bins[q], 0, static_cast<size_t>(c.nbins[q]) * NX * sizeof(double), st);
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaMemsetAsync(c.counter, 0, sizeof(unsigned int), st);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, threads, smem, st>>>(p, ss, stages, tile_rows);
+  FB_LAUNCHED();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colreduce(const ColReduce& c, cudaStream_t st, int num_sms) {
+  if (c.d > 256) return cudaErrorNotSupported;
+  switch (c.nx) {
+#define FB_NX_CASE(N) \
+  case N:             \
+    return launch_colreduce_nx<N>(c, st, num_sms);
+    FB_NX_CASE(1)
+    FB_NX_CASE(2)
+    FB_NX_CASE(3)
+    FB_NX_CASE(4)
+    FB_NX_CASE(5)
+    FB_NX_CASE(6)
+    FB_NX_CASE(7)
+    FB_NX_CASE(8)
+    FB_NX_CASE(10)
+    FB_NX_CASE(12)
+    FB_NX_CASE(16)
+#undef FB_NX_CASE
+    default:
+      return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace fb

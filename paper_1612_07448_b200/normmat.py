@@ -1,0 +1,359 @@
+"""The normalized matrix on a B200: base-table factors resident in HBM.
+
+Mirrors ``factorla.normmat`` (normmat.py:1-375) for the PK-FK and star variants:
+``NormalizedMatrix`` keeps column blocks ``(indicator | None, factor)``, a logical
+transpose flag, and the kept source rows of every attribute table. The factors are
+float64 CUDA tensors (row-major, as the reference's C-contiguous arrays) and each
+indicator is an int32 FK column on the device. Construction (key validation, the
+unreferenced-row drop and remap) runs in the library's kernels (fb_build.cu).
+
+HBM layout per matrix: S (n_S × d_S f64), per part: FK (n_S int32), R_kept
+(n_R' × d_R f64), counts (n_R' f64, cached), plus lazily built caches (the FK-sorted
+permutation used by the segmented reductions).
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _lib
+from .exceptions import DataError, ShapeError
+
+__all__ = [
+    "IndicatorMatrix",
+    "NormalizedMatrix",
+    "ShapeStats",
+    "build_pkfk",
+    "build_star",
+    "materialize",
+    "transpose",
+    "stats",
+]
+
+PKFK = "pkfk"
+STAR = "star"
+DENSE = "dense"  # a regular matrix viewed as T = [S] (q = 0); used by the ML drivers
+
+
+class IndicatorMatrix:
+    """K stored as ``target[i] = j`` (indicator.py:27-95), int32 on the device."""
+
+    def __init__(self, target, cols, counts_i32=None):
+        if not (isinstance(target, torch.Tensor) and target.is_cuda and target.dtype == torch.int32):
+            raise ShapeError("indicator target must be an int32 CUDA tensor")
+        if target.dim() != 1:
+            raise ShapeError("indicator target must be a 1-D index array")
+        if target.numel() == 0:
+            raise ShapeError("indicator matrix must have at least one row")
+        cols = int(cols)
+        if cols < 1:
+            raise ShapeError("indicator matrix must have at least one column")
+        self.target = target.contiguous()
+        self.cols = cols
+        self._counts_i32 = counts_i32
+        self._counts = None
+
+    @property
+    def rows(self):
+        return self.target.numel()
+
+    @property
+    def shape(self):
+        return (self.rows, self.cols)
+
+    @property
+    def nnz(self):
+        return self.rows
+
+    @property
+    def counts_i32(self):
+        """bincount of the targets (indicator.py:61-66), exact int32."""
+        if self._counts_i32 is None:
+            so = _lib.lib()
+            c = torch.empty(self.cols, dtype=torch.int32, device=self.target.device)
+            _lib.check(so.fb_fk_counts(D.ptr(self.target), self.rows, D.ptr(c), self.cols, D.stream_handle()))
+            self._counts_i32 = c
+        return self._counts_i32
+
+    @property
+    def counts(self):
+        """Column sums of K as float64 (the reference's ``counts``), cached."""
+        if self._counts is None:
+            so = _lib.lib()
+            ci = self.counts_i32
+            c = torch.empty(self.cols, dtype=torch.float64, device=ci.device)
+            _lib.check(so.fb_i32_to_f64(D.ptr(ci), self.cols, D.ptr(c), D.stream_handle()))
+            self._counts = c
+        return self._counts
+
+    def all_columns_used(self):
+        return bool((self.counts_i32 > 0).all().item())
+
+    def target_numpy(self):
+        return self.target.cpu().numpy().astype(np.int64)
+
+    def __repr__(self):
+        return f"IndicatorMatrix(rows={self.rows}, cols={self.cols}, device)"
+
+
+class NormalizedMatrix:
+    """Immutable multi-matrix value (normmat.py:47-130); build with ``build_*``."""
+
+    def __init__(self, variant, blocks, transposed=False, source_rows=None, host_io=False):
+        blocks = tuple((e, f) for e, f in blocks)
+        if not blocks:
+            raise ShapeError("normalized matrix needs at least one block")
+        rows = {e.rows if e is not None else f.shape[0] for e, f in blocks}
+        if len(rows) != 1:
+            raise ShapeError(f"blocks disagree on logical row count: {sorted(rows)}")
+        for e, f in blocks:
+            if e is not None and e.cols != f.shape[0]:
+                raise ShapeError(f"indicator cols {e.cols} != factor rows {f.shape[0]}")
+        if blocks[0][0] is not None:
+            raise ShapeError("the first block must be the entity table S (no indicator)")
+        if len(blocks) - 1 > _lib.FB_MAX_PARTS:
+            raise ShapeError(f"at most {_lib.FB_MAX_PARTS} attribute tables are supported")
+        self.variant = variant
+        self.blocks = blocks
+        self.transposed = bool(transposed)
+        self.source_rows = tuple(source_rows) if source_rows is not None else None
+        self.host_io = bool(host_io)
+        self._cache = {}  # per-matrix device caches shared with the transposed view
+
+    # -- shape ------------------------------------------------------------
+    @property
+    def base_rows(self):
+        return self.blocks[0][1].shape[0]
+
+    @property
+    def base_cols(self):
+        return sum(f.shape[1] for _, f in self.blocks)
+
+    @property
+    def shape(self):
+        n, d = self.base_rows, self.base_cols
+        return (d, n) if self.transposed else (n, d)
+
+    def col_offsets(self):
+        widths = [f.shape[1] for _, f in self.blocks]
+        return np.concatenate([[0], np.cumsum(widths)]).astype(int)
+
+    # -- accessors ---------------------------------------------------------
+    @property
+    def s(self):
+        return self.blocks[0][1]
+
+    @property
+    def k(self):
+        if self.variant != PKFK:
+            raise ShapeError("k accessor is pkfk-only")
+        return self.blocks[1][0]
+
+    @property
+    def r(self):
+        if self.variant != PKFK:
+            raise ShapeError("r accessor applies to single-attribute variants")
+        return self.blocks[1][1]
+
+    @property
+    def parts(self):
+        return self.blocks[1:]
+
+    # -- logical ops -------------------------------------------------------
+    @property
+    def T(self):
+        t = NormalizedMatrix(self.variant, self.blocks, not self.transposed, self.source_rows, self.host_io)
+        t._cache = self._cache
+        return t
+
+    def untransposed(self):
+        return self if not self.transposed else self.T
+
+    def with_factors(self, factors):
+        """Same indicators / flag, new factor matrices (closure of scalar ops)."""
+        blocks = [(e, f) for (e, _), f in zip(self.blocks, factors)]
+        return NormalizedMatrix(self.variant, blocks, self.transposed, self.source_rows, self.host_io)
+
+    # -- C ABI view ----------------------------------------------------------
+    def c_struct(self):
+        """``fb_normalized`` describing the untransposed factors (cached)."""
+        st = self._cache.get("c_struct")
+        if st is None:
+            st = _lib.FbNormalized()
+            s = self.blocks[0][1]
+            st.s = D.ptr(s)
+            st.n_s = s.shape[0]
+            st.d_s = s.shape[1]
+            st.q = len(self.blocks) - 1
+            for i, (e, f) in enumerate(self.blocks[1:]):
+                p = st.part[i]
+                p.fk = D.ptr(e.target)
+                p.r = D.ptr(f)
+                p.n_r = f.shape[0]
+                p.d_r = f.shape[1]
+                p.counts = D.ptr(e.counts)
+            self._cache["c_struct"] = st
+        return ctypes.byref(st)
+
+    def __repr__(self):
+        n, d = self.shape
+        flag = ", transposed" if self.transposed else ""
+        return f"NormalizedMatrix({self.variant}, {n}x{d}{flag}, device)"
+
+
+def transpose(nm):
+    """Flip the logical-transpose flag; no data is copied (normmat.py:118-122)."""
+    return nm.T
+
+
+def as_normalized(m):
+    """View a regular matrix as T = [S] (q = 0) so the drivers run on the same kernels."""
+    if isinstance(m, NormalizedMatrix):
+        return m
+    return NormalizedMatrix(DENSE, [(None, D.as_matrix(m))], host_io=D.is_host(m))
+
+
+def materialize(nm):
+    """Expand T = [S, K_1 R_1, ...] on the device (normmat.py:138-161).
+
+    Gathers every attribute block with the library's row-gather kernel; honours the
+    transpose flag. Intended for tests and small inputs — the operators never call it.
+    """
+    so = _lib.lib()
+    n, d = nm.base_rows, nm.base_cols
+    out = torch.empty((n, d), dtype=torch.float64, device=nm.s.device)
+    offs = nm.col_offsets()
+    st = D.stream_handle()
+    for (e, f), c0, c1 in zip(nm.blocks, offs[:-1], offs[1:]):
+        if c1 == c0:
+            continue
+        if e is None:
+            out[:, c0:c1] = f
+        else:
+            _lib.check(so.fb_gather_rows_i32(D.ptr(f), f.shape[1], D.ptr(e.target), n, c1 - c0,
+                                             out.data_ptr() + 8 * int(c0), d, st))
+    out = out.t().contiguous() if nm.transposed else out
+    return D.to_like(out, nm.host_io)
+
+
+# ---------------------------------------------------------------------------
+# construction
+
+
+def _check_keys(key, n_rows, part_label=""):
+    """1-based key validation (normmat.py:182-198) -> int64 device tensor."""
+    k = D.as_vector_i64(key)
+    if not (k.dtype in (torch.int8, torch.int16, torch.int32, torch.int64, torch.uint8)):
+        kf = k.to(torch.float64)
+        if not bool(torch.all(kf == torch.round(kf)).item()):
+            raise DataError(f"key column{part_label} contains non-integer values")
+        k = kf.to(torch.int64)
+    return k.to(torch.int64).contiguous()
+
+
+def _remap_part(key, r, part_label=""):
+    """Validate keys, drop unreferenced rows of r, remap to 0-based (normmat.py:168-179).
+
+    Returns (indicator, r_kept, used) with ``used`` the kept 0-based source rows (int64).
+    """
+    so = _lib.lib()
+    st = D.stream_handle()
+    n_r = r.shape[0]
+    n = key.numel()
+    dev = r.device
+    counts_full = torch.empty(max(n_r, 1), dtype=torch.int32, device=dev)
+    first_bad = torch.empty(1, dtype=torch.int64, device=dev)
+    _lib.check(so.fb_key_check(D.ptr(key), n, n_r, counts_full.data_ptr(), first_bad.data_ptr(), st))
+    bad = int(first_bad.item())
+    if bad != -1:  # UINT64_MAX reads back as -1
+        raise DataError(
+            f"key{part_label} references nonexistent attribute row "
+            f"{int(key[bad].item())} at entity row {bad} (valid range 1..{n_r})"
+        )
+    lookup = torch.empty(n_r, dtype=torch.int32, device=dev)
+    n_used_t = torch.empty(1, dtype=torch.int32, device=dev)
+    target = torch.empty(n, dtype=torch.int32, device=dev)
+    used = torch.empty(n_r, dtype=torch.int64, device=dev)
+    counts_kept = torch.empty(n_r, dtype=torch.int32, device=dev)
+    ws = D.workspace(so.fb_key_remap_workspace_bytes(n_r))
+    _lib.check(so.fb_key_remap(D.ptr(key), n, n_r, counts_full.data_ptr(), lookup.data_ptr(),
+                               n_used_t.data_ptr(), D.ptr(target), used.data_ptr(),
+                               counts_kept.data_ptr(), ws.data_ptr(), ws.numel(), st))
+    n_used = int(n_used_t.item())
+    used = used[:n_used]
+    counts_kept = counts_kept[:n_used].clone()
+    if n_used == n_r:
+        r_kept = r
+    else:
+        r_kept = torch.empty((n_used, r.shape[1]), dtype=torch.float64, device=dev)
+        _lib.check(so.fb_gather_rows(D.ptr(r), r.shape[1], used.data_ptr(), n_used, r.shape[1],
+                                     D.ptr(r_kept), r.shape[1], st))
+    return IndicatorMatrix(target, n_used, counts_i32=counts_kept), r_kept, used
+
+
+def build_pkfk(s, key_column, r):
+    """PK-FK normalized matrix from S, its 1-based key column and R (normmat.py:201-214)."""
+    host = D.is_host(s)
+    s = D.as_matrix(s)
+    r = D.as_matrix(r)
+    key = _check_keys(key_column, r.shape[0])
+    if key.numel() != s.shape[0]:
+        raise ShapeError(f"key column length {key.numel()} != entity rows {s.shape[0]}")
+    ind, r_kept, used = _remap_part(key, r)
+    return NormalizedMatrix(PKFK, [(None, s), (ind, r_kept)], source_rows=[None, used], host_io=host)
+
+
+def build_star(s, parts):
+    """Star-schema normalized matrix: S plus ``[(key_column_i, R_i), ...]`` (normmat.py:217-237)."""
+    host = D.is_host(s)
+    s = D.as_matrix(s)
+    blocks = [(None, s)]
+    source = [None]
+    for idx, (key_column, r) in enumerate(parts):
+        r = D.as_matrix(r)
+        key = _check_keys(key_column, r.shape[0], part_label=f" (part {idx})")
+        if key.numel() != s.shape[0]:
+            raise ShapeError(f"part {idx}: key column length {key.numel()} != entity rows {s.shape[0]}")
+        ind, r_kept, used = _remap_part(key, r, part_label=f" (part {idx})")
+        blocks.append((ind, r_kept))
+        source.append(used)
+    if len(blocks) == 1:
+        raise ShapeError("star join needs at least one attribute table")
+    return NormalizedMatrix(STAR, blocks, source_rows=source, host_io=host)
+
+
+# ---------------------------------------------------------------------------
+# shape statistics
+
+
+@dataclass
+class ShapeStats:
+    """Dimensions plus the tuple/feature ratios (normmat.py:326-375)."""
+
+    variant: str
+    n_s: int
+    d_s: int
+    n_r: tuple
+    d_r: tuple
+    logical_rows: int
+    logical_cols: int
+    tuple_ratio: float
+    feature_ratio: float
+
+    @property
+    def d_total(self):
+        return self.logical_cols
+
+
+def stats(nm):
+    base = nm.untransposed()
+    n_log, d_log = base.shape
+    n_s, d_s = base.s.shape
+    n_r = tuple(f.shape[0] for _, f in base.blocks[1:])
+    d_r = tuple(f.shape[1] for _, f in base.blocks[1:])
+    tr = n_s / max(n_r) if n_r else 1.0
+    fr = (sum(d_r) / d_s) if d_s > 0 else float("inf")
+    return ShapeStats(nm.variant, n_s, d_s, n_r, d_r, n_log, d_log, float(tr), float(fr))

@@ -1,0 +1,277 @@
+"""Factorized operators over device-resident normalized matrices.
+
+Same functions, signatures, transpose-flag dispatch and error behaviour as the
+reference's ``factorla.rewrite`` (rewrite.py:25-39); the arithmetic runs in the
+sm_100a kernels behind ``libfactorla_b200.so``:
+
+====================  ==========================================  =======================
+operator              reference                                   C ABI
+====================  ==========================================  =======================
+``scalar_op``         rewrite.py:75-86 -> kernel.scalar_map        fb_scalar_map
+``scalar_fn``         rewrite.py:89-99 -> kernel.unary_map         fb_unary_map
+``row_sums``          rewrite.py:118-128                           fb_row_sums
+``col_sums``          rewrite.py:131-149                           fb_col_sums
+``sum_all``           rewrite.py:152-165                           fb_sum_all
+``lmm``               rewrite.py:172-191 (T.T: :182-183)           fb_lmm / fb_wt
+``rmm``               rewrite.py:194-212 (T.T: :204-205)           fb_wt / fb_lmm
+``crossprod``         rewrite.py:245-298 (efficient method)        fb_crossprod
+====================  ==========================================  =======================
+
+Operands may be NumPy arrays (results come back as NumPy, like the reference) or
+CUDA tensors (results stay on the device).
+"""
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _lib
+from . import kernel as K
+from .exceptions import NumericError, ShapeError
+from .normmat import NormalizedMatrix
+
+__all__ = [
+    "scalar_op",
+    "scalar_fn",
+    "row_sums",
+    "col_sums",
+    "sum_all",
+    "lmm",
+    "rmm",
+    "crossprod",
+]
+
+_SCALAR_OPS = {"add": 0, "radd": 1, "sub": 2, "rsub": 3, "mul": 4, "rmul": 5, "div": 6, "rdiv": 7, "pow": 8, "rpow": 9}
+_MULTIPLICATIVE = {"mul", "div", "pow", "rdiv", "rpow"}  # as kernel.py:216 ("rmul" tallies additions there)
+
+_UNARY = {
+    np.exp: 0,
+    np.log: 1,
+    np.square: 2,
+    np.sqrt: 3,
+    np.abs: 4,
+    np.negative: 5,
+    np.log1p: 6,
+    np.expm1: 7,
+    np.sin: 8,
+    np.cos: 9,
+    np.tanh: 10,
+    np.reciprocal: 12,
+}
+_UNARY_NAMES = {
+    "exp": 0, "log": 1, "square": 2, "sqrt": 3, "abs": 4, "absolute": 4, "negative": 5,
+    "log1p": 6, "expm1": 7, "sin": 8, "cos": 9, "tanh": 10, "sigmoid": 11, "reciprocal": 12,
+    "identity": 13,
+}
+
+
+def _nm_check(nm):
+    if not isinstance(nm, NormalizedMatrix):
+        raise TypeError(f"expected a NormalizedMatrix, got {type(nm).__name__}")
+
+
+def _operand(x):
+    """(device matrix, caller wanted host results)."""
+    return D.as_matrix(x), D.is_host(x)
+
+
+# ---------------------------------------------------------------------------
+# element-wise scalar operators (closed: output is a normalized matrix)
+
+
+def _map_factors(nm, launch):
+    so = _lib.lib()
+    st = D.stream_handle()
+    new = []
+    for _, f in nm.blocks:
+        out = torch.empty_like(f)
+        _lib.check(launch(so, f, out, st))
+        new.append(out)
+    return nm.with_factors(new)
+
+
+def scalar_op(nm, x, op, counter=None):
+    """``T <op> x`` applied to the factor matrices only (rewrite.py:75-86)."""
+    _nm_check(nm)
+    if op not in _SCALAR_OPS:
+        raise ValueError(f"unknown scalar op {op!r}")
+    x = float(x)
+    if op == "div" and x == 0:
+        raise NumericError("division by zero scalar")
+    code = _SCALAR_OPS[op]
+    out = _map_factors(nm, lambda so, f, o, st: so.fb_scalar_map(D.ptr(f), D.ptr(o), f.numel(), code, x, st))
+    if counter is not None:
+        for _, f in nm.blocks:
+            cost = f.numel()
+            counter.tally(cost, 0) if op in _MULTIPLICATIVE else counter.tally(0, cost)
+    return out
+
+
+def scalar_fn(nm, f, counter=None):
+    """Element-wise ``f(T)`` = (f(S), K, f(R)) (rewrite.py:89-99).
+
+    ``f`` is a NumPy ufunc from the supported set (exp, log, square, sqrt, abs,
+    negative, log1p, expm1, sin, cos, tanh, reciprocal) or one of those names
+    (plus "sigmoid"/"identity"). Arbitrary Python callables cannot run on the device
+    and raise ``NotImplementedError``.
+    """
+    _nm_check(nm)
+    code = _UNARY.get(f) if not isinstance(f, str) else _UNARY_NAMES.get(f)
+    if code is None:
+        raise NotImplementedError(
+            f"scalar_fn: {getattr(f, '__name__', f)!r} has no device kernel; supported: {sorted(_UNARY_NAMES)}"
+        )
+    out = _map_factors(nm, lambda so, fm, o, st: so.fb_unary_map(D.ptr(fm), D.ptr(o), fm.numel(), code, st))
+    if counter is not None:
+        for _, fm in nm.blocks:
+            counter.tally(fm.numel(), 0)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# aggregations
+
+
+def row_sums(nm, counter=None):
+    """Row totals of the logical matrix as a column vector (rewrite.py:118-128)."""
+    _nm_check(nm)
+    if nm.transposed:
+        r = col_sums(nm.T, counter)
+        return D.to_like(_as_dev(r).t().contiguous(), nm.host_io)
+    so = _lib.lib()
+    n = nm.base_rows
+    out = torch.empty((n, 1), dtype=torch.float64, device=nm.s.device)
+    cs = nm.c_struct()
+    ws = D.workspace(so.fb_row_sums_workspace_bytes(cs))
+    _lib.check(so.fb_row_sums(cs, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
+    if counter is not None:
+        for i, (e, f) in enumerate(nm.blocks):
+            K.tally_rowsums(counter, f.shape[0], f.shape[1])
+            if i > 0:
+                K.tally_accumulate(counter, n)
+    return D.to_like(out, nm.host_io)
+
+
+def col_sums(nm, counter=None):
+    """Column totals as a row vector; indicator blocks use cached counts (rewrite.py:131-149)."""
+    _nm_check(nm)
+    if nm.transposed:
+        r = row_sums(nm.T, counter)
+        return D.to_like(_as_dev(r).t().contiguous(), nm.host_io)
+    so = _lib.lib()
+    out = torch.empty((1, nm.base_cols), dtype=torch.float64, device=nm.s.device)
+    cs = nm.c_struct()
+    ws = D.workspace(so.fb_col_sums_workspace_bytes(cs))
+    _lib.check(so.fb_col_sums(cs, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
+    if counter is not None:
+        for e, f in nm.blocks:
+            if e is None:
+                K.tally_colsums(counter, f.shape[0], f.shape[1])
+            else:
+                counter.tally(0, e.rows)
+                K.tally_matmul(counter, 1, f.shape[0], f.shape[1])
+    return D.to_like(out, nm.host_io)
+
+
+def sum_all(nm, counter=None):
+    """Grand total; invariant under transposition (rewrite.py:152-165)."""
+    _nm_check(nm)
+    base = nm.untransposed()
+    so = _lib.lib()
+    cs = base.c_struct()
+    out = torch.empty(1, dtype=torch.float64, device=base.s.device)
+    d = base.base_cols
+    ws = D.workspace(so.fb_col_sums_workspace_bytes(cs) + 8 * d + 512)
+    _lib.check(so.fb_sum_all(cs, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
+    if counter is not None:
+        for e, f in base.blocks:
+            if e is None:
+                K.tally_rowsums(counter, f.shape[0], f.shape[1])
+                counter.tally(0, max(f.shape[0] - 1, 0))
+            else:
+                counter.tally(0, e.rows)
+                K.tally_rowsums(counter, f.shape[0], f.shape[1])
+                K.tally_matmul(counter, 1, f.shape[0], 1)
+    return float(out.item())
+
+
+# ---------------------------------------------------------------------------
+# multiplication
+
+
+def _as_dev(a):
+    return a if isinstance(a, torch.Tensor) else torch.from_numpy(np.asarray(a)).to(D.device())
+
+
+def _lmm_dev(nm, x, counter):
+    """T·X on the untransposed matrix; x is a contiguous device matrix (d × d_x)."""
+    so = _lib.lib()
+    n, d_x = nm.base_rows, x.shape[1]
+    out = torch.empty((n, d_x), dtype=torch.float64, device=x.device)
+    cs = nm.c_struct()
+    ws = D.workspace(so.fb_lmm_workspace_bytes(cs, d_x))
+    _lib.check(so.fb_lmm(cs, D.ptr(x), d_x, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
+    if counter is not None:
+        for i, (e, f) in enumerate(nm.blocks):
+            K.tally_matmul(counter, f.shape[0], f.shape[1], d_x)
+            if i > 0:
+                K.tally_accumulate(counter, n * d_x)
+    return out
+
+
+def _wt_dev(nm, w, w_rs, w_cs, n_w, out, o_js, o_cs, counter):
+    """out(j, c) = Σ_i w(i, j) T(i, c) on the untransposed matrix."""
+    so = _lib.lib()
+    cs = nm.c_struct()
+    ws = D.workspace(so.fb_wt_workspace_bytes(cs, n_w))
+    _lib.check(so.fb_wt(cs, D.ptr(w), n_w, w_rs, w_cs, D.ptr(out), o_js, o_cs, ws.data_ptr(), ws.numel(),
+                        D.stream_handle()))
+    if counter is not None:
+        for e, f in nm.blocks:
+            if e is not None:
+                counter.tally(0, n_w * e.rows)
+            K.tally_matmul(counter, n_w, f.shape[0], f.shape[1])
+    return out
+
+
+def lmm(nm, x, counter=None):
+    """Left multiplication ``T X`` (rewrite.py:172-191); ``T.T X`` via the scatter path."""
+    _nm_check(nm)
+    xd, host = _operand(x)
+    n_log, d_log = nm.shape
+    if xd.shape[0] != d_log:
+        raise ShapeError(f"lmm: X has {xd.shape[0]} rows, normalized matrix has {d_log} columns")
+    if nm.transposed:
+        # T' X = (X' T)'  (rewrite.py:182-183): weights w(i, j) = X[i, j]
+        base = nm.T
+        m = xd.shape[1]
+        out = torch.empty((base.base_cols, m), dtype=torch.float64, device=xd.device)
+        _wt_dev(base, xd, xd.stride(0), xd.stride(1), m, out, 1, m, counter)
+        return D.to_like(out, host)
+    return D.to_like(_lmm_dev(nm, xd, counter), host)
+
+
+def rmm(x, nm, counter=None):
+    """Right multiplication ``X T`` (rewrite.py:194-212)."""
+    _nm_check(nm)
+    xd, host = _operand(x)
+    n_log, d_log = nm.shape
+    if xd.shape[1] != n_log:
+        raise ShapeError(f"rmm: X has {xd.shape[1]} columns, normalized matrix has {n_log} rows")
+    if nm.transposed:
+        # X T' = (T X')'  (rewrite.py:204-205)
+        res = _lmm_dev(nm.T, xd.t().contiguous(), counter)
+        return D.to_like(res.t().contiguous(), host)
+    n_x = xd.shape[0]
+    d = nm.base_cols
+    out = torch.empty((n_x, d), dtype=torch.float64, device=xd.device)
+    # weights w(i, j) = x[j, i]
+    _wt_dev(nm, xd, xd.stride(1), xd.stride(0), n_x, out, d, 1, counter)
+    return D.to_like(out, host)
+
+
+def crossprod(nm, method="efficient", counter=None):
+    """``T' T`` without materializing T; exactly symmetric (rewrite.py:245-298)."""
+    from .crossprod import crossprod as _cp
+
+    return _cp(nm, method=method, counter=counter)

@@ -1,0 +1,20 @@
+"""Load the committed golden fixtures (tests/golden/*.npz, made by oracle/gen_golden.py)."""
+import glob
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def names():
+    return sorted(os.path.splitext(os.path.basename(p))[0] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+
+
+def load(name):
+    with np.load(os.path.join(GOLDEN, name + ".npz")) as z:
+        return {k: z[k] for k in z.files}
+
+
+def parts(g):
+    return [(g[f"key{i}"], g[f"r{i}"]) for i in range(int(g["q"]))]

@@ -1,0 +1,168 @@
+"""GPU parity: the sm_100a operators against the golden vectors and the CPU oracle.
+
+Bars (BASELINE.json north_star): FK remap, source rows and counts bit-exact; float64
+values within normwise rel 1e-9 (the reference's own max_rel_deviation metric,
+bench.py:38-43).
+"""
+import numpy as np
+import pytest
+import torch
+
+import factorla_oracle as O
+import golden_io
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+def _fb():
+    import paper_1612_07448_b200 as fb
+
+    return fb
+
+
+def _close(a, b, tol=TOL):
+    a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+    assert a.shape == np.asarray(b).shape, (a.shape, np.asarray(b).shape)
+    dev = O.max_rel_deviation(a, b)
+    assert dev <= tol, dev
+
+
+def _build_gpu(g):
+    fb = _fb()
+    parts = golden_io.parts(g)
+    if len(parts) == 1:
+        return fb.build_pkfk(g["s"], parts[0][0], parts[0][1])
+    return fb.build_star(g["s"], parts)
+
+
+@pytest.mark.parametrize("name", golden_io.names())
+def test_construction_bit_exact(name):
+    g = golden_io.load(name)
+    nm = _build_gpu(g)
+    for i, (e, rk) in enumerate(nm.parts):
+        np.testing.assert_array_equal(e.target_numpy(), g[f"target{i}"])
+        np.testing.assert_array_equal(nm.source_rows[i + 1].cpu().numpy(), g[f"used{i}"])
+        np.testing.assert_array_equal(e.counts.cpu().numpy(), g[f"counts{i}"])
+        np.testing.assert_array_equal(rk.cpu().numpy(), g[f"rkept{i}"])
+    np.testing.assert_array_equal(_fb().materialize(nm), g["materialize"])
+
+
+@pytest.mark.parametrize("name", golden_io.names())
+def test_operators_vs_reference_golden(name):
+    fb = _fb()
+    g = golden_io.load(name)
+    nm = _build_gpu(g)
+    for key, fn, cnt in (
+        ("lmm_x1", lambda c: fb.lmm(nm, g["x1"], c), "cnt_lmm_x1"),
+        ("lmm_x3", lambda c: fb.lmm(nm, g["x3"], c), None),
+        ("tmm_p2", lambda c: fb.lmm(nm.T, g["p2"], c), "cnt_tmm_p2"),
+        ("rmm_xr", lambda c: fb.rmm(g["xr"], nm, c), "cnt_rmm_xr"),
+        ("rmm_t_xt", lambda c: fb.rmm(g["xt"], nm.T, c), None),
+        ("row_sums", lambda c: fb.row_sums(nm, c), "cnt_row_sums"),
+        ("col_sums", lambda c: fb.col_sums(nm, c), "cnt_col_sums"),
+        ("row_sums_t", lambda c: fb.row_sums(nm.T, c), None),
+        ("col_sums_t", lambda c: fb.col_sums(nm.T, c), None),
+    ):
+        c = fb.OpCounter()
+        out = fn(c)
+        assert isinstance(out, np.ndarray)  # host in -> host out, like the reference
+        _close(out, g[key])
+        if cnt:
+            assert [c.multiplies, c.additions] == list(g[cnt]), key
+    c = fb.OpCounter()
+    tot = fb.sum_all(nm, c)
+    assert abs(tot - float(g["sum_all"])) <= TOL * max(1.0, np.abs(g["materialize"]).sum())
+    assert [c.multiplies, c.additions] == list(g["cnt_sum_all"])
+    for op, x in (("mul", 2.0), ("add", 3.0), ("rsub", 1.5), ("div", 4.0), ("pow", 2.0)):
+        c = fb.OpCounter()
+        _close(fb.materialize(fb.scalar_op(nm, x, op, c)), g[f"scalar_{op}"])
+        assert [c.multiplies, c.additions] == list(g[f"cnt_scalar_{op}"])
+    _close(fb.materialize(fb.scalar_fn(nm, np.exp)), g["fn_exp"])
+    _close(fb.materialize(fb.scalar_fn(nm, np.square)), g["fn_square"])
+
+
+# ---------------------------------------------------------------- seeded, multi-tile cases
+CASES = [
+    # n_s, d_s, [(n_r, d_r)], seed
+    (100_003, 20, [(10_000, 40)], 1),
+    (65_537, 7, [(513, 3)], 2),
+    (40_001, 1, [(97, 5), (1000, 2)], 3),
+    (30_000, 60, [(5000, 120)], 4),
+    (12_345, 0, [(300, 9)], 5),
+    (1, 3, [(1, 2)], 6),
+    (50_000, 10, [(20_000, 80), (7, 1), (400, 33)], 7),
+]
+
+
+def _random_case(n_s, d_s, shapes, seed):
+    rng = np.random.default_rng(seed)
+    s = rng.standard_normal((n_s, d_s))
+    parts = []
+    for n_r, d_r in shapes:
+        keys = rng.integers(1, n_r + 1, size=n_s)
+        parts.append((keys, rng.standard_normal((n_r, d_r))))
+    return s, parts
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"n{c[0]}_d{c[1]}_q{len(c[2])}" for c in CASES])
+def test_seeded_multitile_vs_oracle(case):
+    fb = _fb()
+    n_s, d_s, shapes, seed = case
+    s, parts = _random_case(n_s, d_s, shapes, seed)
+    ref = O.build_star(s, parts)
+    nm = fb.build_star(s, parts) if len(parts) > 1 else fb.build_pkfk(s, parts[0][0], parts[0][1])
+    for i, (e, rk) in enumerate(nm.parts):
+        np.testing.assert_array_equal(e.target_numpy(), ref.parts[i][0])
+        np.testing.assert_array_equal(nm.source_rows[i + 1].cpu().numpy(), ref.source_rows[i + 1])
+    rng = np.random.default_rng(seed + 100)
+    n, d = ref.shape
+    for d_x in (1, 2, 5, 16, 19):
+        x = rng.standard_normal((d, d_x))
+        _close(fb.lmm(nm, x), O.lmm(ref, x))
+    for m in (1, 3, 10, 17):
+        p = rng.standard_normal((n, m))
+        _close(fb.lmm(nm.T, p), O.lmm(ref.T, p))
+        _close(fb.rmm(p.T.copy(), nm), O.rmm(p.T, ref))
+    _close(fb.row_sums(nm), O.row_sums(ref))
+    _close(fb.col_sums(nm), O.col_sums(ref))
+    assert abs(fb.sum_all(nm) - O.sum_all(ref)) <= TOL * max(1.0, np.abs(s).sum() + sum(np.abs(r).sum() * n for _, r in parts))
+
+
+def test_device_tensors_stay_on_device():
+    fb = _fb()
+    s, parts = _random_case(5000, 4, [(100, 6)], 11)
+    nm = fb.build_pkfk(torch.from_numpy(s).cuda(), torch.from_numpy(parts[0][0]).cuda(), torch.from_numpy(parts[0][1]).cuda())
+    x = torch.randn(10, 2, dtype=torch.float64, device="cuda")
+    out = fb.lmm(nm, x)
+    assert isinstance(out, torch.Tensor) and out.is_cuda
+    _close(out, O.lmm(O.build_pkfk(s, parts[0][0], parts[0][1]), x.cpu().numpy()))
+
+
+def test_errors_match_reference_behaviour():
+    fb = _fb()
+    s = np.array([[1.0, 2], [3, 4], [5, 6]])
+    r = np.array([[10.0, 20], [30, 40]])
+    with pytest.raises(fb.DataError, match="entity row 1"):
+        fb.build_pkfk(s, [1, 3, 1], r)
+    with pytest.raises(fb.DataError, match="non-integer"):
+        fb.build_pkfk(s, [1.0, 1.5, 1.0], r)
+    nm = fb.build_pkfk(s, [1, 2, 1], r)
+    with pytest.raises(fb.ShapeError):
+        fb.lmm(nm, np.ones((3, 1)))
+    with pytest.raises(fb.ShapeError):
+        fb.rmm(np.ones((1, 4)), nm)
+    with pytest.raises(fb.NumericError):
+        fb.scalar_op(nm, 0, "div")
+    with pytest.raises(ValueError):
+        fb.scalar_op(nm, 1, "mod")
+
+
+def test_kernels_were_launched():
+    """The CUDA path ran (no silent host fallback)."""
+    fb = _fb()
+    before = fb.launch_count()
+    nm = fb.build_pkfk([[1.0, 2], [3, 4]], [1, 1], [[5.0, 6]])
+    fb.lmm(nm, np.ones((4, 1)))
+    assert fb.launch_count() > before
