@@ -5,9 +5,15 @@
 // product (rewrite.py:187-189, "R·X before K"). On B200 that is two streaming passes:
 //   1. z_q = R_q · X[slice_q]          (one pass over each attribute table)
 //   2. out_i = S_i · X[0:d_S] + Σ_q z_q[fk_q[i]]   (one pass over S and the FK columns)
-// Pass 2 streams S and the FK columns through a shared-memory bulk-copy ring and
-// gathers z from L2 (z is n_R × d_X, L2-resident at the BASELINE shapes).
 // rowSums (rewrite.py:118-128) is the same pass with X = ones.
+//
+// Both passes are the same kernel: factor rows stream through a shared-memory
+// bulk-copy ring (fb_stream.cuh) and the per-tile product runs on the FP64 tensor
+// cores (mma.sync m8n8k4 f64 -> DMMA; tcgen05 has no f64 kind). Each warp owns MT
+// m-tiles of 8 rows; X (d × d_x, zero-padded to NT·8 columns) is the B operand read
+// from a bank-skewed shared copy. The gathered z values are loaded before the k-loop
+// so their L2 latency overlaps the tensor-core work, then added in the reference's
+// order (S·X first, then each part in turn).
 #include "fb_kernels.cuh"
 
 namespace fb {
@@ -24,129 +30,188 @@ struct LmmArgs {
   const double* z[kMaxParts];  // n_R,q × dx row-major
   double* out;                 // n × dx, leading dimension ldo
   int64_t ldo;
-  int tpr;  // threads cooperating on one row (1, 2, 4, 8)
+  int pitch;                   // shared-memory row pitch of the factor tile (doubles)
 };
 
-template <int DX>
-__global__ void __launch_bounds__(256) lmm_rows_kernel(LmmArgs p, StreamSet ss, int stages,
+template <int NT>
+FB_DEV int xs_ld() {
+  return 8 * NT + 4;  // bank skew for the B-fragment loads (see conflict_free_pitch)
+}
+
+template <int NT, int MT>
+__global__ void __launch_bounds__(kRingThreads) lmm_dmma_kernel(LmmArgs p, StreamSet ss, int stages,
                                                        int tile_rows) {
   extern __shared__ __align__(128) char smem[];
   const int d = p.d;
+  const int dpad = (d + 3) & ~3;
+  const int ldxs = xs_ld<NT>();
   double* xs = reinterpret_cast<double*>(smem);
-  const size_t xs_bytes = (static_cast<size_t>(d) * DX * sizeof(double) + 127) & ~size_t(127);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + xs_bytes);
-  char* buf = smem + xs_bytes + 128;
+  const size_t xs_bytes = (static_cast<size_t>(dpad > 0 ? dpad : 4) * ldxs * sizeof(double) + 127) & ~size_t(127);
+  char* buf = smem + xs_bytes;
 
-  for (int i = threadIdx.x; i < d * DX; i += blockDim.x) xs[i] = p.x[(i / DX) * p.ldx + (i % DX)];
+  for (int i = threadIdx.x; i < dpad * ldxs; i += blockDim.x) {
+    const int k = i / ldxs, n = i % ldxs;
+    xs[i] = (k < d && n < p.dx) ? p.x[k * p.ldx + n] : 0.0;
+  }
 
   TileRing ring;
-  ring.buf = buf;
-  ring.bar = bars;
-  ring.stages = stages;
-  ring.tile_rows = tile_rows;
-  ring.n_rows = p.n;
-  ring.policy = policy_evict_first();
-  const int64_t ntiles = (p.n + tile_rows - 1) / tile_rows;
-  cta_tile_range(ntiles, ring.tile_begin, ring.tile_end);
-  ring.start(ss);  // contains __syncthreads (xs visible after it)
+  ring.init(buf, stages, tile_rows, p.n);
+  ring.start();  // contains __syncthreads (xs visible after it)
+  if (is_producer_warp()) {
+    ring.produce(ss);
+    return;
+  }
 
-  const int tpr = p.tpr;
-  const int sub = threadIdx.x % tpr;
-  const int rows_per_pass = blockDim.x / tpr;
+  const int lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int warp = (threadIdx.x >> 5) - 1;  // consumer warp index
+  const int pitch = p.pitch;
 
-  for (int64_t k = 0; k < ring.tile_end - ring.tile_begin; ++k) {
-    const int stage = ring.acquire(ss, k);
-    const int64_t tile = ring.tile_begin + k;
+  for (int64_t kt = 0; kt < ring.count(); ++kt) {
+    const int stage = ring.acquire(ss, kt);
+    const int64_t tile = ring.tile_begin + kt;
     const int rows = ring.rows_of(tile);
     const int64_t r0 = tile * tile_rows;
     const double* A = reinterpret_cast<const double*>(ring.stage_ptr(stage, ss, 0));
+    const int wrow = warp * (8 * MT);
 
-    for (int rb = 0; rb < rows; rb += rows_per_pass) {
-      const int r = rb + static_cast<int>(threadIdx.x) / tpr;
-      const bool live = r < rows;
-      double acc[DX];
+    if (wrow < rows) {
+      // prefetch the first part's gathered z values (they are added after the product)
+      double zpre[MT][NT][2];
+      if (p.nfk > 0) {
+        const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, 1));
 #pragma unroll
-      for (int j = 0; j < DX; ++j) acc[j] = 0.0;
-      if (live) {
-        const double* arow = A + static_cast<size_t>(r) * d;
-        for (int c = sub; c < d; c += tpr) {
-          const double s = arow[c];
-          const double* xr = xs + c * DX;
+        for (int mt = 0; mt < MT; ++mt) {
+          const int r = wrow + 8 * mt + g;
+          const bool live = r < rows;
+          const double* zr = p.z[0] + static_cast<int64_t>(live ? fkt[r] : 0) * p.dx;
 #pragma unroll
-          for (int j = 0; j < DX; ++j) acc[j] = fma(s, xr[j], acc[j]);
+          for (int nt = 0; nt < NT; ++nt) {
+            const int c = 8 * nt + 2 * t;
+            zpre[mt][nt][0] = (live && c < p.dx) ? __ldg(zr + c) : 0.0;
+            zpre[mt][nt][1] = (live && c + 1 < p.dx) ? __ldg(zr + c + 1) : 0.0;
+          }
         }
       }
-      if (tpr > 1) {
-        for (int o = tpr >> 1; o > 0; o >>= 1) {
+
+      double acc[MT][NT][2];
 #pragma unroll
-          for (int j = 0; j < DX; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o, tpr);
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+      const double* arow[MT];
+      bool rlive[MT];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int r = wrow + 8 * mt + g;
+        rlive[mt] = r < rows;
+        arow[mt] = A + static_cast<size_t>(rlive[mt] ? r : 0) * pitch;
+      }
+      for (int k0 = 0; k0 < dpad; k0 += 4) {
+        const int k = k0 + t;
+        double b[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) b[nt] = xs[k * ldxs + 8 * nt + g];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const double a = (rlive[mt] && k < d) ? arow[mt][k] : 0.0;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a, b[nt]);
         }
       }
-      if (live && sub == 0) {
-        for (int q = 0; q < p.nfk; ++q) {
-          const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, 1 + q));
-          const double* zr = p.z[q] + static_cast<int64_t>(fkt[r]) * DX;
+
+      // epilogue: + z_0 (prefetched) + z_1 ... in part order, then store
 #pragma unroll
-          for (int j = 0; j < DX; ++j) acc[j] += __ldg(zr + j);
+      for (int mt = 0; mt < MT; ++mt) {
+        const int r = wrow + 8 * mt + g;
+        if (r >= rows) continue;
+        if (p.nfk > 0) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            acc[mt][nt][0] += zpre[mt][nt][0];
+            acc[mt][nt][1] += zpre[mt][nt][1];
+          }
+          for (int q = 1; q < p.nfk; ++q) {
+            const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, 1 + q));
+            const double* zr = p.z[q] + static_cast<int64_t>(fkt[r]) * p.dx;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const int c = 8 * nt + 2 * t;
+              if (c < p.dx) acc[mt][nt][0] += __ldg(zr + c);
+              if (c + 1 < p.dx) acc[mt][nt][1] += __ldg(zr + c + 1);
+            }
+          }
         }
         double* o = p.out + (r0 + r) * p.ldo;
 #pragma unroll
-        for (int j = 0; j < DX; ++j) o[j] = acc[j];
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = 8 * nt + 2 * t;
+          if (c + 1 < p.dx && ((reinterpret_cast<uintptr_t>(o + c) & 15u) == 0)) {
+            *reinterpret_cast<double2*>(o + c) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+          } else {
+            if (c < p.dx) o[c] = acc[mt][nt][0];
+            if (c + 1 < p.dx) o[c + 1] = acc[mt][nt][1];
+          }
+        }
       }
     }
-    ring.release(ss, k);
+    ring.release();
   }
 }
 
 // ------------------------------------------------------------------ host launcher
-static int pick_tpr(int d) {
-  if (d <= 32) return 1;
-  if (d <= 64) return 2;
-  if (d <= 128) return 4;
-  return 8;
-}
-
-template <int DX>
-static cudaError_t launch_lmm_dx(const LmmArgs& a, cudaStream_t st, int num_sms) {
+template <int NT, int MT>
+static cudaError_t launch_lmm_cfg(const LmmArgs& a, cudaStream_t st, int num_sms) {
   LmmArgs p = a;
-  p.tpr = pick_tpr(p.d);
-  const int threads = 256;
-  const int tile_rows = threads / p.tpr;  // multiple of 4
+  const int tile_rows = kConsumerWarps * 8 * MT;
   StreamSet ss{};
   ss.count = 1 + p.nfk;
   ss.base[0] = reinterpret_cast<const char*>(p.a);
   ss.row_bytes[0] = static_cast<uint32_t>(p.d) * 8u;
+  p.pitch = (p.d % 2 == 0) ? conflict_free_pitch(p.d) : p.d;
+  ss.pitch[0] = static_cast<uint32_t>(p.pitch) * 8u;
   for (int q = 0; q < p.nfk; ++q) {
     ss.base[1 + q] = reinterpret_cast<const char*>(p.fk[q]);
     ss.row_bytes[1 + q] = 4u;
   }
-  stream_layout(ss, tile_rows);
-  const size_t xs_bytes = (static_cast<size_t>(p.d) * DX * 8 + 127) & ~size_t(127);
+  stream_layout(ss, tile_rows, p.n);
+  const int dpad = (p.d + 3) & ~3;
+  const size_t xs_bytes = (static_cast<size_t>(dpad > 0 ? dpad : 4) * (8 * NT + 4) * 8 + 127) & ~size_t(127);
   const size_t budget = 200 * 1024;
-  int stages = static_cast<int>((budget - xs_bytes - 128) / ss.stage_bytes);
+  int stages = static_cast<int>((budget - xs_bytes - 256) / ss.stage_bytes);
   if (stages > 4) stages = 4;
-  if (stages < 2) stages = 2;
-  const size_t smem = xs_bytes + 128 + static_cast<size_t>(stages) * ss.stage_bytes;
-  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  auto kern = lmm_rows_kernel<DX>;
+  if (stages < 2) return cudaErrorNotSupported;
+  const size_t smem = xs_bytes + 256 + static_cast<size_t>(stages) * ss.stage_bytes;
+  auto kern = lmm_dmma_kernel<NT, MT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  int per_sm = static_cast<int>((227 * 1024) / (smem + 1024));
+  int per_sm = static_cast<int>((228 * 1024) / (smem + 1024));
   if (per_sm < 1) per_sm = 1;
   if (per_sm > 4) per_sm = 4;
   const int64_t ntiles = (p.n + tile_rows - 1) / tile_rows;
   const int grid = grid_for(ntiles, 1, per_sm, num_sms);
-  kern<<<grid, threads, smem, st>>>(p, ss, stages, tile_rows);
+  kern<<<grid, kRingThreads, smem, st>>>(p, ss, stages, tile_rows);
   FB_LAUNCHED();
   return cudaGetLastError();
 }
 
+template <int NT>
+static cudaError_t launch_lmm_nt(const LmmArgs& p, cudaStream_t st, int num_sms) {
+  // rows per warp: 32 when a 256-row tile of this width fits 4 stages comfortably
+  const int pitch = (p.d % 2 == 0) ? conflict_free_pitch(p.d) : p.d;
+  const size_t row_bytes = static_cast<size_t>(pitch) * 8 + 4 * p.nfk;
+  if (row_bytes * 256 <= 48 * 1024) return launch_lmm_cfg<NT, 4>(p, st, num_sms);
+  if (row_bytes * 128 <= 48 * 1024) return launch_lmm_cfg<NT, 2>(p, st, num_sms);
+  return launch_lmm_cfg<NT, 1>(p, st, num_sms);
+}
+
 cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, int dx, int64_t ldx,
-                            int nfk,
-                            const int32_t* const* fk, const double* const* z, double* out,
+                            int nfk, const int32_t* const* fk, const double* const* z, double* out,
                             int64_t ldo, cudaStream_t st, int num_sms) {
   if (n <= 0) return cudaSuccess;
+  if (dx < 1 || dx > 16) return cudaErrorNotSupported;
   LmmArgs p{};
   p.a = a;
   p.n = n;
@@ -161,25 +226,8 @@ cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, 
   }
   p.out = out;
   p.ldo = ldo;
-  switch (dx) {
-#define FB_DX_CASE(N) \
-  case N:             \
-    return launch_lmm_dx<N>(p, st, num_sms);
-    FB_DX_CASE(1)
-    FB_DX_CASE(2)
-    FB_DX_CASE(3)
-    FB_DX_CASE(4)
-    FB_DX_CASE(5)
-    FB_DX_CASE(6)
-    FB_DX_CASE(7)
-    FB_DX_CASE(8)
-    FB_DX_CASE(10)
-    FB_DX_CASE(12)
-    FB_DX_CASE(16)
-#undef FB_DX_CASE
-    default:
-      return cudaErrorNotSupported;  // caller splits X into supported column chunks
-  }
+  if (dx <= 8) return launch_lmm_nt<1>(p, st, num_sms);
+  return launch_lmm_nt<2>(p, st, num_sms);
 }
 
 }  // namespace fb

@@ -70,34 +70,28 @@ FB_DEV void scatter_add(double* bins, int key, const double (&vals)[NX], bool ac
 }
 
 template <int NX>
-__global__ void __launch_bounds__(256) colreduce_kernel(ColRedDev p, StreamSet ss, int stages,
-                                                        int tile_rows) {
+__global__ void __launch_bounds__(kRingThreads) colreduce_kernel(ColRedDev p, StreamSet ss, int stages,
+                                                                 int tile_rows) {
   extern __shared__ __align__(128) char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-  char* buf = smem + 128;
   const int d = p.c.d;
-
   TileRing ring;
-  ring.buf = buf;
-  ring.bar = bars;
-  ring.stages = stages;
-  ring.tile_rows = tile_rows;
-  ring.n_rows = p.c.n;
-  ring.policy = policy_evict_first();
-  const int64_t ntiles = (p.c.n + tile_rows - 1) / tile_rows;
-  cta_tile_range(ntiles, ring.tile_begin, ring.tile_end);
-  ring.start(ss);
-
-  const int groups = d > 0 ? static_cast<int>(blockDim.x) / d : 0;
-  const int col = d > 0 ? static_cast<int>(threadIdx.x) % d : 0;
-  const int grp = d > 0 ? static_cast<int>(threadIdx.x) / d : 0;
+  ring.init(smem, stages, tile_rows, p.c.n);
+  ring.start();
+  if (is_producer_warp()) {
+    ring.produce(ss);
+    return;
+  }
+  const int tid = consumer_tid();
+  const int groups = d > 0 ? kConsumerThreads / d : 0;
+  const int col = d > 0 ? tid % d : 0;
+  const int grp = d > 0 ? tid / d : 0;
   const bool colthread = grp < groups;
 
   double acc[NX];
 #pragma unroll
   for (int j = 0; j < NX; ++j) acc[j] = 0.0;
 
-  for (int64_t k = 0; k < ring.tile_end - ring.tile_begin; ++k) {
+  for (int64_t k = 0; k < ring.count(); ++k) {
     const int stage = ring.acquire(ss, k);
     const int64_t tile = ring.tile_begin + k;
     const int rows = ring.rows_of(tile);
@@ -113,8 +107,8 @@ __global__ void __launch_bounds__(256) colreduce_kernel(ColRedDev p, StreamSet s
     // fused Kᵀ scatter of the same weights (row-per-thread)
     for (int q = 0; q < p.c.nfk; ++q) {
       const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, p.fk_stream0 + q));
-      for (int rb = 0; rb < rows; rb += blockDim.x) {
-        const int r = rb + threadIdx.x;
+      for (int rb = 0; rb < rows; rb += kConsumerThreads) {
+        const int r = rb + tid;
         const bool live = r < rows;
         double v[NX];
 #pragma unroll
@@ -122,44 +116,44 @@ __global__ void __launch_bounds__(256) colreduce_kernel(ColRedDev p, StreamSet s
         scatter_add<NX>(p.c.bins[q], live ? fkt[r] : 0, v, live);
       }
     }
-    ring.release(ss, k);
+    ring.release();
   }
 
-  // fold row groups: red[g][j][c]
-  double* red = reinterpret_cast<double*>(buf);  // ring buffers are free now
+  // fold row groups: red[g][j][c] (the ring buffers are idle now)
+  double* red = reinterpret_cast<double*>(ring.buf);
+  consumer_sync();
   if (colthread) {
 #pragma unroll
     for (int j = 0; j < NX; ++j) red[(static_cast<size_t>(grp) * NX + j) * d + col] = acc[j];
   }
-  __syncthreads();
+  consumer_sync();
   double* part = p.c.partials + static_cast<size_t>(blockIdx.x) * NX * d;
-  for (int e = threadIdx.x; e < NX * d; e += blockDim.x) {
+  for (int e = tid; e < NX * d; e += kConsumerThreads) {
     double s = 0.0;
     for (int g = 0; g < groups; ++g) s += red[static_cast<size_t>(g) * NX * d + e];
     part[e] = s;
   }
-  // last CTA sums the partials in CTA order
+  // the last CTA to finish sums the partials in CTA order (deterministic)
   __threadfence();
   __shared__ unsigned int ticket;
-  __syncthreads();
-  if (threadIdx.x == 0) ticket = atomicAdd(p.c.counter, 1u);
-  __syncthreads();
+  consumer_sync();
+  if (tid == 0) ticket = atomicAdd(p.c.counter, 1u);
+  consumer_sync();
   if (ticket != gridDim.x - 1) return;
   __threadfence();
-  for (int e = threadIdx.x; e < NX * d; e += blockDim.x) {
+  for (int e = tid; e < NX * d; e += kConsumerThreads) {
     double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b)
-      s += __ldcg(p.c.partials + static_cast<size_t>(b) * NX * d + e);
+    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(p.c.partials + static_cast<size_t>(b) * NX * d + e);
     const int j = e / d, c = e % d;
     p.c.out[j * p.c.o_js + c * p.c.o_cs] = s;
   }
-  if (threadIdx.x == 0) *p.c.counter = 0u;  // ready for the next launch
+  if (tid == 0) *p.c.counter = 0u;  // ready for the next launch
 }
 
 // ------------------------------------------------------------------ host side
-static int colred_tile_rows(int d) {
-  // ~32 KB of factor rows per stage, a multiple of 4 rows, at least 32
-  int rows = d > 0 ? (32 * 1024) / (d * 8) : 256;
+static int colred_tile_rows(uint32_t row_bytes) {
+  // ~40 KB of staged rows (all streams) per stage, a multiple of 4 rows in [32, 512]
+  int rows = row_bytes > 0 ? static_cast<int>((44u * 1024u) / row_bytes) : 512;
   if (rows > 512) rows = 512;
   if (rows < 32) rows = 32;
   return rows & ~3;
@@ -174,7 +168,6 @@ template <int NX>
 static cudaError_t launch_colreduce_nx(const ColReduce& c, cudaStream_t st, int num_sms) {
   ColRedDev p{};
   p.c = c;
-  const int tile_rows = colred_tile_rows(c.d);
   StreamSet ss{};
   int ns = 0;
   ss.base[ns] = reinterpret_cast<const char*>(c.a);
@@ -204,12 +197,18 @@ static cudaError_t launch_colreduce_nx(const ColReduce& c, cudaStream_t st, int 
     ss.row_bytes[ns++] = 4u;
   }
   ss.count = ns;
-  stream_layout(ss, tile_rows);
-  const int threads = 256;
-  const size_t red_bytes = static_cast<size_t>(threads) * NX * 8 * (c.d > 0 ? 1 : 1);
-  int stages = 3;
-  size_t smem = 128 + static_cast<size_t>(stages) * ss.stage_bytes;
-  if (smem < 128 + red_bytes + 1024) smem = 128 + red_bytes + 1024;
+  uint32_t row_bytes = 0;
+  for (int i = 0; i < ns; ++i) row_bytes += ss.row_bytes[i];
+  const int tile_rows = colred_tile_rows(row_bytes);
+  stream_layout(ss, tile_rows, c.n);
+  const size_t red_bytes = static_cast<size_t>(kConsumerThreads) * NX * 8;
+  int stages = 4;
+  size_t smem = 256 + static_cast<size_t>(stages) * ss.stage_bytes;
+  if (smem > 200 * 1024) {
+    stages = 3;
+    smem = 256 + static_cast<size_t>(stages) * ss.stage_bytes;
+  }
+  if (smem < 256 + red_bytes + 1024) smem = 256 + red_bytes + 1024;
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   auto kern = colreduce_kernel<NX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -226,7 +225,7 @@ static cudaError_t launch_colreduce_nx(const ColReduce& c, cudaStream_t st, int 
   }
   e = cudaMemsetAsync(c.counter, 0, sizeof(unsigned int), st);
   if (e != cudaSuccess) return e;
-  kern<<<grid, threads, smem, st>>>(p, ss, stages, tile_rows);
+  kern<<<grid, kRingThreads, smem, st>>>(p, ss, stages, tile_rows);
   FB_LAUNCHED();
   return cudaGetLastError();
 }

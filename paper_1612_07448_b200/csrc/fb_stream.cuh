@@ -1,144 +1,233 @@
-// fb_stream.cuh — multi-stream bulk-copy tile ring.
+// fb_stream.cuh — warp-specialised multi-stream bulk-copy tile ring.
 //
 // Every factor-matrix pass (LMM, RMM, rowSums/colSums, the driver steps) streams a
 // contiguous range of rows through shared memory. A row range of a row-major f64
 // matrix is one contiguous byte range, so a tile of rows is one 1-D bulk copy
-// (cp.async.bulk -> UBLKCP) — no tensor map needed. Up to kMaxStreams row-aligned
-// arrays (the factor rows, the int32 FK column(s), per-row weights) share one
-// mbarrier per stage; thread 0 is the producer, all threads consume.
+// (cp.async.bulk -> SASS UBLKCP) — no tensor map needed. Up to kMaxStreams row-aligned
+// arrays (the factor rows, the int32 FK column(s), per-row weights) share one "full"
+// mbarrier per stage.
 //
-// Tiles whose byte ranges are not 16-byte aligned (only the final tile, or every
-// tile when a caller passes a misaligned base pointer) are filled by the CTA with
-// plain loads instead; the producer then arrives without a transaction count so the
-// phase bookkeeping stays uniform.
+// Roles: warp 0 is the producer (it only issues copies and waits on the per-stage
+// "empty" barriers); the kConsumerWarps consumer warps wait on "full", compute, and
+// arrive on "empty" — no CTA-wide barrier per tile. Consumers that need to sync among
+// themselves use consumer_sync() (named barrier 1).
+//
+// A stream may ask for a padded shared-memory pitch (bytes per row > row bytes): the
+// producer warp then issues one bulk copy per row, so the tensor-core fragment loads
+// that walk rows hit distinct banks.
+//
+// Tiles that cannot use bulk copies (a misaligned base, or a final tile whose byte
+// count is not a multiple of 16) are filled by the consumers with plain loads; the
+// producer arrives on "full" without a transaction count so phases stay uniform.
+//
+// Measured on B200 (tools/stream_probe.cu): with one CTA per SM the ring needs
+// >= 16-32 KB tiles and 3-4 stages to reach 6.7-7.4 TB/s; per-tile bookkeeping must
+// stay off the consumers' path (incremental stage/phase, no 64-bit division, no
+// fence.proxy.async per issue — that fence waits for the thread's in-flight copies).
 #pragma once
 #include "fb_common.cuh"
 
 namespace fb {
 
 constexpr int kMaxStreams = 8;
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumerThreads = kConsumerWarps * 32;
+constexpr int kRingThreads = kConsumerThreads + 32;
 
 struct StreamSet {
   const char* base[kMaxStreams];
   uint32_t row_bytes[kMaxStreams];
+  uint32_t pitch[kMaxStreams];     // shared-memory bytes per row (>= row_bytes)
   uint32_t smem_off[kMaxStreams];  // byte offset of this stream inside a stage
   int count;
   uint32_t stage_bytes;  // bytes per stage (all streams, 128-byte padded)
-  bool base_aligned;     // all bases 16-byte aligned
+  uint32_t tile_tx;      // transaction bytes of a full tile
+  bool bulk_full;        // full tiles can use bulk copies
+  bool bulk_last;        // the final (possibly partial) tile can use bulk copies
 };
 
-// Host helper: lay out `count` streams for `tile_rows` rows per stage.
-inline void stream_layout(StreamSet& s, int tile_rows) {
+// Host helper: lay out `count` streams for `tile_rows` rows per stage over n_rows rows.
+// A zero pitch means dense (pitch = row_bytes).
+inline void stream_layout(StreamSet& s, int tile_rows, int64_t n_rows) {
   uint32_t off = 0;
-  s.base_aligned = true;
+  bool aligned = true;
+  s.tile_tx = 0;
+  const int last_rows =
+      n_rows > 0 ? static_cast<int>(n_rows - ((n_rows - 1) / tile_rows) * tile_rows) : tile_rows;
+  bool full_ok = true, last_ok = true;
   for (int i = 0; i < s.count; ++i) {
+    if (s.pitch[i] < s.row_bytes[i]) s.pitch[i] = s.row_bytes[i];
     s.smem_off[i] = off;
-    off += (s.row_bytes[i] * static_cast<uint32_t>(tile_rows) + 127u) & ~127u;
-    if (reinterpret_cast<uintptr_t>(s.base[i]) & 15u) s.base_aligned = false;
+    off += (s.pitch[i] * static_cast<uint32_t>(tile_rows) + 127u) & ~127u;
+    if (reinterpret_cast<uintptr_t>(s.base[i]) & 15u) aligned = false;
+    s.tile_tx += s.row_bytes[i] * static_cast<uint32_t>(tile_rows);
+    if (s.pitch[i] != s.row_bytes[i]) {
+      if ((s.row_bytes[i] & 15u) || (s.pitch[i] & 15u)) full_ok = last_ok = false;
+    } else {
+      if ((s.row_bytes[i] * static_cast<uint32_t>(tile_rows)) & 15u) full_ok = false;
+      if ((s.row_bytes[i] * static_cast<uint32_t>(last_rows)) & 15u) last_ok = false;
+    }
   }
   s.stage_bytes = off;
+  s.bulk_full = aligned && full_ok;
+  s.bulk_last = aligned && last_ok && full_ok;
 }
 
+// Pitch (in doubles) that makes m8n8k4 fragment loads (8 rows x 4 columns) conflict
+// free: any width that is 2 (mod 4) or 4/12 (mod 16) works; widths that are a
+// multiple of 8 get 4 doubles of padding. Odd widths cannot be copied row by row.
+inline int conflict_free_pitch(int d) {
+  if (d % 8 == 0) return d + 4;
+  return d;
+}
+
+FB_DEV void consumer_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerThreads) : "memory");
+}
+
+FB_DEV bool is_producer_warp() { return threadIdx.x < 32; }
+FB_DEV int consumer_tid() { return static_cast<int>(threadIdx.x) - 32; }
+
 struct TileRing {
-  char* buf;      // stages * stage_bytes
-  uint64_t* bar;  // stages mbarriers
+  char* buf;        // stages * stage_bytes
+  uint64_t* full;   // stages mbarriers (producer -> consumers)
+  uint64_t* empty;  // stages mbarriers (consumers -> producer)
   int stages;
   int tile_rows;
   int64_t n_rows;
+  int64_t ntiles;                // tiles over the whole matrix
   int64_t tile_begin, tile_end;  // this CTA's contiguous tile range
   uint64_t policy;
+  // consumer iteration state
+  int stage;
+  uint32_t phase;
 
-  FB_DEV char* stage_ptr(int stage, const StreamSet& s, int stream) const {
-    return buf + static_cast<size_t>(stage) * s.stage_bytes + s.smem_off[stream];
+  // Carve `smem` (128-byte aligned): 2*stages barriers in the first 256 bytes, then buffers.
+  FB_DEV void init(char* smem, int stages_, int tile_rows_, int64_t n_rows_) {
+    full = reinterpret_cast<uint64_t*>(smem);
+    empty = full + 16;
+    buf = smem + 256;
+    stages = stages_;
+    tile_rows = tile_rows_;
+    n_rows = n_rows_;
+    ntiles = (n_rows_ + tile_rows_ - 1) / tile_rows_;
+    const int64_t g = gridDim.x, c = blockIdx.x;
+    tile_begin = ntiles * c / g;
+    tile_end = ntiles * (c + 1) / g;
+    policy = policy_evict_first();
+  }
+
+  FB_DEV int64_t count() const { return tile_end - tile_begin; }
+
+  FB_DEV char* stage_ptr(int st, const StreamSet& s, int stream) const {
+    return buf + static_cast<uint32_t>(st) * s.stage_bytes + s.smem_off[stream];
   }
 
   FB_DEV int rows_of(int64_t tile) const {
-    int64_t r0 = tile * tile_rows;
-    int64_t r = n_rows - r0;
-    return static_cast<int>(r < tile_rows ? r : tile_rows);
+    return tile == ntiles - 1 ? static_cast<int>(n_rows - tile * tile_rows) : tile_rows;
   }
 
-  FB_DEV bool bulk_ok(const StreamSet& s, int rows) const {
-    if (!s.base_aligned) return false;
-    for (int i = 0; i < s.count; ++i)
-      if ((s.row_bytes[i] * static_cast<uint32_t>(rows)) & 15u) return false;
-    // interior tiles start at multiples of tile_rows (a multiple of 4 rows), so their
-    // starting offsets are 16-byte aligned for any row size that is a multiple of 4 bytes.
-    return true;
+  FB_DEV bool bulk_ok(const StreamSet& s, int64_t tile) const {
+    return tile == ntiles - 1 ? s.bulk_last : s.bulk_full;
   }
 
-  // Producer side (one thread).
-  FB_DEV void issue(const StreamSet& s, int64_t tile, int stage) const {
-    int rows = rows_of(tile);
-    if (bulk_ok(s, rows)) {
-      uint32_t total = 0;
-      for (int i = 0; i < s.count; ++i) total += s.row_bytes[i] * static_cast<uint32_t>(rows);
-      fence_proxy_async();
-      mbar_arrive_expect_tx(&bar[stage], total);
-      for (int i = 0; i < s.count; ++i) {
-        if (s.row_bytes[i] == 0) continue;
-        const char* src = s.base[i] + static_cast<size_t>(tile) * tile_rows * s.row_bytes[i];
-        bulk_g2s_stream(stage_ptr(stage, s, i), src, s.row_bytes[i] * static_cast<uint32_t>(rows),
-                        &bar[stage], policy);
-      }
-    } else {
-      mbar_arrive(&bar[stage]);
-    }
-  }
-
-  // Consumer side: fill a non-bulk tile cooperatively (4-byte granularity).
-  FB_DEV void manual_fill(const StreamSet& s, int64_t tile, int stage) const {
-    int rows = rows_of(tile);
-    for (int i = 0; i < s.count; ++i) {
-      const uint32_t* src = reinterpret_cast<const uint32_t*>(
-          s.base[i] + static_cast<size_t>(tile) * tile_rows * s.row_bytes[i]);
-      uint32_t* dst = reinterpret_cast<uint32_t*>(stage_ptr(stage, s, i));
-      uint32_t words = s.row_bytes[i] * static_cast<uint32_t>(rows) / 4u;
-      for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
-    }
-  }
-
-  // Set up barriers and prime the pipeline. Must be called by all threads.
-  FB_DEV void start(const StreamSet& s) {
+  // Barrier setup; call from all threads before the role split (contains __syncthreads).
+  FB_DEV void start() {
+    stage = 0;
+    phase = 0;
     if (threadIdx.x == 0) {
-      for (int i = 0; i < stages; ++i) mbar_init(&bar[i], 1);
+      for (int i = 0; i < stages; ++i) {
+        mbar_init(&full[i], 1);
+        mbar_init(&empty[i], kConsumerWarps);
+      }
       fence_mbar_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int64_t ntiles = tile_end - tile_begin;
-      for (int k = 0; k < stages && k < ntiles; ++k) issue(s, tile_begin + k, k);
+  }
+
+  // Producer warp body: issue every tile of this CTA's range, recycling stages.
+  FB_DEV void produce(const StreamSet& s) const {
+    const int lane = threadIdx.x & 31;
+    int st = 0;
+    uint32_t ph = 0;
+    const int64_t n = count();
+    for (int64_t k = 0; k < n; ++k) {
+      if (k >= stages) mbar_wait(&empty[st], ph ^ 1u);
+      const int64_t tile = tile_begin + k;
+      const int rows = rows_of(tile);
+      if (bulk_ok(s, tile)) {
+        if (lane == 0) {
+          uint32_t tx = s.tile_tx;
+          if (rows != tile_rows) {
+            tx = 0;
+#pragma unroll
+            for (int i = 0; i < kMaxStreams; ++i)
+              if (i < s.count) tx += s.row_bytes[i] * static_cast<uint32_t>(rows);
+          }
+          mbar_arrive_expect_tx(&full[st], tx);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < kMaxStreams; ++i) {
+          if (i >= s.count || s.row_bytes[i] == 0) continue;
+          const char* src = s.base[i] + static_cast<size_t>(tile) * tile_rows * s.row_bytes[i];
+          char* dst = stage_ptr(st, s, i);
+          if (s.pitch[i] == s.row_bytes[i]) {
+            if (lane == 0)
+              bulk_g2s_stream(dst, src, s.row_bytes[i] * static_cast<uint32_t>(rows), &full[st], policy);
+          } else {
+            for (int r = lane; r < rows; r += 32)
+              bulk_g2s_stream(dst + static_cast<uint32_t>(r) * s.pitch[i],
+                              src + static_cast<size_t>(r) * s.row_bytes[i], s.row_bytes[i], &full[st], policy);
+          }
+        }
+      } else if (lane == 0) {
+        mbar_arrive(&full[st]);
+      }
+      if (++st == stages) {
+        st = 0;
+        ph ^= 1u;
+      }
     }
   }
 
-  // Wait for local tile index k (0-based within this CTA's range); returns stage index.
-  FB_DEV int acquire(const StreamSet& s, int64_t k) const {
-    int stage = static_cast<int>(k % stages);
-    uint32_t parity = static_cast<uint32_t>((k / stages) & 1);
-    mbar_wait(&bar[stage], parity);
-    int64_t tile = tile_begin + k;
-    if (!bulk_ok(s, rows_of(tile))) {
+  // Consumers: fill a non-bulk tile cooperatively (4-byte granularity).
+  FB_DEV void manual_fill(const StreamSet& s, int64_t tile, int st) const {
+    const int rows = rows_of(tile);
+    for (int i = 0; i < s.count; ++i) {
+      const char* src = s.base[i] + static_cast<size_t>(tile) * tile_rows * s.row_bytes[i];
+      char* dst = stage_ptr(st, s, i);
+      const uint32_t wpr = s.row_bytes[i] / 4u;  // words per row
+      const uint32_t words = wpr * static_cast<uint32_t>(rows);
+      for (uint32_t w = consumer_tid(); w < words; w += kConsumerThreads) {
+        const uint32_t r = w / wpr, c = w % wpr;
+        reinterpret_cast<uint32_t*>(dst + static_cast<size_t>(r) * s.pitch[i])[c] =
+            reinterpret_cast<const uint32_t*>(src + static_cast<size_t>(r) * s.row_bytes[i])[c];
+      }
+    }
+  }
+
+  // Consumers: wait for the next tile (local index k, in order); returns its stage.
+  FB_DEV int acquire(const StreamSet& s, int64_t k) {
+    mbar_wait(&full[stage], phase);
+    const int64_t tile = tile_begin + k;
+    if (!bulk_ok(s, tile)) {
+      consumer_sync();  // everyone is past the wait before the stage is overwritten
       manual_fill(s, tile, stage);
-      __syncthreads();
+      consumer_sync();
     }
     return stage;
   }
 
-  // Release local tile k (all threads done reading it) and refill its stage.
-  FB_DEV void release(const StreamSet& s, int64_t k) const {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int64_t nk = k + stages;
-      if (nk < tile_end - tile_begin) issue(s, tile_begin + nk, static_cast<int>(k % stages));
+  // Consumers: done reading the current stage (each warp arrives once), advance.
+  FB_DEV void release() {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[stage]);
+    if (++stage == stages) {
+      stage = 0;
+      phase ^= 1u;
     }
   }
 };
-
-// Contiguous split of [0, ntiles) over gridDim.x CTAs.
-FB_DEV void cta_tile_range(int64_t ntiles, int64_t& b, int64_t& e) {
-  int64_t g = gridDim.x, c = blockIdx.x;
-  b = ntiles * c / g;
-  e = ntiles * (c + 1) / g;
-}
 
 }  // namespace fb

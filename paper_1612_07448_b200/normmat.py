@@ -85,7 +85,7 @@ class IndicatorMatrix:
             so = _lib.lib()
             ci = self.counts_i32
             c = torch.empty(self.cols, dtype=torch.float64, device=ci.device)
-            _lib.check(so.fb_i32_to_f64(D.ptr(ci), self.cols, D.ptr(c), D.stream_handle()))
+            _lib.check(so.fb_i32_to_f64(D.ptr(ci), D.ptr(c), self.cols, D.stream_handle()))
             self._counts = c
         return self._counts
 

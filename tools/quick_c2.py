@@ -6,6 +6,8 @@ sys.path.insert(0, ".")
 import paper_1612_07448_b200 as fb
 
 n_s, d_s, n_r, d_r = (int(a) for a in (sys.argv[1:5] if len(sys.argv) > 4 else (20_000_000, 20, 1_000_000, 80)))
+only = sys.argv[5].split(",") if len(sys.argv) > 5 else None
+reps = int(sys.argv[6]) if len(sys.argv) > 6 else 10
 g = torch.Generator(device="cuda").manual_seed(0)
 s = torch.randn(n_s, d_s, dtype=torch.float64, device="cuda", generator=g)
 r = torch.randn(n_r, d_r, dtype=torch.float64, device="cuda", generator=g)
@@ -24,9 +26,10 @@ ops = {
 }
 res = {}
 for name, (fn, nbytes) in ops.items():
+    if only and name not in only: continue
     for _ in range(3): fn()
     ts = []
-    for _ in range(10):
+    for _ in range(reps):
         flush.zero_()
         a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
         a.record(); fn(); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
