@@ -1,0 +1,391 @@
+"""Benchmark of the factorized-LA hot path (BASELINE.json configs[1], "c2").
+
+One step = the c2 memory-bound operator suite over the device-resident normalized matrix
+T = [S, K·R] (S 20,000,000×20, R 1,000,000×80 float64 ~N(0,1), FK int32 uniform):
+LMM with X 100×1, LMM with X 100×16, RMM with X 1×n_S, rowSums, colSums.
+``value`` = algorithmic bytes of the suite (every input and output byte once)
+÷ device time, summed over ranks (GB/s). S is 3.2 GB per rank, far larger than the 126 MB
+L2, so no flush is needed between steps.
+
+``--impl reference`` times the CPU restatement of the reference (oracle/factorla_oracle.py,
+same NumPy/SciPy/OpenBLAS primitives as factorla) on a bounded sample of the same workload.
+
+Multi-GPU (torchrun): S/FK rows are sharded (each rank holds its own 20M-row shard: weak
+scaling), R is replicated; RMM and colSums partials are combined with an NCCL all-reduce.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C2 = dict(n_s=20_000_000, d_s=20, n_r=1_000_000, d_r=80)
+HBM_PEAK_FALLBACK = 6650.0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_PEAK_FALLBACK, "fallback"
+
+
+def op_bytes(n_s, d_s, n_r, d_r):
+    """Algorithmic bytes per operator (inputs + outputs once; z/bins intermediates excluded)."""
+    d = d_s + d_r
+    fac = 8 * (n_s * d_s + n_r * d_r)
+    fk = 4 * n_s
+    return {
+        "lmm_x1": fac + fk + 8 * (d + n_s),
+        "lmm_x16": fac + fk + 8 * (16 * d + 16 * n_s),
+        "rmm_x1": fac + fk + 8 * (n_s + d),
+        "row_sums": fac + fk + 8 * n_s,
+        "col_sums": fac + 8 * (n_r + d),  # cached counts (indicator.py:61-66) replace the FK read
+    }
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                rows.append((float(f[0]), float(f[1]), f[3:7], float(f[7]) if f[7] not in ("[N/A]", "") else 0.0))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        loaded = [r for r in rows if r[3] > 0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[2]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median([r[0] for r in loaded])), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+# ----------------------------------------------------------------------------- CPU arms
+def _cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_suite(frac=0.25, reps=1, seed=0):
+    """Time the oracle port (the reference's algorithm on NumPy/SciPy/OpenBLAS) on a c2 sample.
+
+    The sample keeps c2's widths and tuple ratio: n_S = frac·20M, n_R = frac·1M.
+    Returns (GB/s over the suite, seconds per suite, sample description, per-op ms).
+    """
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import factorla_oracle as O
+    from threadpoolctl import threadpool_limits
+
+    n_s, n_r = int(C2["n_s"] * frac), int(C2["n_r"] * frac)
+    d_s, d_r = C2["d_s"], C2["d_r"]
+    rng = np.random.default_rng(seed)
+    s = rng.standard_normal((n_s, d_s))
+    r = rng.standard_normal((n_r, d_r))
+    key = rng.integers(1, n_r + 1, size=n_s, dtype=np.int64)
+    threads = _cpu_threads()
+    with threadpool_limits(threads):
+        nm = O.build_pkfk(s, key, r)
+        d = d_s + d_r
+        x1 = rng.standard_normal((d, 1))
+        x16 = rng.standard_normal((d, 16))
+        xr = rng.standard_normal((1, n_s))
+        cnt = O.counts(nm.parts[0][0], nm.parts[0][1].shape[0])  # cached like IndicatorMatrix.counts
+        nm.k_csr(0)  # CSR cache built once, as the reference caches it (indicator.py:71-76)
+        ops = {
+            "lmm_x1": lambda: O.lmm(nm, x1),
+            "lmm_x16": lambda: O.lmm(nm, x16),
+            "rmm_x1": lambda: O.rmm(xr, nm),
+            "row_sums": lambda: O.row_sums(nm),
+            "col_sums": lambda: O.col_sums(nm),
+        }
+        del cnt
+        for fn in ops.values():  # warm-up (bench._timed, bench.py:46-54)
+            fn()
+        per = {k: [] for k in ops}
+        for _ in range(reps):
+            for k, fn in ops.items():
+                t0 = time.perf_counter()
+                fn()
+                per[k].append(time.perf_counter() - t0)
+    nb = op_bytes(n_s, d_s, nm.parts[0][1].shape[0], d_r)
+    ms = {k: 1e3 * float(np.median(v)) for k, v in per.items()}
+    sec = sum(ms.values()) / 1e3
+    gbs = sum(nb.values()) / sec / 1e9
+    sample = f"c2 sample n_S={n_s:,} d_S={d_s}, n_R={n_r:,} d_R={d_r} (1/{int(1/frac)} of rows, same widths and tuple ratio)"
+    return gbs, sec, sample, threads, {k: round(v, 3) for k, v in ms.items()}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps = []
+    sample = threads = ms = None
+    for i in range(args.warmup + args.steps):
+        gbs, sec, sample, threads, ms = cpu_suite(frac=args.cpu_frac, reps=1, seed=i)
+        if i >= args.warmup:
+            steps.append((gbs, sec))
+    gbs = float(np.median([g for g, _ in steps]))
+    sec = float(np.median([s for _, s in steps]))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sec, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c2 memory-bound operator suite (LMM X100x1, LMM X100x16, RMM X1xn, rowSums, colSums)",
+                   "sample": sample, "parallelism": "host BLAS threads"},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ops_ms": ms,
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "factorized c2 operator-suite algorithmic HBM throughput (LMM x1/x16, RMM, rowSums, colSums)"
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1612_07448_b200 as fb
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = dict(C2)
+    if args.small:
+        cfg.update(n_s=cfg["n_s"] // 20, n_r=cfg["n_r"] // 20)
+    n_s, d_s, n_r, d_r = cfg["n_s"], cfg["d_s"], cfg["n_r"], cfg["d_r"]
+    d = d_s + d_r
+    # synthetic c2 inputs, seeded: S shard per rank, R identical on every rank
+    g_r = torch.Generator(device=dev).manual_seed(1234)
+    g_s = torch.Generator(device=dev).manual_seed(1000 + rank)
+    r = torch.randn(n_r, d_r, dtype=torch.float64, device=dev, generator=g_r)
+    s = torch.randn(n_s, d_s, dtype=torch.float64, device=dev, generator=g_s)
+    key = torch.randint(1, n_r + 1, (n_s,), dtype=torch.int64, device=dev, generator=g_s)
+    nm = fb.build_pkfk(s, key, r)
+    del key
+    n_r_kept = nm.r.shape[0]
+    x1 = torch.randn(d, 1, dtype=torch.float64, device=dev, generator=g_r)
+    x16 = torch.randn(d, 16, dtype=torch.float64, device=dev, generator=g_r)
+    xr = torch.randn(1, n_s, dtype=torch.float64, device=dev, generator=g_s)
+    nm.k.counts  # cache the counts (indicator.py:61-66) outside the timed region
+    torch.cuda.synchronize()
+
+    def allreduce(t):
+        if world > 1:
+            dist.all_reduce(t)
+        return t
+
+    ops = {
+        "lmm_x1": lambda: fb.lmm(nm, x1),
+        "lmm_x16": lambda: fb.lmm(nm, x16),
+        "rmm_x1": lambda: allreduce(fb.rmm(xr, nm)),
+        "row_sums": lambda: fb.row_sums(nm),
+        "col_sums": lambda: allreduce(fb.col_sums(nm)),
+    }
+    nb = op_bytes(n_s, d_s, n_r_kept, d_r)
+    step_bytes = sum(nb.values())
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        for fn in ops.values():
+            fn()
+    barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    ev = {k: [] for k in ops}
+    launches0 = fb.launch_count()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    barrier()
+    start.record(stream)
+    for _ in range(args.steps):
+        for k, fn in ops.items():
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            ev[k].append((a, b))
+    stop.record(stream)
+    barrier()
+    launches = fb.launch_count() - launches0
+    clocks = sampler.stop()
+    total_ms = start.elapsed_time(stop)
+    op_ms = {k: float(np.mean([a.elapsed_time(b) for a, b in v])) for k, v in ev.items()}
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    value = world * step_bytes / (ms_step * 1e-3) / 1e9
+
+    # e2e: the public API with host operands (pinned), result read back to host each step
+    pin = lambda a: a.cpu().pin_memory()
+    hx1, hx16, hxr = pin(x1), pin(x16), pin(xr)
+    e2e_ops = {
+        "lmm_x1": lambda: fb.lmm(nm, hx1),
+        "lmm_x16": lambda: fb.lmm(nm, hx16),
+        "rmm_x1": lambda: _host_allreduce(fb.rmm(hxr, nm), world, dev),
+        "row_sums": lambda: fb.row_sums(nm).cpu(),
+        "col_sums": lambda: _host_allreduce(fb.col_sums(nm), world, dev),
+    }
+    h2d = 8 * (x1.numel() + x16.numel() + xr.numel())
+    d2h = 8 * (n_s * 1 + n_s * 16 + d + n_s + d)
+    for fn in e2e_ops.values():
+        fn()
+    barrier()
+    e2e_steps = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        for fn in e2e_ops.values():
+            fn()
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_val = world * step_bytes / float(te.item()) / 1e9
+
+    peak, peak_kind = _peaks()
+    top = max(op_ms, key=op_ms.get)
+    achieved = nb[top] / (op_ms[top] * 1e-3) / 1e9
+    traffic = _traffic_from_profile(top)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        gbs, sec, sample, threads, ms = cpu_suite(frac=args.cpu_frac, reps=1)
+        cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample,
+               "ops_ms": ms}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded torch RNG on device: N(0,1) S and R, uniform FK)",
+            "config": {"workload": "c2 memory-bound operator suite (BASELINE.json configs[1]): LMM X100x1, LMM X100x16, "
+                                   "RMM X1xn_S, rowSums, colSums",
+                       "n_s_per_gpu": n_s, "d_s": d_s, "n_r": n_r_kept, "d_r": d_r,
+                       "parallelism": f"row-sharded S/FK over {world} GPU(s), R replicated",
+                       "l2": "no flush: S alone is 3.2 GB per GPU (> 126 MB L2)",
+                       "bytes_per_step": step_bytes},
+            "ops": {k: {"ms": round(op_ms[k], 4), "GBps": round(nb[k] / op_ms[k] / 1e6, 1),
+                        "frac": round(nb[k] / op_ms[k] / 1e6 / peak, 3)} for k in ops},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": f"fb_{top} (op-level: R-side z/bins pass + fused S pass)",
+                         "peak_kind": peak_kind, "algorithmic_bytes": nb[top]},
+            "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": e2e_steps, "note": "public API with pinned host X, results returned to host"},
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def _host_allreduce(t, world, dev):
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        d = torch.as_tensor(t).to(dev)
+        dist.all_reduce(d)
+        return d.cpu().numpy()
+    return t
+
+
+def _traffic_from_profile(op):
+    """dram bytes per launch from the committed ncu --set full summary, if present."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(op)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-frac", type=float, default=0.25)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--small", action="store_true", help="1/20 of c2 (development only)")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -54,7 +54,11 @@ def as_vector_i64(a):
 def to_like(t, like_host):
     """Return ``t`` as a NumPy array when the caller handed us host data."""
     if like_host:
-        return t.cpu().numpy()
+        # stage through page-locked memory (torch's caching host allocator reuses it)
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return h.numpy()
     return t
 
 
