@@ -49,6 +49,8 @@ typedef struct fb_part {
   const double* r;      /* n_r x d_r row-major attribute table (unreferenced rows dropped) */
   int64_t n_r;
   int32_t d_r;
+  int32_t skewed;       /* hint: some target holds a large share of rows (scatter kernels then
+                           combine equal keys within a warp before the atomic); 0 = uniform */
   const double* counts; /* optional cached colSums(K) as f64 (indicator.py:61-66); may be NULL */
 } fb_part;
 

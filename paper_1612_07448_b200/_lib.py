@@ -34,6 +34,7 @@ class FbPart(ctypes.Structure):
         ("r", c_vp),
         ("n_r", c_i64),
         ("d_r", c_i32),
+        ("skewed", c_i32),
         ("counts", c_vp),
     ]
 

@@ -264,6 +264,7 @@ static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_
       c.fk[i] = nm->part[i].fk;
       c.bins[i] = bins[i];
       c.nbins[i] = nm->part[i].n_r;
+      c.aggregate[i] = nm->part[i].skewed;
     }
     c.out = out + j0 * o_js;
     c.o_js = o_js;

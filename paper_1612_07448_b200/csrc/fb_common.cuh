@@ -96,6 +96,24 @@ FB_DEV double2 ld_stream_d2(const double2* p) {
   return r;
 }
 
+// Cache-hinted scalar accesses: gathered lookup tables (z, bins) are loaded with an
+// evict_last policy so the multi-GB streams around them do not push them out of L2;
+// streamed outputs are stored evict_first.
+FB_DEV double ld_hint(const double* p, uint64_t policy) {
+  double r;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;\n" : "=d"(r) : "l"(p), "l"(policy));
+  return r;
+}
+
+FB_DEV void st_hint(double* p, double v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(policy) : "memory");
+}
+
+FB_DEV void st_hint2(double* p, double a, double b, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(a), "d"(b), "l"(policy)
+               : "memory");
+}
+
 // ---------------------------------------------------------------- warp helpers
 FB_DEV double warp_sum(double v) {
 #pragma unroll

@@ -25,6 +25,7 @@ struct ColReduce {
   const int32_t* fk[kMaxParts];    // (original row order; warp-aggregated atomics)
   double* bins[kMaxParts];         // n_R,q × nx row-major, zeroed by the launcher
   int64_t nbins[kMaxParts];
+  int aggregate[kMaxParts];        // warp-aggregate equal keys (skewed FK)
   double* out;                     // out(j, c) = out[j*o_js + c*o_cs]
   int64_t o_js, o_cs;
   double* partials;                // workspace: grid × nx × d

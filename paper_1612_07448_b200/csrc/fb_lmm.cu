@@ -7,13 +7,19 @@
 //   2. out_i = S_i · X[0:d_S] + Σ_q z_q[fk_q[i]]   (one pass over S and the FK columns)
 // rowSums (rewrite.py:118-128) is the same pass with X = ones.
 //
-// Both passes are the same kernel: factor rows stream through a shared-memory
-// bulk-copy ring (fb_stream.cuh) and the per-tile product runs on the FP64 tensor
-// cores (mma.sync m8n8k4 f64 -> DMMA; tcgen05 has no f64 kind). Each warp owns MT
-// m-tiles of 8 rows; X (d × d_x, zero-padded to NT·8 columns) is the B operand read
-// from a bank-skewed shared copy. The gathered z values are loaded before the k-loop
-// so their L2 latency overlaps the tensor-core work, then added in the reference's
-// order (S·X first, then each part in turn).
+// Factor rows stream through the warp-specialised bulk-copy ring (fb_stream.cuh). Two
+// consumer bodies:
+//   * rowdot (d_x <= 4): FP64 FMAs. L lanes share a row (L = the largest power of two
+//     dividing the width, so the 8-byte shared loads of a half-warp hit distinct banks),
+//     a butterfly shuffle finishes the dot product, and lane k ends up owning row k of
+//     its 32-row group for a coalesced epilogue.
+//   * DMMA (5 <= d_x <= 16): mma.sync m8n8k4 f64 (SASS DMMA; tcgen05 has no f64 kind),
+//     each warp owning MT m-tiles of 8 rows against X zero-padded to NT·8 columns.
+// Both prefetch the gathered z rows of tile k+1 (its FK column is already in shared
+// memory) before computing tile k, so the L2 latency of the gather overlaps the
+// arithmetic. z is read with an L2 evict_last policy and the streamed output is
+// written evict_first, so the multi-GB streams do not push z out of L2. The z-pass
+// itself (no FK) stores z evict_last.
 #include "fb_kernels.cuh"
 
 namespace fb {
@@ -31,16 +37,134 @@ struct LmmArgs {
   double* out;                 // n × dx, leading dimension ldo
   int64_t ldo;
   int pitch;                   // shared-memory row pitch of the factor tile (doubles)
+  int lanes;                   // rowdot: lanes per row (power of two)
+  int cols;                    // rowdot: columns per lane (d / lanes)
 };
 
+// ------------------------------------------------------------------ rowdot (d_x <= 4)
+template <int NX>
+__global__ void __launch_bounds__(kRingThreads) lmm_rowdot_kernel(LmmArgs p, StreamSet ss, int stages,
+                                                                  int tile_rows) {
+  extern __shared__ __align__(128) char smem[];
+  const int d = p.d;
+  double* xs = reinterpret_cast<double*>(smem);  // X slice, d × NX row-major
+  const size_t xs_bytes = (static_cast<size_t>(d > 0 ? d : 1) * NX * sizeof(double) + 127) & ~size_t(127);
+  char* buf = smem + xs_bytes;
+  for (int i = threadIdx.x; i < d * NX; i += blockDim.x) xs[i] = p.x[(i / NX) * p.ldx + (i % NX)];
+
+  TileRing ring;
+  ring.init(buf, stages, tile_rows, p.n);
+  ring.start();  // __syncthreads: xs visible
+  if (is_producer_warp()) {
+    ring.produce(ss);
+    return;
+  }
+
+  const int lane = lane_id();
+  const int warp = (threadIdx.x >> 5) - 1;
+  const int rw = tile_rows / kConsumerWarps;  // rows per warp per tile (<= 32)
+  const int wrow = warp * rw;
+  const int L = p.lanes, C = p.cols;
+  const int rpi = 32 / L;                     // rows per instruction
+  const int iters = (rw + rpi - 1) / rpi;
+  const int sub = lane % L, rsub = lane / L;
+  const uint64_t keep = policy_evict_last();
+  const uint64_t stream_out = policy_evict_first();
+  const bool is_zpass = p.nfk == 0;
+
+  double zn[kMaxParts][NX];  // gathered z of this lane's row in the next tile
+  auto gather = [&](int st, int64_t tile) {
+    const int rows = ring.rows_of(tile);
+    const int r = wrow + lane;
+#pragma unroll
+    for (int q = 0; q < kMaxParts; ++q) {
+      if (q < p.nfk) {
+        const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(st, ss, 1 + q));
+        const bool live = lane < rw && r < rows;
+        const double* zr = p.z[q] + static_cast<int64_t>(live ? fkt[r] : 0) * NX;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) zn[q][j] = live ? ld_hint(zr + j, keep) : 0.0;
+      }
+    }
+  };
+
+  const int64_t count = ring.count();
+  int cur = 0;
+  if (count > 0) {
+    cur = ring.acquire(ss, 0);
+    gather(cur, ring.tile_begin);
+  }
+  for (int64_t kt = 0; kt < count; ++kt) {
+    double zc[kMaxParts][NX];
+#pragma unroll
+    for (int q = 0; q < kMaxParts; ++q)
+#pragma unroll
+      for (int j = 0; j < NX; ++j) zc[q][j] = zn[q][j];
+    int nxt = cur;
+    if (kt + 1 < count) {
+      nxt = ring.acquire(ss, kt + 1);
+      gather(nxt, ring.tile_begin + kt + 1);
+    }
+    const int64_t tile = ring.tile_begin + kt;
+    const int rows = ring.rows_of(tile);
+    const int64_t r0 = tile * tile_rows;
+    const double* A = reinterpret_cast<const double*>(ring.stage_ptr(cur, ss, 0));
+
+    double res[NX];
+#pragma unroll
+    for (int j = 0; j < NX; ++j) res[j] = 0.0;
+    for (int it = 0; it < iters; ++it) {
+      const int rl = it * rpi + rsub;  // row within the warp's share
+      const bool live = rl < rw && wrow + rl < rows;
+      double acc[NX];
+#pragma unroll
+      for (int j = 0; j < NX; ++j) acc[j] = 0.0;
+      if (live) {
+        const double* arow = A + static_cast<size_t>(wrow + rl) * p.pitch + sub;
+        const double* xc = xs + sub * NX;
+#pragma unroll 4
+        for (int m = 0; m < C; ++m) {
+          const double a = arow[m * L];
+#pragma unroll
+          for (int j = 0; j < NX; ++j) acc[j] = fma(a, xc[m * L * NX + j], acc[j]);
+        }
+      }
+      for (int o = L >> 1; o > 0; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < NX; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+      // lane k of the warp takes row k: produced in iteration k / rpi by lane group k % rpi
+      const int src = (lane % rpi) * L;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+        const double v = __shfl_sync(0xffffffffu, acc[j], src);
+        if (lane / rpi == it) res[j] = v;
+      }
+    }
+    const int r = wrow + lane;
+    if (lane < rw && r < rows) {
+#pragma unroll
+      for (int q = 0; q < kMaxParts; ++q)
+        if (q < p.nfk)
+#pragma unroll
+          for (int j = 0; j < NX; ++j) res[j] += zc[q][j];
+      double* o = p.out + (r0 + r) * p.ldo;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) st_hint(o + j, res[j], is_zpass ? keep : stream_out);
+    }
+    ring.release();
+    cur = nxt;
+  }
+}
+
+// ------------------------------------------------------------------ DMMA (5 <= d_x <= 16)
 template <int NT>
 FB_DEV int xs_ld() {
   return 8 * NT + 4;  // bank skew for the B-fragment loads (see conflict_free_pitch)
 }
 
-template <int NT, int MT>
+template <int NT, int MT, int NQP>
 __global__ void __launch_bounds__(kRingThreads) lmm_dmma_kernel(LmmArgs p, StreamSet ss, int stages,
-                                                       int tile_rows) {
+                                                               int tile_rows) {
   extern __shared__ __align__(128) char smem[];
   const int d = p.d;
   const int dpad = (d + 3) & ~3;
@@ -66,34 +190,60 @@ __global__ void __launch_bounds__(kRingThreads) lmm_dmma_kernel(LmmArgs p, Strea
   const int g = lane >> 2, t = lane & 3;
   const int warp = (threadIdx.x >> 5) - 1;  // consumer warp index
   const int pitch = p.pitch;
+  const int wrow = warp * (8 * MT);
+  const uint64_t keep = policy_evict_last();
+  const uint64_t stream_out = policy_evict_first();
+  const bool is_zpass = p.nfk == 0;
 
-  for (int64_t kt = 0; kt < ring.count(); ++kt) {
-    const int stage = ring.acquire(ss, kt);
+  double zn[NQP > 0 ? NQP : 1][MT][NT][2];
+  auto gather = [&](int st, int64_t tile) {
+    const int rows = ring.rows_of(tile);
+#pragma unroll
+    for (int q = 0; q < NQP; ++q) {
+      const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(st, ss, 1 + q));
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int r = wrow + 8 * mt + g;
+        const bool live = r < rows;
+        const double* zr = p.z[q] + static_cast<int64_t>(live ? fkt[r] : 0) * p.dx;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = 8 * nt + 2 * t;
+          zn[q][mt][nt][0] = (live && c < p.dx) ? ld_hint(zr + c, keep) : 0.0;
+          zn[q][mt][nt][1] = (live && c + 1 < p.dx) ? ld_hint(zr + c + 1, keep) : 0.0;
+        }
+      }
+    }
+  };
+
+  const int64_t count = ring.count();
+  int cur = 0;
+  if (count > 0) {
+    cur = ring.acquire(ss, 0);
+    gather(cur, ring.tile_begin);
+  }
+  for (int64_t kt = 0; kt < count; ++kt) {
+    double zc[NQP > 0 ? NQP : 1][MT][NT][2];
+#pragma unroll
+    for (int q = 0; q < NQP; ++q)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          zc[q][mt][nt][0] = zn[q][mt][nt][0];
+          zc[q][mt][nt][1] = zn[q][mt][nt][1];
+        }
+    int nxt = cur;
+    if (kt + 1 < count) {
+      nxt = ring.acquire(ss, kt + 1);
+      gather(nxt, ring.tile_begin + kt + 1);
+    }
     const int64_t tile = ring.tile_begin + kt;
     const int rows = ring.rows_of(tile);
     const int64_t r0 = tile * tile_rows;
-    const double* A = reinterpret_cast<const double*>(ring.stage_ptr(stage, ss, 0));
-    const int wrow = warp * (8 * MT);
+    const double* A = reinterpret_cast<const double*>(ring.stage_ptr(cur, ss, 0));
 
     if (wrow < rows) {
-      // prefetch the first part's gathered z values (they are added after the product)
-      double zpre[MT][NT][2];
-      if (p.nfk > 0) {
-        const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, 1));
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const int r = wrow + 8 * mt + g;
-          const bool live = r < rows;
-          const double* zr = p.z[0] + static_cast<int64_t>(live ? fkt[r] : 0) * p.dx;
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const int c = 8 * nt + 2 * t;
-            zpre[mt][nt][0] = (live && c < p.dx) ? __ldg(zr + c) : 0.0;
-            zpre[mt][nt][1] = (live && c + 1 < p.dx) ? __ldg(zr + c + 1) : 0.0;
-          }
-        }
-      }
-
       double acc[MT][NT][2];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
@@ -121,71 +271,63 @@ __global__ void __launch_bounds__(kRingThreads) lmm_dmma_kernel(LmmArgs p, Strea
         }
       }
 
-      // epilogue: + z_0 (prefetched) + z_1 ... in part order, then store
+      // epilogue: + z_0 + z_1 ... in part order (rewrite.py:186-190), then store
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const int r = wrow + 8 * mt + g;
         if (r >= rows) continue;
-        if (p.nfk > 0) {
+#pragma unroll
+        for (int q = 0; q < NQP; ++q)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            acc[mt][nt][0] += zpre[mt][nt][0];
-            acc[mt][nt][1] += zpre[mt][nt][1];
+            acc[mt][nt][0] += zc[q][mt][nt][0];
+            acc[mt][nt][1] += zc[q][mt][nt][1];
           }
-          for (int q = 1; q < p.nfk; ++q) {
-            const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, 1 + q));
-            const double* zr = p.z[q] + static_cast<int64_t>(fkt[r]) * p.dx;
+        for (int q = NQP; q < p.nfk; ++q) {
+          const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(cur, ss, 1 + q));
+          const double* zr = p.z[q] + static_cast<int64_t>(fkt[r]) * p.dx;
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              const int c = 8 * nt + 2 * t;
-              if (c < p.dx) acc[mt][nt][0] += __ldg(zr + c);
-              if (c + 1 < p.dx) acc[mt][nt][1] += __ldg(zr + c + 1);
-            }
+          for (int nt = 0; nt < NT; ++nt) {
+            const int c = 8 * nt + 2 * t;
+            if (c < p.dx) acc[mt][nt][0] += ld_hint(zr + c, keep);
+            if (c + 1 < p.dx) acc[mt][nt][1] += ld_hint(zr + c + 1, keep);
           }
         }
         double* o = p.out + (r0 + r) * p.ldo;
+        const uint64_t pol = is_zpass ? keep : stream_out;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int c = 8 * nt + 2 * t;
           if (c + 1 < p.dx && ((reinterpret_cast<uintptr_t>(o + c) & 15u) == 0)) {
-            *reinterpret_cast<double2*>(o + c) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+            st_hint2(o + c, acc[mt][nt][0], acc[mt][nt][1], pol);
           } else {
-            if (c < p.dx) o[c] = acc[mt][nt][0];
-            if (c + 1 < p.dx) o[c + 1] = acc[mt][nt][1];
+            if (c < p.dx) st_hint(o + c, acc[mt][nt][0], pol);
+            if (c + 1 < p.dx) st_hint(o + c + 1, acc[mt][nt][1], pol);
           }
         }
       }
     }
     ring.release();
+    cur = nxt;
   }
 }
 
-// ------------------------------------------------------------------ host launcher
-template <int NT, int MT>
-static cudaError_t launch_lmm_cfg(const LmmArgs& a, cudaStream_t st, int num_sms) {
-  LmmArgs p = a;
-  const int tile_rows = kConsumerWarps * 8 * MT;
-  StreamSet ss{};
-  ss.count = 1 + p.nfk;
-  ss.base[0] = reinterpret_cast<const char*>(p.a);
-  ss.row_bytes[0] = static_cast<uint32_t>(p.d) * 8u;
-  p.pitch = (p.d % 2 == 0) ? conflict_free_pitch(p.d) : p.d;
-  ss.pitch[0] = static_cast<uint32_t>(p.pitch) * 8u;
-  for (int q = 0; q < p.nfk; ++q) {
-    ss.base[1 + q] = reinterpret_cast<const char*>(p.fk[q]);
-    ss.row_bytes[1 + q] = 4u;
-  }
-  stream_layout(ss, tile_rows, p.n);
-  const int dpad = (p.d + 3) & ~3;
-  const size_t xs_bytes = (static_cast<size_t>(dpad > 0 ? dpad : 4) * (8 * NT + 4) * 8 + 127) & ~size_t(127);
+// ------------------------------------------------------------------ host launchers
+static int stages_for(size_t fixed, uint32_t stage_bytes, int max_stages) {
   const size_t budget = 200 * 1024;
-  int stages = static_cast<int>((budget - xs_bytes - 256) / ss.stage_bytes);
-  if (stages > 4) stages = 4;
+  if (fixed + 256 + 2 * static_cast<size_t>(stage_bytes) > budget) return 0;
+  int st = static_cast<int>((budget - fixed - 256) / stage_bytes);
+  return st > max_stages ? max_stages : st;
+}
+
+template <class K>
+static cudaError_t launch_ring(K kern, const LmmArgs& p, StreamSet& ss, size_t fixed, int tile_rows,
+                               cudaStream_t st, int num_sms) {
+  stream_layout(ss, tile_rows, p.n);
+  const int stages = stages_for(fixed, ss.stage_bytes, 4);
   if (stages < 2) return cudaErrorNotSupported;
-  const size_t smem = xs_bytes + 256 + static_cast<size_t>(stages) * ss.stage_bytes;
-  auto kern = lmm_dmma_kernel<NT, MT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  const size_t smem = fixed + 256 + static_cast<size_t>(stages) * ss.stage_bytes;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int per_sm = static_cast<int>((228 * 1024) / (smem + 1024));
   if (per_sm < 1) per_sm = 1;
@@ -197,14 +339,57 @@ static cudaError_t launch_lmm_cfg(const LmmArgs& a, cudaStream_t st, int num_sms
   return cudaGetLastError();
 }
 
+static void fill_streams(const LmmArgs& p, StreamSet& ss, int pitch) {
+  ss = StreamSet{};
+  ss.count = 1 + p.nfk;
+  ss.base[0] = reinterpret_cast<const char*>(p.a);
+  ss.row_bytes[0] = static_cast<uint32_t>(p.d) * 8u;
+  ss.pitch[0] = static_cast<uint32_t>(pitch) * 8u;
+  for (int q = 0; q < p.nfk; ++q) {
+    ss.base[1 + q] = reinterpret_cast<const char*>(p.fk[q]);
+    ss.row_bytes[1 + q] = 4u;
+  }
+}
+
+template <int NX>
+static cudaError_t launch_rowdot(LmmArgs p, cudaStream_t st, int num_sms) {
+  // lanes per row: largest power of two dividing d (<= 32), so half-warp loads are conflict-free
+  int L = 1;
+  while (p.d > 0 && L < 32 && (p.d % (2 * L)) == 0) L *= 2;
+  p.lanes = L;
+  p.cols = p.d / L;
+  p.pitch = p.d;
+  const uint32_t row_bytes = static_cast<uint32_t>(p.d) * 8u + 4u * p.nfk;
+  // rows per warp per tile: 32, fewer for wide rows (stage ~40 KB)
+  int rw = 32;
+  while (rw > 4 && static_cast<size_t>(row_bytes) * rw * kConsumerWarps > 48 * 1024) rw >>= 1;
+  StreamSet ss;
+  fill_streams(p, ss, p.d);
+  const size_t fixed = (static_cast<size_t>(p.d > 0 ? p.d : 1) * NX * 8 + 127) & ~size_t(127);
+  return launch_ring(lmm_rowdot_kernel<NX>, p, ss, fixed, rw * kConsumerWarps, st, num_sms);
+}
+
+template <int NT, int MT>
+static cudaError_t launch_dmma_cfg(LmmArgs p, cudaStream_t st, int num_sms) {
+  const int tile_rows = kConsumerWarps * 8 * MT;
+  p.pitch = (p.d % 2 == 0) ? conflict_free_pitch(p.d) : p.d;
+  StreamSet ss;
+  fill_streams(p, ss, p.pitch);
+  const int dpad = (p.d + 3) & ~3;
+  const size_t fixed = (static_cast<size_t>(dpad > 0 ? dpad : 4) * (8 * NT + 4) * 8 + 127) & ~size_t(127);
+  if (p.nfk == 0) return launch_ring(lmm_dmma_kernel<NT, MT, 0>, p, ss, fixed, tile_rows, st, num_sms);
+  if (p.nfk == 1) return launch_ring(lmm_dmma_kernel<NT, MT, 1>, p, ss, fixed, tile_rows, st, num_sms);
+  return launch_ring(lmm_dmma_kernel<NT, MT, 2>, p, ss, fixed, tile_rows, st, num_sms);
+}
+
 template <int NT>
-static cudaError_t launch_lmm_nt(const LmmArgs& p, cudaStream_t st, int num_sms) {
-  // rows per warp: 32 when a 256-row tile of this width fits 4 stages comfortably
+static cudaError_t launch_dmma(const LmmArgs& p, cudaStream_t st, int num_sms) {
   const int pitch = (p.d % 2 == 0) ? conflict_free_pitch(p.d) : p.d;
   const size_t row_bytes = static_cast<size_t>(pitch) * 8 + 4 * p.nfk;
-  if (row_bytes * 256 <= 48 * 1024) return launch_lmm_cfg<NT, 4>(p, st, num_sms);
-  if (row_bytes * 128 <= 48 * 1024) return launch_lmm_cfg<NT, 2>(p, st, num_sms);
-  return launch_lmm_cfg<NT, 1>(p, st, num_sms);
+  // MT = 4 with two prefetched parts at NT = 2 would spill
+  if (row_bytes * 256 <= 48 * 1024 && !(NT == 2 && p.nfk >= 2)) return launch_dmma_cfg<NT, 4>(p, st, num_sms);
+  if (row_bytes * 128 <= 48 * 1024) return launch_dmma_cfg<NT, 2>(p, st, num_sms);
+  return launch_dmma_cfg<NT, 1>(p, st, num_sms);
 }
 
 cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, int dx, int64_t ldx,
@@ -226,8 +411,20 @@ cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, 
   }
   p.out = out;
   p.ldo = ldo;
-  if (dx <= 8) return launch_lmm_nt<1>(p, st, num_sms);
-  return launch_lmm_nt<2>(p, st, num_sms);
+  switch (dx) {
+    case 1:
+      return launch_rowdot<1>(p, st, num_sms);
+    case 2:
+      return launch_rowdot<2>(p, st, num_sms);
+    case 3:
+      return launch_rowdot<3>(p, st, num_sms);
+    case 4:
+      return launch_rowdot<4>(p, st, num_sms);
+    default:
+      break;
+  }
+  if (dx <= 8) return launch_dmma<1>(p, st, num_sms);
+  return launch_dmma<2>(p, st, num_sms);
 }
 
 }  // namespace fb

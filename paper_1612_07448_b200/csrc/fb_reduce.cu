@@ -40,10 +40,20 @@ FB_DEV double wval(const ColRedDev& p, const TileRing& ring, const StreamSet& ss
   }
 }
 
-// Warp-aggregated scatter-add of vals[0:NX] into bins[key*NX + j].
+// Scatter-add of vals[0:NX] into bins[key*NX + j]. With `aggregate` (skewed keys,
+// e.g. Zipf), lanes holding the same key are first combined with __match_any_sync so a
+// hot bin receives one RED per warp instead of one per row; uniform keys skip it.
 template <int NX>
-FB_DEV void scatter_add(double* bins, int key, const double (&vals)[NX], bool active) {
+FB_DEV void scatter_add(double* bins, int key, const double (&vals)[NX], bool active, bool aggregate) {
   const unsigned full = 0xffffffffu;
+  if (!aggregate) {
+    if (active) {
+      double* b = bins + static_cast<int64_t>(key) * NX;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) atomicAdd(b + j, vals[j]);
+    }
+    return;
+  }
   const int lane = lane_id();
   // inactive lanes use a key no active lane can have
   const int k = active ? key : -1 - lane;
@@ -113,7 +123,7 @@ __global__ void __launch_bounds__(kRingThreads) colreduce_kernel(ColRedDev p, St
         double v[NX];
 #pragma unroll
         for (int j = 0; j < NX; ++j) v[j] = live ? wval<NX>(p, ring, ss, stage, r0, r, j) : 0.0;
-        scatter_add<NX>(p.c.bins[q], live ? fkt[r] : 0, v, live);
+        scatter_add<NX>(p.c.bins[q], live ? fkt[r] : 0, v, live, p.c.aggregate[q] != 0);
       }
     }
     ring.release();

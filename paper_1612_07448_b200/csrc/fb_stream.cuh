@@ -98,9 +98,11 @@ struct TileRing {
   int64_t ntiles;                // tiles over the whole matrix
   int64_t tile_begin, tile_end;  // this CTA's contiguous tile range
   uint64_t policy;
-  // consumer iteration state
+  // consumer iteration state: the next stage to wait on, and the oldest stage still
+  // held (consumers may hold two stages to prefetch gathers one tile ahead)
   int stage;
   uint32_t phase;
+  int rstage;
 
   // Carve `smem` (128-byte aligned): 2*stages barriers in the first 256 bytes, then buffers.
   FB_DEV void init(char* smem, int stages_, int tile_rows_, int64_t n_rows_) {
@@ -135,6 +137,7 @@ struct TileRing {
   FB_DEV void start() {
     stage = 0;
     phase = 0;
+    rstage = 0;
     if (threadIdx.x == 0) {
       for (int i = 0; i < stages; ++i) {
         mbar_init(&full[i], 1);
@@ -209,24 +212,26 @@ struct TileRing {
 
   // Consumers: wait for the next tile (local index k, in order); returns its stage.
   FB_DEV int acquire(const StreamSet& s, int64_t k) {
-    mbar_wait(&full[stage], phase);
+    const int st = stage;
+    mbar_wait(&full[st], phase);
     const int64_t tile = tile_begin + k;
     if (!bulk_ok(s, tile)) {
       consumer_sync();  // everyone is past the wait before the stage is overwritten
-      manual_fill(s, tile, stage);
+      manual_fill(s, tile, st);
       consumer_sync();
     }
-    return stage;
-  }
-
-  // Consumers: done reading the current stage (each warp arrives once), advance.
-  FB_DEV void release() {
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[stage]);
     if (++stage == stages) {
       stage = 0;
       phase ^= 1u;
     }
+    return st;
+  }
+
+  // Consumers: done reading the oldest held stage (each warp arrives once).
+  FB_DEV void release() {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[rstage]);
+    if (++rstage == stages) rstage = 0;
   }
 };
 

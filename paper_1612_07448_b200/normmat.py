@@ -89,6 +89,18 @@ class IndicatorMatrix:
             self._counts = c
         return self._counts
 
+    @property
+    def max_count(self):
+        """Largest group size (cached; one device->host read)."""
+        if getattr(self, "_max_count", None) is None:
+            self._max_count = int(self.counts_i32.max().item())
+        return self._max_count
+
+    @property
+    def skewed(self):
+        """True when one target holds more than 1/256 of the rows (Zipf-like keys)."""
+        return self.max_count * 256 > self.rows
+
     def all_columns_used(self):
         return bool((self.counts_i32 > 0).all().item())
 
@@ -194,6 +206,7 @@ class NormalizedMatrix:
                 p.r = D.ptr(f)
                 p.n_r = f.shape[0]
                 p.d_r = f.shape[1]
+                p.skewed = int(e.skewed)
                 p.counts = D.ptr(e.counts)
             self._cache["c_struct"] = st
         return ctypes.byref(st)

@@ -166,3 +166,32 @@ def test_kernels_were_launched():
     nm = fb.build_pkfk([[1.0, 2], [3, 4]], [1, 1], [[5.0, 6]])
     fb.lmm(nm, np.ones((4, 1)))
     assert fb.launch_count() > before
+
+
+def _zipf_keys(rng, n_s, n_r, s=1.2):
+    p = np.arange(1, n_r + 1, dtype=np.float64) ** -s
+    p /= p.sum()
+    return np.minimum(np.searchsorted(np.cumsum(p), rng.random(n_s), side="right"), n_r - 1) + 1
+
+
+@pytest.mark.parametrize("n_s,d_s,n_r,d_r", [(200_003, 10, 5000, 40), (70_001, 3, 50, 4)])
+def test_skewed_fk_scatter_vs_oracle(n_s, d_s, n_r, d_r):
+    """Zipf(1.2) keys: the warp-aggregated scatter path (hot bins) and the dropped-row remap."""
+    fb = _fb()
+    rng = np.random.default_rng(n_s)
+    s = rng.random((n_s, d_s))
+    r = rng.random((n_r, d_r))
+    key = _zipf_keys(rng, n_s, n_r)
+    nm = fb.build_pkfk(s, key, r)
+    ref = O.build_pkfk(s, key, r)
+    assert nm.k.skewed
+    np.testing.assert_array_equal(nm.k.target_numpy(), ref.parts[0][0])
+    np.testing.assert_array_equal(nm.k.counts.cpu().numpy(), O.counts(*ref.parts[0][0:1], ref.parts[0][1].shape[0]))
+    n, d = ref.shape
+    for m in (1, 5):
+        p = rng.standard_normal((n, m))
+        _close(fb.lmm(nm.T, p), O.lmm(ref.T, p))
+        _close(fb.rmm(p.T.copy(), nm), O.rmm(p.T, ref))
+    x = rng.standard_normal((d, 5))
+    _close(fb.lmm(nm, x), O.lmm(ref, x))
+    _close(fb.col_sums(nm), O.col_sums(ref))
