@@ -119,6 +119,24 @@ int fb_col_sums(const fb_normalized* nm, double* out, void* ws, size_t ws_bytes,
 int fb_sum_all(const fb_normalized* nm, double* out, void* ws, size_t ws_bytes,
                fb_stream_t stream);
 
+/* FK-sorted row order (the GPU analogue of IndicatorMatrix._csr_t's stable argsort,
+ * indicator.py:78-86): perm[j] = j-th row in ascending (fk, row) order, fk_sorted[j] =
+ * fk[perm[j]]. Built once per indicator and cached by the caller. */
+size_t fb_fk_sort_workspace_bytes(int64_t n);
+int fb_fk_sort(const int32_t* fk, int64_t n, int64_t n_r, int32_t* perm, int32_t* fk_sorted, void* ws,
+               size_t ws_bytes, fb_stream_t stream);
+
+/* crossprod(T) = TᵀT (rewrite.py:245-298, efficient method), exactly symmetric; out is
+ * d × d row-major. q = 0 (plain SᵀS) or q = 1 with perm/fk_sorted from fb_fk_sort and
+ * part[0].counts set. */
+size_t fb_crossprod_workspace_bytes(const fb_normalized* nm);
+int fb_crossprod(const fb_normalized* nm, const int32_t* perm, const int32_t* fk_sorted, double* out, void* ws,
+                 size_t ws_bytes, fb_stream_t stream);
+
+/* a[r, c] = a[c, r] for r > c: exact symmetry from the upper triangle of a d × d matrix
+ * (kernel._mirror_upper, kernel.py:132-135). */
+int fb_mirror_upper(double* a, int64_t d, fb_stream_t stream);
+
 /* Element-wise scalar op / function on one factor matrix (kernel.py:219-300).
  * op: 0 add 1 radd 2 sub 3 rsub 4 mul 5 rmul 6 div 7 rdiv 8 pow 9 rpow
  * fn: 0 exp 1 log 2 square 3 sqrt 4 abs 5 negative 6 log1p 7 expm1 8 sin 9 cos 10 tanh

@@ -73,6 +73,11 @@ _SIGS = {
     "fb_col_sums_workspace_bytes": (c_size, [_P]),
     "fb_col_sums": (c_i32, [_P, c_vp, c_vp, c_size, c_vp]),
     "fb_sum_all": (c_i32, [_P, c_vp, c_vp, c_size, c_vp]),
+    "fb_fk_sort_workspace_bytes": (c_size, [c_i64]),
+    "fb_fk_sort": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "fb_crossprod_workspace_bytes": (c_size, [_P]),
+    "fb_crossprod": (c_i32, [_P, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "fb_mirror_upper": (c_i32, [c_vp, c_i64, c_vp]),
     "fb_scalar_map": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_f64, c_vp]),
     "fb_unary_map": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp]),
 }

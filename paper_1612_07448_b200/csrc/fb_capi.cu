@@ -95,6 +95,13 @@ __global__ void fill_kernel(double* p, int64_t n, double v) {
     p[i] = v;
 }
 
+__global__ void mirror_upper_kernel(double* a, int64_t d) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= d * d) return;
+  const int64_t r = e / d, c = e % d;
+  if (r > c) a[e] = a[c * d + r];
+}
+
 __global__ void sum_vector_kernel(const double* v, int64_t n, double* out) {
   // single warp, fixed order per lane then a fixed shuffle tree: deterministic
   double s = 0.0;
@@ -355,6 +362,59 @@ int fb_sum_all(const fb_normalized* nm, double* out, void* ws, size_t ws_bytes, 
   sum_vector_kernel<<<1, 32, 0, cs(stream)>>>(v, d, out);
   FB_LAUNCHED();
   return cuda_status(cudaGetLastError(), "sum_all");
+}
+
+// ------------------------------------------------------------------ crossprod
+size_t fb_fk_sort_workspace_bytes(int64_t n) { return fb::fk_sort_workspace_bytes(n); }
+
+int fb_fk_sort(const int32_t* fk, int64_t n, int64_t n_r, int32_t* perm, int32_t* fk_sorted, void* ws,
+               size_t ws_bytes, fb_stream_t stream) {
+  if (n < 0 || n_r < 1) return fail(FB_ERR_SHAPE, "fk_sort: n=%lld n_r=%lld", (long long)n, (long long)n_r);
+  if (n > 0 && (!fk || !perm || !fk_sorted || !ws)) return fail(FB_ERR_ARG, "fk_sort: NULL pointer");
+  if (ws_bytes < fb::fk_sort_workspace_bytes(n)) return fail(FB_ERR_ARG, "fk_sort: workspace too small");
+  return cuda_status(fb::launch_fk_sort(fk, n, n_r, perm, fk_sorted, ws, ws_bytes, cs(stream), g_num_sms), "fk_sort");
+}
+
+size_t fb_crossprod_workspace_bytes(const fb_normalized* nm) {
+  if (!nm) return 0;
+  const bool q = nm->q > 0;
+  return fb::crossprod_workspace_bytes(nm->n_s, nm->d_s, q ? nm->part[0].n_r : 0, q ? nm->part[0].d_r : 0,
+                                       q ? 1 : 0, g_num_sms);
+}
+
+int fb_crossprod(const fb_normalized* nm, const int32_t* perm, const int32_t* fk_sorted, double* out, void* ws,
+                 size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (nm->q > 1) return fail(FB_ERR_ARG, "crossprod: star schemas (q=%d) are not supported by the device path", nm->q);
+  if (!out) return fail(FB_ERR_ARG, "crossprod: NULL output");
+  if (ws_bytes < fb_crossprod_workspace_bytes(nm)) return fail(FB_ERR_ARG, "crossprod: workspace too small");
+  fb::CrossArgs c{};
+  c.s = nm->s;
+  c.n_s = nm->n_s;
+  c.d_s = nm->d_s;
+  if (nm->q == 1) {
+    const fb_part& p = nm->part[0];
+    if (nm->n_s > 0 && (!perm || !fk_sorted)) return fail(FB_ERR_ARG, "crossprod: FK-sorted order missing");
+    if (!p.counts) return fail(FB_ERR_ARG, "crossprod: counts missing");
+    c.perm = perm;
+    c.fk_sorted = fk_sorted;
+    c.r = p.r;
+    c.n_r = p.n_r;
+    c.d_r = p.d_r;
+    c.counts = p.counts;
+  }
+  c.out = out;
+  return cuda_status(fb::launch_crossprod(c, ws, ws_bytes, cs(stream), g_num_sms), "crossprod");
+}
+
+int fb_mirror_upper(double* a, int64_t d, fb_stream_t stream) {
+  if (d < 0 || (d > 0 && !a)) return fail(FB_ERR_ARG, "mirror_upper: bad argument");
+  if (d == 0) return FB_OK;
+  const int64_t n = d * d;
+  mirror_upper_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, cs(stream)>>>(a, d);
+  FB_LAUNCHED();
+  return cuda_status(cudaGetLastError(), "mirror_upper");
 }
 
 // ------------------------------------------------------------------ element-wise

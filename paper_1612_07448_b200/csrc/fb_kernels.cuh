@@ -64,4 +64,24 @@ cudaError_t launch_gather_rows(const double* in, int64_t ld_in, const int64_t* i
 cudaError_t launch_i32_to_f64(const int32_t* in, double* out, int64_t n, cudaStream_t st,
                               int num_sms);
 
+// fb_crossprod.cu --------------------------------------------------------------------
+// Crossprod of a PK-FK (q = 1) or dense (q = 0) normalized matrix.
+struct CrossArgs {
+  const double* s;
+  int64_t n_s;
+  int d_s;
+  const int32_t* perm;       // FK-sorted order of S rows (q = 1)
+  const int32_t* fk_sorted;  // fk[perm]
+  const double* r;           // nullptr when q = 0
+  int64_t n_r;
+  int d_r;
+  const double* counts;      // f64 colSums(K)
+  double* out;               // d × d, d = d_s + d_r
+};
+size_t fk_sort_workspace_bytes(int64_t n);
+cudaError_t launch_fk_sort(const int32_t* fk, int64_t n, int64_t n_r, int32_t* perm, int32_t* fk_sorted, void* ws,
+                           size_t ws_bytes, cudaStream_t st, int num_sms);
+size_t crossprod_workspace_bytes(int64_t n_s, int d_s, int64_t n_r, int d_r, int q, int num_sms);
+cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cudaStream_t st, int num_sms);
+
 }  // namespace fb

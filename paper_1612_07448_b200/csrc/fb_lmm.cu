@@ -88,9 +88,12 @@ __global__ void __launch_bounds__(kRingThreads) lmm_rowdot_kernel(LmmArgs p, Str
     }
   };
 
+  // with an FK gather the next tile is acquired early (its z loads overlap this tile's
+  // arithmetic); the z-pass (no FK) holds a single stage
   const int64_t count = ring.count();
+  const bool prefetch = p.nfk > 0;
   int cur = 0;
-  if (count > 0) {
+  if (prefetch && count > 0) {
     cur = ring.acquire(ss, 0);
     gather(cur, ring.tile_begin);
   }
@@ -101,7 +104,9 @@ __global__ void __launch_bounds__(kRingThreads) lmm_rowdot_kernel(LmmArgs p, Str
 #pragma unroll
       for (int j = 0; j < NX; ++j) zc[q][j] = zn[q][j];
     int nxt = cur;
-    if (kt + 1 < count) {
+    if (!prefetch) {
+      cur = ring.acquire(ss, kt);
+    } else if (kt + 1 < count) {
       nxt = ring.acquire(ss, kt + 1);
       gather(nxt, ring.tile_begin + kt + 1);
     }
@@ -216,9 +221,12 @@ __global__ void __launch_bounds__(kRingThreads) lmm_dmma_kernel(LmmArgs p, Strea
     }
   };
 
+  // with an FK gather the next tile is acquired early (its z loads overlap this tile's
+  // arithmetic); the z-pass (no FK) holds a single stage
   const int64_t count = ring.count();
+  const bool prefetch = p.nfk > 0;
   int cur = 0;
-  if (count > 0) {
+  if (prefetch && count > 0) {
     cur = ring.acquire(ss, 0);
     gather(cur, ring.tile_begin);
   }
@@ -234,7 +242,9 @@ __global__ void __launch_bounds__(kRingThreads) lmm_dmma_kernel(LmmArgs p, Strea
           zc[q][mt][nt][1] = zn[q][mt][nt][1];
         }
     int nxt = cur;
-    if (kt + 1 < count) {
+    if (!prefetch) {
+      cur = ring.acquire(ss, kt);
+    } else if (kt + 1 < count) {
       nxt = ring.acquire(ss, kt + 1);
       gather(nxt, ring.tile_begin + kt + 1);
     }
@@ -324,7 +334,8 @@ template <class K>
 static cudaError_t launch_ring(K kern, const LmmArgs& p, StreamSet& ss, size_t fixed, int tile_rows,
                                cudaStream_t st, int num_sms) {
   stream_layout(ss, tile_rows, p.n);
-  const int stages = stages_for(fixed, ss.stage_bytes, 4);
+  // consumers hold two stages (current + prefetched next); keep >= ~120 KB in flight
+  const int stages = stages_for(fixed, ss.stage_bytes, 12);
   if (stages < 2) return cudaErrorNotSupported;
   const size_t smem = fixed + 256 + static_cast<size_t>(stages) * ss.stage_bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -360,9 +371,9 @@ static cudaError_t launch_rowdot(LmmArgs p, cudaStream_t st, int num_sms) {
   p.cols = p.d / L;
   p.pitch = p.d;
   const uint32_t row_bytes = static_cast<uint32_t>(p.d) * 8u + 4u * p.nfk;
-  // rows per warp per tile: 32, fewer for wide rows (stage ~40 KB)
+  // rows per warp per tile: 32, fewer for wide rows (stage ~16-24 KB, many stages)
   int rw = 32;
-  while (rw > 4 && static_cast<size_t>(row_bytes) * rw * kConsumerWarps > 48 * 1024) rw >>= 1;
+  while (rw > 4 && static_cast<size_t>(row_bytes) * rw * kConsumerWarps > 24 * 1024) rw >>= 1;
   StreamSet ss;
   fill_streams(p, ss, p.d);
   const size_t fixed = (static_cast<size_t>(p.d > 0 ? p.d : 1) * NX * 8 + 127) & ~size_t(127);
@@ -386,9 +397,10 @@ template <int NT>
 static cudaError_t launch_dmma(const LmmArgs& p, cudaStream_t st, int num_sms) {
   const int pitch = (p.d % 2 == 0) ? conflict_free_pitch(p.d) : p.d;
   const size_t row_bytes = static_cast<size_t>(pitch) * 8 + 4 * p.nfk;
-  // MT = 4 with two prefetched parts at NT = 2 would spill
-  if (row_bytes * 256 <= 48 * 1024 && !(NT == 2 && p.nfk >= 2)) return launch_dmma_cfg<NT, 4>(p, st, num_sms);
-  if (row_bytes * 128 <= 48 * 1024) return launch_dmma_cfg<NT, 2>(p, st, num_sms);
+  // stage ~16-24 KB so that many stages stay in flight; MT = 4 with two prefetched
+  // parts at NT = 2 would spill
+  if (row_bytes * 256 <= 24 * 1024 && !(NT == 2 && p.nfk >= 2)) return launch_dmma_cfg<NT, 4>(p, st, num_sms);
+  if (row_bytes * 128 <= 24 * 1024) return launch_dmma_cfg<NT, 2>(p, st, num_sms);
   return launch_dmma_cfg<NT, 1>(p, st, num_sms);
 }
 

@@ -44,6 +44,8 @@ struct StreamSet {
   uint32_t tile_tx;      // transaction bytes of a full tile
   bool bulk_full;        // full tiles can use bulk copies
   bool bulk_last;        // the final (possibly partial) tile can use bulk copies
+  const int32_t* gidx;   // optional: stream 0 row r of the ring is source row gidx[r]
+                         // (a gathered stream, e.g. rows in FK-sorted order); <= 128 rows/tile
 };
 
 // Host helper: lay out `count` streams for `tile_rows` rows per stage over n_rows rows.
@@ -61,7 +63,7 @@ inline void stream_layout(StreamSet& s, int tile_rows, int64_t n_rows) {
     off += (s.pitch[i] * static_cast<uint32_t>(tile_rows) + 127u) & ~127u;
     if (reinterpret_cast<uintptr_t>(s.base[i]) & 15u) aligned = false;
     s.tile_tx += s.row_bytes[i] * static_cast<uint32_t>(tile_rows);
-    if (s.pitch[i] != s.row_bytes[i]) {
+    if (s.pitch[i] != s.row_bytes[i] || (i == 0 && s.gidx)) {
       if ((s.row_bytes[i] & 15u) || (s.pitch[i] & 15u)) full_ok = last_ok = false;
     } else {
       if ((s.row_bytes[i] * static_cast<uint32_t>(tile_rows)) & 15u) full_ok = false;
@@ -148,15 +150,33 @@ struct TileRing {
     __syncthreads();
   }
 
+  // Gathered stream 0: this lane's source rows (r = lane + 32 i) of `tile`.
+  FB_DEV void load_gidx(const StreamSet& s, int64_t tile, int32_t (&idx)[4]) const {
+    const int lane = threadIdx.x & 31;
+    const int rows = rows_of(tile);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = lane + 32 * i;
+      idx[i] = r < rows ? __ldg(s.gidx + tile * tile_rows + r) : 0;
+    }
+  }
+
   // Producer warp body: issue every tile of this CTA's range, recycling stages.
   FB_DEV void produce(const StreamSet& s) const {
     const int lane = threadIdx.x & 31;
     int st = 0;
     uint32_t ph = 0;
     const int64_t n = count();
+    int32_t gcur[4] = {0, 0, 0, 0}, gnext[4] = {0, 0, 0, 0};
+    if (s.gidx && n > 0) load_gidx(s, tile_begin, gnext);
     for (int64_t k = 0; k < n; ++k) {
-      if (k >= stages) mbar_wait(&empty[st], ph ^ 1u);
       const int64_t tile = tile_begin + k;
+      if (s.gidx) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) gcur[i] = gnext[i];
+        if (k + 1 < n) load_gidx(s, tile + 1, gnext);  // latency overlaps this tile's issue
+      }
+      if (k >= stages) mbar_wait(&empty[st], ph ^ 1u);
       const int rows = rows_of(tile);
       if (bulk_ok(s, tile)) {
         if (lane == 0) {
@@ -175,7 +195,16 @@ struct TileRing {
           if (i >= s.count || s.row_bytes[i] == 0) continue;
           const char* src = s.base[i] + static_cast<size_t>(tile) * tile_rows * s.row_bytes[i];
           char* dst = stage_ptr(st, s, i);
-          if (s.pitch[i] == s.row_bytes[i]) {
+          if (i == 0 && s.gidx) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int r = lane + 32 * j;
+              if (r < rows)
+                bulk_g2s_stream(dst + static_cast<uint32_t>(r) * s.pitch[0],
+                                s.base[0] + static_cast<size_t>(gcur[j]) * s.row_bytes[0], s.row_bytes[0], &full[st],
+                                policy);
+            }
+          } else if (s.pitch[i] == s.row_bytes[i]) {
             if (lane == 0)
               bulk_g2s_stream(dst, src, s.row_bytes[i] * static_cast<uint32_t>(rows), &full[st], policy);
           } else {
@@ -202,10 +231,13 @@ struct TileRing {
       char* dst = stage_ptr(st, s, i);
       const uint32_t wpr = s.row_bytes[i] / 4u;  // words per row
       const uint32_t words = wpr * static_cast<uint32_t>(rows);
+      const bool gather = i == 0 && s.gidx;
       for (uint32_t w = consumer_tid(); w < words; w += kConsumerThreads) {
         const uint32_t r = w / wpr, c = w % wpr;
+        const char* srow = gather ? s.base[0] + static_cast<size_t>(s.gidx[tile * tile_rows + r]) * s.row_bytes[0]
+                                  : src + static_cast<size_t>(r) * s.row_bytes[i];
         reinterpret_cast<uint32_t*>(dst + static_cast<size_t>(r) * s.pitch[i])[c] =
-            reinterpret_cast<const uint32_t*>(src + static_cast<size_t>(r) * s.row_bytes[i])[c];
+            reinterpret_cast<const uint32_t*>(srow)[c];
       }
     }
   }

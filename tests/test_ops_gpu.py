@@ -195,3 +195,71 @@ def test_skewed_fk_scatter_vs_oracle(n_s, d_s, n_r, d_r):
     x = rng.standard_normal((d, 5))
     _close(fb.lmm(nm, x), O.lmm(ref, x))
     _close(fb.col_sums(nm), O.col_sums(ref))
+
+
+# ---------------------------------------------------------------- crossprod (DMMA two-pass)
+@pytest.mark.parametrize("name", [n for n in golden_io.names() if n != "zero_width_s"])
+def test_crossprod_vs_reference_golden(name):
+    fb = _fb()
+    g = golden_io.load(name)
+    nm = _build_gpu(g)
+    c = fb.OpCounter()
+    cp = fb.crossprod(nm, counter=c)
+    _close(cp, g["crossprod"])
+    np.testing.assert_array_equal(cp, cp.T)  # exact symmetry (rewrite.py:298)
+    assert [c.multiplies, c.additions] == list(g["cnt_crossprod"])
+
+
+CP_CASES = [
+    # n_s, d_s, [(n_r, d_r)], key distribution, seed
+    (300_001, 60, [(15_000, 120)], "uniform", 1),
+    (100_003, 20, [(10_000, 40)], "uniform", 2),
+    (200_000, 10, [(50, 40)], "zipf", 3),      # runs spanning many CTAs (carry fixup)
+    (50_001, 7, [(997, 5)], "uniform", 4),     # odd widths: non-bulk gather fill
+    (20_000, 64, [(3, 8)], "uniform", 5),      # huge runs, tiny R
+    (12_345, 0, [(300, 9)], "uniform", 6),     # no entity features
+    (40_001, 5, [(97, 6), (1000, 3)], "uniform", 7),  # star: block-column path
+    (1, 3, [(1, 2)], "uniform", 8),
+]
+
+
+@pytest.mark.parametrize("case", CP_CASES, ids=[f"cp_n{c[0]}_d{c[1]}_{c[3]}_q{len(c[2])}" for c in CP_CASES])
+def test_crossprod_seeded_vs_oracle(case):
+    fb = _fb()
+    n_s, d_s, shapes, dist, seed = case
+    rng = np.random.default_rng(seed)
+    s = rng.random((n_s, d_s))
+    parts = []
+    for n_r, d_r in shapes:
+        keys = _zipf_keys(rng, n_s, n_r) if dist == "zipf" else rng.integers(1, n_r + 1, size=n_s)
+        parts.append((keys, rng.random((n_r, d_r))))
+    ref = O.build_star(s, parts)
+    nm = fb.build_star(s, parts) if len(parts) > 1 else fb.build_pkfk(s, parts[0][0], parts[0][1])
+    cp = fb.crossprod(nm)
+    _close(cp, O.crossprod(ref))
+    np.testing.assert_array_equal(cp, cp.T)
+
+
+def test_fk_sorted_order_is_stable_argsort():
+    fb = _fb()
+    from paper_1612_07448_b200.crossprod import fk_sorted_order
+
+    rng = np.random.default_rng(9)
+    key = rng.integers(1, 200, size=30_001)
+    nm = fb.build_pkfk(rng.random((30_001, 2)), key, rng.random((199, 3)))
+    perm, fks = fk_sorted_order(nm.k)
+    t = nm.k.target_numpy()
+    order = np.argsort(t, kind="stable")
+    np.testing.assert_array_equal(perm.cpu().numpy(), order)
+    np.testing.assert_array_equal(fks.cpu().numpy(), t[order])
+
+
+def test_crossprod_dense_and_transposed_errors():
+    fb = _fb()
+    rng = np.random.default_rng(10)
+    a = rng.standard_normal((5000, 33))
+    m = fb.as_normalized(a)
+    _close(fb.crossprod(m), a.T @ a)
+    nm = fb.build_pkfk(a, rng.integers(1, 5, size=5000), rng.random((4, 2)))
+    with pytest.raises(fb.ShapeError):
+        fb.crossprod(nm.T)
