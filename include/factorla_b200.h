@@ -133,6 +133,36 @@ size_t fb_crossprod_workspace_bytes(const fb_normalized* nm);
 int fb_crossprod(const fb_normalized* nm, const int32_t* perm, const int32_t* fk_sorted, double* out, void* ws,
                  size_t ws_bytes, fb_stream_t stream);
 
+/* ---- ML driver steps (ml.py) ------------------------------------------------------ */
+/* One fused GLM evaluation over T (d = d_s + Σ d_r, w a device d-vector, y n_s targets):
+ *   mode 0 (logistic_gd, ml.py:207-213): p = y/(1+exp(T w)), loss = Σ log1p(exp(-|y·Tw|)) + max(-y·Tw, 0)
+ *   mode 1 (linreg_gd,   ml.py:247-252): p = T w - y,        loss = Σ p²
+ * writes g = Tᵀp (d) and *loss (device). S is read once (Tw, p and Sᵀp in one pass). */
+size_t fb_glm_workspace_bytes(const fb_normalized* nm);
+int fb_glm_eval(const fb_normalized* nm, const double* y, const double* w, int32_t mode, double* g, double* loss,
+                void* ws, size_t ws_bytes, fb_stream_t stream);
+/* fb_glm_eval followed by w += alpha·g, trace[it] = loss, and *diverged = it at the first
+ * iteration whose weights are not finite (ml.py:190-192; *diverged starts at -1). */
+int fb_glm_step(const fb_normalized* nm, const double* y, double* w, int32_t mode, double alpha, int32_t it,
+                double* trace, int32_t* diverged, void* ws, size_t ws_bytes, fb_stream_t stream);
+
+/* One K-Means iteration (ml.py:275-283) on an untransposed T with k <= 16 clusters:
+ * c is the d × k centroid matrix (updated in place; empty clusters keep theirs), cc[j] =
+ * Σ c[:, j]² (in/out), d_t = rowSums(T²) (n_s), assign (n_s int32) the argmin cluster
+ * (ties to the lowest index), trace[it] = Σ_i min_j dist, *nan_row = first row whose
+ * distances hold a NaN (device; start at UINT64_MAX). */
+size_t fb_kmeans_workspace_bytes(const fb_normalized* nm, int32_t k);
+int fb_kmeans_step(const fb_normalized* nm, const double* d_t, double* c, double* cc, int32_t k, int32_t it,
+                   double* trace, int32_t* assign, unsigned long long* nan_row, void* ws, size_t ws_bytes,
+                   fb_stream_t stream);
+
+/* One GNMF multiplicative-update iteration (ml.py:306-315), r <= 16: w (n_s × r), h (d × r),
+ * ttw = Tᵀw (d × r, in: for the current w, out: for the updated w), cpw = wᵀw (r × r,
+ * in/out), sum_t2 = Σ T² (device scalar), trace[it] = Frobenius objective. */
+size_t fb_gnmf_workspace_bytes(const fb_normalized* nm, int32_t r);
+int fb_gnmf_step(const fb_normalized* nm, double* w, double* h, double* ttw, double* cpw, const double* sum_t2,
+                 int32_t r, int32_t it, double* trace, void* ws, size_t ws_bytes, fb_stream_t stream);
+
 /* a[r, c] = a[c, r] for r > c: exact symmetry from the upper triangle of a d × d matrix
  * (kernel._mirror_upper, kernel.py:132-135). */
 int fb_mirror_upper(double* a, int64_t d, fb_stream_t stream);

@@ -29,6 +29,7 @@ from .normmat import (
     transpose,
 )
 from .rewrite import col_sums, crossprod, lmm, rmm, row_sums, scalar_fn, scalar_op, sum_all
+from .ml import ModelOutput, TrainConfig, gnmf, kmeans, linreg_gd, linreg_normal, logistic_gd
 
 __version__ = "0.1.0"
 
@@ -59,4 +60,11 @@ __all__ = [
     "scalar_op",
     "sum_all",
     "launch_count",
+    "ModelOutput",
+    "TrainConfig",
+    "gnmf",
+    "kmeans",
+    "linreg_gd",
+    "linreg_normal",
+    "logistic_gd",
 ]

@@ -77,6 +77,13 @@ _SIGS = {
     "fb_fk_sort": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_size, c_vp]),
     "fb_crossprod_workspace_bytes": (c_size, [_P]),
     "fb_crossprod": (c_i32, [_P, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "fb_glm_workspace_bytes": (c_size, [_P]),
+    "fb_glm_eval": (c_i32, [_P, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "fb_glm_step": (c_i32, [_P, c_vp, c_vp, c_i32, c_f64, c_i32, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "fb_kmeans_workspace_bytes": (c_size, [_P, c_i32]),
+    "fb_kmeans_step": (c_i32, [_P, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "fb_gnmf_workspace_bytes": (c_size, [_P, c_i32]),
+    "fb_gnmf_step": (c_i32, [_P, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_size, c_vp]),
     "fb_mirror_upper": (c_i32, [c_vp, c_i64, c_vp]),
     "fb_scalar_map": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_f64, c_vp]),
     "fb_unary_map": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp]),

@@ -3,6 +3,7 @@
 // Validation (shapes, nulls, supported sizes) happens here, before any launch, and
 // failures come back as FB_ERR_* codes with a thread-local message; the Python layer
 // maps them onto the reference's exception classes (exceptions.py).
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -177,7 +178,8 @@ size_t fb_lmm_workspace_bytes(const fb_normalized* nm, int32_t d_x) {
   if (!nm) return 0;
   int w = d_x < 16 ? d_x : 16;
   size_t b = 0;
-  for (int i = 0; i < nm->q; ++i) b += align256(static_cast<size_t>(nm->part[i].n_r) * w * sizeof(double));
+  for (int i = 0; i < nm->q; ++i)
+    b += align256(static_cast<size_t>(nm->part[i].n_r) * fb::z_stride(w) * sizeof(double));
   return b + 256;
 }
 
@@ -197,10 +199,11 @@ int fb_lmm(const fb_normalized* nm, const double* x, int32_t d_x, double* out, v
     int64_t off = nm->d_s;
     for (int i = 0; i < nm->q; ++i) {
       const fb_part& p = nm->part[i];
-      double* z = cv.take<double>(static_cast<size_t>(p.n_r) * w);
+      const int zst = fb::z_stride(w);
+      double* z = cv.take<double>(static_cast<size_t>(p.n_r) * zst);
       // z_i = R_i · X[off:off+d_r, c0:c0+w]   (rewrite.py:187)
       cudaError_t e = fb::launch_lmm_rows(p.r, p.n_r, p.d_r, x + off * d_x + c0, w, d_x, 0, nullptr,
-                                          nullptr, z, w, cs(stream), g_num_sms);
+                                          nullptr, 0, z, zst, cs(stream), g_num_sms);
       if (e != cudaSuccess) return cuda_status(e, "lmm(z)");
       fks[i] = p.fk;
       zs[i] = z;
@@ -208,7 +211,7 @@ int fb_lmm(const fb_normalized* nm, const double* x, int32_t d_x, double* out, v
     }
     // out = S · X[0:d_s, c0:c0+w] + Σ z_i[fk_i]   (rewrite.py:186-190)
     cudaError_t e = fb::launch_lmm_rows(nm->s, nm->n_s, nm->d_s, x + c0, w, d_x, nm->q, fks, zs,
-                                        out + c0, d_x, cs(stream), g_num_sms);
+                                        fb::z_stride(w), out + c0, d_x, cs(stream), g_num_sms);
     if (e != cudaSuccess) return cuda_status(e, "lmm(S)");
     c0 += w;
   }
@@ -406,6 +409,250 @@ int fb_crossprod(const fb_normalized* nm, const int32_t* perm, const int32_t* fk
   }
   c.out = out;
   return cuda_status(fb::launch_crossprod(c, ws, ws_bytes, cs(stream), g_num_sms), "crossprod");
+}
+
+// ------------------------------------------------------------------ GLM steps
+size_t fb_glm_workspace_bytes(const fb_normalized* nm) {
+  if (!nm) return 0;
+  size_t b = 0;
+  for (int i = 0; i < nm->q; ++i) b += 3 * align256(static_cast<size_t>(nm->part[i].n_r) * sizeof(double));
+  const int64_t d = total_cols(nm);
+  b += align256(static_cast<size_t>(d + 1) * sizeof(double));                                 // g
+  b += align256(sizeof(double));                                                               // loss
+  b += align256(fb::glm_partials_doubles(nm->d_s, g_num_sms) * sizeof(double));                // S partials
+  b += align256(fb::colreduce_workspace_doubles(0, static_cast<int>(max_width(nm)), 1, g_num_sms) * sizeof(double));
+  b += 2 * 256;                                                                                // counters
+  return b + 256;
+}
+
+static int glm_eval_impl(const fb_normalized* nm, const double* y, const double* w, int32_t mode, double* g,
+                         double* loss, Carver& cv, fb_stream_t stream) {
+  cudaStream_t st = cs(stream);
+  fb::GlmArgs a{};
+  a.s = nm->s;
+  a.n = nm->n_s;
+  a.d = nm->d_s;
+  a.y = y;
+  a.w = w;
+  a.mode = mode;
+  a.nfk = nm->q;
+  int64_t off = nm->d_s;
+  double* bins[FB_MAX_PARTS] = {};
+  for (int i = 0; i < nm->q; ++i) {
+    const fb_part& p = nm->part[i];
+    double* z = cv.take<double>(static_cast<size_t>(p.n_r) * fb::z_stride(1));
+    bins[i] = cv.take<double>(static_cast<size_t>(p.n_r));
+    if (!z || !bins[i]) return fail(FB_ERR_ARG, "glm: workspace too small");
+    // z_q = R_q · w_q  (rewrite.py:187, R·X before K)
+    cudaError_t e = fb::launch_lmm_rows(p.r, p.n_r, p.d_r, w + off, 1, 1, 0, nullptr, nullptr, 0, z, fb::z_stride(1),
+                                        st, g_num_sms);
+    if (e == cudaSuccess) e = cudaMemsetAsync(bins[i], 0, static_cast<size_t>(p.n_r) * sizeof(double), st);
+    if (e != cudaSuccess) return cuda_status(e, "glm(z)");
+    a.fk[i] = p.fk;
+    a.z[i] = z;
+    a.bins[i] = bins[i];
+    off += p.d_r;
+  }
+  a.g_out = g;
+  a.loss_out = loss;
+  a.partials = cv.take<double>(fb::glm_partials_doubles(nm->d_s, g_num_sms));
+  a.counter = cv.take<unsigned>(1);
+  double* cpart = cv.take<double>(fb::colreduce_workspace_doubles(0, static_cast<int>(max_width(nm)), 1, g_num_sms));
+  unsigned* ccnt = cv.take<unsigned>(1);
+  if (!a.partials || !a.counter || !cpart || !ccnt) return fail(FB_ERR_ARG, "glm: workspace too small");
+  if (nm->n_s > 0) {
+    cudaError_t e = fb::launch_glm_spass(a, st, g_num_sms);
+    if (e != cudaSuccess) return cuda_status(e, "glm(S pass)");
+  }
+  // g_q = bins_qᵀ R_q  (rmm's (X·K)·R half, rewrite.py:207-209)
+  off = nm->d_s;
+  for (int i = 0; i < nm->q; ++i) {
+    const fb_part& p = nm->part[i];
+    fb::ColReduce r{};
+    r.a = p.r;
+    r.n = p.n_r;
+    r.d = p.d_r;
+    r.nx = 1;
+    r.w = bins[i];
+    r.w_rs = 1;
+    r.w_cs = 1;
+    r.out = g + off;
+    r.o_js = 0;
+    r.o_cs = 1;
+    r.partials = cpart;
+    r.counter = ccnt;
+    cudaError_t e = fb::launch_colreduce(r, st, g_num_sms);
+    if (e != cudaSuccess) return cuda_status(e, "glm(R pass)");
+    off += p.d_r;
+  }
+  return FB_OK;
+}
+
+int fb_glm_eval(const fb_normalized* nm, const double* y, const double* w, int32_t mode, double* g, double* loss,
+                void* ws, size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (mode != 0 && mode != 1) return fail(FB_ERR_ARG, "glm: unknown mode %d", mode);
+  if ((!y && nm->n_s > 0) || !w || !g || !loss) return fail(FB_ERR_ARG, "glm: NULL pointer");
+  if (nm->d_s > 256 || max_width(nm) > 256) return fail(FB_ERR_ARG, "glm: factor widths above 256 are not supported");
+  if (ws_bytes < fb_glm_workspace_bytes(nm)) return fail(FB_ERR_ARG, "glm: workspace too small");
+  Carver cv{static_cast<char*>(ws), ws_bytes};
+  return glm_eval_impl(nm, y, w, mode, g, loss, cv, stream);
+}
+
+int fb_glm_step(const fb_normalized* nm, const double* y, double* w, int32_t mode, double alpha, int32_t it,
+                double* trace, int32_t* diverged, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (mode != 0 && mode != 1) return fail(FB_ERR_ARG, "glm: unknown mode %d", mode);
+  if ((!y && nm->n_s > 0) || !w || !trace || !diverged) return fail(FB_ERR_ARG, "glm: NULL pointer");
+  if (nm->d_s > 256 || max_width(nm) > 256) return fail(FB_ERR_ARG, "glm: factor widths above 256 are not supported");
+  if (ws_bytes < fb_glm_workspace_bytes(nm)) return fail(FB_ERR_ARG, "glm: workspace too small");
+  Carver cv{static_cast<char*>(ws), ws_bytes};
+  const int64_t d = total_cols(nm);
+  double* g = cv.take<double>(static_cast<size_t>(d + 1));
+  double* loss = cv.take<double>(1);
+  st = glm_eval_impl(nm, y, w, mode, g, loss, cv, stream);
+  if (st) return st;
+  // logistic: w += α Tᵀp (ml.py:212); least squares: w -= α Tᵀ(Tw - y) (ml.py:251)
+  return cuda_status(fb::launch_glm_update(w, g, static_cast<int>(d), mode == 0 ? alpha : -alpha, loss, trace, it,
+                                           diverged, cs(stream)),
+                     "glm(update)");
+}
+
+// ------------------------------------------------------------------ K-Means / GNMF steps
+size_t fb_kmeans_workspace_bytes(const fb_normalized* nm, int32_t k) {
+  if (!nm || k < 1) return 0;
+  const int64_t d = total_cols(nm);
+  size_t b = 0;
+  b += align256(static_cast<size_t>(d) * k * 8);            // 2c
+  b += align256(static_cast<size_t>(nm->n_s) * k * 8);      // tc
+  b += align256(static_cast<size_t>(d) * k * 8);            // TᵀA
+  b += align256(static_cast<size_t>(k) * 4);                // sizes
+  b += align256(static_cast<size_t>(g_num_sms) * 8 * 8);    // assign partials
+  b += align256(fb::onehot_partials_doubles(nm->d_s > 0 ? nm->d_s : 1, k, g_num_sms) * 8);
+  b += align256(fb::colreduce_workspace_doubles(0, static_cast<int>(max_width(nm)), k, g_num_sms) * 8);
+  b += 3 * 256;                                             // counters
+  for (int i = 0; i < nm->q; ++i) b += align256(static_cast<size_t>(nm->part[i].n_r) * k * 4) +
+                                       align256(static_cast<size_t>(nm->part[i].n_r) * k * 8);
+  return b + fb_lmm_workspace_bytes(nm, k) + 256;
+}
+
+int fb_kmeans_step(const fb_normalized* nm, const double* d_t, double* c, double* cc, int32_t k, int32_t it,
+                   double* trace, int32_t* assign, unsigned long long* nan_row, void* ws, size_t ws_bytes,
+                   fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (k < 1 || k > 16) return fail(FB_ERR_ARG, "kmeans: k=%d outside [1, 16]", k);
+  if (!d_t || !c || !cc || !trace || !assign || !nan_row) return fail(FB_ERR_ARG, "kmeans: NULL pointer");
+  if (max_width(nm) > 256) return fail(FB_ERR_ARG, "kmeans: factor widths above 256 are not supported");
+  if (ws_bytes < fb_kmeans_workspace_bytes(nm, k)) return fail(FB_ERR_ARG, "kmeans: workspace too small");
+  cudaStream_t s = cs(stream);
+  const int64_t d = total_cols(nm);
+  Carver cv{static_cast<char*>(ws), ws_bytes};
+  double* c2 = cv.take<double>(static_cast<size_t>(d) * k);
+  double* tc = cv.take<double>(static_cast<size_t>(nm->n_s) * k);
+  double* tta = cv.take<double>(static_cast<size_t>(d) * k);
+  int32_t* sizes = cv.take<int32_t>(k);
+  double* apart = cv.take<double>(static_cast<size_t>(g_num_sms) * 8);
+  double* opart = cv.take<double>(fb::onehot_partials_doubles(nm->d_s > 0 ? nm->d_s : 1, k, g_num_sms));
+  double* cpart = cv.take<double>(fb::colreduce_workspace_doubles(0, static_cast<int>(max_width(nm)), k, g_num_sms));
+  unsigned* cnt0 = cv.take<unsigned>(1);
+  unsigned* cnt1 = cv.take<unsigned>(1);
+  unsigned* cnt2 = cv.take<unsigned>(1);
+  fb::KmFk fks{};
+  fks.nfk = nm->q;
+  double* fbins[FB_MAX_PARTS] = {};
+  for (int i = 0; i < nm->q; ++i) {
+    fks.fk[i] = nm->part[i].fk;
+    fks.bins[i] = cv.take<int32_t>(static_cast<size_t>(nm->part[i].n_r) * k);
+    fbins[i] = cv.take<double>(static_cast<size_t>(nm->part[i].n_r) * k);
+  }
+  // tc = (2T)·C computed as T·(2C): scaling by two is exact, so the products match bit for bit
+  cudaError_t e = fb::launch_scalar_map(c, c2, d * k, fb::kMul, 2.0, s, g_num_sms);
+  if (e != cudaSuccess) return cuda_status(e, "kmeans(2c)");
+  st = fb_lmm(nm, c2, k, tc, cv.p, cv.left, stream);
+  if (st) return st;
+  for (int i = 0; i < nm->q; ++i) {
+    e = cudaMemsetAsync(fks.bins[i], 0, static_cast<size_t>(nm->part[i].n_r) * k * 4, s);
+    if (e != cudaSuccess) return cuda_status(e, "kmeans(memset)");
+  }
+  e = fb::launch_kmeans_assign(tc, d_t, cc, nm->n_s, k, fks, assign, sizes, apart, cnt0, trace, it, nan_row, s,
+                               g_num_sms);
+  if (e != cudaSuccess) return cuda_status(e, "kmeans(assign)");
+  // TᵀA: S part by one-hot column sums, R parts as R_qᵀ (A_qᵀ K_q) from the integer histograms
+  if (nm->d_s > 0) {
+    e = fb::launch_onehot_colsum(nm->s, nm->n_s, nm->d_s, assign, k, opart, cnt1, tta, s, g_num_sms);
+    if (e != cudaSuccess) return cuda_status(e, "kmeans(onehot)");
+  }
+  int64_t off = nm->d_s;
+  for (int i = 0; i < nm->q; ++i) {
+    const fb_part& p = nm->part[i];
+    e = fb::launch_i32_to_f64(fks.bins[i], fbins[i], p.n_r * k, s, g_num_sms);
+    if (e != cudaSuccess) return cuda_status(e, "kmeans(bins)");
+    fb::ColReduce r{};
+    r.a = p.r;
+    r.n = p.n_r;
+    r.d = p.d_r;
+    r.nx = k;
+    r.w = fbins[i];
+    r.w_rs = k;
+    r.w_cs = 1;
+    r.out = tta + off * k;
+    r.o_js = 1;
+    r.o_cs = k;
+    r.partials = cpart;
+    r.counter = cnt2;
+    e = fb::launch_colreduce(r, s, g_num_sms);
+    if (e != cudaSuccess) return cuda_status(e, "kmeans(R pass)");
+    off += p.d_r;
+  }
+  return cuda_status(fb::launch_kmeans_update(c, tta, sizes, static_cast<int>(d), k, cc, s), "kmeans(update)");
+}
+
+size_t fb_gnmf_workspace_bytes(const fb_normalized* nm, int32_t r) {
+  if (!nm || r < 1) return 0;
+  fb_normalized wm{};
+  wm.n_s = nm->n_s;
+  wm.d_s = r;
+  size_t inner = fb_lmm_workspace_bytes(nm, r);
+  inner = std::max(inner, fb_wt_workspace_bytes(nm, r));
+  inner = std::max(inner, fb_crossprod_workspace_bytes(&wm));
+  return align256(static_cast<size_t>(nm->n_s) * r * 8) + align256(static_cast<size_t>(r) * r * 8) + inner + 256;
+}
+
+int fb_gnmf_step(const fb_normalized* nm, double* w, double* h, double* ttw, double* cpw, const double* sum_t2,
+                 int32_t r, int32_t it, double* trace, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (r < 1 || r > 16) return fail(FB_ERR_ARG, "gnmf: r=%d outside [1, 16]", r);
+  if (!w || !h || !ttw || !cpw || !sum_t2 || !trace) return fail(FB_ERR_ARG, "gnmf: NULL pointer");
+  if (ws_bytes < fb_gnmf_workspace_bytes(nm, r)) return fail(FB_ERR_ARG, "gnmf: workspace too small");
+  cudaStream_t s = cs(stream);
+  const int64_t d = total_cols(nm);
+  const double eps = 1e-12;
+  Carver cv{static_cast<char*>(ws), ws_bytes};
+  double* th = cv.take<double>(static_cast<size_t>(nm->n_s) * r);
+  double* cph = cv.take<double>(static_cast<size_t>(r) * r);
+  // h = h ∘ ttw / (h·cpw + eps); cph = hᵀh
+  cudaError_t e = fb::launch_nmf_update(h, ttw, cpw, d, r, eps, s, g_num_sms);
+  if (e == cudaSuccess) e = fb::launch_small_gram(h, d, r, cph, s);
+  if (e != cudaSuccess) return cuda_status(e, "gnmf(h)");
+  // th = T·h; w = w ∘ th / (w·cph + eps)
+  st = fb_lmm(nm, h, r, th, cv.p, cv.left, stream);
+  if (st) return st;
+  e = fb::launch_nmf_update(w, th, cph, nm->n_s, r, eps, s, g_num_sms);
+  if (e != cudaSuccess) return cuda_status(e, "gnmf(w)");
+  // ttw = Tᵀw (also the next iteration's ttw, ml.py:307/312); cpw = wᵀw
+  st = fb_wt(nm, w, r, r, 1, ttw, 1, r, cv.p, cv.left, stream);
+  if (st) return st;
+  fb_normalized wm{};
+  wm.s = w;
+  wm.n_s = nm->n_s;
+  wm.d_s = r;
+  st = fb_crossprod(&wm, nullptr, nullptr, cpw, cv.p, cv.left, stream);
+  if (st) return st;
+  return cuda_status(fb::launch_nmf_objective(sum_t2, ttw, h, d * r, cpw, cph, r * r, trace, it, s), "gnmf(objective)");
 }
 
 int fb_mirror_upper(double* a, int64_t d, fb_stream_t stream) {

@@ -138,12 +138,9 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
   extern __shared__ __align__(128) char smem[];
   TileRing ring;
   ring.init(smem, stages, tile_rows, a.n);
-  ring.start();
-  if (is_producer_warp()) {
-    ring.produce(ss);
-    return;
-  }
-  const int warp = (threadIdx.x >> 5) - 1;
+  ring.start(ss);
+  if (ring.service(ss)) return;
+  const int warp = consumer_warp();
   const int grp = blockIdx.y;
   const int nsplit = jobs.row_split;
   const int jidx = warp / nsplit, split = warp % nsplit;
@@ -417,10 +414,10 @@ template <class Setup>
 static cudaError_t run_gram(GramJobs& J, GramArgs& a, StreamSet& ss, int tile_rows, cudaStream_t st, int num_sms,
                             Setup) {
   stream_layout(ss, tile_rows, a.n);
-  int stages = static_cast<int>((200 * 1024 - 256) / ss.stage_bytes);
+  int stages = static_cast<int>((200 * 1024 - kRingHeader) / ss.stage_bytes);
   if (stages > 6) stages = 6;
   if (stages < 2) return cudaErrorNotSupported;
-  const size_t smem = 256 + static_cast<size_t>(stages) * ss.stage_bytes;
+  const size_t smem = kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes;
   int ngroups = 0;
   for (int gI = 0; gI < kMaxJobGroups; ++gI)
     if (J.njobs[gI] > 0) ngroups = gI + 1;

@@ -8,9 +8,10 @@ constexpr int kMaxParts = 4;  // attribute tables per star schema handled in one
 
 // fb_lmm.cu ------------------------------------------------------------------------
 // out[i, 0:dx] (ld ldo) = a[i, :] · x (d × dx, ld ldx) + Σ_q z_q[fk_q[i], 0:dx]
+// z_q rows have zstride doubles (even, >= dx): see z_stride().
+inline int z_stride(int dx) { return dx < 2 ? 2 : (dx + 1) & ~1; }
 cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, int dx, int64_t ldx,
-                            int nfk,
-                            const int32_t* const* fk, const double* const* z, double* out,
+                            int nfk, const int32_t* const* fk, const double* const* z, int zstride, double* out,
                             int64_t ldo, cudaStream_t st, int num_sms);
 
 // fb_reduce.cu ---------------------------------------------------------------------
@@ -83,5 +84,47 @@ cudaError_t launch_fk_sort(const int32_t* fk, int64_t n, int64_t n_r, int32_t* p
                            size_t ws_bytes, cudaStream_t st, int num_sms);
 size_t crossprod_workspace_bytes(int64_t n_s, int d_s, int64_t n_r, int d_r, int q, int num_sms);
 cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cudaStream_t st, int num_sms);
+
+// fb_ml.cu --------------------------------------------------------------------------
+struct GlmArgs {
+  const double* s;  // n × d entity rows
+  int64_t n;
+  int d;
+  const double* y;  // n labels / targets
+  const double* w;  // d entity weights
+  int mode;         // 0: logistic (ml.py:207-213), 1: least squares (ml.py:247-252)
+  int nfk;
+  const int32_t* fk[kMaxParts];
+  const double* z[kMaxParts];  // R_q·w_q
+  double* bins[kMaxParts];     // Kᵀp accumulators (zeroed by the caller)
+  double* g_out;               // d: Sᵀp
+  double* loss_out;            // 1
+  double* partials;            // glm_partials_doubles
+  unsigned* counter;           // one zeroed word
+};
+size_t glm_partials_doubles(int d, int num_sms);
+cudaError_t launch_glm_spass(const GlmArgs& g, cudaStream_t st, int num_sms);
+cudaError_t launch_glm_update(double* w, const double* g, int d, double alpha, const double* loss, double* trace,
+                              int it, int* diverged, cudaStream_t st);
+
+struct KmFk {
+  int nfk;
+  const int32_t* fk[kMaxParts];
+  int32_t* bins[kMaxParts];  // n_R,q × k integer histograms (zeroed by the caller)
+};
+cudaError_t launch_kmeans_assign(const double* tc, const double* d_t, const double* cc, int64_t n, int k,
+                                 const KmFk& fks, int32_t* assign, int32_t* sizes, double* partials, unsigned* counter,
+                                 double* trace, int it, unsigned long long* nan_row, cudaStream_t st, int num_sms);
+size_t onehot_partials_doubles(int d, int k, int num_sms);
+cudaError_t launch_onehot_colsum(const double* s, int64_t n, int d, const int32_t* assign, int k, double* partials,
+                                 unsigned* counter, double* out, cudaStream_t st, int num_sms);
+cudaError_t launch_kmeans_update(double* c, const double* tta, const int32_t* sizes, int d, int k, double* cc,
+                                 cudaStream_t st);
+cudaError_t launch_nmf_update(double* f, const double* num, const double* g, int64_t rows, int r, double eps,
+                              cudaStream_t st, int num_sms);
+cudaError_t launch_small_gram(const double* f, int64_t rows, int r, double* g, cudaStream_t st);
+cudaError_t launch_nmf_objective(const double* sum_t2, const double* ttw, const double* h, int64_t dr,
+                                 const double* cpw, const double* cph, int rr, double* trace, int it,
+                                 cudaStream_t st);
 
 }  // namespace fb

@@ -15,11 +15,12 @@
 //     its 32-row group for a coalesced epilogue.
 //   * DMMA (5 <= d_x <= 16): mma.sync m8n8k4 f64 (SASS DMMA; tcgen05 has no f64 kind),
 //     each warp owning MT m-tiles of 8 rows against X zero-padded to NT·8 columns.
-// Both prefetch the gathered z rows of tile k+1 (its FK column is already in shared
-// memory) before computing tile k, so the L2 latency of the gather overlaps the
-// arithmetic. z is read with an L2 evict_last policy and the streamed output is
-// written evict_first, so the multi-GB streams do not push z out of L2. The z-pass
-// itself (no FK) stores z evict_last.
+// The z[fk] rows are keyed gathers of the ring (fb_stream.cuh): the gatherer warp bulk-
+// copies them into the stage as soon as the FK column lands, so they arrive as many
+// stages ahead as the S rows and the consumers only read shared memory. z rows are
+// padded to an even number of doubles (16-byte bulk copies) and read with an L2
+// evict_last policy; the streamed output is written evict_first; the z-pass (no FK)
+// stores z evict_last so it stays L2-resident for the S pass.
 #include "fb_kernels.cuh"
 
 namespace fb {
@@ -37,13 +38,14 @@ struct LmmArgs {
   double* out;                 // n × dx, leading dimension ldo
   int64_t ldo;
   int pitch;                   // shared-memory row pitch of the factor tile (doubles)
+  int zstride;                 // doubles per z row (even: gathered rows are 16-byte bulk copies)
   int lanes;                   // rowdot: lanes per row (power of two)
   int cols;                    // rowdot: columns per lane (d / lanes)
 };
 
 // ------------------------------------------------------------------ rowdot (d_x <= 4)
 template <int NX>
-__global__ void __launch_bounds__(kRingThreads) lmm_rowdot_kernel(LmmArgs p, StreamSet ss, int stages,
+__global__ void __launch_bounds__(kRingThreads, 1) lmm_rowdot_kernel(LmmArgs p, StreamSet ss, int stages,
                                                                   int tile_rows) {
   extern __shared__ __align__(128) char smem[];
   const int d = p.d;
@@ -54,62 +56,21 @@ __global__ void __launch_bounds__(kRingThreads) lmm_rowdot_kernel(LmmArgs p, Str
 
   TileRing ring;
   ring.init(buf, stages, tile_rows, p.n);
-  ring.start();  // __syncthreads: xs visible
-  if (is_producer_warp()) {
-    ring.produce(ss);
-    return;
-  }
+  ring.start(ss);  // __syncthreads: xs visible
+  if (ring.service(ss)) return;
 
   const int lane = lane_id();
-  const int warp = (threadIdx.x >> 5) - 1;
+  const int warp = consumer_warp();
   const int rw = tile_rows / kConsumerWarps;  // rows per warp per tile (<= 32)
   const int wrow = warp * rw;
   const int L = p.lanes, C = p.cols;
   const int rpi = 32 / L;                     // rows per instruction
   const int iters = (rw + rpi - 1) / rpi;
   const int sub = lane % L, rsub = lane / L;
-  const uint64_t keep = policy_evict_last();
-  const uint64_t stream_out = policy_evict_first();
-  const bool is_zpass = p.nfk == 0;
+  const uint64_t pol = p.nfk == 0 ? policy_evict_last() : policy_evict_first();  // z stays in L2
 
-  double zn[kMaxParts][NX];  // gathered z of this lane's row in the next tile
-  auto gather = [&](int st, int64_t tile) {
-    const int rows = ring.rows_of(tile);
-    const int r = wrow + lane;
-#pragma unroll
-    for (int q = 0; q < kMaxParts; ++q) {
-      if (q < p.nfk) {
-        const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(st, ss, 1 + q));
-        const bool live = lane < rw && r < rows;
-        const double* zr = p.z[q] + static_cast<int64_t>(live ? fkt[r] : 0) * NX;
-#pragma unroll
-        for (int j = 0; j < NX; ++j) zn[q][j] = live ? ld_hint(zr + j, keep) : 0.0;
-      }
-    }
-  };
-
-  // with an FK gather the next tile is acquired early (its z loads overlap this tile's
-  // arithmetic); the z-pass (no FK) holds a single stage
-  const int64_t count = ring.count();
-  const bool prefetch = p.nfk > 0;
-  int cur = 0;
-  if (prefetch && count > 0) {
-    cur = ring.acquire(ss, 0);
-    gather(cur, ring.tile_begin);
-  }
-  for (int64_t kt = 0; kt < count; ++kt) {
-    double zc[kMaxParts][NX];
-#pragma unroll
-    for (int q = 0; q < kMaxParts; ++q)
-#pragma unroll
-      for (int j = 0; j < NX; ++j) zc[q][j] = zn[q][j];
-    int nxt = cur;
-    if (!prefetch) {
-      cur = ring.acquire(ss, kt);
-    } else if (kt + 1 < count) {
-      nxt = ring.acquire(ss, kt + 1);
-      gather(nxt, ring.tile_begin + kt + 1);
-    }
+  for (int64_t kt = 0; kt < ring.count(); ++kt) {
+    const int cur = ring.acquire(ss, kt);
     const int64_t tile = ring.tile_begin + kt;
     const int rows = ring.rows_of(tile);
     const int64_t r0 = tile * tile_rows;
@@ -127,7 +88,7 @@ __global__ void __launch_bounds__(kRingThreads) lmm_rowdot_kernel(LmmArgs p, Str
       if (live) {
         const double* arow = A + static_cast<size_t>(wrow + rl) * p.pitch + sub;
         const double* xc = xs + sub * NX;
-#pragma unroll 4
+#pragma unroll 5
         for (int m = 0; m < C; ++m) {
           const double a = arow[m * L];
 #pragma unroll
@@ -147,17 +108,17 @@ __global__ void __launch_bounds__(kRingThreads) lmm_rowdot_kernel(LmmArgs p, Str
     }
     const int r = wrow + lane;
     if (lane < rw && r < rows) {
+      // + z_0[fk_0] + z_1[fk_1] ... in part order (rewrite.py:186-190), gathered into smem
+      for (int q = 0; q < p.nfk; ++q) {
+        const double* zr = reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, q)) + r * p.zstride;
 #pragma unroll
-      for (int q = 0; q < kMaxParts; ++q)
-        if (q < p.nfk)
-#pragma unroll
-          for (int j = 0; j < NX; ++j) res[j] += zc[q][j];
+        for (int j = 0; j < NX; ++j) res[j] += zr[j];
+      }
       double* o = p.out + (r0 + r) * p.ldo;
 #pragma unroll
-      for (int j = 0; j < NX; ++j) st_hint(o + j, res[j], is_zpass ? keep : stream_out);
+      for (int j = 0; j < NX; ++j) st_hint(o + j, res[j], pol);
     }
     ring.release();
-    cur = nxt;
   }
 }
 
@@ -167,8 +128,8 @@ FB_DEV int xs_ld() {
   return 8 * NT + 4;  // bank skew for the B-fragment loads (see conflict_free_pitch)
 }
 
-template <int NT, int MT, int NQP>
-__global__ void __launch_bounds__(kRingThreads) lmm_dmma_kernel(LmmArgs p, StreamSet ss, int stages,
+template <int NT, int MT>
+__global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, StreamSet ss, int stages,
                                                                int tile_rows) {
   extern __shared__ __align__(128) char smem[];
   const int d = p.d;
@@ -185,69 +146,18 @@ __global__ void __launch_bounds__(kRingThreads) lmm_dmma_kernel(LmmArgs p, Strea
 
   TileRing ring;
   ring.init(buf, stages, tile_rows, p.n);
-  ring.start();  // contains __syncthreads (xs visible after it)
-  if (is_producer_warp()) {
-    ring.produce(ss);
-    return;
-  }
+  ring.start(ss);  // contains __syncthreads (xs visible after it)
+  if (ring.service(ss)) return;
 
   const int lane = lane_id();
   const int g = lane >> 2, t = lane & 3;
-  const int warp = (threadIdx.x >> 5) - 1;  // consumer warp index
+  const int warp = consumer_warp();
   const int pitch = p.pitch;
   const int wrow = warp * (8 * MT);
-  const uint64_t keep = policy_evict_last();
-  const uint64_t stream_out = policy_evict_first();
-  const bool is_zpass = p.nfk == 0;
+  const uint64_t pol = p.nfk == 0 ? policy_evict_last() : policy_evict_first();
 
-  double zn[NQP > 0 ? NQP : 1][MT][NT][2];
-  auto gather = [&](int st, int64_t tile) {
-    const int rows = ring.rows_of(tile);
-#pragma unroll
-    for (int q = 0; q < NQP; ++q) {
-      const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(st, ss, 1 + q));
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const int r = wrow + 8 * mt + g;
-        const bool live = r < rows;
-        const double* zr = p.z[q] + static_cast<int64_t>(live ? fkt[r] : 0) * p.dx;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int c = 8 * nt + 2 * t;
-          zn[q][mt][nt][0] = (live && c < p.dx) ? ld_hint(zr + c, keep) : 0.0;
-          zn[q][mt][nt][1] = (live && c + 1 < p.dx) ? ld_hint(zr + c + 1, keep) : 0.0;
-        }
-      }
-    }
-  };
-
-  // with an FK gather the next tile is acquired early (its z loads overlap this tile's
-  // arithmetic); the z-pass (no FK) holds a single stage
-  const int64_t count = ring.count();
-  const bool prefetch = p.nfk > 0;
-  int cur = 0;
-  if (prefetch && count > 0) {
-    cur = ring.acquire(ss, 0);
-    gather(cur, ring.tile_begin);
-  }
-  for (int64_t kt = 0; kt < count; ++kt) {
-    double zc[NQP > 0 ? NQP : 1][MT][NT][2];
-#pragma unroll
-    for (int q = 0; q < NQP; ++q)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          zc[q][mt][nt][0] = zn[q][mt][nt][0];
-          zc[q][mt][nt][1] = zn[q][mt][nt][1];
-        }
-    int nxt = cur;
-    if (!prefetch) {
-      cur = ring.acquire(ss, kt);
-    } else if (kt + 1 < count) {
-      nxt = ring.acquire(ss, kt + 1);
-      gather(nxt, ring.tile_begin + kt + 1);
-    }
+  for (int64_t kt = 0; kt < ring.count(); ++kt) {
+    const int cur = ring.acquire(ss, kt);
     const int64_t tile = ring.tile_begin + kt;
     const int rows = ring.rows_of(tile);
     const int64_t r0 = tile * tile_rows;
@@ -286,25 +196,16 @@ __global__ void __launch_bounds__(kRingThreads) lmm_dmma_kernel(LmmArgs p, Strea
       for (int mt = 0; mt < MT; ++mt) {
         const int r = wrow + 8 * mt + g;
         if (r >= rows) continue;
-#pragma unroll
-        for (int q = 0; q < NQP; ++q)
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            acc[mt][nt][0] += zc[q][mt][nt][0];
-            acc[mt][nt][1] += zc[q][mt][nt][1];
-          }
-        for (int q = NQP; q < p.nfk; ++q) {
-          const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(cur, ss, 1 + q));
-          const double* zr = p.z[q] + static_cast<int64_t>(fkt[r]) * p.dx;
+        for (int q = 0; q < p.nfk; ++q) {
+          const double* zr = reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, q)) + r * p.zstride;
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             const int c = 8 * nt + 2 * t;
-            if (c < p.dx) acc[mt][nt][0] += ld_hint(zr + c, keep);
-            if (c + 1 < p.dx) acc[mt][nt][1] += ld_hint(zr + c + 1, keep);
+            if (c < p.dx) acc[mt][nt][0] += zr[c];
+            if (c + 1 < p.dx) acc[mt][nt][1] += zr[c + 1];
           }
         }
         double* o = p.out + (r0 + r) * p.ldo;
-        const uint64_t pol = is_zpass ? keep : stream_out;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int c = 8 * nt + 2 * t;
@@ -318,15 +219,14 @@ __global__ void __launch_bounds__(kRingThreads) lmm_dmma_kernel(LmmArgs p, Strea
       }
     }
     ring.release();
-    cur = nxt;
   }
 }
 
 // ------------------------------------------------------------------ host launchers
 static int stages_for(size_t fixed, uint32_t stage_bytes, int max_stages) {
   const size_t budget = 200 * 1024;
-  if (fixed + 256 + 2 * static_cast<size_t>(stage_bytes) > budget) return 0;
-  int st = static_cast<int>((budget - fixed - 256) / stage_bytes);
+  if (fixed + kRingHeader + 2 * static_cast<size_t>(stage_bytes) > budget) return 0;
+  int st = static_cast<int>((budget - fixed - kRingHeader) / stage_bytes);
   return st > max_stages ? max_stages : st;
 }
 
@@ -334,10 +234,9 @@ template <class K>
 static cudaError_t launch_ring(K kern, const LmmArgs& p, StreamSet& ss, size_t fixed, int tile_rows,
                                cudaStream_t st, int num_sms) {
   stream_layout(ss, tile_rows, p.n);
-  // consumers hold two stages (current + prefetched next); keep >= ~120 KB in flight
-  const int stages = stages_for(fixed, ss.stage_bytes, 12);
+  const int stages = stages_for(fixed, ss.stage_bytes, 8);
   if (stages < 2) return cudaErrorNotSupported;
-  const size_t smem = fixed + 256 + static_cast<size_t>(stages) * ss.stage_bytes;
+  const size_t smem = fixed + kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int per_sm = static_cast<int>((228 * 1024) / (smem + 1024));
@@ -359,7 +258,11 @@ static void fill_streams(const LmmArgs& p, StreamSet& ss, int pitch) {
   for (int q = 0; q < p.nfk; ++q) {
     ss.base[1 + q] = reinterpret_cast<const char*>(p.fk[q]);
     ss.row_bytes[1 + q] = 4u;
+    ss.gkey[q] = 1 + q;
+    ss.gbase[q] = reinterpret_cast<const char*>(p.z[q]);
+    ss.grow_bytes[q] = static_cast<uint32_t>(p.zstride) * 8u;
   }
+  ss.ngather = p.nfk;
 }
 
 template <int NX>
@@ -370,10 +273,10 @@ static cudaError_t launch_rowdot(LmmArgs p, cudaStream_t st, int num_sms) {
   p.lanes = L;
   p.cols = p.d / L;
   p.pitch = p.d;
-  const uint32_t row_bytes = static_cast<uint32_t>(p.d) * 8u + 4u * p.nfk;
-  // rows per warp per tile: 32, fewer for wide rows (stage ~16-24 KB, many stages)
+  const uint32_t row_bytes = static_cast<uint32_t>(p.d) * 8u + (4u + 8u * p.zstride) * p.nfk;
+  // rows per warp per tile: 32, fewer for wide rows (stage <= ~44 KB)
   int rw = 32;
-  while (rw > 4 && static_cast<size_t>(row_bytes) * rw * kConsumerWarps > 24 * 1024) rw >>= 1;
+  while (rw > 4 && static_cast<size_t>(row_bytes) * rw * kConsumerWarps > 48 * 1024) rw >>= 1;
   StreamSet ss;
   fill_streams(p, ss, p.d);
   const size_t fixed = (static_cast<size_t>(p.d > 0 ? p.d : 1) * NX * 8 + 127) & ~size_t(127);
@@ -388,24 +291,21 @@ static cudaError_t launch_dmma_cfg(LmmArgs p, cudaStream_t st, int num_sms) {
   fill_streams(p, ss, p.pitch);
   const int dpad = (p.d + 3) & ~3;
   const size_t fixed = (static_cast<size_t>(dpad > 0 ? dpad : 4) * (8 * NT + 4) * 8 + 127) & ~size_t(127);
-  if (p.nfk == 0) return launch_ring(lmm_dmma_kernel<NT, MT, 0>, p, ss, fixed, tile_rows, st, num_sms);
-  if (p.nfk == 1) return launch_ring(lmm_dmma_kernel<NT, MT, 1>, p, ss, fixed, tile_rows, st, num_sms);
-  return launch_ring(lmm_dmma_kernel<NT, MT, 2>, p, ss, fixed, tile_rows, st, num_sms);
+  return launch_ring(lmm_dmma_kernel<NT, MT>, p, ss, fixed, tile_rows, st, num_sms);
 }
 
 template <int NT>
 static cudaError_t launch_dmma(const LmmArgs& p, cudaStream_t st, int num_sms) {
   const int pitch = (p.d % 2 == 0) ? conflict_free_pitch(p.d) : p.d;
-  const size_t row_bytes = static_cast<size_t>(pitch) * 8 + 4 * p.nfk;
-  // stage ~16-24 KB so that many stages stay in flight; MT = 4 with two prefetched
-  // parts at NT = 2 would spill
-  if (row_bytes * 256 <= 24 * 1024 && !(NT == 2 && p.nfk >= 2)) return launch_dmma_cfg<NT, 4>(p, st, num_sms);
-  if (row_bytes * 128 <= 24 * 1024) return launch_dmma_cfg<NT, 2>(p, st, num_sms);
+  const size_t row_bytes = static_cast<size_t>(pitch) * 8 + (4 + 8 * static_cast<size_t>(p.zstride)) * p.nfk;
+  // stage <= ~48 KB
+  if (row_bytes * 256 <= 48 * 1024) return launch_dmma_cfg<NT, 4>(p, st, num_sms);
+  if (row_bytes * 128 <= 48 * 1024) return launch_dmma_cfg<NT, 2>(p, st, num_sms);
   return launch_dmma_cfg<NT, 1>(p, st, num_sms);
 }
 
 cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, int dx, int64_t ldx,
-                            int nfk, const int32_t* const* fk, const double* const* z, double* out,
+                            int nfk, const int32_t* const* fk, const double* const* z, int zstride, double* out,
                             int64_t ldo, cudaStream_t st, int num_sms) {
   if (n <= 0) return cudaSuccess;
   if (dx < 1 || dx > 16) return cudaErrorNotSupported;
@@ -421,6 +321,8 @@ cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, 
     p.fk[q] = fk[q];
     p.z[q] = z[q];
   }
+  p.zstride = zstride;
+  if (nfk > 0 && (zstride < dx || (zstride & 1))) return cudaErrorInvalidValue;
   p.out = out;
   p.ldo = ldo;
   switch (dx) {

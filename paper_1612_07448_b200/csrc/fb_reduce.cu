@@ -80,17 +80,14 @@ FB_DEV void scatter_add(double* bins, int key, const double (&vals)[NX], bool ac
 }
 
 template <int NX>
-__global__ void __launch_bounds__(kRingThreads) colreduce_kernel(ColRedDev p, StreamSet ss, int stages,
+__global__ void __launch_bounds__(kRingThreads, 1) colreduce_kernel(ColRedDev p, StreamSet ss, int stages,
                                                                  int tile_rows) {
   extern __shared__ __align__(128) char smem[];
   const int d = p.c.d;
   TileRing ring;
   ring.init(smem, stages, tile_rows, p.c.n);
-  ring.start();
-  if (is_producer_warp()) {
-    ring.produce(ss);
-    return;
-  }
+  ring.start(ss);
+  if (ring.service(ss)) return;
   const int tid = consumer_tid();
   const int groups = d > 0 ? kConsumerThreads / d : 0;
   const int col = d > 0 ? tid % d : 0;
@@ -213,12 +210,12 @@ static cudaError_t launch_colreduce_nx(const ColReduce& c, cudaStream_t st, int 
   stream_layout(ss, tile_rows, c.n);
   const size_t red_bytes = static_cast<size_t>(kConsumerThreads) * NX * 8;
   int stages = 4;
-  size_t smem = 256 + static_cast<size_t>(stages) * ss.stage_bytes;
+  size_t smem = kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes;
   if (smem > 200 * 1024) {
     stages = 3;
-    smem = 256 + static_cast<size_t>(stages) * ss.stage_bytes;
+    smem = kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes;
   }
-  if (smem < 256 + red_bytes + 1024) smem = 256 + red_bytes + 1024;
+  if (smem < kRingHeader + red_bytes + 1024) smem = kRingHeader + red_bytes + 1024;
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   auto kern = colreduce_kernel<NX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,38 +1,50 @@
 // fb_stream.cuh — warp-specialised multi-stream bulk-copy tile ring.
 //
-// Every factor-matrix pass (LMM, RMM, rowSums/colSums, the driver steps) streams a
-// contiguous range of rows through shared memory. A row range of a row-major f64
-// matrix is one contiguous byte range, so a tile of rows is one 1-D bulk copy
+// Every factor-matrix pass (LMM, RMM, rowSums/colSums, crossprod, the driver steps)
+// streams a contiguous range of rows through shared memory. A row range of a row-major
+// f64 matrix is one contiguous byte range, so a tile of rows is one 1-D bulk copy
 // (cp.async.bulk -> SASS UBLKCP) — no tensor map needed. Up to kMaxStreams row-aligned
 // arrays (the factor rows, the int32 FK column(s), per-row weights) share one "full"
 // mbarrier per stage.
 //
-// Roles: warp 0 is the producer (it only issues copies and waits on the per-stage
-// "empty" barriers); the kConsumerWarps consumer warps wait on "full", compute, and
-// arrive on "empty" — no CTA-wide barrier per tile. Consumers that need to sync among
-// themselves use consumer_sync() (named barrier 1).
+// Roles (kRingThreads = 2 service warps + kConsumerWarps):
+//   warp 0  producer: issues the stream copies of each stage once its "empty" barrier
+//           says the consumers are done with it;
+//   warp 1  gatherer: for keyed gather streams (z[fk] rows of an LMM, ...) it waits for
+//           the stage's keys to land, then issues one bulk copy per row from the lookup
+//           table into the stage, completing on a second per-stage barrier ("gfull").
+//           Gathers therefore run as many stages ahead as the ring is deep, and the
+//           consumers never wait on an L2 round trip;
+//   warps 2+ consumers: wait on "full" (+ "gfull"), compute, arrive on "empty".
+// Consumers that need to sync among themselves use consumer_sync() (named barrier 1).
 //
 // A stream may ask for a padded shared-memory pitch (bytes per row > row bytes): the
-// producer warp then issues one bulk copy per row, so the tensor-core fragment loads
-// that walk rows hit distinct banks.
+// producer then issues one bulk copy per row, so tensor-core fragment loads that walk
+// rows hit distinct banks. Stream 0 may instead be gathered by a global row index array
+// (gidx: rows in FK-sorted order for the crossprod).
 //
 // Tiles that cannot use bulk copies (a misaligned base, or a final tile whose byte
 // count is not a multiple of 16) are filled by the consumers with plain loads; the
-// producer arrives on "full" without a transaction count so phases stay uniform.
+// producer arrives on "full" without a transaction count so phases stay uniform, and the
+// gatherer then reads the keys from global memory.
 //
-// Measured on B200 (tools/stream_probe.cu): with one CTA per SM the ring needs
-// >= 16-32 KB tiles and 3-4 stages to reach 6.7-7.4 TB/s; per-tile bookkeeping must
-// stay off the consumers' path (incremental stage/phase, no 64-bit division, no
-// fence.proxy.async per issue — that fence waits for the thread's in-flight copies).
+// Measured on B200 (tools/stream_probe.cu): with one CTA per SM the ring needs >= ~130 KB
+// in flight (e.g. 3 × 44 KB) to reach 6.7-7.4 TB/s; per-tile bookkeeping must stay off
+// the consumers' path (incremental stage/phase, no 64-bit division, no fence.proxy.async
+// per issue — that fence waits for the thread's in-flight copies).
 #pragma once
 #include "fb_common.cuh"
 
 namespace fb {
 
 constexpr int kMaxStreams = 8;
+constexpr int kMaxGather = 4;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
-constexpr int kRingThreads = kConsumerThreads + 32;
+constexpr int kServiceWarps = 2;
+constexpr int kRingThreads = kConsumerThreads + 32 * kServiceWarps;
+constexpr int kRingHeader = 512;  // 3 × 16 mbarriers (full, empty, gfull) + padding
+constexpr int kMaxStages = 16;
 
 struct StreamSet {
   const char* base[kMaxStreams];
@@ -46,10 +58,17 @@ struct StreamSet {
   bool bulk_last;        // the final (possibly partial) tile can use bulk copies
   const int32_t* gidx;   // optional: stream 0 row r of the ring is source row gidx[r]
                          // (a gathered stream, e.g. rows in FK-sorted order); <= 128 rows/tile
+  // keyed gathers: row r of gather g = gbase[g] + key * grow_bytes[g], key = int32 row r
+  // of regular stream gkey[g]; grow_bytes a multiple of 16, gbase 16-byte aligned
+  int ngather;
+  int gkey[kMaxGather];
+  const char* gbase[kMaxGather];
+  uint32_t grow_bytes[kMaxGather];
+  uint32_t gsmem_off[kMaxGather];
 };
 
-// Host helper: lay out `count` streams for `tile_rows` rows per stage over n_rows rows.
-// A zero pitch means dense (pitch = row_bytes).
+// Host helper: lay out `count` streams (+ `ngather` gathers) for `tile_rows` rows per
+// stage over n_rows rows. A zero pitch means dense (pitch = row_bytes).
 inline void stream_layout(StreamSet& s, int tile_rows, int64_t n_rows) {
   uint32_t off = 0;
   bool aligned = true;
@@ -70,6 +89,10 @@ inline void stream_layout(StreamSet& s, int tile_rows, int64_t n_rows) {
       if ((s.row_bytes[i] * static_cast<uint32_t>(last_rows)) & 15u) last_ok = false;
     }
   }
+  for (int g = 0; g < s.ngather; ++g) {
+    s.gsmem_off[g] = off;
+    off += (s.grow_bytes[g] * static_cast<uint32_t>(tile_rows) + 127u) & ~127u;
+  }
   s.stage_bytes = off;
   s.bulk_full = aligned && full_ok;
   s.bulk_last = aligned && last_ok && full_ok;
@@ -88,29 +111,33 @@ FB_DEV void consumer_sync() {
 }
 
 FB_DEV bool is_producer_warp() { return threadIdx.x < 32; }
-FB_DEV int consumer_tid() { return static_cast<int>(threadIdx.x) - 32; }
+FB_DEV bool is_gather_warp() { return threadIdx.x >= 32 && threadIdx.x < 64; }
+FB_DEV int consumer_tid() { return static_cast<int>(threadIdx.x) - 32 * kServiceWarps; }
+FB_DEV int consumer_warp() { return (static_cast<int>(threadIdx.x) >> 5) - kServiceWarps; }
 
 struct TileRing {
   char* buf;        // stages * stage_bytes
-  uint64_t* full;   // stages mbarriers (producer -> consumers)
+  uint64_t* full;   // stages mbarriers (producer -> consumers, gatherer)
   uint64_t* empty;  // stages mbarriers (consumers -> producer)
+  uint64_t* gfull;  // stages mbarriers (gatherer -> consumers)
   int stages;
   int tile_rows;
   int64_t n_rows;
   int64_t ntiles;                // tiles over the whole matrix
   int64_t tile_begin, tile_end;  // this CTA's contiguous tile range
   uint64_t policy;
-  // consumer iteration state: the next stage to wait on, and the oldest stage still
-  // held (consumers may hold two stages to prefetch gathers one tile ahead)
+  bool gathers;
+  // consumer iteration state: the next stage to wait on, and the oldest stage still held
   int stage;
   uint32_t phase;
   int rstage;
 
-  // Carve `smem` (128-byte aligned): 2*stages barriers in the first 256 bytes, then buffers.
+  // Carve `smem` (128-byte aligned): barriers in the first kRingHeader bytes, then buffers.
   FB_DEV void init(char* smem, int stages_, int tile_rows_, int64_t n_rows_) {
     full = reinterpret_cast<uint64_t*>(smem);
-    empty = full + 16;
-    buf = smem + 256;
+    empty = full + kMaxStages;
+    gfull = empty + kMaxStages;
+    buf = smem + kRingHeader;
     stages = stages_;
     tile_rows = tile_rows_;
     n_rows = n_rows_;
@@ -119,12 +146,17 @@ struct TileRing {
     tile_begin = ntiles * c / g;
     tile_end = ntiles * (c + 1) / g;
     policy = policy_evict_first();
+    gathers = false;
   }
 
   FB_DEV int64_t count() const { return tile_end - tile_begin; }
 
   FB_DEV char* stage_ptr(int st, const StreamSet& s, int stream) const {
     return buf + static_cast<uint32_t>(st) * s.stage_bytes + s.smem_off[stream];
+  }
+
+  FB_DEV char* gather_ptr(int st, const StreamSet& s, int g) const {
+    return buf + static_cast<uint32_t>(st) * s.stage_bytes + s.gsmem_off[g];
   }
 
   FB_DEV int rows_of(int64_t tile) const {
@@ -136,18 +168,33 @@ struct TileRing {
   }
 
   // Barrier setup; call from all threads before the role split (contains __syncthreads).
-  FB_DEV void start() {
+  FB_DEV void start(const StreamSet& s) {
     stage = 0;
     phase = 0;
     rstage = 0;
+    gathers = s.ngather > 0;
     if (threadIdx.x == 0) {
       for (int i = 0; i < stages; ++i) {
         mbar_init(&full[i], 1);
         mbar_init(&empty[i], kConsumerWarps);
+        mbar_init(&gfull[i], 1);
       }
       fence_mbar_init();
     }
     __syncthreads();
+  }
+
+  // Service warps run their loop and return true; consumers get false.
+  FB_DEV bool service(const StreamSet& s) const {
+    if (is_producer_warp()) {
+      produce(s);
+      return true;
+    }
+    if (is_gather_warp()) {
+      if (s.ngather > 0) gather(s);
+      return true;
+    }
+    return false;
   }
 
   // Gathered stream 0: this lane's source rows (r = lane + 32 i) of `tile`.
@@ -223,6 +270,44 @@ struct TileRing {
     }
   }
 
+  // Gatherer warp body: once a stage's keys have landed, bulk-copy the keyed rows of
+  // every gather table into it (evict_last: the tables are re-read across the pass).
+  FB_DEV void gather(const StreamSet& s) const {
+    const int lane = threadIdx.x & 31;
+    const uint64_t keep = policy_evict_last();
+    int st = 0;
+    uint32_t ph = 0;
+    const int64_t n = count();
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t tile = tile_begin + k;
+      const int rows = rows_of(tile);
+      mbar_wait(&full[st], ph);
+      const bool keys_in_smem = bulk_ok(s, tile);
+      if (lane == 0) {
+        uint32_t tx = 0;
+        for (int g = 0; g < s.ngather; ++g) tx += s.grow_bytes[g] * static_cast<uint32_t>(rows);
+        mbar_arrive_expect_tx(&gfull[st], tx);
+      }
+      __syncwarp();
+      for (int g = 0; g < s.ngather; ++g) {
+        const int ks = s.gkey[g];
+        const int32_t* keys = reinterpret_cast<const int32_t*>(stage_ptr(st, s, ks));
+        const int32_t* gkeys = reinterpret_cast<const int32_t*>(s.base[ks]) + tile * tile_rows;
+        char* dst = gather_ptr(st, s, g);
+        const uint32_t rb = s.grow_bytes[g];
+        for (int r = lane; r < rows; r += 32) {
+          const int32_t key = keys_in_smem ? keys[r] : __ldg(gkeys + r);
+          bulk_g2s_stream(dst + static_cast<uint32_t>(r) * rb, s.gbase[g] + static_cast<size_t>(key) * rb, rb,
+                          &gfull[st], keep);
+        }
+      }
+      if (++st == stages) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
+  }
+
   // Consumers: fill a non-bulk tile cooperatively (4-byte granularity).
   FB_DEV void manual_fill(const StreamSet& s, int64_t tile, int st) const {
     const int rows = rows_of(tile);
@@ -252,6 +337,7 @@ struct TileRing {
       manual_fill(s, tile, st);
       consumer_sync();
     }
+    if (gathers) mbar_wait(&gfull[st], phase);
     if (++stage == stages) {
       stage = 0;
       phase ^= 1u;

@@ -181,6 +181,14 @@ class NormalizedMatrix:
         t._cache = self._cache
         return t
 
+    def device_view(self):
+        """The same matrix with results returned as CUDA tensors (shares the caches)."""
+        if not self.host_io:
+            return self
+        v = NormalizedMatrix(self.variant, self.blocks, self.transposed, self.source_rows, False)
+        v._cache = self._cache
+        return v
+
     def untransposed(self):
         return self if not self.transposed else self.T
 

@@ -272,6 +272,6 @@ def rmm(x, nm, counter=None):
 
 def crossprod(nm, method="efficient", counter=None):
     """``T' T`` without materializing T; exactly symmetric (rewrite.py:245-298)."""
-    from .crossprod import crossprod as _cp
+    from .crossprod_impl import crossprod as _cp
 
     return _cp(nm, method=method, counter=counter)

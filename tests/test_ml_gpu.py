@@ -1,0 +1,153 @@
+"""GPU parity of the ML drivers (ml.py) against the reference golden traces and the oracle.
+
+Bars: float64 model state and objective traces within normwise rel 1e-9 of the reference
+(bench.py:38-43 metric); K-Means assignments compared through the centroids and trace.
+"""
+import numpy as np
+import pytest
+import torch
+
+import factorla_oracle as O
+import golden_io
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+def _fb():
+    import paper_1612_07448_b200 as fb
+
+    return fb
+
+
+def _close(a, b, tol=TOL):
+    a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    assert a.shape == b.shape, (a.shape, b.shape)
+    dev = O.max_rel_deviation(a, b)
+    assert dev <= tol, dev
+
+
+def _build_gpu(g):
+    fb = _fb()
+    parts = golden_io.parts(g)
+    if len(parts) == 1:
+        return fb.build_pkfk(g["s"], parts[0][0], parts[0][1])
+    return fb.build_star(g["s"], parts)
+
+
+GOLD = [n for n in golden_io.names() if n != "zero_width_s"]
+
+
+@pytest.mark.parametrize("name", GOLD)
+def test_drivers_vs_reference_golden(name):
+    fb = _fb()
+    g = golden_io.load(name)
+    nm = _build_gpu(g)
+    cfg = fb.TrainConfig(iterations=5, step_size=1e-3, k=3, r=2, rng_seed=3)
+    out = fb.linreg_normal(nm, g["y_lin"])
+    _close(out.weights, g["linreg_w"])
+    _close(out.objective, g["linreg_obj"])
+    out = fb.logistic_gd(nm, g["y_log"], cfg)
+    _close(out.weights, g["logreg_w"])
+    _close(out.objective, g["logreg_obj"])
+    out = fb.linreg_gd(nm, g["y_lin"], cfg)
+    _close(out.weights, g["linreg_gd_w"])
+    out = fb.kmeans(nm, cfg)
+    _close(out.centroids, g["kmeans_c"])
+    _close(out.objective, g["kmeans_obj"])
+    if "gnmf_w" in g:
+        out = fb.gnmf(nm, cfg)
+        _close(out.factors[0], g["gnmf_w"])
+        _close(out.factors[1], g["gnmf_h"])
+        _close(out.objective, g["gnmf_obj"])
+
+
+def _c1_like(seed, n_s=100_000, d_s=20, n_r=10_000, d_r=40, star=False):
+    rng = np.random.default_rng(seed)
+    s = rng.standard_normal((n_s, d_s))
+    parts = [(rng.integers(1, n_r + 1, size=n_s), rng.standard_normal((n_r, d_r)))]
+    if star:
+        parts.append((rng.integers(1, 501, size=n_s), rng.standard_normal((500, 7))))
+    return rng, s, parts
+
+
+def _both(s, parts):
+    fb = _fb()
+    nm = fb.build_star(s, parts) if len(parts) > 1 else fb.build_pkfk(s, parts[0][0], parts[0][1])
+    return nm, O.build_star(s, parts)
+
+
+def test_logreg_c1_shape_20_iterations():
+    fb = _fb()
+    rng, s, parts = _c1_like(11)
+    nm, ref = _both(s, parts)
+    w_true = rng.standard_normal((ref.d, 1))
+    y = np.where(O.lmm(ref, w_true) >= 0, 1.0, -1.0)
+    out = fb.logistic_gd(nm, y, fb.TrainConfig(iterations=20, step_size=1e-3))
+    w, obj = O.logistic_gd(ref, y, 20, 1e-3)
+    _close(out.weights, w)
+    _close(out.objective, obj)
+    assert out.counts.multiplies > 0
+
+
+def test_linreg_gd_and_normal_star():
+    fb = _fb()
+    rng, s, parts = _c1_like(12, n_s=60_001, d_s=9, n_r=3000, d_r=13, star=True)
+    nm, ref = _both(s, parts)
+    y = O.lmm(ref, rng.standard_normal((ref.d, 1))) + 0.01 * rng.standard_normal((ref.n, 1))
+    out = fb.linreg_gd(nm, y, fb.TrainConfig(iterations=7, step_size=1e-6))
+    w, obj = O.linreg_gd(ref, y, 7, 1e-6)
+    _close(out.weights, w)
+    _close(out.objective, obj)
+    out = fb.linreg_normal(nm, y)
+    w, obj = O.linreg_normal(ref, y)
+    _close(out.weights, w, 1e-8)
+    _close(out.objective, obj, 1e-8)
+
+
+def test_kmeans_star_vs_oracle():
+    fb = _fb()
+    rng, s, parts = _c1_like(13, n_s=80_000, d_s=6, n_r=2000, d_r=5, star=True)
+    nm, ref = _both(s, parts)
+    out = fb.kmeans(nm, fb.TrainConfig(iterations=6, k=10, rng_seed=5))
+    c, obj, _ = O.kmeans(ref, 10, 6, 5)
+    _close(out.centroids, c)
+    _close(out.objective, obj)
+
+
+def test_gnmf_zipf_vs_oracle():
+    fb = _fb()
+    rng = np.random.default_rng(14)
+    n_s, n_r = 50_000, 500
+    p = np.arange(1, n_r + 1, dtype=np.float64) ** -1.2
+    p /= p.sum()
+    key = np.minimum(np.searchsorted(np.cumsum(p), rng.random(n_s), side="right"), n_r - 1) + 1
+    s = rng.random((n_s, 10))
+    r = rng.random((n_r, 40))
+    nm, ref = _both(s, [(key, r)])
+    out = fb.gnmf(nm, fb.TrainConfig(iterations=6, r=5, rng_seed=2))
+    w, h, obj = O.gnmf(ref, 5, 6, 2)
+    _close(out.factors[0], w)
+    _close(out.factors[1], h)
+    _close(out.objective, obj)
+
+
+def test_dense_matrix_input():
+    fb = _fb()
+    rng = np.random.default_rng(15)
+    a = rng.standard_normal((20_000, 12))
+    y = np.where(a @ rng.standard_normal((12, 1)) >= 0, 1.0, -1.0)
+    out = fb.logistic_gd(a, y, fb.TrainConfig(iterations=4, step_size=1e-3))
+    w, obj = O.logistic_gd(O.NM(a, []), y, 4, 1e-3)
+    _close(out.weights, w)
+
+
+def test_divergence_error_iteration():
+    fb = _fb()
+    a = np.full((100, 2), 1e300)
+    y = np.ones((100, 1))
+    with pytest.raises(fb.DivergenceError) as ei:
+        fb.linreg_gd(a, y, fb.TrainConfig(iterations=3, step_size=1.0))
+    assert ei.value.iteration == 0

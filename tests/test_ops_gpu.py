@@ -242,7 +242,7 @@ def test_crossprod_seeded_vs_oracle(case):
 
 def test_fk_sorted_order_is_stable_argsort():
     fb = _fb()
-    from paper_1612_07448_b200.crossprod import fk_sorted_order
+    from paper_1612_07448_b200.crossprod_impl import fk_sorted_order
 
     rng = np.random.default_rng(9)
     key = rng.integers(1, 200, size=30_001)
