@@ -75,6 +75,19 @@ FB_DEV void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes, uint64_t
       : "memory");
 }
 
+// 16-byte cp.async (LDGSTS) global -> shared, L2-only, with a cache policy. Completion is
+// signalled per thread with cp_async_arrive_noinc on an mbarrier whose expected count
+// includes that arrival.
+FB_DEV void cp_async16(void* dst, const void* src, uint64_t policy) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "l"(policy)
+               : "memory");
+}
+
+FB_DEV void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
 FB_DEV uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));

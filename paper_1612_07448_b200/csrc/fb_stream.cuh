@@ -11,17 +11,19 @@
 //   warp 0  producer: issues the stream copies of each stage once its "empty" barrier
 //           says the consumers are done with it;
 //   warp 1  gatherer: for keyed gather streams (z[fk] rows of an LMM, ...) it waits for
-//           the stage's keys to land, then issues one bulk copy per row from the lookup
-//           table into the stage, completing on a second per-stage barrier ("gfull").
-//           Gathers therefore run as many stages ahead as the ring is deep, and the
-//           consumers never wait on an L2 round trip;
+//           the stage's keys to land, then copies the keyed rows from the lookup table
+//           into the stage with 16-byte cp.async (one warp instruction moves 32 chunks;
+//           a per-row bulk copy costs ~60 issue cycles, measured), each lane completing
+//           on a second per-stage barrier ("gfull"). Gathers therefore run as many stages
+//           ahead as the ring is deep, and the consumers never wait on an L2 round trip;
 //   warps 2+ consumers: wait on "full" (+ "gfull"), compute, arrive on "empty".
 // Consumers that need to sync among themselves use consumer_sync() (named barrier 1).
 //
 // A stream may ask for a padded shared-memory pitch (bytes per row > row bytes): the
 // producer then issues one bulk copy per row, so tensor-core fragment loads that walk
 // rows hit distinct banks. Stream 0 may instead be gathered by a global row index array
-// (gidx: rows in FK-sorted order for the crossprod).
+// (gidx: rows in FK-sorted order for the crossprod); the producer moves those rows with
+// 16-byte cp.async and all its lanes arrive on "full" (expected count 1 + 32).
 //
 // Tiles that cannot use bulk copies (a misaligned base, or a final tile whose byte
 // count is not a multiple of 16) are filled by the consumers with plain loads; the
@@ -175,9 +177,9 @@ struct TileRing {
     gathers = s.ngather > 0;
     if (threadIdx.x == 0) {
       for (int i = 0; i < stages; ++i) {
-        mbar_init(&full[i], 1);
+        mbar_init(&full[i], s.gidx ? 33 : 1);
         mbar_init(&empty[i], kConsumerWarps);
-        mbar_init(&gfull[i], 1);
+        mbar_init(&gfull[i], 32);
       }
       fence_mbar_init();
     }
@@ -234,6 +236,7 @@ struct TileRing {
             for (int i = 0; i < kMaxStreams; ++i)
               if (i < s.count) tx += s.row_bytes[i] * static_cast<uint32_t>(rows);
           }
+          if (s.gidx) tx -= s.row_bytes[0] * static_cast<uint32_t>(rows);  // cp.async, not tx-counted
           mbar_arrive_expect_tx(&full[st], tx);
         }
         __syncwarp();
@@ -243,13 +246,22 @@ struct TileRing {
           const char* src = s.base[i] + static_cast<size_t>(tile) * tile_rows * s.row_bytes[i];
           char* dst = stage_ptr(st, s, i);
           if (i == 0 && s.gidx) {
+            // rows of the gathered stream: (row, 16-byte chunk) items spread over the lanes
+            const uint32_t nch = s.row_bytes[0] >> 4;
+            const uint32_t items = nch * static_cast<uint32_t>(rows);
+            for (uint32_t base = 0; base < items; base += 32) {  // warp-uniform trip count
+              const uint32_t it = base + lane;
+              const uint32_t r = (it < items ? it : 0) / nch, c = it - r * nch;
+              // source row of ring row r lives in lane r % 32, slot r / 32
+              int32_t srow = 0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int r = lane + 32 * j;
-              if (r < rows)
-                bulk_g2s_stream(dst + static_cast<uint32_t>(r) * s.pitch[0],
-                                s.base[0] + static_cast<size_t>(gcur[j]) * s.row_bytes[0], s.row_bytes[0], &full[st],
-                                policy);
+              for (int j = 0; j < 4; ++j) {
+                const int32_t v = __shfl_sync(0xffffffffu, gcur[j], r & 31);
+                if (static_cast<int>(r >> 5) == j) srow = v;
+              }
+              if (it < items)
+                cp_async16(dst + r * s.pitch[0] + 16u * c,
+                           s.base[0] + static_cast<size_t>(srow) * s.row_bytes[0] + 16u * c, policy);
             }
           } else if (s.pitch[i] == s.row_bytes[i]) {
             if (lane == 0)
@@ -263,6 +275,7 @@ struct TileRing {
       } else if (lane == 0) {
         mbar_arrive(&full[st]);
       }
+      if (s.gidx) cp_async_arrive_noinc(&full[st]);  // all 32 lanes, after their copies
       if (++st == stages) {
         st = 0;
         ph ^= 1u;
@@ -283,24 +296,21 @@ struct TileRing {
       const int rows = rows_of(tile);
       mbar_wait(&full[st], ph);
       const bool keys_in_smem = bulk_ok(s, tile);
-      if (lane == 0) {
-        uint32_t tx = 0;
-        for (int g = 0; g < s.ngather; ++g) tx += s.grow_bytes[g] * static_cast<uint32_t>(rows);
-        mbar_arrive_expect_tx(&gfull[st], tx);
-      }
-      __syncwarp();
       for (int g = 0; g < s.ngather; ++g) {
         const int ks = s.gkey[g];
         const int32_t* keys = reinterpret_cast<const int32_t*>(stage_ptr(st, s, ks));
         const int32_t* gkeys = reinterpret_cast<const int32_t*>(s.base[ks]) + tile * tile_rows;
         char* dst = gather_ptr(st, s, g);
         const uint32_t rb = s.grow_bytes[g];
-        for (int r = lane; r < rows; r += 32) {
+        const uint32_t nch = rb >> 4;
+        const uint32_t items = nch * static_cast<uint32_t>(rows);
+        for (uint32_t it = lane; it < items; it += 32) {
+          const uint32_t r = nch == 1 ? it : it / nch, c = it - r * nch;
           const int32_t key = keys_in_smem ? keys[r] : __ldg(gkeys + r);
-          bulk_g2s_stream(dst + static_cast<uint32_t>(r) * rb, s.gbase[g] + static_cast<size_t>(key) * rb, rb,
-                          &gfull[st], keep);
+          cp_async16(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c, keep);
         }
       }
+      cp_async_arrive_noinc(&gfull[st]);
       if (++st == stages) {
         st = 0;
         ph ^= 1u;

@@ -21,12 +21,12 @@ def _fb():
     return fb
 
 
-def _close(a, b, tol=TOL):
+def _close(a, b, tol=TOL, what=""):
     a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
-    assert a.shape == b.shape, (a.shape, b.shape)
+    assert a.shape == b.shape, (what, a.shape, b.shape)
     dev = O.max_rel_deviation(a, b)
-    assert dev <= tol, dev
+    assert dev <= tol, (what, dev, a.ravel()[:6], b.ravel()[:6])
 
 
 def _build_gpu(g):
@@ -46,22 +46,22 @@ def test_drivers_vs_reference_golden(name):
     g = golden_io.load(name)
     nm = _build_gpu(g)
     cfg = fb.TrainConfig(iterations=5, step_size=1e-3, k=3, r=2, rng_seed=3)
-    out = fb.linreg_normal(nm, g["y_lin"])
-    _close(out.weights, g["linreg_w"])
-    _close(out.objective, g["linreg_obj"])
     out = fb.logistic_gd(nm, g["y_log"], cfg)
-    _close(out.weights, g["logreg_w"])
-    _close(out.objective, g["logreg_obj"])
+    _close(out.weights, g["logreg_w"], what="logreg_w")
+    _close(out.objective, g["logreg_obj"], what="logreg_obj")
     out = fb.linreg_gd(nm, g["y_lin"], cfg)
-    _close(out.weights, g["linreg_gd_w"])
+    _close(out.weights, g["linreg_gd_w"], what="linreg_gd_w")
     out = fb.kmeans(nm, cfg)
-    _close(out.centroids, g["kmeans_c"])
-    _close(out.objective, g["kmeans_obj"])
+    _close(out.centroids, g["kmeans_c"], what="kmeans_c")
+    _close(out.objective, g["kmeans_obj"], what="kmeans_obj")
     if "gnmf_w" in g:
         out = fb.gnmf(nm, cfg)
-        _close(out.factors[0], g["gnmf_w"])
-        _close(out.factors[1], g["gnmf_h"])
-        _close(out.objective, g["gnmf_obj"])
+        _close(out.factors[0], g["gnmf_w"], what="gnmf_w")
+        _close(out.factors[1], g["gnmf_h"], what="gnmf_h")
+        _close(out.objective, g["gnmf_obj"], what="gnmf_obj")
+    out = fb.linreg_normal(nm, g["y_lin"])
+    _close(out.weights, g["linreg_w"], what="linreg_w")
+    _close(out.objective, g["linreg_obj"], what="linreg_obj")
 
 
 def _c1_like(seed, n_s=100_000, d_s=20, n_r=10_000, d_r=40, star=False):
