@@ -78,6 +78,7 @@ FB_DEV void gram_tile(const GramJob& jb, const uint32_t (&codes)[SLOTS / 2], con
                                         : nullptr;
   const int p0 = a.reg[0].pitch, p1 = a.reg[1].pitch;
   const int ao0 = 8 * jb.a0 + g, ao1 = 8 * jb.a1 + g;
+  __syncwarp();  // mma.sync.aligned needs the whole warp converged (after the barrier spin)
   for (int k0 = 4 * split; k0 < rows; k0 += 4 * nsplit) {
     const int k = k0 + t;
     const bool live = k < rows;

@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, St
     const int64_t r0 = tile * tile_rows;
     const double* A = reinterpret_cast<const double*>(ring.stage_ptr(cur, ss, 0));
 
+    __syncwarp();  // mma.sync.aligned needs the whole warp converged (after the barrier spin)
     if (wrow < rows) {
       double acc[MT][NT][2];
 #pragma unroll

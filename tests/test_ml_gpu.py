@@ -61,7 +61,9 @@ def test_drivers_vs_reference_golden(name):
         _close(out.objective, g["gnmf_obj"], what="gnmf_obj")
     out = fb.linreg_normal(nm, g["y_lin"])
     _close(out.weights, g["linreg_w"], what="linreg_w")
-    _close(out.objective, g["linreg_obj"], what="linreg_obj")
+    # the residual of an exact fit is rounding noise: compare against ‖y‖²
+    scale = max(float(g["linreg_obj"][0]), float(np.sum(g["y_lin"] ** 2)))
+    assert abs(out.objective[0] - float(g["linreg_obj"][0])) <= TOL * scale
 
 
 def _c1_like(seed, n_s=100_000, d_s=20, n_r=10_000, d_r=40, star=False):
