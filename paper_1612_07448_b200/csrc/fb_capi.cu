@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "factorla_b200.h"
@@ -14,7 +15,19 @@
 
 namespace fb {
 static std::atomic<unsigned long long> g_launches{0};
-void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static int g_debug_sync = -1;
+void count_launch(const char* file, int line) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (g_debug_sync < 0) {
+    const char* e = getenv("FB_DEBUG_SYNC");
+    g_debug_sync = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (g_debug_sync) {
+    cudaError_t err = cudaDeviceSynchronize();
+    if (err == cudaSuccess) err = cudaGetLastError();
+    if (err != cudaSuccess) fprintf(stderr, "[fb] kernel launched at %s:%d failed: %s\n", file, line, cudaGetErrorString(err));
+  }
+}
 }  // namespace fb
 
 namespace {

@@ -148,8 +148,10 @@ FB_DEV void dmma_8x8x4(double& c0, double& c1, double a, double b) {
 // ---------------------------------------------------------------- launch accounting
 // Every kernel launch in the library goes through FB_LAUNCHED() so fb_launch_count()
 // can report how many of our kernels ran (bench.py's gpu_launches).
-void count_launch();
-#define FB_LAUNCHED() ::fb::count_launch()
+// With FB_DEBUG_SYNC=1 in the environment every launch is followed by a device sync and
+// a failing kernel is reported with its source location (development aid).
+void count_launch(const char* file, int line);
+#define FB_LAUNCHED() ::fb::count_launch(__FILE__, __LINE__)
 
 // ---------------------------------------------------------------- launch geometry
 inline int grid_for(int64_t work_items, int per_cta, int ctas_per_sm, int num_sms) {

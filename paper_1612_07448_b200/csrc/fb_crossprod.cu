@@ -19,6 +19,8 @@
 // are summed in a fixed order by cp_reduce_kernel, which also writes the exact mirror
 // (lower = upperᵀ, rewrite.py:298 / kernel.py:132-135).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -430,6 +432,17 @@ static cudaError_t run_gram(GramJobs& J, GramArgs& a, StreamSet& ss, int tile_ro
   cudaError_t e =
       cudaFuncSetAttribute(cp_gram_kernel<kMaxSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
+  if (const char* dbg = getenv("FB_CP_DEBUG")) {  // development bisection switches
+    const int bits = atoi(dbg);
+    if (bits & 1) a.seg = 0;
+    if (bits & 2) ss.bulk_full = ss.bulk_last = false;
+    if (bits & 4)
+      for (int gI = 0; gI < kMaxJobGroups; ++gI) J.njobs[gI] = 0;
+  }
+  if (getenv("FB_DEBUG_SYNC"))
+    fprintf(stderr, "[fb] gram pass n=%lld tile_rows=%d stages=%d grid=%dx%d split=%d seg=%d bulk=%d/%d gidx=%d\n",
+            (long long)a.n, tile_rows, stages, gdim.x, gdim.y, J.row_split, a.seg, (int)ss.bulk_full,
+            (int)ss.bulk_last, ss.gidx != nullptr);
   cp_gram_kernel<kMaxSlots><<<gdim, kRingThreads, smem, st>>>(J, a, ss, stages, tile_rows);
   FB_LAUNCHED();
   return cudaGetLastError();

@@ -22,8 +22,8 @@
 // A stream may ask for a padded shared-memory pitch (bytes per row > row bytes): the
 // producer then issues one bulk copy per row, so tensor-core fragment loads that walk
 // rows hit distinct banks. Stream 0 may instead be gathered by a global row index array
-// (gidx: rows in FK-sorted order for the crossprod); the producer moves those rows with
-// 16-byte cp.async and all its lanes arrive on "full" (expected count 1 + 32).
+// (gidx: rows in FK-sorted order for the crossprod); the gatherer moves those rows with
+// 16-byte cp.async too, once the stage is free (its "full" phase for the other streams).
 //
 // Tiles that cannot use bulk copies (a misaligned base, or a final tile whose byte
 // count is not a multiple of 16) are filled by the consumers with plain loads; the
@@ -174,10 +174,10 @@ struct TileRing {
     stage = 0;
     phase = 0;
     rstage = 0;
-    gathers = s.ngather > 0;
+    gathers = s.ngather > 0 || s.gidx != nullptr;
     if (threadIdx.x == 0) {
       for (int i = 0; i < stages; ++i) {
-        mbar_init(&full[i], s.gidx ? 33 : 1);
+        mbar_init(&full[i], 1);
         mbar_init(&empty[i], kConsumerWarps);
         mbar_init(&gfull[i], 32);
       }
@@ -193,7 +193,7 @@ struct TileRing {
       return true;
     }
     if (is_gather_warp()) {
-      if (s.ngather > 0) gather(s);
+      if (s.ngather > 0 || s.gidx) gather(s);
       return true;
     }
     return false;
@@ -210,60 +210,32 @@ struct TileRing {
     }
   }
 
-  // Producer warp body: issue every tile of this CTA's range, recycling stages.
+  // Producer warp body: issue every tile of this CTA's range, recycling stages. A gidx
+  // stream 0 is left to the gatherer.
   FB_DEV void produce(const StreamSet& s) const {
     const int lane = threadIdx.x & 31;
     int st = 0;
     uint32_t ph = 0;
     const int64_t n = count();
-    int32_t gcur[4] = {0, 0, 0, 0}, gnext[4] = {0, 0, 0, 0};
-    if (s.gidx && n > 0) load_gidx(s, tile_begin, gnext);
     for (int64_t k = 0; k < n; ++k) {
       const int64_t tile = tile_begin + k;
-      if (s.gidx) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) gcur[i] = gnext[i];
-        if (k + 1 < n) load_gidx(s, tile + 1, gnext);  // latency overlaps this tile's issue
-      }
       if (k >= stages) mbar_wait(&empty[st], ph ^ 1u);
       const int rows = rows_of(tile);
       if (bulk_ok(s, tile)) {
         if (lane == 0) {
-          uint32_t tx = s.tile_tx;
-          if (rows != tile_rows) {
-            tx = 0;
+          uint32_t tx = 0;
 #pragma unroll
-            for (int i = 0; i < kMaxStreams; ++i)
-              if (i < s.count) tx += s.row_bytes[i] * static_cast<uint32_t>(rows);
-          }
-          if (s.gidx) tx -= s.row_bytes[0] * static_cast<uint32_t>(rows);  // cp.async, not tx-counted
+          for (int i = 0; i < kMaxStreams; ++i)
+            if (i < s.count && !(i == 0 && s.gidx)) tx += s.row_bytes[i] * static_cast<uint32_t>(rows);
           mbar_arrive_expect_tx(&full[st], tx);
         }
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < kMaxStreams; ++i) {
-          if (i >= s.count || s.row_bytes[i] == 0) continue;
+          if (i >= s.count || s.row_bytes[i] == 0 || (i == 0 && s.gidx)) continue;
           const char* src = s.base[i] + static_cast<size_t>(tile) * tile_rows * s.row_bytes[i];
           char* dst = stage_ptr(st, s, i);
-          if (i == 0 && s.gidx) {
-            // rows of the gathered stream: (row, 16-byte chunk) items spread over the lanes
-            const uint32_t nch = s.row_bytes[0] >> 4;
-            const uint32_t items = nch * static_cast<uint32_t>(rows);
-            for (uint32_t base = 0; base < items; base += 32) {  // warp-uniform trip count
-              const uint32_t it = base + lane;
-              const uint32_t r = (it < items ? it : 0) / nch, c = it - r * nch;
-              // source row of ring row r lives in lane r % 32, slot r / 32
-              int32_t srow = 0;
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int32_t v = __shfl_sync(0xffffffffu, gcur[j], r & 31);
-                if (static_cast<int>(r >> 5) == j) srow = v;
-              }
-              if (it < items)
-                cp_async16(dst + r * s.pitch[0] + 16u * c,
-                           s.base[0] + static_cast<size_t>(srow) * s.row_bytes[0] + 16u * c, policy);
-            }
-          } else if (s.pitch[i] == s.row_bytes[i]) {
+          if (s.pitch[i] == s.row_bytes[i]) {
             if (lane == 0)
               bulk_g2s_stream(dst, src, s.row_bytes[i] * static_cast<uint32_t>(rows), &full[st], policy);
           } else {
@@ -275,7 +247,6 @@ struct TileRing {
       } else if (lane == 0) {
         mbar_arrive(&full[st]);
       }
-      if (s.gidx) cp_async_arrive_noinc(&full[st]);  // all 32 lanes, after their copies
       if (++st == stages) {
         st = 0;
         ph ^= 1u;
@@ -291,11 +262,37 @@ struct TileRing {
     int st = 0;
     uint32_t ph = 0;
     const int64_t n = count();
+    int32_t gcur[4] = {0, 0, 0, 0}, gnext[4] = {0, 0, 0, 0};
+    if (s.gidx && n > 0) load_gidx(s, tile_begin, gnext);
     for (int64_t k = 0; k < n; ++k) {
       const int64_t tile = tile_begin + k;
       const int rows = rows_of(tile);
-      mbar_wait(&full[st], ph);
+      if (s.gidx) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) gcur[i] = gnext[i];
+        if (k + 1 < n) load_gidx(s, tile + 1, gnext);  // latency overlaps this stage's wait
+      }
+      mbar_wait(&full[st], ph);  // the stage is free again and its keys have landed
       const bool keys_in_smem = bulk_ok(s, tile);
+      if (s.gidx && keys_in_smem) {
+        // stream 0 rows in gidx order: (row, 16-byte chunk) items spread over the lanes
+        char* dst = stage_ptr(st, s, 0);
+        const uint32_t nch = s.row_bytes[0] >> 4;
+        const uint32_t items = nch * static_cast<uint32_t>(rows);
+        for (uint32_t base = 0; base < items; base += 32) {  // warp-uniform trip count
+          const uint32_t it = base + lane;
+          const uint32_t r = (it < items ? it : 0) / nch, c = it - r * nch;
+          int32_t srow = 0;  // source row of ring row r: lane r % 32, slot r / 32
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int32_t v = __shfl_sync(0xffffffffu, gcur[j], r & 31);
+            if (static_cast<int>(r >> 5) == j) srow = v;
+          }
+          if (it < items)
+            cp_async16(dst + r * s.pitch[0] + 16u * c, s.base[0] + static_cast<size_t>(srow) * s.row_bytes[0] + 16u * c,
+                       policy);
+        }
+      }
       for (int g = 0; g < s.ngather; ++g) {
         const int ks = s.gkey[g];
         const int32_t* keys = reinterpret_cast<const int32_t*>(stage_ptr(st, s, ks));
