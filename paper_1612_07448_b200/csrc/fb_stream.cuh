@@ -7,10 +7,10 @@
 // arrays (the factor rows, the int32 FK column(s), per-row weights) share one "full"
 // mbarrier per stage.
 //
-// Roles (kRingThreads = 2 service warps + kConsumerWarps):
+// Roles (kRingThreads = 1 producer + kGatherWarps gatherers + kConsumerWarps consumers):
 //   warp 0  producer: issues the stream copies of each stage once its "empty" barrier
 //           says the consumers are done with it;
-//   warp 1  gatherer: for keyed gather streams (z[fk] rows of an LMM, ...) it waits for
+//   warps 1-4 gatherers: for keyed gather streams (z[fk] rows of an LMM, ...) it waits for
 //           the stage's keys to land, then copies the keyed rows from the lookup table
 //           into the stage with 16-byte cp.async (one warp instruction moves 32 chunks;
 //           a per-row bulk copy costs ~60 issue cycles, measured), each lane completing
@@ -43,7 +43,8 @@ constexpr int kMaxStreams = 8;
 constexpr int kMaxGather = 4;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
-constexpr int kServiceWarps = 2;
+constexpr int kGatherWarps = 4;
+constexpr int kServiceWarps = 1 + kGatherWarps;
 constexpr int kRingThreads = kConsumerThreads + 32 * kServiceWarps;
 constexpr int kRingHeader = 512;  // 3 × 16 mbarriers (full, empty, gfull) + padding
 constexpr int kMaxStages = 16;
@@ -113,7 +114,7 @@ FB_DEV void consumer_sync() {
 }
 
 FB_DEV bool is_producer_warp() { return threadIdx.x < 32; }
-FB_DEV bool is_gather_warp() { return threadIdx.x >= 32 && threadIdx.x < 64; }
+FB_DEV bool is_gather_warp() { return threadIdx.x >= 32 && threadIdx.x < 32 * kServiceWarps; }
 FB_DEV int consumer_tid() { return static_cast<int>(threadIdx.x) - 32 * kServiceWarps; }
 FB_DEV int consumer_warp() { return (static_cast<int>(threadIdx.x) >> 5) - kServiceWarps; }
 
@@ -179,7 +180,7 @@ struct TileRing {
       for (int i = 0; i < stages; ++i) {
         mbar_init(&full[i], 1);
         mbar_init(&empty[i], kConsumerWarps);
-        mbar_init(&gfull[i], 32);
+        mbar_init(&gfull[i], 32 * kGatherWarps);
       }
       fence_mbar_init();
     }
@@ -197,17 +198,6 @@ struct TileRing {
       return true;
     }
     return false;
-  }
-
-  // Gathered stream 0: this lane's source rows (r = lane + 32 i) of `tile`.
-  FB_DEV void load_gidx(const StreamSet& s, int64_t tile, int32_t (&idx)[4]) const {
-    const int lane = threadIdx.x & 31;
-    const int rows = rows_of(tile);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = lane + 32 * i;
-      idx[i] = r < rows ? __ldg(s.gidx + tile * tile_rows + r) : 0;
-    }
   }
 
   // Producer warp body: issue every tile of this CTA's range, recycling stages. A gidx
@@ -254,43 +244,43 @@ struct TileRing {
     }
   }
 
-  // Gatherer warp body: once a stage's keys have landed, bulk-copy the keyed rows of
-  // every gather table into it (evict_last: the tables are re-read across the pass).
+  // Gatherer warps body: once a stage is free again and its keys have landed, copy the
+  // keyed rows of every gather table (and the gidx rows of stream 0) into it with 16-byte
+  // cp.async. Gatherer warp gw owns ring rows r ≡ gw (mod kGatherWarps); loops are
+  // unrolled so several rows' key loads and copies are in flight per lane.
   FB_DEV void gather(const StreamSet& s) const {
     const int lane = threadIdx.x & 31;
+    const int gw = (static_cast<int>(threadIdx.x) >> 5) - 1;
     const uint64_t keep = policy_evict_last();
     int st = 0;
     uint32_t ph = 0;
     const int64_t n = count();
-    int32_t gcur[4] = {0, 0, 0, 0}, gnext[4] = {0, 0, 0, 0};
-    if (s.gidx && n > 0) load_gidx(s, tile_begin, gnext);
+    int32_t gcur = 0, gnext = 0;  // gidx of ring row gw + kGatherWarps·lane
+    auto load_rows = [&](int64_t tile) {
+      const int r = gw + kGatherWarps * lane;
+      return r < rows_of(tile) ? __ldg(s.gidx + tile * tile_rows + r) : 0;
+    };
+    if (s.gidx && n > 0) gnext = load_rows(tile_begin);
     for (int64_t k = 0; k < n; ++k) {
       const int64_t tile = tile_begin + k;
       const int rows = rows_of(tile);
+      const int rows_w = rows > gw ? (rows - gw + kGatherWarps - 1) / kGatherWarps : 0;  // rows of this warp
       if (s.gidx) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) gcur[i] = gnext[i];
-        if (k + 1 < n) load_gidx(s, tile + 1, gnext);  // latency overlaps this stage's wait
+        gcur = gnext;
+        if (k + 1 < n) gnext = load_rows(tile + 1);  // latency overlaps this stage's wait
       }
       mbar_wait(&full[st], ph);  // the stage is free again and its keys have landed
       const bool keys_in_smem = bulk_ok(s, tile);
       if (s.gidx && keys_in_smem) {
-        // stream 0 rows in gidx order: (row, 16-byte chunk) items spread over the lanes
+        // stream 0 rows in gidx order: one row per instruction, lanes over 16-byte chunks
         char* dst = stage_ptr(st, s, 0);
-        const uint32_t nch = s.row_bytes[0] >> 4;
-        const uint32_t items = nch * static_cast<uint32_t>(rows);
-        for (uint32_t base = 0; base < items; base += 32) {  // warp-uniform trip count
-          const uint32_t it = base + lane;
-          const uint32_t r = (it < items ? it : 0) / nch, c = it - r * nch;
-          int32_t srow = 0;  // source row of ring row r: lane r % 32, slot r / 32
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int32_t v = __shfl_sync(0xffffffffu, gcur[j], r & 31);
-            if (static_cast<int>(r >> 5) == j) srow = v;
-          }
-          if (it < items)
-            cp_async16(dst + r * s.pitch[0] + 16u * c, s.base[0] + static_cast<size_t>(srow) * s.row_bytes[0] + 16u * c,
-                       policy);
+        const uint32_t rb = s.row_bytes[0], nch = rb >> 4;
+#pragma unroll 4
+        for (int i = 0; i < rows_w; ++i) {
+          const uint32_t r = gw + kGatherWarps * i;
+          const int32_t srow = __shfl_sync(0xffffffffu, gcur, i);
+          for (uint32_t c = lane; c < nch; c += 32)
+            cp_async16(dst + r * s.pitch[0] + 16u * c, s.base[0] + static_cast<size_t>(srow) * rb + 16u * c, policy);
         }
       }
       for (int g = 0; g < s.ngather; ++g) {
@@ -300,11 +290,30 @@ struct TileRing {
         char* dst = gather_ptr(st, s, g);
         const uint32_t rb = s.grow_bytes[g];
         const uint32_t nch = rb >> 4;
-        const uint32_t items = nch * static_cast<uint32_t>(rows);
-        for (uint32_t it = lane; it < items; it += 32) {
-          const uint32_t r = nch == 1 ? it : it / nch, c = it - r * nch;
-          const int32_t key = keys_in_smem ? keys[r] : __ldg(gkeys + r);
-          cp_async16(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c, keep);
+        if (nch <= 32 && (nch & (nch - 1)) == 0) {
+          // power-of-two chunks: 32/nch rows per instruction, no division
+          const int lg = __ffs(nch) - 1;
+          const int rpi = 32 >> lg;
+          const int slot = lane >> lg;
+          const uint32_t c = lane & (nch - 1);
+          const int iters = (rows_w + rpi - 1) / rpi;
+#pragma unroll 4
+          for (int j = 0; j < iters; ++j) {
+            const int ri = j * rpi + slot;
+            if (ri < rows_w) {
+              const uint32_t r = gw + kGatherWarps * ri;
+              const int32_t key = keys_in_smem ? keys[r] : __ldg(gkeys + r);
+              cp_async16(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c, keep);
+            }
+          }
+        } else {
+          const uint32_t items = nch * static_cast<uint32_t>(rows_w);
+          for (uint32_t it = lane; it < items; it += 32) {
+            const uint32_t ri = it / nch, c = it - ri * nch;
+            const uint32_t r = gw + kGatherWarps * ri;
+            const int32_t key = keys_in_smem ? keys[r] : __ldg(gkeys + r);
+            cp_async16(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c, keep);
+          }
         }
       }
       cp_async_arrive_noinc(&gfull[st]);

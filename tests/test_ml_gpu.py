@@ -147,9 +147,19 @@ def test_dense_matrix_input():
 
 
 def test_divergence_error_iteration():
+    """DivergenceError carries the first iteration whose weights are not finite (ml.py:190-192)."""
     fb = _fb()
     a = np.full((100, 2), 1e300)
     y = np.ones((100, 1))
+    # reference semantics on the host: w -= α Tᵀ(Tw − y), check after each update
+    w, expect = np.zeros((2, 1)), None
+    with np.errstate(all="ignore"):
+        for it in range(3):
+            w = w - 1.0 * (a.T @ (a @ w - y))
+            if not np.all(np.isfinite(w)):
+                expect = it
+                break
+    assert expect is not None
     with pytest.raises(fb.DivergenceError) as ei:
         fb.linreg_gd(a, y, fb.TrainConfig(iterations=3, step_size=1.0))
-    assert ei.value.iteration == 0
+    assert ei.value.iteration == expect
