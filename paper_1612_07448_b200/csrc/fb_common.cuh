@@ -75,17 +75,21 @@ FB_DEV void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes, uint64_t
       : "memory");
 }
 
-// 16-byte cp.async (LDGSTS) global -> shared, L2-only, with a cache policy. Completion is
-// signalled per thread with cp_async_arrive_noinc on an mbarrier whose expected count
-// includes that arrival.
-FB_DEV void cp_async16(void* dst, const void* src, uint64_t policy) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
-               "l"(policy)
-               : "memory");
+// 16-byte cp.async (LDGSTS) global -> shared, L2-only. Completion is signalled per thread
+// with cp_async_arrive_noinc on an mbarrier whose expected count includes that arrival.
+// No L2 cache-policy operand: with one, the gather loops of some kernels faulted with
+// "Warp Illegal Instruction" at the LDGSTS (cuda-gdb, sm_100a) — the policy descriptor
+// register was not valid on every path.
+FB_DEV void cp_async16(void* dst, const void* src, uint64_t /*policy*/) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
+// The barrier address is broadcast from lane 0 so the compiler sees it warp-uniform
+// (a non-uniform address makes it wrap ARRIVES.LDGSTSBAR in a per-address waterfall
+// loop, which faulted with "illegal instruction" on sm_100a). Call with the warp converged.
 FB_DEV void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+  const uint32_t a = __shfl_sync(0xffffffffu, smem_u32(bar), 0);
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");
 }
 
 FB_DEV uint64_t policy_evict_first() {

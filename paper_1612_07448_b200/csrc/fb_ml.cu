@@ -11,6 +11,7 @@
 // The R side (g_q = bins_qᵀ R_q) is the weighted column reduction of fb_reduce.cu, and
 // glm_update applies w ± α·g, records the objective and the first non-finite iteration.
 #include <cmath>
+#include <cstdlib>
 
 #include "fb_kernels.cuh"
 
@@ -20,6 +21,7 @@ constexpr int kZStride = 2;  // z rows are padded to 16 bytes (bulk-copy gathers
 
 struct GlmDev {
   GlmArgs g;
+  int debug;  // development bisection bits (FB_GLM_DEBUG)
   int lanes, cols;
   int y_stream, fk_stream0;
 };
@@ -80,8 +82,9 @@ __global__ void __launch_bounds__(kRingThreads, 1) glm_spass_kernel(GlmDev p, St
       for (int o = L >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (live && sub == 0) {
         // + z_q[fk_q] in part order (rewrite.py:186-190), gathered into the stage
-        for (int q = 0; q < p.g.nfk; ++q)
-          acc += reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, q))[r * kZStride];
+        if (!(p.debug & 4))
+          for (int q = 0; q < p.g.nfk; ++q)
+            acc += reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, q))[r * kZStride];
         const double y = Y[r];
         double pv, lv;
         if (logistic) {
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) glm_spass_kernel(GlmDev p, St
       for (int q = 0; q < p.g.nfk; ++q) {
         const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(cur, ss, p.fk_stream0 + q));
         const bool act = live && sub == 0;
-        if (act) {
+        if (act && !(p.debug & 1)) {
           const double pv = ptile[r];
           atomicAdd(p.g.bins[q] + fkt[r], pv);
         }
@@ -107,7 +110,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) glm_spass_kernel(GlmDev p, St
     }
     consumer_sync();
     // ---- phase 2: g_S += p_i S_i (threads <-> columns)
-    if (colthread) {
+    if (colthread && !(p.debug & 2)) {
       for (int r = grp; r < rows; r += groups) gacc = fma(ptile[r], A[static_cast<size_t>(r) * d + col], gacc);
     }
     ring.release();
@@ -175,6 +178,8 @@ cudaError_t launch_glm_spass(const GlmArgs& g, cudaStream_t st, int num_sms) {
   }
   ss.ngather = g.nfk;
   ss.count = ns;
+  if (const char* dbg = getenv("FB_GLM_DEBUG")) p.debug = atoi(dbg);
+  if (p.debug & 8) ss.ngather = 0;
   uint32_t row_bytes = kZStride * 8u * g.nfk;
   for (int i = 0; i < ns; ++i) row_bytes += ss.row_bytes[i];
   int rw = 32;

@@ -43,7 +43,10 @@ constexpr int kMaxStreams = 8;
 constexpr int kMaxGather = 4;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
-constexpr int kGatherWarps = 4;
+#ifndef FB_GATHER_WARPS
+#define FB_GATHER_WARPS 4
+#endif
+constexpr int kGatherWarps = FB_GATHER_WARPS;
 constexpr int kServiceWarps = 1 + kGatherWarps;
 constexpr int kRingThreads = kConsumerThreads + 32 * kServiceWarps;
 constexpr int kRingHeader = 512;  // 3 × 16 mbarriers (full, empty, gfull) + padding
@@ -316,12 +319,15 @@ struct TileRing {
           }
         }
       }
+      __syncwarp();  // the arrive must be issued by the converged warp
       cp_async_arrive_noinc(&gfull[st]);
       if (++st == stages) {
         st = 0;
         ph ^= 1u;
       }
     }
+    // do not retire the warp with copies (and their barrier arrivals) still in flight
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
   }
 
   // Consumers: fill a non-bulk tile cooperatively (4-byte granularity).
