@@ -250,16 +250,16 @@ static cudaError_t launch_ring(K kern, const LmmArgs& p, StreamSet& ss, size_t f
   return cudaGetLastError();
 }
 
+// The ring carries the factor rows; the FK columns are read by the gatherer warps only
+// (keys straight from global memory), which copy z[fk] rows into the stage.
 static void fill_streams(const LmmArgs& p, StreamSet& ss, int pitch) {
   ss = StreamSet{};
-  ss.count = 1 + p.nfk;
+  ss.count = 1;
   ss.base[0] = reinterpret_cast<const char*>(p.a);
   ss.row_bytes[0] = static_cast<uint32_t>(p.d) * 8u;
   ss.pitch[0] = static_cast<uint32_t>(pitch) * 8u;
   for (int q = 0; q < p.nfk; ++q) {
-    ss.base[1 + q] = reinterpret_cast<const char*>(p.fk[q]);
-    ss.row_bytes[1 + q] = 4u;
-    ss.gkey[q] = 1 + q;
+    ss.gkeys[q] = p.fk[q];
     ss.gbase[q] = reinterpret_cast<const char*>(p.z[q]);
     ss.grow_bytes[q] = static_cast<uint32_t>(p.zstride) * 8u;
   }
@@ -274,7 +274,7 @@ static cudaError_t launch_rowdot(LmmArgs p, cudaStream_t st, int num_sms) {
   p.lanes = L;
   p.cols = p.d / L;
   p.pitch = p.d;
-  const uint32_t row_bytes = static_cast<uint32_t>(p.d) * 8u + (4u + 8u * p.zstride) * p.nfk;
+  const uint32_t row_bytes = static_cast<uint32_t>(p.d) * 8u + 8u * p.zstride * p.nfk;
   // rows per warp per tile: 32, fewer for wide rows (stage <= ~44 KB)
   int rw = 32;
   while (rw > 4 && static_cast<size_t>(row_bytes) * rw * kConsumerWarps > 48 * 1024) rw >>= 1;
@@ -298,7 +298,7 @@ static cudaError_t launch_dmma_cfg(LmmArgs p, cudaStream_t st, int num_sms) {
 template <int NT>
 static cudaError_t launch_dmma(const LmmArgs& p, cudaStream_t st, int num_sms) {
   const int pitch = (p.d % 2 == 0) ? conflict_free_pitch(p.d) : p.d;
-  const size_t row_bytes = static_cast<size_t>(pitch) * 8 + (4 + 8 * static_cast<size_t>(p.zstride)) * p.nfk;
+  const size_t row_bytes = static_cast<size_t>(pitch) * 8 + 8 * static_cast<size_t>(p.zstride) * p.nfk;
   // stage <= ~48 KB
   if (row_bytes * 256 <= 48 * 1024) return launch_dmma_cfg<NT, 4>(p, st, num_sms);
   if (row_bytes * 128 <= 48 * 1024) return launch_dmma_cfg<NT, 2>(p, st, num_sms);

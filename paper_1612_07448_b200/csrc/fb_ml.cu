@@ -170,7 +170,7 @@ cudaError_t launch_glm_spass(const GlmArgs& g, cudaStream_t st, int num_sms) {
   ss.row_bytes[ns++] = 8u;
   p.fk_stream0 = ns;
   for (int q = 0; q < g.nfk; ++q) {
-    ss.gkey[q] = ns;
+    ss.gkeys[q] = g.fk[q];
     ss.gbase[q] = reinterpret_cast<const char*>(g.z[q]);
     ss.grow_bytes[q] = kZStride * 8u;
     ss.base[ns] = reinterpret_cast<const char*>(g.fk[q]);

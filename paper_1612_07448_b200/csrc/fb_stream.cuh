@@ -64,10 +64,11 @@ struct StreamSet {
   bool bulk_last;        // the final (possibly partial) tile can use bulk copies
   const int32_t* gidx;   // optional: stream 0 row r of the ring is source row gidx[r]
                          // (a gathered stream, e.g. rows in FK-sorted order); <= 128 rows/tile
-  // keyed gathers: row r of gather g = gbase[g] + key * grow_bytes[g], key = int32 row r
-  // of regular stream gkey[g]; grow_bytes a multiple of 16, gbase 16-byte aligned
+  // keyed gathers: row r of gather g = gbase[g] + key * grow_bytes[g], key = gkeys[g][row]
+  // (int32, row-aligned with the ring's rows); grow_bytes a multiple of 16, gbase 16-byte
+  // aligned; tiles of at most 256 rows
   int ngather;
-  int gkey[kMaxGather];
+  const int32_t* gkeys[kMaxGather];
   const char* gbase[kMaxGather];
   uint32_t grow_bytes[kMaxGather];
   uint32_t gsmem_off[kMaxGather];
@@ -247,49 +248,62 @@ struct TileRing {
     }
   }
 
-  // Gatherer warps body: once a stage is free again and its keys have landed, copy the
-  // keyed rows of every gather table (and the gidx rows of stream 0) into it with 16-byte
-  // cp.async. Gatherer warp gw owns ring rows r ≡ gw (mod kGatherWarps); loops are
-  // unrolled so several rows' key loads and copies are in flight per lane.
+  // Gatherer warps body. A stage's gathers start as soon as the stage is free (its
+  // "empty" phase), in parallel with the producer's stream copies: the keys come from
+  // global memory, loaded one tile ahead, so a gathered tile costs max(stream, key +
+  // gather) latency rather than their sum. Gatherer warp gw owns ring rows
+  // r ≡ gw (mod kGatherWarps) (<= 64 of them: tiles of at most 256 rows).
   FB_DEV void gather(const StreamSet& s) const {
     const int lane = threadIdx.x & 31;
     const int gw = (static_cast<int>(threadIdx.x) >> 5) - 1;
-    const uint64_t keep = policy_evict_last();
     int st = 0;
     uint32_t ph = 0;
     const int64_t n = count();
-    int32_t gcur = 0, gnext = 0;  // gidx of ring row gw + kGatherWarps·lane
-    auto load_rows = [&](int64_t tile) {
-      const int r = gw + kGatherWarps * lane;
-      return r < rows_of(tile) ? __ldg(s.gidx + tile * tile_rows + r) : 0;
+    // keys / gidx of this warp's rows gw + kGatherWarps·(lane + 32 j), j < 2
+    int32_t kc[kMaxGather + 1][2], kn[kMaxGather + 1][2];
+    auto load_keys = [&](int64_t tile) {
+      const int rows = rows_of(tile);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int r = gw + kGatherWarps * (lane + 32 * j);
+        const bool live = r < rows;
+#pragma unroll
+        for (int g = 0; g < kMaxGather; ++g)
+          kn[g][j] = (g < s.ngather && live) ? __ldg(s.gkeys[g] + tile * tile_rows + r) : 0;
+        kn[kMaxGather][j] = (s.gidx && live) ? __ldg(s.gidx + tile * tile_rows + r) : 0;
+      }
     };
-    if (s.gidx && n > 0) gnext = load_rows(tile_begin);
+    // key of this warp's row index ri (warp-uniform call; ri may differ per lane)
+    auto key_of = [&](int g, int ri) {
+      const int v0 = __shfl_sync(0xffffffffu, kc[g][0], ri & 31);
+      const int v1 = __shfl_sync(0xffffffffu, kc[g][1], ri & 31);
+      return ri < 32 ? v0 : v1;
+    };
+    if (n > 0) load_keys(tile_begin);
     for (int64_t k = 0; k < n; ++k) {
       const int64_t tile = tile_begin + k;
       const int rows = rows_of(tile);
       const int rows_w = rows > gw ? (rows - gw + kGatherWarps - 1) / kGatherWarps : 0;  // rows of this warp
-      if (s.gidx) {
-        gcur = gnext;
-        if (k + 1 < n) gnext = load_rows(tile + 1);  // latency overlaps this stage's wait
+#pragma unroll
+      for (int g = 0; g <= kMaxGather; ++g) {
+        kc[g][0] = kn[g][0];
+        kc[g][1] = kn[g][1];
       }
-      mbar_wait(&full[st], ph);  // the stage is free again and its keys have landed
-      const bool keys_in_smem = bulk_ok(s, tile);
-      if (s.gidx && keys_in_smem) {
+      if (k + 1 < n) load_keys(tile + 1);  // latency overlaps this stage's wait and copies
+      if (k >= stages) mbar_wait(&empty[st], ph ^ 1u);  // the stage is free again
+      if (s.gidx && bulk_ok(s, tile)) {
         // stream 0 rows in gidx order: one row per instruction, lanes over 16-byte chunks
         char* dst = stage_ptr(st, s, 0);
         const uint32_t rb = s.row_bytes[0], nch = rb >> 4;
 #pragma unroll 4
         for (int i = 0; i < rows_w; ++i) {
           const uint32_t r = gw + kGatherWarps * i;
-          const int32_t srow = __shfl_sync(0xffffffffu, gcur, i);
+          const int32_t srow = key_of(kMaxGather, i);
           for (uint32_t c = lane; c < nch; c += 32)
-            cp_async16(dst + r * s.pitch[0] + 16u * c, s.base[0] + static_cast<size_t>(srow) * rb + 16u * c, policy);
+            cp_async16(dst + r * s.pitch[0] + 16u * c, s.base[0] + static_cast<size_t>(srow) * rb + 16u * c, 0);
         }
       }
       for (int g = 0; g < s.ngather; ++g) {
-        const int ks = s.gkey[g];
-        const int32_t* keys = reinterpret_cast<const int32_t*>(stage_ptr(st, s, ks));
-        const int32_t* gkeys = reinterpret_cast<const int32_t*>(s.base[ks]) + tile * tile_rows;
         char* dst = gather_ptr(st, s, g);
         const uint32_t rb = s.grow_bytes[g];
         const uint32_t nch = rb >> 4;
@@ -303,19 +317,18 @@ struct TileRing {
 #pragma unroll 4
           for (int j = 0; j < iters; ++j) {
             const int ri = j * rpi + slot;
+            const int32_t key = key_of(g, ri);
             if (ri < rows_w) {
               const uint32_t r = gw + kGatherWarps * ri;
-              const int32_t key = keys_in_smem ? keys[r] : __ldg(gkeys + r);
-              cp_async16(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c, keep);
+              cp_async16(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c, 0);
             }
           }
         } else {
-          const uint32_t items = nch * static_cast<uint32_t>(rows_w);
-          for (uint32_t it = lane; it < items; it += 32) {
-            const uint32_t ri = it / nch, c = it - ri * nch;
+          for (int ri = 0; ri < rows_w; ++ri) {
+            const int32_t key = key_of(g, ri);
             const uint32_t r = gw + kGatherWarps * ri;
-            const int32_t key = keys_in_smem ? keys[r] : __ldg(gkeys + r);
-            cp_async16(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c, keep);
+            for (uint32_t c = lane; c < nch; c += 32)
+              cp_async16(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c, 0);
           }
         }
       }
