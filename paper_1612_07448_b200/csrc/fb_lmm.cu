@@ -44,9 +44,11 @@ struct LmmArgs {
 };
 
 // ------------------------------------------------------------------ rowdot (d_x <= 4)
-template <int NX>
+// IT = rows each lane group handles per tile; their dot products run interleaved (IT
+// independent FMA chains and shuffle trees) so the per-tile latency is one chain, not IT.
+template <int NX, int IT>
 __global__ void __launch_bounds__(kRingThreads, 1) lmm_rowdot_kernel(LmmArgs p, StreamSet ss, int stages,
-                                                                  int tile_rows) {
+                                                                     int tile_rows) {
   extern __shared__ __align__(128) char smem[];
   const int d = p.d;
   double* xs = reinterpret_cast<double*>(smem);  // X slice, d × NX row-major
@@ -65,9 +67,11 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_rowdot_kernel(LmmArgs p, 
   const int wrow = warp * rw;
   const int L = p.lanes, C = p.cols;
   const int rpi = 32 / L;                     // rows per instruction
-  const int iters = (rw + rpi - 1) / rpi;
   const int sub = lane % L, rsub = lane / L;
+  const int src = (lane % rpi) * L;           // lane k takes row k: iteration k / rpi, group k % rpi
+  const int myit = lane / rpi;
   const uint64_t pol = p.nfk == 0 ? policy_evict_last() : policy_evict_first();  // z stays in L2
+  const double* xc = xs + sub * NX;
 
   for (int64_t kt = 0; kt < ring.count(); ++kt) {
     const int cur = ring.acquire(ss, kt);
@@ -76,36 +80,44 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_rowdot_kernel(LmmArgs p, 
     const int64_t r0 = tile * tile_rows;
     const double* A = reinterpret_cast<const double*>(ring.stage_ptr(cur, ss, 0));
 
+    double acc[IT][NX];
+    const double* arow[IT];
+    bool live[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int rl = it * rpi + rsub;  // row within the warp's share
+      live[it] = rl < rw && wrow + rl < rows;
+      arow[it] = A + static_cast<size_t>(live[it] ? wrow + rl : 0) * p.pitch + sub;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) acc[it][j] = 0.0;
+    }
+#pragma unroll 2
+    for (int m = 0; m < C; ++m) {
+      double xv[NX];
+#pragma unroll
+      for (int j = 0; j < NX; ++j) xv[j] = xc[m * L * NX + j];
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const double a = arow[it][m * L];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) acc[it][j] = fma(a, xv[j], acc[it][j]);
+      }
+    }
+    for (int o = L >> 1; o > 0; o >>= 1)
+#pragma unroll
+      for (int it = 0; it < IT; ++it)
+#pragma unroll
+        for (int j = 0; j < NX; ++j) acc[it][j] += __shfl_xor_sync(0xffffffffu, acc[it][j], o);
     double res[NX];
 #pragma unroll
     for (int j = 0; j < NX; ++j) res[j] = 0.0;
-    for (int it = 0; it < iters; ++it) {
-      const int rl = it * rpi + rsub;  // row within the warp's share
-      const bool live = rl < rw && wrow + rl < rows;
-      double acc[NX];
 #pragma unroll
-      for (int j = 0; j < NX; ++j) acc[j] = 0.0;
-      if (live) {
-        const double* arow = A + static_cast<size_t>(wrow + rl) * p.pitch + sub;
-        const double* xc = xs + sub * NX;
-#pragma unroll 5
-        for (int m = 0; m < C; ++m) {
-          const double a = arow[m * L];
-#pragma unroll
-          for (int j = 0; j < NX; ++j) acc[j] = fma(a, xc[m * L * NX + j], acc[j]);
-        }
-      }
-      for (int o = L >> 1; o > 0; o >>= 1)
-#pragma unroll
-        for (int j = 0; j < NX; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-      // lane k of the warp takes row k: produced in iteration k / rpi by lane group k % rpi
-      const int src = (lane % rpi) * L;
+    for (int it = 0; it < IT; ++it)
 #pragma unroll
       for (int j = 0; j < NX; ++j) {
-        const double v = __shfl_sync(0xffffffffu, acc[j], src);
-        if (lane / rpi == it) res[j] = v;
+        const double v = __shfl_sync(0xffffffffu, acc[it][j], src);
+        if (myit == it) res[j] = v;
       }
-    }
     const int r = wrow + lane;
     if (lane < rw && r < rows) {
       // + z_0[fk_0] + z_1[fk_1] ... in part order (rewrite.py:186-190), gathered into smem
@@ -281,7 +293,11 @@ static cudaError_t launch_rowdot(LmmArgs p, cudaStream_t st, int num_sms) {
   StreamSet ss;
   fill_streams(p, ss, p.d);
   const size_t fixed = (static_cast<size_t>(p.d > 0 ? p.d : 1) * NX * 8 + 127) & ~size_t(127);
-  return launch_ring(lmm_rowdot_kernel<NX>, p, ss, fixed, rw * kConsumerWarps, st, num_sms);
+  const int it = (rw * L + 31) / 32;  // rows per lane group per tile
+  if (it <= 1) return launch_ring(lmm_rowdot_kernel<NX, 1>, p, ss, fixed, rw * kConsumerWarps, st, num_sms);
+  if (it <= 2) return launch_ring(lmm_rowdot_kernel<NX, 2>, p, ss, fixed, rw * kConsumerWarps, st, num_sms);
+  if (it <= 4) return launch_ring(lmm_rowdot_kernel<NX, 4>, p, ss, fixed, rw * kConsumerWarps, st, num_sms);
+  return launch_ring(lmm_rowdot_kernel<NX, 8>, p, ss, fixed, rw * kConsumerWarps, st, num_sms);
 }
 
 template <int NT, int MT>

@@ -303,7 +303,9 @@ struct TileRing {
             cp_async16(dst + r * s.pitch[0] + 16u * c, s.base[0] + static_cast<size_t>(srow) * rb + 16u * c, 0);
         }
       }
-      for (int g = 0; g < s.ngather; ++g) {
+#pragma unroll
+      for (int g = 0; g < kMaxGather; ++g) {  // unrolled: kc[g] stays in registers
+        if (g >= s.ngather) break;
         char* dst = gather_ptr(st, s, g);
         const uint32_t rb = s.grow_bytes[g];
         const uint32_t nch = rb >> 4;
