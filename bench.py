@@ -309,6 +309,9 @@ def run_gpu(args, rank, world, local_rank):
         gbs, sec, sample, threads, ms = cpu_suite(frac=args.cpu_frac, reps=1)
         cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample,
                "ops_ms": ms}
+    extras = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras = run_extras(dev, cpu=not args.no_cpu)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -331,8 +334,143 @@ def run_gpu(args, rank, world, local_rank):
             "cpu_baseline": cpu,
             "gpu_launches": launches,
             "clocks": clocks,
+            "extras": extras,
         }
         print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- secondary workloads
+def _events_ms(fn, reps, stream=None):
+    import torch
+
+    st = stream or torch.cuda.current_stream()
+    ts = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn()
+        b.record(st)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def dgemm_peak_tflops():
+    """cuBLAS DGEMM 8192³ (best of 5) — the FP64 tensor roofline denominator for crossprod."""
+    import torch
+
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        torch.mm(a, b)
+    torch.cuda.synchronize()
+    best = min(_events_ms(lambda: torch.mm(a, b), 1) for _ in range(5))
+    del a, b
+    return 2 * n**3 / (best * 1e-3) / 1e12
+
+
+def zipf_keys_dev(n, n_r, s, gen, dev):
+    import torch
+
+    p = torch.arange(1, n_r + 1, dtype=torch.float64, device=dev) ** (-s)
+    cdf = torch.cumsum(p / p.sum(), 0)
+    u = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
+    return torch.clamp(torch.searchsorted(cdf, u, right=True), max=n_r - 1) + 1
+
+
+def run_extras(dev, cpu=True):
+    """c3 crossprod + LinReg normal, c1 LogReg iter/s, c4 K-Means, c5 GNMF (BASELINE.json configs)."""
+    import torch
+
+    import paper_1612_07448_b200 as fb
+
+    out = {}
+    g = torch.Generator(device=dev).manual_seed(7)
+    peak_fp64 = dgemm_peak_tflops()
+    out["fp64_dgemm_peak_tflops"] = round(peak_fp64, 2)
+    # ---- c3: crossprod + linreg_normal (S 10M×60, R 500k×120 U[0,1))
+    n_s, d_s, n_r, d_r = 10_000_000, 60, 500_000, 120
+    s = torch.rand(n_s, d_s, dtype=torch.float64, device=dev, generator=g)
+    r = torch.rand(n_r, d_r, dtype=torch.float64, device=dev, generator=g)
+    key = torch.randint(1, n_r + 1, (n_s,), device=dev, generator=g)
+    nm = fb.build_pkfk(s, key, r)
+    del key
+    from paper_1612_07448_b200.crossprod_impl import fk_sorted_order
+
+    fk_sorted_order(nm.k)  # one-time cache (the reference caches _csr_t the same way)
+    flops = 2 * (0.5 * n_s * d_s * d_s + 0.5 * n_r * d_r * d_r + d_s * d_r * n_r)  # costmodel.py:85-88
+    nbytes = 8 * (n_s * d_s + n_r * d_r) + 4 * n_s + 8 * (d_s + d_r) ** 2
+    for _ in range(2):
+        fb.crossprod(nm)
+    ms = _events_ms(lambda: fb.crossprod(nm), 5)
+    out["c3_crossprod"] = {"ms": round(ms, 3), "TFLOPs": round(flops / ms / 1e9, 2),
+                           "frac_fp64_peak": round(flops / ms / 1e9 / peak_fp64, 3),
+                           "GBps": round(nbytes / ms / 1e6, 1), "algorithmic_gflop": round(flops / 1e9, 2)}
+    w = torch.randn(d_s + d_r, 1, dtype=torch.float64, device=dev, generator=g)
+    y = fb.lmm(nm, w) + 0.01 * torch.randn(n_s, 1, dtype=torch.float64, device=dev, generator=g)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = fb.linreg_normal(nm, y)
+    out["c3_linreg_normal"] = {"s": round(time.perf_counter() - t0, 4), "objective": res.objective[0],
+                               "note": "noise N(0, 0.01^2) (σ = 0.01)"}
+    del nm, s, r, y
+    torch.cuda.empty_cache()
+    # ---- c1: LogReg GD, 20 iterations (S 100k×20, R 10k×40 N(0,1)), step 1e-3
+    n_s, d_s, n_r, d_r = 100_000, 20, 10_000, 40
+    rng = np.random.default_rng(1)
+    s1 = rng.standard_normal((n_s, d_s))
+    r1 = rng.standard_normal((n_r, d_r))
+    k1 = rng.integers(1, n_r + 1, size=n_s)
+    nm = fb.build_pkfk(torch.from_numpy(s1).to(dev), torch.from_numpy(k1).to(dev), torch.from_numpy(r1).to(dev))
+    wt = rng.standard_normal((d_s + d_r, 1))
+    y1 = torch.from_numpy(np.where(fb.lmm(nm, torch.from_numpy(wt).to(dev)).cpu().numpy() >= 0, 1.0, -1.0)).to(dev)
+    cfg = fb.TrainConfig(iterations=20, step_size=1e-3)
+    fb.logistic_gd(nm, y1, cfg)
+    walls = [fb.logistic_gd(nm, y1, cfg).wall_time_s for _ in range(5)]
+    out["c1_logreg"] = {"iter_per_s": round(20 / float(np.median(walls)), 1), "ms_per_iter": round(1e3 * float(np.median(walls)) / 20, 4),
+                        "timing": "wall clock over 20 iterations incl. the final device->host read"}
+    if cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import factorla_oracle as O
+        from threadpoolctl import threadpool_limits
+
+        with threadpool_limits(_cpu_threads()):
+            ref = O.build_pkfk(s1, k1, r1)
+            y1h = y1.cpu().numpy()
+            O.logistic_gd(ref, y1h, 2, 1e-3)
+            t0 = time.perf_counter()
+            O.logistic_gd(ref, y1h, 20, 1e-3)
+            out["c1_logreg"]["cpu_iter_per_s"] = round(20 / (time.perf_counter() - t0), 1)
+            out["c1_logreg"]["cpu_cores"] = _cpu_threads()
+    # ---- c4: K-Means k=10, 20 iterations, star schema (S 10M×20, R1 1M×40, R2 100k×60)
+    n_s = 10_000_000
+    s = torch.randn(n_s, 20, dtype=torch.float64, device=dev, generator=g)
+    r1t = torch.randn(1_000_000, 40, dtype=torch.float64, device=dev, generator=g)
+    r2t = torch.randn(100_000, 60, dtype=torch.float64, device=dev, generator=g)
+    k1t = torch.randint(1, 1_000_001, (n_s,), device=dev, generator=g)
+    k2t = torch.randint(1, 100_001, (n_s,), device=dev, generator=g)
+    nm = fb.build_star(s, [(k1t, r1t), (k2t, r2t)])
+    del k1t, k2t
+    res = fb.kmeans(nm, fb.TrainConfig(iterations=20, k=10, rng_seed=0))
+    out["c4_kmeans"] = {"iter_per_s": round(20 / res.wall_time_s, 1), "s_total": round(res.wall_time_s, 4),
+                        "timing": "wall clock incl. seeding, rowSums(T²) and the final read"}
+    del nm, s, r1t, r2t
+    torch.cuda.empty_cache()
+    # ---- c5: GNMF r=5, 20 iterations, Zipf(1.2) FK (S 5M×10, R 50k×40 U[0,1))
+    n_s, n_r = 5_000_000, 50_000
+    s = torch.rand(n_s, 10, dtype=torch.float64, device=dev, generator=g)
+    r = torch.rand(n_r, 40, dtype=torch.float64, device=dev, generator=g)
+    key = zipf_keys_dev(n_s, n_r, 1.2, g, dev)
+    nm = fb.build_pkfk(s, key, r)
+    res = fb.gnmf(nm, fb.TrainConfig(iterations=20, r=5, rng_seed=0))
+    out["c5_gnmf"] = {"iter_per_s": round(20 / res.wall_time_s, 1), "s_total": round(res.wall_time_s, 4),
+                      "kept_r_rows": int(nm.r.shape[0]),
+                      "timing": "wall clock incl. host RNG init of W (5M×5) and its upload"}
+    del nm, s, r, key
+    torch.cuda.empty_cache()
+    return out
 
 
 def _host_allreduce(t, world, dev):
@@ -365,6 +503,7 @@ def main():
     ap.add_argument("--cpu-frac", type=float, default=0.25)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--small", action="store_true", help="1/20 of c2 (development only)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the c1/c3/c4/c5 secondary workloads")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
