@@ -156,12 +156,32 @@ int fb_kmeans_step(const fb_normalized* nm, const double* d_t, double* c, double
                    double* trace, int32_t* assign, unsigned long long* nan_row, void* ws, size_t ws_bytes,
                    fb_stream_t stream);
 
+/* The two halves of fb_kmeans_step, for row-sharded data: the partial writes this shard's
+ * TᵀA (d × k row-major) and integer cluster sizes (k) and its objective into trace[it];
+ * after summing those over the shards, fb_kmeans_update moves the centroids (empty
+ * clusters keep theirs) and refreshes cc. */
+int fb_kmeans_partial(const fb_normalized* nm, const double* d_t, const double* c, const double* cc, int32_t k,
+                      int32_t it, double* trace, int32_t* assign, unsigned long long* nan_row, double* tta,
+                      int32_t* sizes, void* ws, size_t ws_bytes, fb_stream_t stream);
+int fb_kmeans_update(double* c, const double* tta, const int32_t* sizes, int64_t d, int32_t k, double* cc,
+                     fb_stream_t stream);
+
 /* One GNMF multiplicative-update iteration (ml.py:306-315), r <= 16: w (n_s × r), h (d × r),
  * ttw = Tᵀw (d × r, in: for the current w, out: for the updated w), cpw = wᵀw (r × r,
  * in/out), sum_t2 = Σ T² (device scalar), trace[it] = Frobenius objective. */
 size_t fb_gnmf_workspace_bytes(const fb_normalized* nm, int32_t r);
 int fb_gnmf_step(const fb_normalized* nm, double* w, double* h, double* ttw, double* cpw, const double* sum_t2,
                  int32_t r, int32_t it, double* trace, void* ws, size_t ws_bytes, fb_stream_t stream);
+
+/* GLM update on its own (after an all-reduce of g and loss over the shards). */
+int fb_glm_update(double* w, const double* g, int64_t d, double alpha, const double* loss, double* trace, int32_t it,
+                  int32_t* diverged, fb_stream_t stream);
+/* GNMF building blocks (ml.py:306-315): f = f ∘ num / (f·g + 1e-12) for a rows × r factor
+ * and r × r g; g = fᵀf with an exact mirror; the Frobenius objective into trace[it]. */
+int fb_nmf_update(double* f, const double* num, const double* g, int64_t rows, int32_t r, fb_stream_t stream);
+int fb_small_gram(const double* f, int64_t rows, int32_t r, double* g, fb_stream_t stream);
+int fb_nmf_objective(const double* sum_t2, const double* ttw, const double* h, int64_t dr, const double* cpw,
+                     const double* cph, int32_t rr, double* trace, int32_t it, fb_stream_t stream);
 
 /* a[r, c] = a[c, r] for r > c: exact symmetry from the upper triangle of a d × d matrix
  * (kernel._mirror_upper, kernel.py:132-135). */

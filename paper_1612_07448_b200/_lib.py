@@ -84,6 +84,12 @@ _SIGS = {
     "fb_kmeans_step": (c_i32, [_P, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "fb_gnmf_workspace_bytes": (c_size, [_P, c_i32]),
     "fb_gnmf_step": (c_i32, [_P, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_size, c_vp]),
+    "fb_kmeans_partial": (c_i32, [_P, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "fb_kmeans_update": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "fb_glm_update": (c_i32, [c_vp, c_vp, c_i64, c_f64, c_vp, c_vp, c_i32, c_vp, c_vp]),
+    "fb_nmf_update": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
+    "fb_small_gram": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "fb_nmf_objective": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp]),
     "fb_mirror_upper": (c_i32, [c_vp, c_i64, c_vp]),
     "fb_scalar_map": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_f64, c_vp]),
     "fb_unary_map": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp]),

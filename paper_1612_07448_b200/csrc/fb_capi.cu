@@ -551,9 +551,41 @@ size_t fb_kmeans_workspace_bytes(const fb_normalized* nm, int32_t k) {
   return b + fb_lmm_workspace_bytes(nm, k) + 256;
 }
 
+static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const double* c, const double* cc,
+                               int32_t k, int32_t it, double* trace, int32_t* assign, unsigned long long* nan_row,
+                               double* tta_out, int32_t* sizes_out, void* ws, size_t ws_bytes, fb_stream_t stream);
+
 int fb_kmeans_step(const fb_normalized* nm, const double* d_t, double* c, double* cc, int32_t k, int32_t it,
                    double* trace, int32_t* assign, unsigned long long* nan_row, void* ws, size_t ws_bytes,
                    fb_stream_t stream) {
+  int st = kmeans_partial_impl(nm, d_t, c, cc, k, it, trace, assign, nan_row, nullptr, nullptr, ws, ws_bytes, stream);
+  if (st) return st;
+  // the partial left TᵀA and the sizes at the head of the workspace
+  const int64_t d = total_cols(nm);
+  Carver cv{static_cast<char*>(ws), ws_bytes};
+  cv.take<double>(static_cast<size_t>(d) * k);
+  cv.take<double>(static_cast<size_t>(nm->n_s) * k);
+  double* tta = cv.take<double>(static_cast<size_t>(d) * k);
+  int32_t* sizes = cv.take<int32_t>(k);
+  return cuda_status(fb::launch_kmeans_update(c, tta, sizes, static_cast<int>(d), k, cc, cs(stream)), "kmeans(update)");
+}
+
+int fb_kmeans_partial(const fb_normalized* nm, const double* d_t, const double* c, const double* cc, int32_t k,
+                      int32_t it, double* trace, int32_t* assign, unsigned long long* nan_row, double* tta,
+                      int32_t* sizes, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  if (!tta || !sizes) return fail(FB_ERR_ARG, "kmeans_partial: NULL output");
+  return kmeans_partial_impl(nm, d_t, c, cc, k, it, trace, assign, nan_row, tta, sizes, ws, ws_bytes, stream);
+}
+
+int fb_kmeans_update(double* c, const double* tta, const int32_t* sizes, int64_t d, int32_t k, double* cc,
+                     fb_stream_t stream) {
+  if (!c || !tta || !sizes || !cc || d < 1 || k < 1) return fail(FB_ERR_ARG, "kmeans_update: bad argument");
+  return cuda_status(fb::launch_kmeans_update(c, tta, sizes, static_cast<int>(d), k, cc, cs(stream)), "kmeans(update)");
+}
+
+static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const double* c, const double* cc,
+                               int32_t k, int32_t it, double* trace, int32_t* assign, unsigned long long* nan_row,
+                               double* tta_out, int32_t* sizes_out, void* ws, size_t ws_bytes, fb_stream_t stream) {
   int st = check_nm(nm);
   if (st) return st;
   if (k < 1 || k > 16) return fail(FB_ERR_ARG, "kmeans: k=%d outside [1, 16]", k);
@@ -567,6 +599,8 @@ int fb_kmeans_step(const fb_normalized* nm, const double* d_t, double* c, double
   double* tc = cv.take<double>(static_cast<size_t>(nm->n_s) * k);
   double* tta = cv.take<double>(static_cast<size_t>(d) * k);
   int32_t* sizes = cv.take<int32_t>(k);
+  if (tta_out) tta = tta_out;
+  if (sizes_out) sizes = sizes_out;
   double* apart = cv.take<double>(static_cast<size_t>(g_num_sms) * 8);
   double* opart = cv.take<double>(fb::onehot_partials_doubles(nm->d_s > 0 ? nm->d_s : 1, k, g_num_sms));
   double* cpart = cv.take<double>(fb::colreduce_workspace_doubles(0, static_cast<int>(max_width(nm)), k, g_num_sms));
@@ -620,7 +654,7 @@ int fb_kmeans_step(const fb_normalized* nm, const double* d_t, double* c, double
     if (e != cudaSuccess) return cuda_status(e, "kmeans(R pass)");
     off += p.d_r;
   }
-  return cuda_status(fb::launch_kmeans_update(c, tta, sizes, static_cast<int>(d), k, cc, s), "kmeans(update)");
+  return FB_OK;
 }
 
 size_t fb_gnmf_workspace_bytes(const fb_normalized* nm, int32_t r) {
@@ -666,6 +700,30 @@ int fb_gnmf_step(const fb_normalized* nm, double* w, double* h, double* ttw, dou
   st = fb_crossprod(&wm, nullptr, nullptr, cpw, cv.p, cv.left, stream);
   if (st) return st;
   return cuda_status(fb::launch_nmf_objective(sum_t2, ttw, h, d * r, cpw, cph, r * r, trace, it, s), "gnmf(objective)");
+}
+
+int fb_glm_update(double* w, const double* g, int64_t d, double alpha, const double* loss, double* trace, int32_t it,
+                  int32_t* diverged, fb_stream_t stream) {
+  if (!w || !g || !loss || !trace || !diverged || d < 1) return fail(FB_ERR_ARG, "glm_update: bad argument");
+  return cuda_status(fb::launch_glm_update(w, g, static_cast<int>(d), alpha, loss, trace, it, diverged, cs(stream)),
+                     "glm(update)");
+}
+
+int fb_nmf_update(double* f, const double* num, const double* g, int64_t rows, int32_t r, fb_stream_t stream) {
+  if (!f || !num || !g || r < 1 || r > 32 || rows < 0) return fail(FB_ERR_ARG, "nmf_update: bad argument");
+  return cuda_status(fb::launch_nmf_update(f, num, g, rows, r, 1e-12, cs(stream), g_num_sms), "nmf_update");
+}
+
+int fb_small_gram(const double* f, int64_t rows, int32_t r, double* g, fb_stream_t stream) {
+  if (!f || !g || r < 1 || rows < 0) return fail(FB_ERR_ARG, "small_gram: bad argument");
+  return cuda_status(fb::launch_small_gram(f, rows, r, g, cs(stream)), "small_gram");
+}
+
+int fb_nmf_objective(const double* sum_t2, const double* ttw, const double* h, int64_t dr, const double* cpw,
+                     const double* cph, int32_t rr, double* trace, int32_t it, fb_stream_t stream) {
+  if (!sum_t2 || !ttw || !h || !cpw || !cph || !trace) return fail(FB_ERR_ARG, "nmf_objective: NULL pointer");
+  return cuda_status(fb::launch_nmf_objective(sum_t2, ttw, h, dr, cpw, cph, rr, trace, it, cs(stream)),
+                     "nmf_objective");
 }
 
 int fb_mirror_upper(double* a, int64_t d, fb_stream_t stream) {
