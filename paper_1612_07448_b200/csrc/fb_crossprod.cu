@@ -417,10 +417,12 @@ template <class Setup>
 static cudaError_t run_gram(GramJobs& J, GramArgs& a, StreamSet& ss, int tile_rows, cudaStream_t st, int num_sms,
                             Setup) {
   stream_layout(ss, tile_rows, a.n);
-  int stages = static_cast<int>((200 * 1024 - kRingHeader) / ss.stage_bytes);
+  int stages = static_cast<int>((200 * 1024 - kRingHeader - 256) / ss.stage_bytes);
   if (stages > 6) stages = 6;
   if (stages < 2) return cudaErrorNotSupported;
-  const size_t smem = kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes;
+  // + slack: fragment loads of the last 8-column block read up to 7 doubles past a row, so
+  // the last row of the last stage must not sit at the end of the allocation
+  const size_t smem = kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes + 256;
   int ngroups = 0;
   for (int gI = 0; gI < kMaxJobGroups; ++gI)
     if (J.njobs[gI] > 0) ngroups = gI + 1;

@@ -263,3 +263,14 @@ def test_crossprod_dense_and_transposed_errors():
     nm = fb.build_pkfk(a, rng.integers(1, 5, size=5000), rng.random((4, 2)))
     with pytest.raises(fb.ShapeError):
         fb.crossprod(nm.T)
+
+
+@pytest.mark.parametrize("n,d", [(300_001, 5), (70_000, 3), (1000, 1), (50_000, 17)])
+def test_crossprod_dense_narrow(n, d):
+    """q = 0 crossprod of narrow dense factors (GNMF's WᵀW): padded-column fragment reads stay in bounds."""
+    fb = _fb()
+    rng = np.random.default_rng(n + d)
+    a = rng.random((n, d))
+    cp = fb.crossprod(fb.as_normalized(torch.from_numpy(a).cuda()))
+    _close(cp, a.T @ a)
+    assert torch.equal(cp, cp.t())
