@@ -80,7 +80,7 @@ FB_DEV void seg_flush(const GramArgs& a, SegState& st, int col, int slot) {
   }
 }
 
-template <int BPW>
+template <int BPW, bool SCALE>
 __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_constant__ BlockJobs jobs, GramArgs a,
                                                                   StreamSet ss, int stages, int tile_rows) {
   extern __shared__ __align__(128) char smem[];
@@ -124,20 +124,15 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
     const double* cnt =
         a.cnt_stream >= 0 ? reinterpret_cast<const double*>(ring.stage_ptr(stage, ss, a.cnt_stream)) : nullptr;
     __syncwarp();  // mma.sync.aligned needs the whole warp converged (after the barrier spin)
-    for (int k0 = 4 * kidx; k0 < rows; k0 += 4 * ks) {
-      const int k = k0 + t;
-      const bool live = k < rows;
-      const int kr = live ? k : 0;
-      const double* r0 = R0 + kr * a.p0;
-      const double* r1 = R1 + kr * a.p1;
-      const double c = cnt ? cnt[kr] : 1.0;
+    // one k-step: rows k0..k0+3 (lane t takes row k0 + t)
+    auto kstep = [&](const double* r0, const double* r1, double c, bool live) {
 #pragma unroll
       for (int b = 0; b < BPW; ++b) {
         if (b < nbt) {
           double a_lo = r0[aoff[b]], a_hi = r0[aoff[b] + 8];
           const double* wr = reg1[b] ? r1 : r0;
           double w_lo = wr[woff[b]], w_hi = wr[woff[b] + 8];
-          if (!reg1[b]) {
+          if (SCALE && !reg1[b]) {
             w_lo *= c;
             w_hi *= c;
           }
@@ -147,6 +142,25 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
           dmma_8x8x4(acc[b][2][0], acc[b][2][1], a_hi, w_lo);
           dmma_8x8x4(acc[b][3][0], acc[b][3][1], a_hi, w_hi);
         }
+      }
+    };
+    if (nbt > 0) {
+      const int full = rows & ~3;  // k-steps whose four rows all exist
+      const int step0 = 4 * ks * a.p0, step1 = 4 * ks * a.p1;
+      const double* r0 = R0 + (4 * kidx + t) * a.p0;
+      const double* r1 = R1 + (4 * kidx + t) * a.p1;
+      const double* cp = SCALE ? cnt + 4 * kidx + t : nullptr;
+      int k0 = 4 * kidx;
+      for (; k0 < full; k0 += 4 * ks) {
+        kstep(r0, r1, SCALE ? *cp : 1.0, true);
+        r0 += step0;
+        r1 += step1;
+        if (SCALE) cp += 4 * ks;
+      }
+      if (k0 < rows) {  // ragged last k-step of the last tile
+        const bool live = k0 + t < rows;
+        const int kr = live ? k0 + t : 0;
+        kstep(R0 + kr * a.p0, R1 + kr * a.p1, SCALE ? cnt[kr] : 1.0, live);
       }
     }
     if (seg) {
@@ -279,7 +293,9 @@ __global__ void cp_reduce_kernel(ReduceArgs r) {
 namespace {
 
 // Upper-triangle block tiles of a T2a × T2a gram, plus a full T2a × T2b rectangle (region 1).
-bool build_block_jobs(int T2a, int T2b, BlockJobs& J) {
+// With `reserve_set0` the first set of warps (consumer warps 0..ks-1, which run the
+// segmented KᵀS walk in the S pass) gets no block tiles when that keeps the others <= kMaxBPW.
+bool build_block_jobs(int T2a, int T2b, BlockJobs& J, bool reserve_set0 = false) {
   std::vector<uint16_t> list;
   for (int bi = 0; bi < T2a; ++bi) {
     for (int bj = bi; bj < T2a; ++bj) list.push_back(static_cast<uint16_t>(bi | (bj << 6)));
@@ -298,11 +314,16 @@ bool build_block_jobs(int T2a, int T2b, BlockJobs& J) {
   // sets per group: the smallest power of two with sets · kMaxBPW >= per_group
   int sets = 1;
   while (sets * kMaxBPW < per_group) sets *= 2;
+  int first = 0;
+  if (reserve_set0 && J.ngroups == 1) {
+    while (sets < kConsumerWarps && (sets - 1) * kMaxBPW < per_group) sets *= 2;
+    if (sets > 1 && (sets - 1) * kMaxBPW >= per_group) first = 1;
+  }
   J.ks = kConsumerWarps / sets;
   for (int gi = 0; gi < J.ngroups; ++gi) {
     const int b0 = gi * per_group, b1 = std::min(bt, b0 + per_group);
     for (int b = b0; b < b1; ++b) {
-      const int set = (b - b0) % sets;
+      const int set = first + (b - b0) % (sets - first);
       for (int k = 0; k < J.ks; ++k) {  // every warp of the set carries the same tiles
         const int w = set * J.ks + k;
         J.bt[gi][w][J.nbt[gi][w]++] = list[b];
@@ -321,7 +342,7 @@ int gram_grid(int64_t n, int tile_rows, int ngroups, int num_sms) {
 }
 
 int gram_tile_rows(uint32_t row_bytes, int ks, bool gather) {
-  int rows = static_cast<int>((32u * 1024u) / (row_bytes > 0 ? row_bytes : 1));
+  int rows = static_cast<int>((48u * 1024u) / (row_bytes > 0 ? row_bytes : 1));
   const int unit = 4 * ks;
   if (rows > (gather ? 128 : 256)) rows = gather ? 128 : 256;
   rows = (rows / unit) * unit;
@@ -350,10 +371,10 @@ cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_ro
   cudaError_t e;
 #define FB_GRAM_CASE(B)                                                                                         \
   if (bpw <= B) {                                                                                               \
-    e = cudaFuncSetAttribute(cp_gram_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
-                             static_cast<int>(smem));                                                           \
+    auto kern = a.cnt_stream >= 0 ? cp_gram_kernel<B, true> : cp_gram_kernel<B, false>;                        \
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));        \
     if (e != cudaSuccess) return e;                                                                             \
-    cp_gram_kernel<B><<<gdim, kRingThreads, smem, st>>>(J, a, ss, stages, tile_rows);                           \
+    kern<<<gdim, kRingThreads, smem, st>>>(J, a, ss, stages, tile_rows);                                        \
     FB_LAUNCHED();                                                                                              \
     return cudaGetLastError();                                                                                  \
   }
@@ -446,7 +467,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
   // ---- S pass: SᵀS (+ KᵀS when q = 1)
   if (c.d_s > 0 && c.n_s > 0) {
     BlockJobs JS;
-    if (!build_block_jobs(t2s, 0, JS)) return cudaErrorNotSupported;
+    if (!build_block_jobs(t2s, 0, JS, q != 0)) return cudaErrorNotSupported;
     GramArgs a{};
     a.n = c.n_s;
     a.p0 = a.p1 = c.d_s;
