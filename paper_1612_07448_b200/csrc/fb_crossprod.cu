@@ -61,6 +61,7 @@ struct GramArgs {
   double* bins;         // n_R × d_S
   int* carry_key;       // [gridDim.x][2]
   double* carry_val;    // [gridDim.x][2][d_S]
+  int debug;            // development bisection bits (FB_CP_DEBUG): 1 no walk, 2 no DMMA
 };
 
 // Segmented column sums over FK-sorted rows (thread c < d_S owns column c).
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
   const int grp = blockIdx.y;
   const int ks = jobs.ks;
   const int kidx = warp % ks;
-  const int nbt = jobs.nbt[grp][warp];
+  const int nbt = (a.debug & 2) ? 0 : jobs.nbt[grp][warp];
   const int lane = lane_id();
   const int g = lane >> 2, t = lane & 3;
 
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
     for (int u = 0; u < 4; ++u) acc[b][u][0] = acc[b][u][1] = 0.0;
 
   const int tid = consumer_tid();
-  const bool seg = a.seg && grp == 0 && tid < a.seg_cols;
+  const bool seg = a.seg && grp == 0 && tid < a.seg_cols && !(a.debug & 1);
   SegState sst{-1, 0.0, true};
 
   for (int64_t kt = 0; kt < ring.count(); ++kt) {
@@ -360,6 +361,7 @@ cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_ro
   // + slack: fragment loads of a padded 16-column block read up to 15 doubles past a row,
   // so the last row of the last stage must not sit at the end of the allocation
   const size_t smem = kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes + 256;
+  if (const char* dbg = getenv("FB_CP_DEBUG")) a.debug = atoi(dbg);
   int bpw = 0;
   for (int gi = 0; gi < J.ngroups; ++gi)
     for (int w = 0; w < kConsumerWarps; ++w) bpw = std::max(bpw, static_cast<int>(J.nbt[gi][w]));
