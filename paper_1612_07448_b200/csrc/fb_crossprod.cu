@@ -61,16 +61,10 @@ struct GramArgs {
   double* bins;         // n_R × d_S
   int* carry_key;       // [gridDim.x][2]
   double* carry_val;    // [gridDim.x][2][d_S]
-  int seg_parts;        // row parts of the walk (seg_parts · seg_cols <= kConsumerThreads)
-  int debug;            // development bisection bits (FB_CP_DEBUG): 1 no walk, 2 no DMMA, 4 no gather
+  int debug;            // development bisection bits (FB_CP_DEBUG): 1 no walk, 2 no DMMA
 };
 
-// Segmented column sums over FK-sorted rows.
-constexpr int kMaxSegParts = 8;
-struct SegPart {
-  int first_key, last_key;  // -1: the part had no rows
-  bool single;              // the part holds one run only
-};
+// Segmented column sums over FK-sorted rows (thread c < d_S owns column c).
 struct SegState {
   int key;     // current run key (-1: none yet)
   double sum;
@@ -120,16 +114,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
     for (int u = 0; u < 4; ++u) acc[b][u][0] = acc[b][u][1] = 0.0;
 
   const int tid = consumer_tid();
-  // segmented walk layout: P row parts × seg_cols columns over the consumer threads
-  const bool seg_on = a.seg && grp == 0 && !(a.debug & 1);
-  const int P = a.seg_parts;
-  const int part = a.seg_cols > 0 ? tid / a.seg_cols : 0, col = a.seg_cols > 0 ? tid % a.seg_cols : 0;
-  const bool walker = seg_on && part < P;
-  const bool seg = walker && part == 0;  // owns the CTA's running run for column col
+  const bool seg = a.seg && grp == 0 && tid < a.seg_cols && !(a.debug & 1);
   SegState sst{-1, 0.0, true};
-  __shared__ SegPart seg_rec[2][kMaxSegParts];
-  __shared__ double seg_first[2][kConsumerThreads];  // [parity][part · seg_cols + col]
-  __shared__ double seg_last[2][kConsumerThreads];
 
   for (int64_t kt = 0; kt < ring.count(); ++kt) {
     const int stage = ring.acquire(ss, kt);
@@ -178,74 +164,23 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
         kstep(R0 + kr * a.p0, R1 + kr * a.p1, SCALE ? cnt[kr] : 1.0, live);
       }
     }
-    if (seg_on) {
-      // ---- segmented KᵀS, parallel over row parts: thread (part, col) walks rows
-      // [lo, hi) of the tile, stores the runs that start and end inside its part, and
-      // records its first / last run; after a consumer barrier the part-0 thread of each
-      // column chains the parts' boundary runs onto the CTA's running run (sst).
+    if (seg) {
       const double* S = R0;
       const int32_t* keys = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, 1));
       const int p = a.p0;
-      const int par = static_cast<int>(kt & 1);
-      if (walker) {
-        const int lo = part * rows / P, hi = (part + 1) * rows / P;
-        double fsum = 0.0, cur_sum = 0.0;
-        int cur = -1;
-        bool first_done = false;
-        if (lo < hi) {
-          cur = keys[lo];
-          cur_sum = S[lo * p + col];
-#pragma unroll 4
-          for (int r = lo + 1; r < hi; ++r) {
-            const int key = keys[r];
-            const double v = S[r * p + col];
-            if (key != cur) {
-              if (!first_done) {
-                fsum = cur_sum;
-                first_done = true;
-              } else {
-                a.bins[static_cast<int64_t>(cur) * a.seg_cols + col] = cur_sum;  // interior run: complete
-              }
-              for (int z = cur + 1; z < key; ++z) a.bins[static_cast<int64_t>(z) * a.seg_cols + col] = 0.0;
-              cur = key;
-              cur_sum = v;
-            } else {
-              cur_sum += v;
-            }
-          }
-        }
-        SegPart& rec = seg_rec[par][part];
-        seg_first[par][tid] = first_done ? fsum : cur_sum;
-        seg_last[par][tid] = cur_sum;
-        if (col == 0) {
-          rec.first_key = lo < hi ? keys[lo] : -1;
-          rec.last_key = cur;
-          rec.single = !first_done;
-        }
-      }
-      consumer_sync();
-      if (walker && part == 0) {
-        for (int q = 0; q < P; ++q) {
-          const SegPart& rec = seg_rec[par][q];
-          if (rec.first_key < 0) continue;  // empty part
-          const double f = seg_first[par][q * a.seg_cols + col];
-          if (rec.first_key == sst.key) {
-            sst.sum += f;
-          } else {
-            seg_flush(a, sst, col, 0);
-            if (sst.key >= 0) {
-              sst.first = false;
-              for (int z = sst.key + 1; z < rec.first_key; ++z) a.bins[static_cast<int64_t>(z) * a.seg_cols + col] = 0.0;
-            }
-            sst.key = rec.first_key;
-            sst.sum = f;
-          }
-          if (!rec.single) {  // the part's first run ended inside it; its last run is open
-            seg_flush(a, sst, col, 0);
+      for (int r = 0; r < rows; ++r) {
+        const int key = keys[r];
+        const double v = S[r * p + tid];
+        if (key != sst.key) {
+          seg_flush(a, sst, tid, 0);
+          if (sst.key >= 0) {
             sst.first = false;
-            sst.key = rec.last_key;
-            sst.sum = seg_last[par][q * a.seg_cols + col];
+            for (int z = sst.key + 1; z < key; ++z) a.bins[static_cast<int64_t>(z) * a.seg_cols + tid] = 0.0;
           }
+          sst.key = key;
+          sst.sum = v;
+        } else {
+          sst.sum += v;
         }
       }
     }
@@ -267,7 +202,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
     }
   }
   // this (CTA, k-split) partial: block tile b covers rows 16 bi + 8u + g, cols 16 bj + 8v + 2t
-  double* pout = a.partials + static_cast<size_t>(blockIdx.x * ks + kidx) * a.ra * a.cw;
+  double* part = a.partials + static_cast<size_t>(blockIdx.x * ks + kidx) * a.ra * a.cw;
 #pragma unroll
   for (int b = 0; b < BPW; ++b) {
     if (b < nbt) {
@@ -277,7 +212,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
       for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          double* dst = pout + static_cast<size_t>(row0 + 8 * u + g) * a.cw + col0 + 8 * v + 2 * t;
+          double* dst = part + static_cast<size_t>(row0 + 8 * u + g) * a.cw + col0 + 8 * v + 2 * t;
           dst[0] = acc[b][2 * u + v][0];
           dst[1] = acc[b][2 * u + v][1];
         }
@@ -427,10 +362,6 @@ cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_ro
   // so the last row of the last stage must not sit at the end of the allocation
   const size_t smem = kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes + 256;
   if (const char* dbg = getenv("FB_CP_DEBUG")) a.debug = atoi(dbg);
-  if ((a.debug & 4) && ss.gidx) {  // rows in storage order: isolates the gather's cost (wrong KᵀS)
-    ss.gidx = nullptr;
-    stream_layout(ss, tile_rows, a.n);
-  }
   int bpw = 0;
   for (int gi = 0; gi < J.ngroups; ++gi)
     for (int w = 0; w < kConsumerWarps; ++w) bpw = std::max(bpw, static_cast<int>(J.nbt[gi][w]));
@@ -559,8 +490,6 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
       ss.count = 2;
       a.seg = 1;
       a.seg_cols = c.d_s;
-      a.seg_parts = 1;
-      while (a.seg_parts * 2 <= kMaxSegParts && a.seg_parts * 2 * c.d_s <= kConsumerThreads) a.seg_parts *= 2;
       a.bins = bins;
       a.carry_key = ckey;
       a.carry_val = cval;
