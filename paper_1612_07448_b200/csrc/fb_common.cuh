@@ -44,18 +44,17 @@ FB_DEV void mbar_arrive(uint64_t* bar) {
       : "memory");
 }
 
-// try_wait with a suspend-time hint: the waiting warp sleeps until the phase completes (or
-// the hint expires) instead of re-issuing the probe, so idle producer/gatherer warps do not
-// steal issue slots from the consumers (ncu: spin BRA/NOP were ~40% of a gram pass's samples).
+// Plain try_wait spin. (A suspend-time hint compiles to NANOSLEEP.SYNCS with that bound;
+// with 1 ms it visibly delayed wake-ups in the LMM S pass, so waits use the default.)
 FB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "FB_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
       "@!P1 bra FB_WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(1000000u)
+      "r"(parity)
       : "memory");
 }
 

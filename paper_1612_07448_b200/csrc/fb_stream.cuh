@@ -309,18 +309,19 @@ struct TileRing {
         char* dst = gather_ptr(st, s, g);
         const uint32_t rb = s.grow_bytes[g];
         const uint32_t nch = rb >> 4;
-        if (nch <= 32 && (nch & (nch - 1)) == 0) {
-          // power-of-two chunks: 32/nch rows per instruction, no division
-          const int lg = __ffs(nch) - 1;
+        if (nch <= 32) {
+          // lanes per row: nch rounded up to a power of two; 32/that rows per instruction
+          int lg = 0;
+          while ((1u << lg) < nch) ++lg;
           const int rpi = 32 >> lg;
           const int slot = lane >> lg;
-          const uint32_t c = lane & (nch - 1);
+          const uint32_t c = lane & ((1u << lg) - 1);
           const int iters = (rows_w + rpi - 1) / rpi;
 #pragma unroll 4
           for (int j = 0; j < iters; ++j) {
             const int ri = j * rpi + slot;
             const int32_t key = key_of(g, ri);
-            if (ri < rows_w) {
+            if (ri < rows_w && c < nch) {
               const uint32_t r = gw + kGatherWarps * ri;
               cp_async16(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c, 0);
             }
