@@ -30,7 +30,7 @@ extern "C" {
 
 typedef struct CUstream_st* fb_stream_t; /* == cudaStream_t */
 
-#define FB_ABI_VERSION 1
+#define FB_ABI_VERSION 2
 #define FB_MAX_PARTS 4
 
 enum {
@@ -52,6 +52,12 @@ typedef struct fb_part {
   int32_t skewed;       /* hint: some target holds a large share of rows (scatter kernels then
                            combine equal keys within a warp before the atomic); 0 = uniform */
   const double* counts; /* optional cached colSums(K) as f64 (indicator.py:61-66); may be NULL */
+  /* optional hot-target tables for skewed FKs (scatter kernels privatise these bins per CTA):
+     hot_slot[n_r] = slot in [0, nhot) for the nhot most frequent targets, -1 otherwise;
+     hot_key[nhot] = the targets. nhot = 0 disables. */
+  const int16_t* hot_slot;
+  const int32_t* hot_key;
+  int32_t nhot;
 } fb_part;
 
 /* Untransposed PK-FK / star normalized matrix T = [S, K_1 R_1, ..., K_q R_q]. */

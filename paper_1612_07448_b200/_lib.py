@@ -36,6 +36,9 @@ class FbPart(ctypes.Structure):
         ("d_r", c_i32),
         ("skewed", c_i32),
         ("counts", c_vp),
+        ("hot_slot", c_vp),
+        ("hot_key", c_vp),
+        ("nhot", c_i32),
     ]
 
 

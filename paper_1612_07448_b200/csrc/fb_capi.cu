@@ -288,6 +288,11 @@ static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_
       c.bins[i] = bins[i];
       c.nbins[i] = nm->part[i].n_r;
       c.aggregate[i] = nm->part[i].skewed;
+      if (nm->part[i].nhot > 0 && nm->part[i].hot_slot && nm->part[i].hot_key) {
+        c.nhot[i] = nm->part[i].nhot < 64 ? nm->part[i].nhot : 64;
+        c.hot_slot[i] = nm->part[i].hot_slot;
+        c.hot_key[i] = nm->part[i].hot_key;
+      }
     }
     c.out = out + j0 * o_js;
     c.o_js = o_js;
@@ -712,7 +717,7 @@ int fb_glm_update(double* w, const double* g, int64_t d, double alpha, const dou
 }
 
 int fb_nmf_update(double* f, const double* num, const double* g, int64_t rows, int32_t r, fb_stream_t stream) {
-  if (!f || !num || !g || r < 1 || r > 32 || rows < 0) return fail(FB_ERR_ARG, "nmf_update: bad argument");
+  if (!f || !num || !g || r < 1 || r > 16 || rows < 0) return fail(FB_ERR_ARG, "nmf_update: bad argument");
   return cuda_status(fb::launch_nmf_update(f, num, g, rows, r, 1e-12, cs(stream), g_num_sms), "nmf_update");
 }
 

@@ -290,6 +290,54 @@ __global__ void cp_reduce_kernel(ReduceArgs r) {
   r.out[ocol * r.ldo + orow] = s;
 }
 
+// Small outputs (e.g. WᵀW with r = 5) over many partials: one CTA per element, a fixed
+// strided split over the partials and a fixed shared-memory tree (deterministic).
+__global__ void cp_reduce_small_kernel(ReduceArgs r) {
+  const int e = blockIdx.x;
+  const int n0 = r.da * r.da;
+  int i, j, pc, orow, ocol;
+  if (e < n0) {
+    i = e / r.da;
+    j = e % r.da;
+    if (i > j) return;
+    pc = j;
+    orow = r.off0 + i;
+    ocol = r.off0 + j;
+  } else {
+    const int f = e - n0;
+    i = f / r.db;
+    j = f % r.db;
+    pc = r.w1_col0 + j;
+    orow = r.off0 + i;
+    ocol = r.off1 + j;
+  }
+  const double* p = r.partials + static_cast<size_t>(i) * r.cw + pc;
+  const size_t stride = static_cast<size_t>(r.ra) * r.cw;
+  double s = 0.0;
+  for (int q = threadIdx.x; q < r.nparts; q += blockDim.x) s += p[q * stride];
+  __shared__ double red[256];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    r.out[orow * r.ldo + ocol] = red[0];
+    r.out[ocol * r.ldo + orow] = red[0];
+  }
+}
+
+static void launch_reduce(const ReduceArgs& r, cudaStream_t st) {
+  const int n = r.da * r.da + r.da * r.db;
+  if (n <= 2048 && r.nparts >= 64) {
+    cp_reduce_small_kernel<<<n, 256, 0, st>>>(r);
+  } else {
+    cp_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(r);
+  }
+  FB_LAUNCHED();
+}
+
 // ------------------------------------------------------------------ host side
 namespace {
 
@@ -504,9 +552,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
       FB_LAUNCHED();
     }
     ReduceArgs r{sp, nparts, a.ra, a.cw, a.w1_col0, c.d_s, 0, 0, 0, c.out, d};
-    const int n = c.d_s * c.d_s;
-    cp_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(r);
-    FB_LAUNCHED();
+    launch_reduce(r, st);
   } else if (q && c.d_s > 0) {
     e = cudaMemsetAsync(bins, 0, static_cast<size_t>(c.n_r) * c.d_s * 8, st);  // no rows: KᵀS = 0
     if (e != cudaSuccess) return e;
@@ -543,9 +589,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     e = run_gram(JR, a, ss, tr, st, num_sms, &nparts);
     if (e != cudaSuccess) return e;
     ReduceArgs r{rp, nparts, a.ra, a.cw, a.w1_col0, c.d_r, c.d_s, c.d_s, 0, c.out, d};
-    const int n = c.d_r * c.d_r + c.d_r * c.d_s;
-    cp_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(r);
-    FB_LAUNCHED();
+    launch_reduce(r, st);
   }
   return cudaGetLastError();
 }

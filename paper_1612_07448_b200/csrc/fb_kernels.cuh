@@ -27,6 +27,9 @@ struct ColReduce {
   double* bins[kMaxParts];         // n_R,q × nx row-major, zeroed by the launcher
   int64_t nbins[kMaxParts];
   int aggregate[kMaxParts];        // warp-aggregate equal keys (skewed FK)
+  const int16_t* hot_slot[kMaxParts];  // per target: slot of the hottest targets, -1 otherwise
+  const int32_t* hot_key[kMaxParts];   // slot -> target
+  int nhot[kMaxParts];                 // hot slots (0: none)
   double* out;                     // out(j, c) = out[j*o_js + c*o_cs]
   int64_t o_js, o_cs;
   double* partials;                // workspace: grid × nx × d

@@ -331,11 +331,21 @@ __global__ void onehot_colsum_kernel(const double* __restrict__ s, int64_t n, in
   const int groups = blockDim.x / d;
   const int col = tid % d, grp = tid / d;
   if (grp < groups) {
-    for (int64_t r = blockIdx.x * static_cast<int64_t>(groups) + grp; r < n;
-         r += static_cast<int64_t>(gridDim.x) * groups) {
-      const int a = assign[r];
-      accs[tid * ks + a] += s[r * d + col];
+    // 8 rows per batch: all loads issued before the shared-memory updates (ILP)
+    const int64_t step = static_cast<int64_t>(gridDim.x) * groups;
+    int64_t r = blockIdx.x * static_cast<int64_t>(groups) + grp;
+    for (; r + 7 * step < n; r += 8 * step) {
+      int a[8];
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a[u] = __ldg(assign + r + u * step);
+        v[u] = __ldg(s + (r + u * step) * d + col);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) accs[tid * ks + a[u]] += v[u];
     }
+    for (; r < n; r += step) accs[tid * ks + assign[r]] += s[r * d + col];
   }
   __syncthreads();
   // fold groups -> per-CTA partial [d][k]
@@ -406,29 +416,44 @@ cudaError_t launch_kmeans_update(double* c, const double* tta, const int32_t* si
 // ======================================================================== GNMF
 // (ml.py:288-317) Multiplicative updates with the 1e-12 guard, in the reference's
 // operation order: h = h*ttw / (h@cpw + eps); w = w*th / (w@cph + eps).
+template <int R>
 __global__ void nmf_update_kernel(double* __restrict__ f, const double* __restrict__ num, const double* __restrict__ g,
-                                  int64_t rows, int r, double eps) {
-  __shared__ double gs[32 * 32];
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) gs[e] = g[e];
+                                  int64_t rows, double eps) {
+  __shared__ double gs[R * R];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) gs[e] = g[e];
   __syncthreads();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    double fr[32];
-#pragma unroll 8
-    for (int s = 0; s < r; ++s) fr[s] = f[i * r + s];
-    for (int s = 0; s < r; ++s) {
+    double fr[R], nr[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      fr[s] = f[i * R + s];
+      nr[s] = num[i * R + s];
+    }
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
       double den = 0.0;
-      for (int t = 0; t < r; ++t) den = fma(fr[t], gs[t * r + s], den);
-      f[i * r + s] = fr[s] * num[i * r + s] / (den + eps);
+#pragma unroll
+      for (int t = 0; t < R; ++t) den = fma(fr[t], gs[t * R + s], den);
+      f[i * R + s] = fr[s] * nr[s] / (den + eps);
     }
   }
 }
 
 cudaError_t launch_nmf_update(double* f, const double* num, const double* g, int64_t rows, int r, double eps,
                               cudaStream_t st, int num_sms) {
-  if (r < 1 || r > 32) return cudaErrorNotSupported;
-  const int grid = grid_for(rows, 256, 4, num_sms);
-  nmf_update_kernel<<<grid, 256, 0, st>>>(f, num, g, rows, r, eps);
+  const int grid = grid_for(rows, 256, 8, num_sms);
+  switch (r) {
+#define FB_R_CASE(R)                                                     \
+  case R:                                                                \
+    nmf_update_kernel<R><<<grid, 256, 0, st>>>(f, num, g, rows, eps);   \
+    break;
+    FB_R_CASE(1) FB_R_CASE(2) FB_R_CASE(3) FB_R_CASE(4) FB_R_CASE(5) FB_R_CASE(6) FB_R_CASE(7) FB_R_CASE(8)
+    FB_R_CASE(9) FB_R_CASE(10) FB_R_CASE(11) FB_R_CASE(12) FB_R_CASE(13) FB_R_CASE(14) FB_R_CASE(15) FB_R_CASE(16)
+#undef FB_R_CASE
+    default:
+      return cudaErrorNotSupported;
+  }
   FB_LAUNCHED();
   return cudaGetLastError();
 }

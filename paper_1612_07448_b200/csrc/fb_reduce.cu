@@ -79,14 +79,62 @@ FB_DEV void scatter_add(double* bins, int key, const double (&vals)[NX], bool ac
   }
 }
 
+// Skewed keys: the hottest targets of an indicator (IndicatorMatrix.hot_tables) get a
+// slot each; rows that hit a hot slot are combined within the warp (__match_any_sync on
+// the slot) and added by the group leader into the warp's private shared-memory bins (no
+// atomics, no cross-SM contention on one L2 line), flushed once per CTA; other keys RED
+// straight to global.
+template <int NX>
+FB_DEV void scatter_hot(double* bins, double* whot, int key, int slot, const double (&vals)[NX], bool active) {
+  const unsigned full = 0xffffffffu;
+  const int lane = lane_id();
+  const bool hot = active && slot >= 0;
+  if (active && !hot) {
+    double* b = bins + static_cast<int64_t>(key) * NX;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) atomicAdd(b + j, vals[j]);
+  }
+  if (!__any_sync(full, hot)) return;
+  const int k = hot ? slot : -1 - lane;  // non-hot lanes get keys no hot lane has
+  const unsigned peers = __match_any_sync(full, k);
+  const int leader = __ffs(peers) - 1;
+  double acc[NX];
+#pragma unroll
+  for (int j = 0; j < NX; ++j) acc[j] = vals[j];
+  unsigned rem = (hot && lane == leader) ? (peers & ~(1u << lane)) : 0u;
+  while (__any_sync(full, rem != 0)) {
+    const int src = rem ? (__ffs(rem) - 1) : lane;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      const double t = __shfl_sync(full, vals[j], src);
+      if (rem) acc[j] += t;
+    }
+    if (rem) rem &= rem - 1;
+  }
+  if (hot && lane == leader) {
+    double* b = whot + slot * NX;  // this warp's private bins: plain read-modify-write
+#pragma unroll
+    for (int j = 0; j < NX; ++j) b[j] += acc[j];
+  }
+  __syncwarp();
+}
+
 template <int NX>
 __global__ void __launch_bounds__(kRingThreads, 1) colreduce_kernel(ColRedDev p, StreamSet ss, int stages,
                                                                  int tile_rows) {
   extern __shared__ __align__(128) char smem[];
   const int d = p.c.d;
+  // warp-private hot bins after the ring: [warp][Σ_q nhot_q][NX]
+  double* hotbins = reinterpret_cast<double*>(smem + kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes);
+  int hot_off[kMaxParts + 1];
+  hot_off[0] = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxParts; ++q) hot_off[q + 1] = hot_off[q] + (q < p.c.nfk ? p.c.nhot[q] : 0) * NX;
+  const int hot_per_warp = hot_off[kMaxParts];
+  for (int i = threadIdx.x; i < hot_per_warp * kConsumerWarps; i += blockDim.x) hotbins[i] = 0.0;
   TileRing ring;
   ring.init(smem, stages, tile_rows, p.c.n);
-  ring.start(ss);
+  ring.start(ss);  // __syncthreads: hot bins zeroed
   if (ring.service(ss)) return;
   const int tid = consumer_tid();
   const int groups = d > 0 ? kConsumerThreads / d : 0;
@@ -120,12 +168,28 @@ __global__ void __launch_bounds__(kRingThreads, 1) colreduce_kernel(ColRedDev p,
         double v[NX];
 #pragma unroll
         for (int j = 0; j < NX; ++j) v[j] = live ? wval<NX>(p, ring, ss, stage, r0, r, j) : 0.0;
-        scatter_add<NX>(p.c.bins[q], live ? fkt[r] : 0, v, live, p.c.aggregate[q] != 0);
+        const int key = live ? fkt[r] : 0;
+        if (p.c.nhot[q] > 0) {
+          const int slot = live ? p.c.hot_slot[q][key] : -1;
+          scatter_hot<NX>(p.c.bins[q], hotbins + (tid >> 5) * hot_per_warp + hot_off[q], key, slot, v, live);
+        } else {
+          scatter_add<NX>(p.c.bins[q], key, v, live, p.c.aggregate[q] != 0);
+        }
       }
     }
     ring.release();
   }
 
+  // flush the hot bins: Σ over warps in warp order, one RED per (slot, column) per CTA
+  consumer_sync();
+  for (int i = tid; i < hot_per_warp; i += kConsumerThreads) {
+    int q = 0;
+    while (q + 1 < kMaxParts && i >= hot_off[q + 1]) ++q;
+    const int slot = (i - hot_off[q]) / NX, j = (i - hot_off[q]) % NX;
+    double s = 0.0;
+    for (int w = 0; w < kConsumerWarps; ++w) s += hotbins[w * hot_per_warp + i];
+    atomicAdd(p.c.bins[q] + static_cast<int64_t>(p.c.hot_key[q][slot]) * NX + j, s);
+  }
   // fold row groups: red[g][j][c] (the ring buffers are idle now)
   double* red = reinterpret_cast<double*>(ring.buf);
   consumer_sync();
@@ -216,6 +280,10 @@ static cudaError_t launch_colreduce_nx(const ColReduce& c, cudaStream_t st, int 
     smem = kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes;
   }
   if (smem < kRingHeader + red_bytes + 1024) smem = kRingHeader + red_bytes + 1024;
+  size_t hot = 0;
+  for (int q = 0; q < c.nfk; ++q) hot += static_cast<size_t>(c.nhot[q]) * NX;
+  const size_t ring_end = kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes;
+  if (smem < ring_end + hot * kConsumerWarps * 8) smem = ring_end + hot * kConsumerWarps * 8;
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   auto kern = colreduce_kernel<NX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -101,6 +101,27 @@ class IndicatorMatrix:
         """True when one target holds more than 1/256 of the rows (Zipf-like keys)."""
         return self.max_count * 256 > self.rows
 
+    def hot_tables(self, nhot=64):
+        """(hot_slot int16[cols], hot_key int32[k], k) for skewed targets, cached.
+
+        The k <= nhot most frequent targets holding more than 1/4096 of the rows each get a
+        slot; scatter kernels keep their bins in per-warp shared memory instead of hammering
+        one L2 line with atomics (Zipf keys: the top target holds ~20% of the rows).
+        """
+        if getattr(self, "_hot", None) is None:
+            if not self.skewed:
+                self._hot = (None, None, 0)
+            else:
+                cnt = self.counts_i32
+                k = min(nhot, self.cols)
+                vals, keys = torch.topk(cnt, k)
+                keep = vals.to(torch.int64) * 4096 > self.rows
+                keys = keys[keep].to(torch.int32).contiguous()
+                slot = torch.full((self.cols,), -1, dtype=torch.int16, device=cnt.device)
+                slot[keys.to(torch.int64)] = torch.arange(keys.numel(), dtype=torch.int16, device=cnt.device)
+                self._hot = (slot, keys, int(keys.numel()))
+        return self._hot
+
     def all_columns_used(self):
         return bool((self.counts_i32 > 0).all().item())
 
@@ -216,6 +237,8 @@ class NormalizedMatrix:
                 p.d_r = f.shape[1]
                 p.skewed = int(e.skewed)
                 p.counts = D.ptr(e.counts)
+                hs, hk, nh = e.hot_tables()
+                p.hot_slot, p.hot_key, p.nhot = D.ptr(hs), D.ptr(hk), nh
             self._cache["c_struct"] = st
         return ctypes.byref(st)
 
