@@ -89,6 +89,12 @@ FB_DEV void cp_async16(void* dst, const void* src, uint64_t /*policy*/) {
 // The barrier address is broadcast from lane 0 so the compiler sees it warp-uniform
 // (a non-uniform address makes it wrap ARRIVES.LDGSTSBAR in a per-address waterfall
 // loop, which faulted with "illegal instruction" on sm_100a). Call with the warp converged.
+// L1-allocating variant for lookup-table gathers: with skewed keys the hot rows are served
+// from L1 instead of hammering one L2 line from every SM.
+FB_DEV void cp_async16_ca(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
 FB_DEV void cp_async_arrive_noinc(uint64_t* bar) {
   const uint32_t a = __shfl_sync(0xffffffffu, smem_u32(bar), 0);
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");

@@ -323,7 +323,7 @@ struct TileRing {
             const int32_t key = key_of(g, ri);
             if (ri < rows_w && c < nch) {
               const uint32_t r = gw + kGatherWarps * ri;
-              cp_async16(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c, 0);
+              cp_async16_ca(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c);
             }
           }
         } else {
@@ -331,7 +331,7 @@ struct TileRing {
             const int32_t key = key_of(g, ri);
             const uint32_t r = gw + kGatherWarps * ri;
             for (uint32_t c = lane; c < nch; c += 32)
-              cp_async16(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c, 0);
+              cp_async16_ca(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c);
           }
         }
       }
