@@ -453,9 +453,12 @@ def run_extras(dev, cpu=True):
     k2t = torch.randint(1, 100_001, (n_s,), device=dev, generator=g)
     nm = fb.build_star(s, [(k1t, r1t), (k2t, r2t)])
     del k1t, k2t
+    res1 = fb.kmeans(nm, fb.TrainConfig(iterations=1, k=10, rng_seed=0))
     res = fb.kmeans(nm, fb.TrainConfig(iterations=20, k=10, rng_seed=0))
-    out["c4_kmeans"] = {"iter_per_s": round(20 / res.wall_time_s, 1), "s_total": round(res.wall_time_s, 4),
-                        "timing": "wall clock incl. seeding, rowSums(T²) and the final read"}
+    per = (res.wall_time_s - res1.wall_time_s) / 19
+    out["c4_kmeans"] = {"iter_per_s": round(1 / per, 1), "ms_per_iter": round(1e3 * per, 3),
+                        "s_total_20_iters": round(res.wall_time_s, 4),
+                        "timing": "per iteration = (wall(20 iters) - wall(1 iter)) / 19; total incl. seeding and rowSums(T²)"}
     del nm, s, r1t, r2t
     torch.cuda.empty_cache()
     # ---- c5: GNMF r=5, 20 iterations, Zipf(1.2) FK (S 5M×10, R 50k×40 U[0,1))
@@ -464,10 +467,13 @@ def run_extras(dev, cpu=True):
     r = torch.rand(n_r, 40, dtype=torch.float64, device=dev, generator=g)
     key = zipf_keys_dev(n_s, n_r, 1.2, g, dev)
     nm = fb.build_pkfk(s, key, r)
+    res1 = fb.gnmf(nm, fb.TrainConfig(iterations=1, r=5, rng_seed=0))
     res = fb.gnmf(nm, fb.TrainConfig(iterations=20, r=5, rng_seed=0))
-    out["c5_gnmf"] = {"iter_per_s": round(20 / res.wall_time_s, 1), "s_total": round(res.wall_time_s, 4),
-                      "kept_r_rows": int(nm.r.shape[0]),
-                      "timing": "wall clock incl. host RNG init of W (5M×5) and its upload"}
+    per = (res.wall_time_s - res1.wall_time_s) / 19
+    out["c5_gnmf"] = {"iter_per_s": round(1 / per, 1), "ms_per_iter": round(1e3 * per, 3),
+                      "s_total_20_iters": round(res.wall_time_s, 4), "kept_r_rows": int(nm.r.shape[0]),
+                      "timing": "per iteration = (wall(20 iters) - wall(1 iter)) / 19; total incl. the host "
+                                "RNG draw of W (5M×5, the reference's default_rng call) and its upload"}
     del nm, s, r, key
     torch.cuda.empty_cache()
     return out
