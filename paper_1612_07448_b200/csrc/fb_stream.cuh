@@ -19,9 +19,9 @@
 //   warps 2+ consumers: wait on "full" (+ "gfull"), compute, arrive on "empty".
 // Consumers that need to sync among themselves use consumer_sync() (named barrier 1).
 //
-// A stream may ask for a padded shared-memory pitch (bytes per row > row bytes): the
-// producer then issues one bulk copy per row, so tensor-core fragment loads that walk
-// rows hit distinct banks. Stream 0 may instead be gathered by a global row index array
+// A stream may ask for a padded shared-memory pitch (bytes per row > row bytes) so that
+// tensor-core fragment loads that walk rows hit distinct banks: the producer then copies
+// it with 16-byte cp.async and all its lanes arrive on "full" (expected count 1 + 32). Stream 0 may instead be gathered by a global row index array
 // (gidx: rows in FK-sorted order for the crossprod); the gatherer moves those rows with
 // 16-byte cp.async too, once the stage is free (its "full" phase for the other streams).
 //
@@ -182,13 +182,23 @@ struct TileRing {
     gathers = s.ngather > 0 || s.gidx != nullptr;
     if (threadIdx.x == 0) {
       for (int i = 0; i < stages; ++i) {
-        mbar_init(&full[i], 1);
+        mbar_init(&full[i], has_pitched(s) ? 33 : 1);
         mbar_init(&empty[i], kConsumerWarps);
         mbar_init(&gfull[i], 32 * kGatherWarps);
       }
       fence_mbar_init();
     }
     __syncthreads();
+  }
+
+  // Streams copied with cp.async by the producer (padded pitch): its 32 lanes then arrive
+  // on "full" as well.
+  FB_DEV static bool has_pitched(const StreamSet& s) {
+    bool p = false;
+#pragma unroll
+    for (int i = 0; i < kMaxStreams; ++i)
+      if (i < s.count && s.row_bytes[i] > 0 && s.pitch[i] != s.row_bytes[i] && !(i == 0 && s.gidx)) p = true;
+    return p;
   }
 
   // Service warps run their loop and return true; consumers get false.
@@ -208,6 +218,7 @@ struct TileRing {
   // stream 0 is left to the gatherer.
   FB_DEV void produce(const StreamSet& s) const {
     const int lane = threadIdx.x & 31;
+    const bool pitched = has_pitched(s);
     int st = 0;
     uint32_t ph = 0;
     const int64_t n = count();
@@ -220,7 +231,8 @@ struct TileRing {
           uint32_t tx = 0;
 #pragma unroll
           for (int i = 0; i < kMaxStreams; ++i)
-            if (i < s.count && !(i == 0 && s.gidx)) tx += s.row_bytes[i] * static_cast<uint32_t>(rows);
+            if (i < s.count && !(i == 0 && s.gidx) && s.pitch[i] == s.row_bytes[i])
+              tx += s.row_bytes[i] * static_cast<uint32_t>(rows);
           mbar_arrive_expect_tx(&full[st], tx);
         }
         __syncwarp();
@@ -233,13 +245,22 @@ struct TileRing {
             if (lane == 0)
               bulk_g2s_stream(dst, src, s.row_bytes[i] * static_cast<uint32_t>(rows), &full[st], policy);
           } else {
-            for (int r = lane; r < rows; r += 32)
-              bulk_g2s_stream(dst + static_cast<uint32_t>(r) * s.pitch[i],
-                              src + static_cast<size_t>(r) * s.row_bytes[i], s.row_bytes[i], &full[st], policy);
+            // padded pitch: (row, 16-byte chunk) items over the lanes with cp.async — one warp
+            // instruction moves 512 bytes (a per-row bulk copy costs ~60 issue cycles)
+            const uint32_t nch = s.row_bytes[i] >> 4;
+            const uint32_t items = nch * static_cast<uint32_t>(rows);
+            for (uint32_t it = lane; it < items; it += 32) {
+              const uint32_t r = it / nch, c = it - r * nch;
+              cp_async16(dst + r * s.pitch[i] + 16u * c, src + static_cast<size_t>(r) * s.row_bytes[i] + 16u * c, 0);
+            }
           }
         }
       } else if (lane == 0) {
         mbar_arrive(&full[st]);
+      }
+      if (pitched) {
+        __syncwarp();
+        cp_async_arrive_noinc(&full[st]);  // all 32 lanes, after their copies
       }
       if (++st == stages) {
         st = 0;
