@@ -303,7 +303,9 @@ static cudaError_t launch_rowdot(LmmArgs p, cudaStream_t st, int num_sms) {
 template <int NT, int MT>
 static cudaError_t launch_dmma_cfg(LmmArgs p, cudaStream_t st, int num_sms) {
   const int tile_rows = kConsumerWarps * 8 * MT;
-  p.pitch = (p.d % 2 == 0) ? conflict_free_pitch(p.d) : p.d;
+  // dense rows (one bulk copy per tile): a padded pitch needs one copy per row, which costs
+  // more than the 8-way A-fragment bank conflicts of a width ≡ 0 (mod 16)
+  p.pitch = p.d;
   StreamSet ss;
   fill_streams(p, ss, p.pitch);
   const int dpad = (p.d + 3) & ~3;
@@ -313,8 +315,7 @@ static cudaError_t launch_dmma_cfg(LmmArgs p, cudaStream_t st, int num_sms) {
 
 template <int NT>
 static cudaError_t launch_dmma(const LmmArgs& p, cudaStream_t st, int num_sms) {
-  const int pitch = (p.d % 2 == 0) ? conflict_free_pitch(p.d) : p.d;
-  const size_t row_bytes = static_cast<size_t>(pitch) * 8 + 8 * static_cast<size_t>(p.zstride) * p.nfk;
+  const size_t row_bytes = static_cast<size_t>(p.d) * 8 + 8 * static_cast<size_t>(p.zstride) * p.nfk;
   // stage <= ~48 KB
   if (row_bytes * 256 <= 48 * 1024) return launch_dmma_cfg<NT, 4>(p, st, num_sms);
   if (row_bytes * 128 <= 48 * 1024) return launch_dmma_cfg<NT, 2>(p, st, num_sms);
