@@ -30,7 +30,7 @@ extern "C" {
 
 typedef struct CUstream_st* fb_stream_t; /* == cudaStream_t */
 
-#define FB_ABI_VERSION 2
+#define FB_ABI_VERSION 3
 #define FB_MAX_PARTS 4
 
 enum {
@@ -58,6 +58,10 @@ typedef struct fb_part {
   const int16_t* hot_slot;
   const int32_t* hot_key;
   int32_t nhot;
+  /* optional FK-sorted order (fb_fk_sort): when set, X·K scatters run as segmented sums
+     over sorted positions instead of one atomic per row */
+  const int32_t* perm;
+  const int32_t* fk_sorted;
 } fb_part;
 
 /* Untransposed PK-FK / star normalized matrix T = [S, K_1 R_1, ..., K_q R_q]. */

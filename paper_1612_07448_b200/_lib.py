@@ -39,6 +39,8 @@ class FbPart(ctypes.Structure):
         ("hot_slot", c_vp),
         ("hot_key", c_vp),
         ("nhot", c_i32),
+        ("perm", c_vp),
+        ("fk_sorted", c_vp),
     ]
 
 

@@ -24,18 +24,7 @@ __all__ = ["crossprod", "fk_sorted_order"]
 
 def fk_sorted_order(ind):
     """(perm, fk_sorted) of an indicator: rows in ascending (target, row) order; cached."""
-    cached = getattr(ind, "_sorted", None)
-    if cached is None:
-        so = _lib.lib()
-        n = ind.rows
-        perm = torch.empty(n, dtype=torch.int32, device=ind.target.device)
-        fks = torch.empty(n, dtype=torch.int32, device=ind.target.device)
-        ws = D.workspace(so.fb_fk_sort_workspace_bytes(n))
-        _lib.check(so.fb_fk_sort(D.ptr(ind.target), n, ind.cols, D.ptr(perm), D.ptr(fks), ws.data_ptr(), ws.numel(),
-                                 D.stream_handle()))
-        cached = (perm, fks)
-        ind._sorted = cached
-    return cached
+    return ind.sorted_order()
 
 
 def _tally(nm, counter):
@@ -95,6 +84,7 @@ def crossprod(nm, method="efficient", counter=None):
 
 
 def _star_crossprod(nm, out, so, st):
+    nm.ensure_sorted()
     n = nm.base_rows
     d = nm.base_cols
     offs = nm.col_offsets()

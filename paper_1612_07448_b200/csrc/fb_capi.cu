@@ -282,16 +282,25 @@ static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_
     c.w = w ? w + j0 * w_cs : nullptr;
     c.w_rs = w_rs;
     c.w_cs = w_cs;
-    c.nfk = part_weights ? 0 : nm->q;
-    for (int i = 0; i < c.nfk; ++i) {
-      c.fk[i] = nm->part[i].fk;
-      c.bins[i] = bins[i];
-      c.nbins[i] = nm->part[i].n_r;
-      c.aggregate[i] = nm->part[i].skewed;
-      if (nm->part[i].nhot > 0 && nm->part[i].hot_slot && nm->part[i].hot_key) {
-        c.nhot[i] = nm->part[i].nhot < 64 ? nm->part[i].nhot : 64;
-        c.hot_slot[i] = nm->part[i].hot_slot;
-        c.hot_key[i] = nm->part[i].hot_key;
+    c.nfk = 0;
+    for (int i = 0; !part_weights && i < nm->q; ++i) {
+      const fb_part& pt = nm->part[i];
+      if (pt.perm && pt.fk_sorted && nm->n_s > 0) {
+        // X·K_i as segmented sums over the FK-sorted order (few atomics, no hot-line contention)
+        cudaError_t e = fb::launch_segsum(pt.perm, pt.fk_sorted, nm->n_s, w + j0 * w_cs, w_rs, w_cs, nx, bins[i],
+                                          pt.n_r, cs(stream), g_num_sms);
+        if (e != cudaSuccess) return cuda_status(e, "wt(segsum)");
+        continue;
+      }
+      const int f = c.nfk++;  // fused into the S pass: one atomic per row
+      c.fk[f] = pt.fk;
+      c.bins[f] = bins[i];
+      c.nbins[f] = pt.n_r;
+      c.aggregate[f] = pt.skewed;
+      if (pt.nhot > 0 && pt.hot_slot && pt.hot_key) {
+        c.nhot[f] = pt.nhot < 64 ? pt.nhot : 64;
+        c.hot_slot[f] = pt.hot_slot;
+        c.hot_key[f] = pt.hot_key;
       }
     }
     c.out = out + j0 * o_js;

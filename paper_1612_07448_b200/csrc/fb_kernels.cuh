@@ -36,6 +36,9 @@ struct ColReduce {
   unsigned int* counter;           // workspace: one zeroed word
 };
 size_t colreduce_workspace_doubles(int64_t n, int d, int nx, int num_sms);
+// bins(key, j) = Σ_{p: keys[p] = key} w(perm[p], j) over FK-sorted positions (zeroes bins first)
+cudaError_t launch_segsum(const int32_t* perm, const int32_t* keys, int64_t n, const double* w, int64_t w_rs,
+                          int64_t w_cs, int nx, double* bins, int64_t n_bins, cudaStream_t st, int num_sms);
 cudaError_t launch_colreduce(const ColReduce& c, cudaStream_t st, int num_sms);
 
 // fb_elementwise.cu ------------------------------------------------------------------

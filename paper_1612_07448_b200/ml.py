@@ -350,6 +350,7 @@ def gnmf(m, cfg):
     so = _lib.lib()
     st = D.stream_handle()
     cs = nm.c_struct()
+    nm.ensure_sorted()  # Tᵀ·W scatters as segmented sums over the cached FK-sorted order
     dev = nm.s.device
     rng = np.random.default_rng(cfg.rng_seed)
     counter = OpCounter()

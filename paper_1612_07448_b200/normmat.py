@@ -122,6 +122,23 @@ class IndicatorMatrix:
                 self._hot = (slot, keys, int(keys.numel()))
         return self._hot
 
+    def sorted_order(self):
+        """(perm, fk_sorted): rows in ascending (target, row) order, cached.
+
+        The device analogue of the reference's cached ``_csr_t`` stable argsort
+        (indicator.py:78-86), built once by a stable radix sort (fb_fk_sort).
+        """
+        if getattr(self, "_sorted", None) is None:
+            so = _lib.lib()
+            n = self.rows
+            perm = torch.empty(n, dtype=torch.int32, device=self.target.device)
+            fks = torch.empty(n, dtype=torch.int32, device=self.target.device)
+            ws = D.workspace(so.fb_fk_sort_workspace_bytes(n))
+            _lib.check(so.fb_fk_sort(D.ptr(self.target), n, self.cols, D.ptr(perm), D.ptr(fks), ws.data_ptr(),
+                                     ws.numel(), D.stream_handle()))
+            self._sorted = (perm, fks)
+        return self._sorted
+
     def all_columns_used(self):
         return bool((self.counts_i32 > 0).all().item())
 
@@ -239,8 +256,19 @@ class NormalizedMatrix:
                 p.counts = D.ptr(e.counts)
                 hs, hk, nh = e.hot_tables()
                 p.hot_slot, p.hot_key, p.nhot = D.ptr(hs), D.ptr(hk), nh
+                srt = getattr(e, "_sorted", None)
+                if srt is not None:
+                    p.perm, p.fk_sorted = D.ptr(srt[0]), D.ptr(srt[1])
             self._cache["c_struct"] = st
         return ctypes.byref(st)
+
+    def ensure_sorted(self):
+        """Build (once) the FK-sorted order of every indicator and expose it to the kernels."""
+        st = self._cache.get("c_struct")
+        for i, (e, _) in enumerate(self.blocks[1:]):
+            perm, fks = e.sorted_order()
+            if st is not None:
+                st.part[i].perm, st.part[i].fk_sorted = D.ptr(perm), D.ptr(fks)
 
     def __repr__(self):
         n, d = self.shape

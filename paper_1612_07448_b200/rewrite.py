@@ -220,9 +220,14 @@ def _lmm_dev(nm, x, counter):
 
 
 def _wt_dev(nm, w, w_rs, w_cs, n_w, out, o_js, o_cs, counter):
-    """out(j, c) = Σ_i w(i, j) T(i, c) on the untransposed matrix."""
+    """out(j, c) = Σ_i w(i, j) T(i, c) on the untransposed matrix.
+
+    The X·K halves run as segmented sums over the cached FK-sorted order (built on first use,
+    like the reference's cached CSR of K, indicator.py:71-86).
+    """
     so = _lib.lib()
     cs = nm.c_struct()
+    nm.ensure_sorted()
     ws = D.workspace(so.fb_wt_workspace_bytes(cs, n_w))
     _lib.check(so.fb_wt(cs, D.ptr(w), n_w, w_rs, w_cs, D.ptr(out), o_js, o_cs, ws.data_ptr(), ws.numel(),
                         D.stream_handle()))

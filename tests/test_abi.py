@@ -28,16 +28,16 @@ def test_abi_version_without_device():
     from paper_1612_07448_b200 import _lib
 
     so = _lib.load_library()
-    assert so.fb_abi_version() == 2
+    assert so.fb_abi_version() == 3
     assert so.fb_launch_count() >= 0
 
 
 def test_struct_layout_matches_header():
     from paper_1612_07448_b200 import _lib
 
-    # fb_part: ptr, ptr, i64, i32, i32, ptr, ptr, ptr, i32 (+pad) = 64 bytes
-    assert ctypes.sizeof(_lib.FbPart) == 64
-    assert ctypes.sizeof(_lib.FbNormalized) == 24 + 4 * 64
+    # fb_part: ptr, ptr, i64, i32, i32, ptr, ptr, ptr, i32 (+pad), ptr, ptr = 80 bytes
+    assert ctypes.sizeof(_lib.FbPart) == 80
+    assert ctypes.sizeof(_lib.FbNormalized) == 24 + 4 * 80
 
 
 def test_product_path_fails_loudly_without_gpu():
