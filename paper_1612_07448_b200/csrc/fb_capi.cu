@@ -34,6 +34,38 @@ namespace {
 
 thread_local char g_err[512] = "";
 int g_num_sms = 148;
+int g_persist_max = 0;  // bytes of L2 that may hold persisting lines (cudaLimitPersistingL2CacheSize)
+
+// Fork/join onto a library-owned side stream so independent passes of one operator overlap
+// (stream-ordered and CUDA-graph capturable: record → wait → launch → record → wait).
+struct SideStream {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int device = -1;
+};
+thread_local SideStream g_side;
+
+cudaError_t side_fork(cudaStream_t main, cudaStream_t* side) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (g_side.side == nullptr || g_side.device != dev) {
+    cudaError_t e = cudaStreamCreateWithFlags(&g_side.side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_side.join, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    g_side.device = dev;
+  }
+  cudaError_t e = cudaEventRecord(g_side.fork, main);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(g_side.side, g_side.fork, 0);
+  *side = g_side.side;
+  return e;
+}
+
+cudaError_t side_join(cudaStream_t main) {
+  cudaError_t e = cudaEventRecord(g_side.join, g_side.side);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(main, g_side.join, 0);
+  return e;
+}
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -139,6 +171,11 @@ int fb_init(int device) {
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
   g_num_sms = sms;
+  int maxp = 0;
+  if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess && maxp > 0 &&
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(maxp)) == cudaSuccess)
+    g_persist_max = maxp;
+  cudaGetLastError();  // the limit is an optimisation; ignore a refusal
   return FB_OK;
 }
 
@@ -223,8 +260,26 @@ int fb_lmm(const fb_normalized* nm, const double* x, int32_t d_x, double* out, v
       off += p.d_r;
     }
     // out = S · X[0:d_s, c0:c0+w] + Σ z_i[fk_i]   (rewrite.py:186-190)
+    // A z table too large for L2 under the S/out streams (e.g. 1M × 16 doubles) gets an L2
+    // access-policy window: a hitRatio share of its lines persists across the pass.
+    const size_t zb0 = nm->q > 0 ? static_cast<size_t>(nm->part[0].n_r) * fb::z_stride(w) * 8 : 0;
+    const bool window = g_persist_max > 0 && zb0 > (32u << 20) && getenv("FB_NO_L2_WINDOW") == nullptr;
+    if (window) {
+      cudaStreamAttrValue v{};
+      v.accessPolicyWindow.base_ptr = const_cast<double*>(zs[0]);
+      v.accessPolicyWindow.num_bytes = zb0;
+      v.accessPolicyWindow.hitRatio = std::min(1.0f, static_cast<float>(g_persist_max) / static_cast<float>(zb0));
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(cs(stream), cudaStreamAttributeAccessPolicyWindow, &v);
+    }
     cudaError_t e = fb::launch_lmm_rows(nm->s, nm->n_s, nm->d_s, x + c0, w, d_x, nm->q, fks, zs,
                                         fb::z_stride(w), out + c0, d_x, cs(stream), g_num_sms);
+    if (window) {
+      cudaStreamAttrValue v{};
+      v.accessPolicyWindow.num_bytes = 0;
+      cudaStreamSetAttribute(cs(stream), cudaStreamAttributeAccessPolicyWindow, &v);
+    }
     if (e != cudaSuccess) return cuda_status(e, "lmm(S)");
     c0 += w;
   }
@@ -274,6 +329,8 @@ static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_
     unsigned int* counter = cv.take<unsigned int>(1);
     if (!partials || !counter) return fail(FB_ERR_ARG, "wt: workspace too small");
 
+    bool forked = false;
+    cudaStream_t side = nullptr;
     fb::ColReduce c{};
     c.a = nm->s;
     c.n = nm->n_s;
@@ -286,9 +343,15 @@ static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_
     for (int i = 0; !part_weights && i < nm->q; ++i) {
       const fb_part& pt = nm->part[i];
       if (pt.perm && pt.fk_sorted && nm->n_s > 0) {
-        // X·K_i as segmented sums over the FK-sorted order (few atomics, no hot-line contention)
+        // X·K_i as segmented sums over the FK-sorted order (few atomics, no hot-line
+        // contention), on the side stream so they overlap the S pass
+        if (!forked) {
+          cudaError_t e = side_fork(cs(stream), &side);
+          if (e != cudaSuccess) return cuda_status(e, "wt(fork)");
+          forked = true;
+        }
         cudaError_t e = fb::launch_segsum(pt.perm, pt.fk_sorted, nm->n_s, w + j0 * w_cs, w_rs, w_cs, nx, bins[i],
-                                          pt.n_r, cs(stream), g_num_sms);
+                                          pt.n_r, side, g_num_sms);
         if (e != cudaSuccess) return cuda_status(e, "wt(segsum)");
         continue;
       }
@@ -310,6 +373,10 @@ static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_
     c.counter = counter;
     cudaError_t e = fb::launch_colreduce(c, cs(stream), g_num_sms);
     if (e != cudaSuccess) return cuda_status(e, "wt(S)");
+    if (forked) {
+      e = side_join(cs(stream));  // the R passes below read the segmented bins
+      if (e != cudaSuccess) return cuda_status(e, "wt(join)");
+    }
     int64_t off = nm->d_s;
     for (int i = 0; i < nm->q; ++i) {
       const fb_part& p = nm->part[i];
