@@ -34,7 +34,6 @@ namespace {
 
 thread_local char g_err[512] = "";
 int g_num_sms = 148;
-int g_persist_max = 0;  // bytes of L2 that may hold persisting lines (cudaLimitPersistingL2CacheSize)
 
 // Fork/join onto a library-owned side stream so independent passes of one operator overlap
 // (stream-ordered and CUDA-graph capturable: record → wait → launch → record → wait).
@@ -171,11 +170,6 @@ int fb_init(int device) {
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
   g_num_sms = sms;
-  int maxp = 0;
-  if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess && maxp > 0 &&
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(maxp)) == cudaSuccess)
-    g_persist_max = maxp;
-  cudaGetLastError();  // the limit is an optimisation; ignore a refusal
   return FB_OK;
 }
 
@@ -260,26 +254,8 @@ int fb_lmm(const fb_normalized* nm, const double* x, int32_t d_x, double* out, v
       off += p.d_r;
     }
     // out = S · X[0:d_s, c0:c0+w] + Σ z_i[fk_i]   (rewrite.py:186-190)
-    // A z table too large for L2 under the S/out streams (e.g. 1M × 16 doubles) gets an L2
-    // access-policy window: a hitRatio share of its lines persists across the pass.
-    const size_t zb0 = nm->q > 0 ? static_cast<size_t>(nm->part[0].n_r) * fb::z_stride(w) * 8 : 0;
-    const bool window = g_persist_max > 0 && zb0 > (32u << 20) && getenv("FB_NO_L2_WINDOW") == nullptr;
-    if (window) {
-      cudaStreamAttrValue v{};
-      v.accessPolicyWindow.base_ptr = const_cast<double*>(zs[0]);
-      v.accessPolicyWindow.num_bytes = zb0;
-      v.accessPolicyWindow.hitRatio = std::min(1.0f, static_cast<float>(g_persist_max) / static_cast<float>(zb0));
-      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      cudaStreamSetAttribute(cs(stream), cudaStreamAttributeAccessPolicyWindow, &v);
-    }
     cudaError_t e = fb::launch_lmm_rows(nm->s, nm->n_s, nm->d_s, x + c0, w, d_x, nm->q, fks, zs,
                                         fb::z_stride(w), out + c0, d_x, cs(stream), g_num_sms);
-    if (window) {
-      cudaStreamAttrValue v{};
-      v.accessPolicyWindow.num_bytes = 0;
-      cudaStreamSetAttribute(cs(stream), cudaStreamAttributeAccessPolicyWindow, &v);
-    }
     if (e != cudaSuccess) return cuda_status(e, "lmm(S)");
     c0 += w;
   }
