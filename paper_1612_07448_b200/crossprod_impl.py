@@ -71,7 +71,9 @@ def crossprod(nm, method="efficient", counter=None):
     out = torch.empty((d, d), dtype=torch.float64, device=dev)
     q = len(nm.blocks) - 1
     cs = nm.c_struct()
-    if q <= 1:
+    if q == 1 and nm.blocks[0][1].shape[1] > 128:
+        _star_crossprod(nm, out, so, st)  # the fused segmented KᵀS covers d_S <= 128
+    elif q <= 1:
         perm = fks = None
         if q == 1:
             perm, fks = fk_sorted_order(nm.blocks[1][0])

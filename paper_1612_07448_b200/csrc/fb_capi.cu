@@ -460,8 +460,8 @@ int fb_crossprod(const fb_normalized* nm, const int32_t* perm, const int32_t* fk
   int st = check_nm(nm);
   if (st) return st;
   if (nm->q > 1) return fail(FB_ERR_ARG, "crossprod: star schemas (q=%d) are not supported by the device path", nm->q);
-  if (nm->d_s > 256 || max_width(nm) > 256)
-    return fail(FB_ERR_ARG, "crossprod: factor widths above 256 are not supported");
+  if (nm->d_s > 256 || max_width(nm) > 256 || (nm->q == 1 && nm->d_s > 128))
+    return fail(FB_ERR_ARG, "crossprod: factor widths above 256 (d_S above 128 with an FK) are not supported");
   if (!out) return fail(FB_ERR_ARG, "crossprod: NULL output");
   if (ws_bytes < fb_crossprod_workspace_bytes(nm)) return fail(FB_ERR_ARG, "crossprod: workspace too small");
   fb::CrossArgs c{};
