@@ -106,6 +106,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
   bool cfirst[2] = {true, true};     // the open run is this CTA's first run
   double csum[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // lanes g == 0: columns 8 cb + 2t, +1
   (void)tid;
+  __shared__ uint8_t seg_rid[kConsumerWarps][128];
+  __shared__ uint8_t seg_start[kConsumerWarps][132];
 
   for (int64_t kt = 0; kt < ring.count(); ++kt) {
     const int stage = ring.acquire(ss, kt);
@@ -156,33 +158,26 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
     }
     if (seg) {
       const int32_t* keys = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, 1));
-      // run starts: bit i of mask[c] = row 32c + i starts a new key run
-      unsigned mask[4];
-      int before[5];
-      before[0] = 0;
+      // per-warp run tables of this tile (no CTA barrier): rid[r] = run of row r,
+      // rstart[j] = first row of run j (rstart[nruns] = rows)
+      uint8_t* rid = seg_rid[warp];
+      uint8_t* rstart = seg_start[warp];
+      int nruns = 0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int r = 32 * c + lane;
-        const bool st = r < rows && (r == 0 || keys[r] != keys[r - 1]);
-        mask[c] = __ballot_sync(0xffffffffu, st);
-        before[c + 1] = before[c] + __popc(mask[c]);
+        const bool live = r < rows;
+        const bool st = live && (r == 0 || keys[r] != keys[r - 1]);
+        const unsigned m = __ballot_sync(0xffffffffu, st);
+        const int id = nruns + __popc(m & (0xffffffffu >> (31 - lane))) - 1;
+        if (live) rid[r] = static_cast<uint8_t>(id);
+        if (st) rstart[id] = static_cast<uint8_t>(r);
+        nruns += __popc(m);
       }
-      const int nruns = before[4];
-      // row where run j starts (j < nruns), rows for j == nruns
-      auto run_start = [&](int j) {
-        int r = rows;
+      if (lane == 0) rstart[nruns] = static_cast<uint8_t>(rows);
+      __syncwarp();
+      auto run_start = [&](int j) { return static_cast<int>(rstart[j]); };
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (j >= before[c] && j < before[c + 1]) r = 32 * c + static_cast<int>(__fns(mask[c], 0, j - before[c] + 1));
-        return r;
-      };
-      auto run_id = [&](int r) {  // run of row r (r < rows)
-        int id = -1;
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if ((r >> 5) == c) id = before[c] + __popc(mask[c] & (0xffffffffu >> (31 - (r & 31)))) - 1;
-        return id;
-      };
       for (int slot = 0; slot < 2; ++slot) {
         const int cb = warp + kConsumerWarps * slot;
         if (cb >= nbs) break;
@@ -194,7 +189,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
           for (int k0 = r_lo & ~3; k0 < r_hi; k0 += 4) {
             const int r = k0 + t;
             const bool in = r >= r_lo && r < r_hi;
-            const double av = (in && run_id(r) - 8 * rb == g) ? 1.0 : 0.0;
+            const double av = (in && static_cast<int>(rid[r]) - 8 * rb == g) ? 1.0 : 0.0;
             const double bv = in ? R0[r * a.p0 + 8 * cb + g] : 0.0;
             dmma_8x8x4(d0, d1, av, bv);
           }
@@ -269,6 +264,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
   if (seg) {
     // the open run may continue into the next CTA: carry slot 1 (slot 0 when it is also the
     // CTA's first run, slot 1 then marked empty); an empty CTA marks both slots empty
+#pragma unroll
     for (int slot = 0; slot < 2; ++slot) {
       const int cb = warp + kConsumerWarps * slot;
       if (cb >= nbs || g != 0) continue;
