@@ -64,6 +64,23 @@ struct GramArgs {
   int debug;            // development bisection bits (FB_CP_DEBUG): 1 no walk, 2 no DMMA
 };
 
+// Segmented column sums over FK-sorted rows (thread c < d_S owns column c).
+struct SegState {
+  int key;     // current run key (-1: none yet)
+  double sum;
+  bool first;  // the current run is this CTA's first (may continue from the previous CTA)
+};
+
+FB_DEV void seg_flush(const GramArgs& a, SegState& st, int col, int slot) {
+  if (st.key < 0) return;
+  if (st.first) {
+    a.carry_val[(static_cast<size_t>(blockIdx.x) * 2 + slot) * a.seg_cols + col] = st.sum;
+    if (col == 0) a.carry_key[blockIdx.x * 2 + slot] = st.key;
+  } else {
+    a.bins[static_cast<int64_t>(st.key) * a.seg_cols + col] = st.sum;
+  }
+}
+
 template <int BPW, bool SCALE>
 __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_constant__ BlockJobs jobs, GramArgs a,
                                                                   StreamSet ss, int stages, int tile_rows) {
@@ -74,7 +91,6 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
   if (ring.service(ss)) return;
   const int warp = consumer_warp();
   const int grp = blockIdx.y;
-  if (a.seg && a.seg_cols > 8 * 2 * kConsumerWarps) __trap();  // host guarantees d_S <= 128
   const int ks = jobs.ks;
   const int kidx = warp % ks;
   const int nbt = (a.debug & 2) ? 0 : jobs.nbt[grp][warp];
@@ -98,16 +114,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
     for (int u = 0; u < 4; ++u) acc[b][u][0] = acc[b][u][1] = 0.0;
 
   const int tid = consumer_tid();
-  // Segmented KᵀS on the tensor cores: warp w owns S column blocks w, w+8, ... (8 columns
-  // each); its lanes g == 0 hold the CTA's open run (carry) for those columns.
-  const bool seg = a.seg && grp == 0 && !(a.debug & 1);
-  const int nbs = (a.seg_cols + 7) / 8;
-  int ckey[2] = {-1, -1};            // open run key per owned column block (<= 2 blocks: d_S <= 128)
-  bool cfirst[2] = {true, true};     // the open run is this CTA's first run
-  double csum[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // lanes g == 0: columns 8 cb + 2t, +1
-  (void)tid;
-  __shared__ uint8_t seg_rid[kConsumerWarps][128];
-  __shared__ uint8_t seg_start[kConsumerWarps][132];
+  const bool seg = a.seg && grp == 0 && tid < a.seg_cols && !(a.debug & 1);
+  SegState sst{-1, 0.0, true};
 
   for (int64_t kt = 0; kt < ring.count(); ++kt) {
     const int stage = ring.acquire(ss, kt);
@@ -144,6 +152,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
       const double* r1 = R1 + (4 * kidx + t) * a.p1;
       const double* cp = SCALE ? cnt + 4 * kidx + t : nullptr;
       int k0 = 4 * kidx;
+#pragma unroll 2
       for (; k0 < full; k0 += 4 * ks) {
         kstep(r0, r1, SCALE ? *cp : 1.0, true);
         r0 += step0;
@@ -157,133 +166,40 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
       }
     }
     if (seg) {
+      const double* S = R0;
       const int32_t* keys = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, 1));
-      // per-warp run tables of this tile (no CTA barrier): rid[r] = run of row r,
-      // rstart[j] = first row of run j (rstart[nruns] = rows)
-      uint8_t* rid = seg_rid[warp];
-      uint8_t* rstart = seg_start[warp];
-      int nruns = 0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int r = 32 * c + lane;
-        const bool live = r < rows;
-        const bool st = live && (r == 0 || keys[r] != keys[r - 1]);
-        const unsigned m = __ballot_sync(0xffffffffu, st);
-        const int id = nruns + __popc(m & (0xffffffffu >> (31 - lane))) - 1;
-        if (live) rid[r] = static_cast<uint8_t>(id);
-        if (st) rstart[id] = static_cast<uint8_t>(r);
-        nruns += __popc(m);
-      }
-      if (lane == 0) rstart[nruns] = static_cast<uint8_t>(rows);
-      __syncwarp();
-      auto run_start = [&](int j) { return static_cast<int>(rstart[j]); };
-#pragma unroll
-      for (int slot = 0; slot < 2; ++slot) {
-        const int cb = warp + kConsumerWarps * slot;
-        if (cb >= nbs) break;
-        const int col = 8 * cb + 2 * t;  // this lane's output columns col, col + 1
-        for (int rb = 0; 8 * rb < nruns; ++rb) {
-          const int r_lo = run_start(8 * rb), r_hi = run_start(min(8 * rb + 8, nruns));
-          double d0 = 0.0, d1 = 0.0;
-          __syncwarp();
-          for (int k0 = r_lo & ~3; k0 < r_hi; k0 += 4) {
-            const int r = k0 + t;
-            const bool in = r >= r_lo && r < r_hi;
-            const double av = (in && static_cast<int>(rid[r]) - 8 * rb == g) ? 1.0 : 0.0;
-            const double bv = in ? R0[r * a.p0 + 8 * cb + g] : 0.0;
-            dmma_8x8x4(d0, d1, av, bv);
+      const int p = a.p0;
+      for (int r = 0; r < rows; ++r) {
+        const int key = keys[r];
+        const double v = S[r * p + tid];
+        if (key != sst.key) {
+          seg_flush(a, sst, tid, 0);
+          if (sst.key >= 0) {
+            sst.first = false;
+            for (int z = sst.key + 1; z < key; ++z) a.bins[static_cast<int64_t>(z) * a.seg_cols + tid] = 0.0;
           }
-          // lane (g, t) holds run 8 rb + g, columns col, col + 1
-          const int j = 8 * rb + g;
-          const bool valid = j < nruns;
-          const int key = valid ? keys[run_start(j)] : -1;
-          const int prev_key = (valid && j > 0) ? keys[run_start(j - 1)] : -1;
-          const bool c0ok = col < a.seg_cols, c1ok = col + 1 < a.seg_cols;
-          // run 0 of the tile continues or closes the open run (lanes g == 0)
-          if (rb == 0 && g == 0) {
-            if (key == ckey[slot]) {
-              csum[slot][0] += d0;
-              csum[slot][1] += d1;
-            } else {
-              if (ckey[slot] >= 0) {
-                double* dst = cfirst[slot] ? a.carry_val + (static_cast<size_t>(blockIdx.x) * 2) * a.seg_cols
-                                           : a.bins + static_cast<int64_t>(ckey[slot]) * a.seg_cols;
-                if (c0ok) dst[col] = csum[slot][0];
-                if (c1ok) dst[col + 1] = csum[slot][1];
-                if (cfirst[slot] && cb == 0 && t == 0) a.carry_key[blockIdx.x * 2] = ckey[slot];
-                for (int z = ckey[slot] + 1; z < key; ++z) {  // keys no row maps to
-                  if (c0ok) a.bins[static_cast<int64_t>(z) * a.seg_cols + col] = 0.0;
-                  if (c1ok) a.bins[static_cast<int64_t>(z) * a.seg_cols + col + 1] = 0.0;
-                }
-                cfirst[slot] = false;
-              }
-              ckey[slot] = key;
-              csum[slot][0] = d0;
-              csum[slot][1] = d1;
-            }
-          }
-          // runs strictly inside the tile are complete: store them (and zero the key gap)
-          if (valid && j > 0 && j < nruns - 1) {
-            double* dst = a.bins + static_cast<int64_t>(key) * a.seg_cols;
-            if (c0ok) dst[col] = d0;
-            if (c1ok) dst[col + 1] = d1;
-            for (int z = prev_key + 1; z < key; ++z) {
-              if (c0ok) a.bins[static_cast<int64_t>(z) * a.seg_cols + col] = 0.0;
-              if (c1ok) a.bins[static_cast<int64_t>(z) * a.seg_cols + col + 1] = 0.0;
-            }
-          }
-          // the tile's last run (if not run 0) becomes the open run: close run 0 first
-          const int last = nruns - 1;
-          if (last > 0 && rb == last / 8) {
-            const double l0 = __shfl_sync(0xffffffffu, d0, (last % 8) * 4 + t);
-            const double l1 = __shfl_sync(0xffffffffu, d1, (last % 8) * 4 + t);
-            const int lkey = keys[run_start(last)];
-            const int pkey = keys[run_start(last - 1)];
-            if (g == 0) {
-              // the open run (run 0, merged) ended inside this tile
-              double* dst = cfirst[slot] ? a.carry_val + (static_cast<size_t>(blockIdx.x) * 2) * a.seg_cols
-                                         : a.bins + static_cast<int64_t>(ckey[slot]) * a.seg_cols;
-              if (c0ok) dst[col] = csum[slot][0];
-              if (c1ok) dst[col + 1] = csum[slot][1];
-              if (cfirst[slot] && cb == 0 && t == 0) a.carry_key[blockIdx.x * 2] = ckey[slot];
-              cfirst[slot] = false;
-              for (int z = pkey + 1; z < lkey; ++z) {
-                if (c0ok) a.bins[static_cast<int64_t>(z) * a.seg_cols + col] = 0.0;
-                if (c1ok) a.bins[static_cast<int64_t>(z) * a.seg_cols + col + 1] = 0.0;
-              }
-              ckey[slot] = lkey;
-              csum[slot][0] = l0;
-              csum[slot][1] = l1;
-            }
-          }
+          sst.key = key;
+          sst.sum = v;
+        } else {
+          sst.sum += v;
         }
       }
     }
     ring.release();
   }
   if (seg) {
-    // the open run may continue into the next CTA: carry slot 1 (slot 0 when it is also the
-    // CTA's first run, slot 1 then marked empty); an empty CTA marks both slots empty
-#pragma unroll
-    for (int slot = 0; slot < 2; ++slot) {
-      const int cb = warp + kConsumerWarps * slot;
-      if (cb >= nbs || g != 0) continue;
-      const int col = 8 * cb + 2 * t;
-      const int sl = cfirst[slot] ? 0 : 1;
-      double* dst = a.carry_val + (static_cast<size_t>(blockIdx.x) * 2 + sl) * a.seg_cols;
-      if (ckey[slot] >= 0) {
-        if (col < a.seg_cols) dst[col] = csum[slot][0];
-        if (col + 1 < a.seg_cols) dst[col + 1] = csum[slot][1];
-      }
-      if (cb == 0 && t == 0) {
-        if (ckey[slot] < 0) {
-          a.carry_key[blockIdx.x * 2] = -1;
-          a.carry_key[blockIdx.x * 2 + 1] = -1;
-        } else {
-          a.carry_key[blockIdx.x * 2 + sl] = ckey[slot];
-          if (sl == 0) a.carry_key[blockIdx.x * 2 + 1] = -1;
-        }
-      }
+    // the last run may continue into the next CTA: carry slot 1 (slot 0 if it is also the
+    // first run, in which case slot 1 is marked empty)
+    if (sst.first) {
+      seg_flush(a, sst, tid, 0);
+      if (tid == 0) a.carry_key[blockIdx.x * 2 + 1] = -1;
+    } else {
+      a.carry_val[(static_cast<size_t>(blockIdx.x) * 2 + 1) * a.seg_cols + tid] = sst.sum;
+      if (tid == 0) a.carry_key[blockIdx.x * 2 + 1] = sst.key;
+    }
+    if (sst.key < 0 && tid == 0) {  // empty CTA
+      a.carry_key[blockIdx.x * 2] = -1;
+      a.carry_key[blockIdx.x * 2 + 1] = -1;
     }
   }
   // this (CTA, k-split) partial: block tile b covers rows 16 bi + 8u + g, cols 16 bj + 8v + 2t
@@ -602,7 +518,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
   // ---- S pass: SᵀS (+ KᵀS when q = 1)
   if (c.d_s > 0 && c.n_s > 0) {
     BlockJobs JS;
-    if (!build_block_jobs(t2s, 0, JS)) return cudaErrorNotSupported;
+    if (!build_block_jobs(t2s, 0, JS, q != 0)) return cudaErrorNotSupported;
     GramArgs a{};
     a.n = c.n_s;
     a.p0 = a.p1 = c.d_s;
