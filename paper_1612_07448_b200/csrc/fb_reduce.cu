@@ -222,25 +222,52 @@ __global__ void __launch_bounds__(kRingThreads, 1) colreduce_kernel(ColRedDev p,
 }
 
 // X·K over FK-sorted rows (the device analogue of SciPy's CSC scatter at indicator.py:130-141):
-// bins(key, j) += Σ_{sorted p with key} w(perm[p], j). Each warp takes 32 consecutive sorted
-// positions, runs a segmented inclusive scan keyed on the (sorted, hence contiguous) keys,
-// and only the last lane of each key segment issues an atomic — about n/20 + n/32 atomics
-// at c2 instead of n, and one per warp for a hot Zipf key.
+// bins(key, j) += Σ_{sorted p with key} w(perm[p], j). Each warp owns a contiguous range of
+// sorted positions and walks it 32 at a time: a segmented inclusive scan keyed on the
+// (sorted, hence contiguous) keys sums each key run, the run still open at lane 31 is carried
+// into the next chunk, and only runs that touch the ends of the warp's range use atomics —
+// interior runs are complete and are stored plainly (bins are zeroed first). A hot Zipf key
+// costs one atomic per warp range it spans.
 template <int NX>
 __global__ void segsum_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ keys, int64_t n,
                               const double* __restrict__ w, int64_t w_rs, int64_t w_cs, double* __restrict__ bins) {
   const unsigned full = 0xffffffffu;
   const int lane = lane_id();
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t base = (blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < n;
-       base += warps * 32) {
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t wid = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t lo = n * wid / nwarps, hi = n * (wid + 1) / nwarps;
+  int ckey = -1;        // run open at the end of the previous chunk (valid in every lane)
+  bool cfirst = true;   // no run of this warp's range has closed yet: the open / first run may
+                        // have started in the previous warp's range (atomics)
+  double csum[NX];
+#pragma unroll
+  for (int j = 0; j < NX; ++j) csum[j] = 0.0;
+  for (int64_t base = lo; base < hi; base += 32) {
     const int64_t p = base + lane;
-    const bool live = p < n;
+    const bool live = p < hi;
     const int key = live ? keys[p] : -1 - lane;
     const int64_t row = live ? perm[p] : 0;
     double v[NX];
 #pragma unroll
     for (int j = 0; j < NX; ++j) v[j] = live ? w[row * w_rs + j * w_cs] : 0.0;
+    const int first_key = __shfl_sync(full, key, 0);
+    if (ckey >= 0 && first_key != ckey) {
+      // the carried run ended exactly at the chunk boundary
+      if (lane == 0) {
+        double* b = bins + static_cast<int64_t>(ckey) * NX;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) {
+          if (cfirst)
+            atomicAdd(b + j, csum[j]);
+          else
+            b[j] = csum[j];
+        }
+      }
+      cfirst = false;
+    } else if (ckey >= 0 && lane == 0) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) v[j] += csum[j];  // the carried run continues
+    }
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const int kk = __shfl_up_sync(full, key, off);
@@ -251,12 +278,29 @@ __global__ void segsum_kernel(const int32_t* __restrict__ perm, const int32_t* _
         if (same) v[j] += t;
       }
     }
+    const int last_lane = (hi - 1 - base) < 31 ? static_cast<int>(hi - 1 - base) : 31;
     const int next = __shfl_down_sync(full, key, 1);
-    if (live && (lane == 31 || next != key || p + 1 >= n)) {
+    const bool seg_end = live && lane < last_lane && next != key;  // a run that ends inside the chunk
+    if (seg_end) {
       double* b = bins + static_cast<int64_t>(key) * NX;
+      if (key == first_key && cfirst) {
 #pragma unroll
-      for (int j = 0; j < NX; ++j) atomicAdd(b + j, v[j]);
+        for (int j = 0; j < NX; ++j) atomicAdd(b + j, v[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < NX; ++j) b[j] = v[j];  // complete run inside the range
+      }
     }
+    if (__any_sync(full, seg_end)) cfirst = false;
+    ckey = __shfl_sync(full, key, last_lane);
+#pragma unroll
+    for (int j = 0; j < NX; ++j) csum[j] = __shfl_sync(full, v[j], last_lane);
+  }
+  // the last open run may continue into the next warp's range
+  if (lane == 0 && ckey >= 0) {
+    double* b = bins + static_cast<int64_t>(ckey) * NX;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) atomicAdd(b + j, csum[j]);
   }
 }
 
@@ -264,7 +308,7 @@ cudaError_t launch_segsum(const int32_t* perm, const int32_t* keys, int64_t n, c
                           int64_t w_cs, int nx, double* bins, int64_t n_bins, cudaStream_t st, int num_sms) {
   cudaError_t e = cudaMemsetAsync(bins, 0, static_cast<size_t>(n_bins) * nx * sizeof(double), st);
   if (e != cudaSuccess || n <= 0) return e;
-  const int grid = grid_for((n + 31) / 32, 8, 8, num_sms);
+  const int grid = grid_for((n + 255) / 256, 8, 8, num_sms);  // >= 256 sorted positions per warp
   switch (nx) {
 #define FB_SEG_CASE(N)                                                                   \
   case N:                                                                                \
