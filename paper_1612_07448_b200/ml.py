@@ -14,6 +14,8 @@ to what the reference itself does on tiny host matrices: the seeded NumPy RNG dr
 (kernel.pinv_dense, kernel.py:303-324).
 """
 
+import collections
+import os
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -148,24 +150,61 @@ def _ws(nbytes):
 # gradient descent (logistic / least squares)
 
 
+# CUDA graphs of whole GD runs, keyed on the operands' device pointers (a replay reads the
+# same buffers, so later in-place changes to S / R / y are seen). Small LRU; the entry keeps
+# the normalized matrix alive so its pointers stay valid.
+_GLM_GRAPHS = collections.OrderedDict()
+_GLM_GRAPHS_MAX = 4
+
+
+def _glm_run(so, cs, yd, w, trace, diverged, ws, mode, cfg, st):
+    w.zero_()
+    trace.zero_()
+    diverged.fill_(-1)
+    for it in range(cfg.iterations):
+        _lib.check(so.fb_glm_step(cs, D.ptr(yd), D.ptr(w), mode, float(cfg.step_size), it, D.ptr(trace),
+                                  D.ptr(diverged), ws.data_ptr(), ws.numel(), st))
+
+
 def _glm_gd(m, y, cfg, mode, name):
+    """GD loop; each iteration is one fused pass (fb_glm_step). The whole run is captured once
+    into a CUDA graph and replayed (c1 is launch-latency bound: ~5 kernels per iteration)."""
     nm = _matrix(m)
     n, d = nm.shape
     yd = _column(y, n)
     so = _lib.lib()
-    st = D.stream_handle()
     cs = nm.c_struct()
     dev = nm.s.device
     counter = OpCounter()
-    w = torch.zeros(d, dtype=torch.float64, device=dev)
-    trace = torch.zeros(cfg.iterations, dtype=torch.float64, device=dev)
-    diverged = torch.full((1,), -1, dtype=torch.int32, device=dev)
-    ws = _ws(so.fb_glm_workspace_bytes(cs))
+    key = (id(nm._cache), nm.s.data_ptr(), yd.data_ptr(), cfg.iterations, float(cfg.step_size), mode, dev.index)
+    entry = _GLM_GRAPHS.get(key) if os.environ.get("FB_NO_GRAPHS") is None else None
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for it in range(cfg.iterations):
-        _lib.check(so.fb_glm_step(cs, D.ptr(yd), D.ptr(w), mode, float(cfg.step_size), it, D.ptr(trace),
-                                  D.ptr(diverged), ws.data_ptr(), ws.numel(), st))
+    if entry is None:
+        w = torch.zeros(d, dtype=torch.float64, device=dev)
+        trace = torch.zeros(cfg.iterations, dtype=torch.float64, device=dev)
+        diverged = torch.full((1,), -1, dtype=torch.int32, device=dev)
+        ws = torch.empty(max(int(so.fb_glm_workspace_bytes(cs)), 256), dtype=torch.uint8, device=dev)
+        _glm_run(so, cs, yd, w, trace, diverged, ws, mode, cfg, D.stream_handle())  # eager run (and warm-up)
+        if os.environ.get("FB_NO_GRAPHS") is None:
+            graph = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                snap = (w.clone(), trace.clone(), diverged.clone())
+                with torch.cuda.graph(graph, stream=side):
+                    _glm_run(so, cs, yd, w, trace, diverged, ws, mode, cfg, side.cuda_stream)
+                w.copy_(snap[0])
+                trace.copy_(snap[1])
+                diverged.copy_(snap[2])
+            torch.cuda.current_stream().wait_stream(side)
+            _GLM_GRAPHS[key] = (graph, w, trace, diverged, ws, yd, nm)
+            while len(_GLM_GRAPHS) > _GLM_GRAPHS_MAX:
+                _GLM_GRAPHS.popitem(last=False)
+    else:
+        _GLM_GRAPHS.move_to_end(key)
+        graph, w, trace, diverged, ws, _, _ = entry
+        graph.replay()
     bad = int(diverged.item())  # synchronises
     wall = time.perf_counter() - t0
     for _ in range(cfg.iterations):
@@ -173,7 +212,7 @@ def _glm_gd(m, y, cfg, mode, name):
         _tally_tmm(counter, nm, 1)
     if bad >= 0:
         raise DivergenceError(bad)
-    return ModelOutput(name, (n, d), cfg, _np(trace).tolist(), weights=_np(w).reshape(d, 1), wall_time_s=wall,
+    return ModelOutput(name, (n, d), cfg, _np(trace).tolist(), weights=_np(w).reshape(d, 1).copy(), wall_time_s=wall,
                        counts=counter)
 
 

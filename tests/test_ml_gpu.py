@@ -163,3 +163,22 @@ def test_divergence_error_iteration():
     with pytest.raises(fb.DivergenceError) as ei:
         fb.linreg_gd(a, y, fb.TrainConfig(iterations=3, step_size=1.0))
     assert ei.value.iteration == expect
+
+
+def test_logreg_graph_replay_matches_eager(monkeypatch):
+    """The captured CUDA graph of a GD run reproduces the eager run bit for bit."""
+    fb = _fb()
+    rng, s, parts = _c1_like(21, n_s=30_000, n_r=3000)
+    nm, ref = _both(s, parts)
+    y = np.where(O.lmm(ref, rng.standard_normal((ref.d, 1))) >= 0, 1.0, -1.0)
+    yd = torch.from_numpy(y).cuda()
+    cfg = fb.TrainConfig(iterations=6, step_size=1e-3)
+    first = fb.logistic_gd(nm, yd, cfg)   # eager run + capture
+    again = fb.logistic_gd(nm, yd, cfg)   # graph replay
+    np.testing.assert_array_equal(first.weights, again.weights)
+    np.testing.assert_array_equal(first.objective, again.objective)
+    monkeypatch.setenv("FB_NO_GRAPHS", "1")
+    eager = fb.logistic_gd(nm, yd, cfg)
+    np.testing.assert_array_equal(first.weights, eager.weights)
+    w, obj = O.logistic_gd(ref, y, 6, 1e-3)
+    _close(again.weights, w)
