@@ -148,6 +148,17 @@ FB_DEV double warp_sum(double v) {
 
 FB_DEV int lane_id() { return threadIdx.x & 31; }
 
+// Fixed-order sum of `count` per-CTA partials of one output: lane i adds partials i, i+32,
+// ... in order, then a fixed xor tree. Deterministic for a fixed grid; the loads of one warp
+// are independent, so the last CTA's tail costs a few L2 round trips instead of `count`.
+FB_DEV double warp_sum_strided(const double* p, int count, size_t stride) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+#pragma unroll 4
+  for (int b = lane; b < count; b += 32) s += __ldcg(p + static_cast<size_t>(b) * stride);
+  return warp_sum(s);
+}
+
 // ---------------------------------------------------------------- FP64 tensor core
 // D(8x8) += A(8x4, row) * B(4x8, col). Fragment ownership (lane l, g = l>>2, t = l&3):
 //   a = A[g][t], b = B[t][g], c0/c1 = C[g][2t], C[g][2t+1].

@@ -121,10 +121,11 @@ __global__ void __launch_bounds__(kRingThreads, 1) glm_spass_kernel(GlmDev p, St
   red[tid] = lacc;
   consumer_sync();
   double* part = p.g.partials + static_cast<size_t>(blockIdx.x) * (d + 1);
-  if (tid == 0) {
+  if (tid < 32) {  // fixed order: lane i adds red[i], red[i + 32], ..., then an xor tree
     double s = 0.0;
-    for (int i = 0; i < kConsumerThreads; ++i) s += red[i];
-    part[d] = s;
+    for (int i = tid; i < kConsumerThreads; i += 32) s += red[i];
+    s = warp_sum(s);
+    if (tid == 0) part[d] = s;
   }
   consumer_sync();
   if (colthread) red[grp * d + col] = gacc;
@@ -141,13 +142,14 @@ __global__ void __launch_bounds__(kRingThreads, 1) glm_spass_kernel(GlmDev p, St
   consumer_sync();
   if (ticket != gridDim.x - 1) return;
   __threadfence();
-  for (int c = tid; c <= d; c += kConsumerThreads) {
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(p.g.partials + static_cast<size_t>(b) * (d + 1) + c);
-    if (c < d)
-      p.g.g_out[c] = s;
-    else
-      *p.g.loss_out = s;
+  for (int c = tid >> 5; c <= d; c += kConsumerWarps) {  // one warp per output
+    const double s = warp_sum_strided(p.g.partials + c, gridDim.x, static_cast<size_t>(d + 1));
+    if ((tid & 31) == 0) {
+      if (c < d)
+        p.g.g_out[c] = s;
+      else
+        *p.g.loss_out = s;
+    }
   }
   if (tid == 0) *p.g.counter = 0u;
 }
@@ -297,11 +299,12 @@ __global__ void kmeans_assign_kernel(const double* __restrict__ tc, const double
   __syncthreads();
   if (ticket != gridDim.x - 1) return;
   __threadfence();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(partials + b);
-    trace[it] = s;
-    *counter = 0u;
+  if (threadIdx.x < 32) {
+    const double s = warp_sum_strided(partials, gridDim.x, 1);
+    if (threadIdx.x == 0) {
+      trace[it] = s;
+      *counter = 0u;
+    }
   }
 }
 
@@ -363,10 +366,9 @@ __global__ void onehot_colsum_kernel(const double* __restrict__ s, int64_t n, in
   __syncthreads();
   if (ticket != gridDim.x - 1) return;
   __threadfence();
-  for (int e = tid; e < d * k; e += blockDim.x) {
-    double v = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) v += __ldcg(partials + static_cast<size_t>(b) * d * k + e);
-    out[e] = v;
+  for (int e = tid >> 5; e < d * k; e += blockDim.x >> 5) {  // one warp per output
+    const double v = warp_sum_strided(partials + e, gridDim.x, static_cast<size_t>(d) * k);
+    if ((tid & 31) == 0) out[e] = v;
   }
   if (tid == 0) *counter = 0u;
 }

@@ -212,11 +212,12 @@ __global__ void __launch_bounds__(kRingThreads, 1) colreduce_kernel(ColRedDev p,
   consumer_sync();
   if (ticket != gridDim.x - 1) return;
   __threadfence();
-  for (int e = tid; e < NX * d; e += kConsumerThreads) {
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(p.c.partials + static_cast<size_t>(b) * NX * d + e);
-    const int j = e / d, c = e % d;
-    p.c.out[j * p.c.o_js + c * p.c.o_cs] = s;
+  for (int e = tid >> 5; e < NX * d; e += kConsumerWarps) {  // one warp per output
+    const double s = warp_sum_strided(p.c.partials + e, gridDim.x, static_cast<size_t>(NX) * d);
+    if ((tid & 31) == 0) {
+      const int j = e / d, c = e % d;
+      p.c.out[j * p.c.o_js + c * p.c.o_cs] = s;
+    }
   }
   if (tid == 0) *p.c.counter = 0u;  // ready for the next launch
 }

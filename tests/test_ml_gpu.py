@@ -166,7 +166,7 @@ def test_divergence_error_iteration():
 
 
 def test_logreg_graph_replay_matches_eager(monkeypatch):
-    """The captured CUDA graph of a GD run reproduces the eager run bit for bit."""
+    """The captured CUDA graph of a GD run reproduces the eager run (and the oracle)."""
     fb = _fb()
     rng, s, parts = _c1_like(21, n_s=30_000, n_r=3000)
     nm, ref = _both(s, parts)
@@ -175,10 +175,12 @@ def test_logreg_graph_replay_matches_eager(monkeypatch):
     cfg = fb.TrainConfig(iterations=6, step_size=1e-3)
     first = fb.logistic_gd(nm, yd, cfg)   # eager run + capture
     again = fb.logistic_gd(nm, yd, cfg)   # graph replay
-    np.testing.assert_array_equal(first.weights, again.weights)
-    np.testing.assert_array_equal(first.objective, again.objective)
+    # the Kᵀp scatter uses atomics, so runs agree to rounding, not bit for bit
+    _close(again.weights, first.weights, 1e-12)
+    _close(again.objective, first.objective, 1e-12)
     monkeypatch.setenv("FB_NO_GRAPHS", "1")
     eager = fb.logistic_gd(nm, yd, cfg)
-    np.testing.assert_array_equal(first.weights, eager.weights)
+    _close(eager.weights, first.weights, 1e-12)
     w, obj = O.logistic_gd(ref, y, 6, 1e-3)
     _close(again.weights, w)
+    _close(again.objective, obj)
