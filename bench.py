@@ -196,9 +196,11 @@ def run_gpu(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_1612_07448_b200 as fb
+    from paper_1612_07448_b200 import dist as fbd
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    ngpu = max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_rank % ngpu)
+    dev = torch.device("cuda", local_rank % ngpu)
     cfg = dict(C2)
     if args.small:
         cfg.update(n_s=cfg["n_s"] // 20, n_r=cfg["n_r"] // 20)
@@ -210,7 +212,9 @@ def run_gpu(args, rank, world, local_rank):
     r = torch.randn(n_r, d_r, dtype=torch.float64, device=dev, generator=g_r)
     s = torch.randn(n_s, d_s, dtype=torch.float64, device=dev, generator=g_s)
     key = torch.randint(1, n_r + 1, (n_s,), dtype=torch.int64, device=dev, generator=g_s)
-    nm = fb.build_pkfk(s, key, r)
+    # row-sharded build with the global key histogram (every rank keeps the same R rows)
+    sm = fbd.build_pkfk(s, key, r, n_s * world)
+    nm = sm.local
     del key
     n_r_kept = nm.r.shape[0]
     x1 = torch.randn(d, 1, dtype=torch.float64, device=dev, generator=g_r)
@@ -224,12 +228,13 @@ def run_gpu(args, rank, world, local_rank):
             dist.all_reduce(t)
         return t
 
+    # LMM / rowSums are row-local; RMM and colSums all-reduce a 1 × 100 partial (dist.py)
     ops = {
-        "lmm_x1": lambda: fb.lmm(nm, x1),
-        "lmm_x16": lambda: fb.lmm(nm, x16),
-        "rmm_x1": lambda: allreduce(fb.rmm(xr, nm)),
-        "row_sums": lambda: fb.row_sums(nm),
-        "col_sums": lambda: allreduce(fb.col_sums(nm)),
+        "lmm_x1": lambda: fbd.lmm(sm, x1),
+        "lmm_x16": lambda: fbd.lmm(sm, x16),
+        "rmm_x1": lambda: fbd.rmm(xr, sm),
+        "row_sums": lambda: fbd.row_sums(sm),
+        "col_sums": lambda: fbd.col_sums(sm),
     }
     nb = op_bytes(n_s, d_s, n_r_kept, d_r)
     step_bytes = sum(nb.values())
@@ -523,8 +528,13 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("FB_DIST_BACKEND", "nccl")  # gloo: functional check with ranks sharing a GPU
+        ngpu = max(1, torch.cuda.device_count())
+        torch.cuda.set_device(local_rank % ngpu)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank % ngpu))
+        else:
+            dist.init_process_group(backend)
     try:
         run_gpu(args, rank, world, local_rank)
     finally:
