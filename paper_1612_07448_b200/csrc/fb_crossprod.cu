@@ -81,7 +81,7 @@ FB_DEV void seg_flush(const GramArgs& a, SegState& st, int col, int slot) {
   }
 }
 
-template <int BPW, bool SCALE>
+template <int BPW, int BS, bool SCALE>
 __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_constant__ BlockJobs jobs, GramArgs a,
                                                                   StreamSet ss, int stages, int tile_rows) {
   extern __shared__ __align__(128) char smem[];
@@ -103,15 +103,15 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
 #pragma unroll
   for (int b = 0; b < BPW; ++b) {
     const int code = b < nbt ? jobs.bt[grp][warp][b] : 0;
-    aoff[b] = 16 * (code & 63) + g;
-    woff[b] = 16 * ((code >> 6) & 63) + g;
+    aoff[b] = 8 * BS * (code & 63) + g;
+    woff[b] = 8 * BS * ((code >> 6) & 63) + g;
     reg1[b] = (code >> 12) & 1;
   }
-  double acc[BPW][4][2];
+  double acc[BPW][BS * BS][2];
 #pragma unroll
   for (int b = 0; b < BPW; ++b)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc[b][u][0] = acc[b][u][1] = 0.0;
+    for (int u = 0; u < BS * BS; ++u) acc[b][u][0] = acc[b][u][1] = 0.0;
 
   const int tid = consumer_tid();
   const bool seg = a.seg && grp == 0 && tid < a.seg_cols && !(a.debug & 1);
@@ -130,18 +130,18 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
 #pragma unroll
       for (int b = 0; b < BPW; ++b) {
         if (b < nbt) {
-          double a_lo = r0[aoff[b]], a_hi = r0[aoff[b] + 8];
+          double av[BS], wv[BS];
           const double* wr = reg1[b] ? r1 : r0;
-          double w_lo = wr[woff[b]], w_hi = wr[woff[b] + 8];
-          if (SCALE && !reg1[b]) {
-            w_lo *= c;
-            w_hi *= c;
+#pragma unroll
+          for (int u = 0; u < BS; ++u) {
+            av[u] = live ? r0[aoff[b] + 8 * u] : 0.0;
+            wv[u] = wr[woff[b] + 8 * u];
+            if (SCALE && !reg1[b]) wv[u] *= c;
           }
-          if (!live) a_lo = a_hi = 0.0;
-          dmma_8x8x4(acc[b][0][0], acc[b][0][1], a_lo, w_lo);
-          dmma_8x8x4(acc[b][1][0], acc[b][1][1], a_lo, w_hi);
-          dmma_8x8x4(acc[b][2][0], acc[b][2][1], a_hi, w_lo);
-          dmma_8x8x4(acc[b][3][0], acc[b][3][1], a_hi, w_hi);
+#pragma unroll
+          for (int u = 0; u < BS; ++u)
+#pragma unroll
+            for (int v = 0; v < BS; ++v) dmma_8x8x4(acc[b][u * BS + v][0], acc[b][u * BS + v][1], av[u], wv[v]);
         }
       }
     };
@@ -345,7 +345,7 @@ namespace {
 // Upper-triangle block tiles of a T2a × T2a gram, plus a full T2a × T2b rectangle (region 1).
 // With `reserve_set0` the first set of warps (consumer warps 0..ks-1, which run the
 // segmented KᵀS walk in the S pass) gets no block tiles when that keeps the others <= kMaxBPW.
-bool build_block_jobs(int T2a, int T2b, BlockJobs& J, bool reserve_set0 = false) {
+bool build_block_jobs(int T2a, int T2b, BlockJobs& J, bool reserve_set0 = false, int bpw_max = kMaxBPW) {
   std::vector<uint16_t> list;
   for (int bi = 0; bi < T2a; ++bi) {
     for (int bj = bi; bj < T2a; ++bj) list.push_back(static_cast<uint16_t>(bi | (bj << 6)));
@@ -357,17 +357,17 @@ bool build_block_jobs(int T2a, int T2b, BlockJobs& J, bool reserve_set0 = false)
   J.ngroups = 1;
   if (bt == 0) return true;
   if (T2a > 63 || T2b > 63) return false;
-  const int cap = kConsumerWarps * kMaxBPW;  // block tiles one group can hold
+  const int cap = kConsumerWarps * bpw_max;  // block tiles one group can hold
   J.ngroups = (bt + cap - 1) / cap;
   if (J.ngroups > kMaxGroups) return false;
   const int per_group = (bt + J.ngroups - 1) / J.ngroups;
   // sets per group: the smallest power of two with sets · kMaxBPW >= per_group
   int sets = 1;
-  while (sets * kMaxBPW < per_group) sets *= 2;
+  while (sets * bpw_max < per_group) sets *= 2;
   int first = 0;
   if (reserve_set0 && J.ngroups == 1) {
-    while (sets < kConsumerWarps && (sets - 1) * kMaxBPW < per_group) sets *= 2;
-    if (sets > 1 && (sets - 1) * kMaxBPW >= per_group) first = 1;
+    while (sets < kConsumerWarps && (sets - 1) * bpw_max < per_group) sets *= 2;
+    if (sets > 1 && (sets - 1) * bpw_max >= per_group) first = 1;
   }
   J.ks = kConsumerWarps / sets;
   for (int gi = 0; gi < J.ngroups; ++gi) {
@@ -402,7 +402,7 @@ int gram_tile_rows(uint32_t row_bytes, int ks, bool gather) {
 
 // Launch one pass; *nparts = partials written (grid.x · ks).
 cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_rows, cudaStream_t st, int num_sms,
-                     int* nparts) {
+                     int* nparts, int bs) {
   stream_layout(ss, tile_rows, a.n);
   int stages = static_cast<int>((200 * 1024 - kRingHeader - 256) / ss.stage_bytes);
   if (stages > 6) stages = 6;
@@ -420,26 +420,36 @@ cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_ro
     fprintf(stderr, "[fb] gram pass n=%lld tile_rows=%d stages=%d grid=%dx%d ks=%d bpw=%d seg=%d gidx=%d\n",
             (long long)a.n, tile_rows, stages, gdim.x, gdim.y, J.ks, bpw, a.seg, ss.gidx != nullptr);
   cudaError_t e;
-#define FB_GRAM_CASE(B)                                                                                         \
-  if (bpw <= B) {                                                                                               \
-    auto kern = a.cnt_stream >= 0 ? cp_gram_kernel<B, true> : cp_gram_kernel<B, false>;                        \
+#define FB_GRAM_CASE(B, S)                                                                                      \
+  if (bpw <= B && bs == S) {                                                                                    \
+    auto kern = a.cnt_stream >= 0 ? cp_gram_kernel<B, S, true> : cp_gram_kernel<B, S, false>;                  \
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));        \
     if (e != cudaSuccess) return e;                                                                             \
     kern<<<gdim, kRingThreads, smem, st>>>(J, a, ss, stages, tile_rows);                                        \
     FB_LAUNCHED();                                                                                              \
     return cudaGetLastError();                                                                                  \
   }
-  FB_GRAM_CASE(1)
-  FB_GRAM_CASE(2)
-  FB_GRAM_CASE(4)
+  FB_GRAM_CASE(1, 1)
+  FB_GRAM_CASE(2, 1)
+  FB_GRAM_CASE(4, 1)
+  FB_GRAM_CASE(1, 2)
+  FB_GRAM_CASE(2, 2)
+  FB_GRAM_CASE(4, 2)
+  FB_GRAM_CASE(1, 4)
 #undef FB_GRAM_CASE
   return cudaErrorNotSupported;
 }
 
-size_t partial_doubles(int T2a, int T2b, int num_sms) {
+size_t partial_doubles(int T2a, int T2b, int num_sms, int bs) {
   // worst case: one group with ks = kConsumerWarps (several groups share the SMs)
-  return static_cast<size_t>(num_sms) * kConsumerWarps * (16 * T2a) * (16 * (T2a + T2b));
+  return static_cast<size_t>(num_sms) * kConsumerWarps * (8 * bs * T2a) * (8 * bs * (T2a + T2b));
 }
+
+// Block size (8-column blocks per side) of a pass over widths da (A) and db (region 1): large
+// blocks reuse fragments (4 + 4 loads per 16 DMMAs) at the cost of triangle padding.
+int block_size(int da) { return da <= 8 ? 1 : (da <= 40 ? 2 : 4); }
+
+int bpw_for(int bs) { return bs == 4 ? 1 : kMaxBPW; }
 
 }  // namespace
 
@@ -479,9 +489,11 @@ cudaError_t launch_fk_sort(const int32_t* fk, int64_t n, int64_t n_r, int32_t* p
 }
 
 size_t crossprod_workspace_bytes(int64_t n_s, int d_s, int64_t n_r, int d_r, int q, int num_sms) {
-  const int t2s = (d_s + 15) / 16, t2r = (d_r + 15) / 16;
-  size_t b = al(partial_doubles(t2s, 0, num_sms) * 8);
-  b += al(partial_doubles(t2r, q ? t2s : 0, num_sms) * 8);
+  const int bs_s = block_size(d_s), bs_r = block_size(d_r);
+  const int t2s = (d_s + 8 * bs_s - 1) / (8 * bs_s), t2r = (d_r + 8 * bs_r - 1) / (8 * bs_r);
+  const int t2b = q ? (d_s + 8 * bs_r - 1) / (8 * bs_r) : 0;
+  size_t b = al(partial_doubles(t2s, 0, num_sms, bs_s) * 8);
+  b += al(partial_doubles(t2r, t2b, num_sms, bs_r) * 8);
   if (q > 0) {
     b += al(static_cast<size_t>(n_r) * d_s * 8);                          // B = KᵀS
     b += al(static_cast<size_t>(num_sms) * 2 * sizeof(int));              // carry keys
@@ -493,16 +505,18 @@ size_t crossprod_workspace_bytes(int64_t n_s, int d_s, int64_t n_r, int d_r, int
 
 cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cudaStream_t st, int num_sms) {
   const int d = c.d_s + c.d_r;
-  const int t2s = (c.d_s + 15) / 16, t2r = (c.d_r + 15) / 16;
   const int q = c.r ? 1 : 0;
+  const int bs_s = block_size(c.d_s), bs_r = block_size(c.d_r);
+  const int t2s = (c.d_s + 8 * bs_s - 1) / (8 * bs_s), t2r = (c.d_r + 8 * bs_r - 1) / (8 * bs_r);
+  const int t2b = q && c.d_s > 0 ? (c.d_s + 8 * bs_r - 1) / (8 * bs_r) : 0;
   char* p = static_cast<char*>(ws);
   auto take = [&](size_t b) {
     char* r = p;
     p += al(b);
     return r;
   };
-  double* sp = reinterpret_cast<double*>(take(partial_doubles(t2s, 0, num_sms) * 8));
-  double* rp = reinterpret_cast<double*>(take(partial_doubles(t2r, q ? t2s : 0, num_sms) * 8));
+  double* sp = reinterpret_cast<double*>(take(partial_doubles(t2s, 0, num_sms, bs_s) * 8));
+  double* rp = reinterpret_cast<double*>(take(partial_doubles(t2r, t2b, num_sms, bs_r) * 8));
   double* bins = nullptr;
   int* ckey = nullptr;
   double* cval = nullptr;
@@ -518,15 +532,15 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
   // ---- S pass: SᵀS (+ KᵀS when q = 1)
   if (c.d_s > 0 && c.n_s > 0) {
     BlockJobs JS;
-    if (!build_block_jobs(t2s, 0, JS, q != 0)) return cudaErrorNotSupported;
+    if (!build_block_jobs(t2s, 0, JS, q != 0, bpw_for(bs_s))) return cudaErrorNotSupported;
     GramArgs a{};
     a.n = c.n_s;
     a.p0 = a.p1 = c.d_s;
     a.s1 = -1;
     a.cnt_stream = -1;
-    a.ra = 16 * t2s;
-    a.cw = 16 * t2s;
-    a.w1_col0 = 16 * t2s;
+    a.ra = 8 * bs_s * t2s;
+    a.cw = 8 * bs_s * t2s;
+    a.w1_col0 = 8 * bs_s * t2s;
     a.partials = sp;
     StreamSet ss{};
     ss.base[0] = reinterpret_cast<const char*>(c.s);
@@ -545,7 +559,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     }
     const int tr = gram_tile_rows(ss.row_bytes[0] + (q ? 4u : 0u), JS.ks, q != 0);
     int nparts = 0;
-    e = run_gram(JS, a, ss, tr, st, num_sms, &nparts);
+    e = run_gram(JS, a, ss, tr, st, num_sms, &nparts, bs_s);
     if (e != cudaSuccess) return e;
     if (q) {
       const int grid = nparts / JS.ks;
@@ -561,9 +575,8 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
 
   // ---- R pass: Rᵀ diag(c) R (upper) and RᵀB
   if (q && c.d_r > 0 && c.n_r > 0) {
-    const int t2b = c.d_s > 0 ? t2s : 0;
     BlockJobs JR;
-    if (!build_block_jobs(t2r, t2b, JR)) return cudaErrorNotSupported;
+    if (!build_block_jobs(t2r, t2b, JR, false, bpw_for(bs_r))) return cudaErrorNotSupported;
     GramArgs a{};
     a.n = c.n_r;
     // pitch ≡ 4 (mod 8) doubles keeps the 8-row fragment loads bank-conflict free
@@ -572,9 +585,9 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     a.p1 = c.d_s > 0 ? c.d_s : 1;
     a.s1 = c.d_s > 0 ? 1 : -1;
     a.cnt_stream = 2;
-    a.ra = 16 * t2r;
-    a.cw = 16 * (t2r + t2b);
-    a.w1_col0 = 16 * t2r;
+    a.ra = 8 * bs_r * t2r;
+    a.cw = 8 * bs_r * (t2r + t2b);
+    a.w1_col0 = 8 * bs_r * t2r;
     a.partials = rp;
     StreamSet ss{};
     ss.base[0] = reinterpret_cast<const char*>(c.r);
@@ -587,7 +600,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     ss.count = 3;
     const int tr = gram_tile_rows(pr * 8u + c.d_s * 8u + 8u, JR.ks, false);
     int nparts = 0;
-    e = run_gram(JR, a, ss, tr, st, num_sms, &nparts);
+    e = run_gram(JR, a, ss, tr, st, num_sms, &nparts, bs_r);
     if (e != cudaSuccess) return e;
     ReduceArgs r{rp, nparts, a.ra, a.cw, a.w1_col0, c.d_r, c.d_s, c.d_s, 0, c.out, d};
     launch_reduce(r, st);
