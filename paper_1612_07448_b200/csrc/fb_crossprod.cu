@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
       a.carry_key[blockIdx.x * 2 + 1] = -1;
     }
   }
-  // this (CTA, k-split) partial: block tile b covers rows 16 bi + 8u + g, cols 16 bj + 8v + 2t
+  // this (CTA, k-split) partial: block tile b covers rows 8·BS·bi + 8u + g, cols 8·BS·bj + 8v + 2t
   double* part = a.partials + static_cast<size_t>(blockIdx.x * ks + kidx) * a.ra * a.cw;
 #pragma unroll
   for (int b = 0; b < BPW; ++b) {
@@ -210,12 +210,12 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
       const int row0 = aoff[b] - g;
       const int col0 = (woff[b] - g) + (reg1[b] ? a.w1_col0 : 0);
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < BS; ++u)
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
+        for (int v = 0; v < BS; ++v) {
           double* dst = part + static_cast<size_t>(row0 + 8 * u + g) * a.cw + col0 + 8 * v + 2 * t;
-          dst[0] = acc[b][2 * u + v][0];
-          dst[1] = acc[b][2 * u + v][1];
+          dst[0] = acc[b][BS * u + v][0];
+          dst[1] = acc[b][BS * u + v][1];
         }
     }
   }
