@@ -36,15 +36,19 @@
 
 namespace fb {
 
-constexpr int kMaxBPW = 4;     // block tiles per warp (16 DMMA accumulators; 13-warp CTAs cap registers at 128)
-constexpr int kMaxGroups = 8;  // gridDim.y job groups
+constexpr int kMaxBTG = 8;      // block tiles per job group (a warp's unit range then spans <= 2 of them)
+constexpr int kMaxGroups = 16;  // gridDim.y job groups
 
-// block tile code: bits 0-5 A block pair bi, bits 6-11 W block pair bj, bit 12 W from region 1
+// block tile code: bits 0-5 A block bi, bits 6-11 W block bj, bit 12 W from region 1.
+// Within a group, the (block tile, k-step) units of a tile are split evenly over the 8
+// consumer warps (block-tile major), so every SM sub-partition gets the same DMMA work
+// whatever the block-tile count; warp w takes units [w·U/8, (w+1)·U/8), U = nbt · tile_rows/4.
 struct BlockJobs {
-  uint16_t bt[kMaxGroups][kConsumerWarps][kMaxBPW];
-  uint8_t nbt[kMaxGroups][kConsumerWarps];
-  int ks;       // warps of a set split the k-steps ks ways
+  uint16_t code[kMaxGroups][kMaxBTG];
+  uint8_t nbt[kMaxGroups];
   int ngroups;
+  int per_group;  // block tiles per group (the last may hold fewer)
+  int total;      // block tiles of the pass
 };
 
 struct GramArgs {
@@ -52,9 +56,9 @@ struct GramArgs {
   int p0, p1;           // smem row pitch (doubles) of region 0 (A, and W when bit 12 clear) / region 1
   int s1;               // ring stream of region 1 (-1: none)
   int cnt_stream;       // stream holding per-row f64 counts that scale region-0 W frags (-1: none)
-  int ra, cw;           // partial matrix: ra rows (16·T2a) × cw cols (16·(T2a + T2b))
-  int w1_col0;          // first partial column of region 1 (16·T2a)
-  double* partials;     // [gridDim.x · ks][ra][cw]
+  int ra, cw;           // partial matrix: ra rows (8·BS·T2a) × cw cols (8·BS·(T2a + T2b))
+  int w1_col0;          // first partial column of region 1 (8·BS·T2a)
+  double* partials;     // [gridDim.x · 8 warps][ra][cw] (a warp writes only its block tiles)
   // S pass only: segmented KᵀS
   int seg;              // 1: run the segmented walk (stream 1 = sorted keys, int32)
   int seg_cols;         // d_S
@@ -81,7 +85,22 @@ FB_DEV void seg_flush(const GramArgs& a, SegState& st, int col, int slot) {
   }
 }
 
-template <int BPW, int BS, bool SCALE>
+// one row of the walk: extend the current run or close it and open the run of `key`
+FB_DEV void seg_row(const GramArgs& a, SegState& st, int col, int key, double v) {
+  if (key == st.key) {
+    st.sum += v;
+    return;
+  }
+  seg_flush(a, st, col, 0);
+  if (st.key >= 0) {
+    st.first = false;
+    for (int z = st.key + 1; z < key; ++z) a.bins[static_cast<int64_t>(z) * a.seg_cols + col] = 0.0;
+  }
+  st.key = key;
+  st.sum = v;
+}
+
+template <int BS, bool SCALE>
 __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_constant__ BlockJobs jobs, GramArgs a,
                                                                   StreamSet ss, int stages, int tile_rows) {
   extern __shared__ __align__(128) char smem[];
@@ -91,25 +110,53 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
   if (ring.service(ss)) return;
   const int warp = consumer_warp();
   const int grp = blockIdx.y;
-  const int ks = jobs.ks;
-  const int kidx = warp % ks;
-  const int nbt = (a.debug & 2) ? 0 : jobs.nbt[grp][warp];
   const int lane = lane_id();
   const int g = lane >> 2, t = lane & 3;
 
-  // per block tile: A column offset and W column offset (this lane's row of the fragments)
-  int aoff[BPW], woff[BPW];
-  bool reg1[BPW];
-#pragma unroll
-  for (int b = 0; b < BPW; ++b) {
-    const int code = b < nbt ? jobs.bt[grp][warp][b] : 0;
-    aoff[b] = 8 * BS * (code & 63) + g;
-    woff[b] = 8 * BS * ((code >> 6) & 63) + g;
-    reg1[b] = (code >> 12) & 1;
+  // this warp's units: NB = 2 (BS < 4): the (block tile, k-step) units of a tile are split
+  // evenly over the 8 warps, block-tile major, so a warp meets at most two block tiles.
+  // NB = 1 (BS = 4: a 32×32 accumulator is 64 registers): block tile i gets warps
+  // [8i/nbt, 8(i+1)/nbt), which split its k-steps evenly.
+  constexpr int NB = BS == 4 ? 1 : 2;
+  const int nks = tile_rows >> 2;
+  const int nbtg = (a.debug & 2) ? 0 : jobs.nbt[grp];
+  int nb = 0, ka[2] = {0, 0}, kb[2] = {0, 0}, code[2] = {0, 0};
+  if (NB == 2) {
+    const int U = nbtg * nks;
+    const int u0 = warp * U / kConsumerWarps, u1 = (warp + 1) * U / kConsumerWarps;
+    if (u1 > u0) {
+      const int b0 = u0 / nks;
+      code[0] = jobs.code[grp][b0];
+      ka[0] = u0 - b0 * nks;
+      kb[0] = min(nks, u1 - b0 * nks);
+      nb = 1;
+      if (u1 > (b0 + 1) * nks) {
+        code[1] = jobs.code[grp][b0 + 1];
+        kb[1] = u1 - (b0 + 1) * nks;
+        nb = 2;
+      }
+    }
+  } else if (nbtg > 0) {
+    int b = 0;
+    while ((b + 1) * kConsumerWarps / nbtg <= warp) ++b;
+    const int w0 = b * kConsumerWarps / nbtg, m = (b + 1) * kConsumerWarps / nbtg - w0;
+    code[0] = jobs.code[grp][b];
+    ka[0] = (warp - w0) * nks / m;
+    kb[0] = (warp - w0 + 1) * nks / m;
+    nb = kb[0] > ka[0] ? 1 : 0;
   }
-  double acc[BPW][BS * BS][2];
+  // per block tile: A column offset and W column offset (this lane's row of the fragments)
+  int aoff[NB], woff[NB];
+  bool reg1[NB];
 #pragma unroll
-  for (int b = 0; b < BPW; ++b)
+  for (int b = 0; b < NB; ++b) {
+    aoff[b] = 8 * BS * (code[b] & 63) + g;
+    woff[b] = 8 * BS * ((code[b] >> 6) & 63) + g;
+    reg1[b] = (code[b] >> 12) & 1;
+  }
+  double acc[NB][BS * BS][2];
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
 #pragma unroll
     for (int u = 0; u < BS * BS; ++u) acc[b][u][0] = acc[b][u][1] = 0.0;
 
@@ -125,11 +172,12 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
     const double* cnt =
         a.cnt_stream >= 0 ? reinterpret_cast<const double*>(ring.stage_ptr(stage, ss, a.cnt_stream)) : nullptr;
     __syncwarp();  // mma.sync.aligned needs the whole warp converged (after the barrier spin)
-    // one k-step: rows k0..k0+3 (lane t takes row k0 + t)
-    auto kstep = [&](const double* r0, const double* r1, double c, bool live) {
+    const int full = rows >> 2;  // k-steps whose four rows all exist
 #pragma unroll
-      for (int b = 0; b < BPW; ++b) {
-        if (b < nbt) {
+    for (int b = 0; b < NB; ++b) {
+      if (b < nb) {
+        // one k-step of block tile b: rows k0..k0+3 (lane t takes row k0 + t)
+        auto kstep = [&](const double* r0, const double* r1, double c, bool live) {
           double av[BS], wv[BS];
           const double* wr = reg1[b] ? r1 : r0;
 #pragma unroll
@@ -142,48 +190,48 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
           for (int u = 0; u < BS; ++u)
 #pragma unroll
             for (int v = 0; v < BS; ++v) dmma_8x8x4(acc[b][u * BS + v][0], acc[b][u * BS + v][1], av[u], wv[v]);
+        };
+        const int kend = min(kb[b], full);
+        const double* r0 = R0 + (4 * ka[b] + t) * a.p0;
+        const double* r1 = R1 + (4 * ka[b] + t) * a.p1;
+        const double* cp = SCALE ? cnt + 4 * ka[b] + t : nullptr;
+#pragma unroll 1
+        for (int k = ka[b]; k < kend; ++k) {
+          kstep(r0, r1, SCALE ? *cp : 1.0, true);
+          r0 += 4 * a.p0;
+          r1 += 4 * a.p1;
+          if (SCALE) cp += 4;
         }
-      }
-    };
-    if (nbt > 0) {
-      const int full = rows & ~3;  // k-steps whose four rows all exist
-      const int step0 = 4 * ks * a.p0, step1 = 4 * ks * a.p1;
-      const double* r0 = R0 + (4 * kidx + t) * a.p0;
-      const double* r1 = R1 + (4 * kidx + t) * a.p1;
-      const double* cp = SCALE ? cnt + 4 * kidx + t : nullptr;
-      int k0 = 4 * kidx;
-#pragma unroll 2
-      for (; k0 < full; k0 += 4 * ks) {
-        kstep(r0, r1, SCALE ? *cp : 1.0, true);
-        r0 += step0;
-        r1 += step1;
-        if (SCALE) cp += 4 * ks;
-      }
-      if (k0 < rows) {  // ragged last k-step of the last tile
-        const bool live = k0 + t < rows;
-        const int kr = live ? k0 + t : 0;
-        kstep(R0 + kr * a.p0, R1 + kr * a.p1, SCALE ? cnt[kr] : 1.0, live);
+        if ((rows & 3) && full >= ka[b] && full < kb[b]) {  // ragged last k-step of the last tile
+          const bool live = 4 * full + t < rows;
+          const int kr = live ? 4 * full + t : 0;
+          kstep(R0 + kr * a.p0, R1 + kr * a.p1, SCALE ? cnt[kr] : 1.0, live);
+        }
       }
     }
     if (seg) {
       const double* S = R0;
       const int32_t* keys = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, 1));
       const int p = a.p0;
-      for (int r = 0; r < rows; ++r) {
-        const int key = keys[r];
-        const double v = S[r * p + tid];
-        if (key != sst.key) {
-          seg_flush(a, sst, tid, 0);
-          if (sst.key >= 0) {
-            sst.first = false;
-            for (int z = sst.key + 1; z < key; ++z) a.bins[static_cast<int64_t>(z) * a.seg_cols + tid] = 0.0;
-          }
-          sst.key = key;
-          sst.sum = v;
+      int r = 0;
+      // batches of 8 rows: loads issued together; keys are sorted, so the batch lies
+      // inside the current run iff its last key equals the run's key
+      for (; r + 8 <= rows; r += 8) {
+        int kk[8];
+        double vv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          kk[j] = keys[r + j];
+          vv[j] = S[(r + j) * p + tid];
+        }
+        if (kk[7] == sst.key) {
+          sst.sum += ((vv[0] + vv[1]) + (vv[2] + vv[3])) + ((vv[4] + vv[5]) + (vv[6] + vv[7]));
         } else {
-          sst.sum += v;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) seg_row(a, sst, tid, kk[j], vv[j]);
         }
       }
+      for (; r < rows; ++r) seg_row(a, sst, tid, keys[r], S[r * p + tid]);
     }
     ring.release();
   }
@@ -202,11 +250,11 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
       a.carry_key[blockIdx.x * 2 + 1] = -1;
     }
   }
-  // this (CTA, k-split) partial: block tile b covers rows 8·BS·bi + 8u + g, cols 8·BS·bj + 8v + 2t
-  double* part = a.partials + static_cast<size_t>(blockIdx.x * ks + kidx) * a.ra * a.cw;
+  // this (CTA, warp) partial: block tile b covers rows 8·BS·bi + 8u + g, cols 8·BS·bj + 8v + 2t
+  double* part = a.partials + static_cast<size_t>(blockIdx.x * kConsumerWarps + warp) * a.ra * a.cw;
 #pragma unroll
-  for (int b = 0; b < BPW; ++b) {
-    if (b < nbt) {
+  for (int b = 0; b < NB; ++b) {
+    if (b < nb) {
       const int row0 = aoff[b] - g;
       const int col0 = (woff[b] - g) + (reg1[b] ? a.w1_col0 : 0);
 #pragma unroll
@@ -249,28 +297,55 @@ __global__ void cp_carry_fixup_kernel(const int* carry_key, const double* carry_
   for (int64_t z = prev + 1; z < n_bins; ++z) bins[z * cols + c] = 0.0;
 }
 
-// Final assembly of one pass: element (i, j) of the pass = Σ_p partials[p][i][j] in p order.
+// Final assembly of one pass: element (i, j) of the pass = Σ over CTAs x, then over the
+// warps w that hold units of its block tile, of partials[x·8 + w][i][j] (fixed order).
 //   region 0 (j < w1_col0): the upper triangle (i <= j < da) of a gram block at (off0, off0)
 //   region 1: a full da × db block at (off0, off1)
 // Written at its position of the d × d output and mirrored exactly.
 struct ReduceArgs {
   const double* partials;
-  int nparts, ra, cw, w1_col0;
+  int gridx, ra, cw, w1_col0;
   int da, db;       // valid widths of region 0 / region 1
   int off0, off1;   // output offsets
   double* out;
   int64_t ldo;
+  int bsz, t2a, t2b, per_group, total, nks;  // the job layout of the pass (BlockJobs, build_block_jobs)
+  int nb;                                     // block tiles per warp: 2 (linear unit split) or 1 (BS = 4)
 };
 
-__global__ void cp_reduce_kernel(ReduceArgs r) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int n0 = r.da * r.da, n1 = r.da * r.db;
-  if (e >= n0 + n1) return;
-  int i, j, pc, orow, ocol;
+// Partial element (i, pc) -> its block tile -> the consumer warps [wf, wf + nw) that wrote it.
+FB_DEV void tile_writers(const ReduceArgs& r, int i, int pc, int& wf, int& nw) {
+  const int bi = i / r.bsz;
+  int idx = bi * (r.t2a + r.t2b) - bi * (bi - 1) / 2;
+  idx += pc < r.w1_col0 ? pc / r.bsz - bi : (r.t2a - bi) + (pc - r.w1_col0) / r.bsz;
+  const int gi = idx / r.per_group, lb = idx - gi * r.per_group;
+  const int nbtg = min(r.per_group, r.total - gi * r.per_group);
+  if (r.nb == 1) {  // proportional warp sets (cp_gram_kernel, NB = 1)
+    wf = lb * kConsumerWarps / nbtg;
+    nw = (lb + 1) * kConsumerWarps / nbtg - wf;
+    return;
+  }
+  const int U = nbtg * r.nks;
+  const int lo = lb * r.nks, hi = lo + r.nks;
+  wf = kConsumerWarps;
+  int wl = -1;
+  for (int w = 0; w < kConsumerWarps; ++w) {
+    const int u0 = w * U / kConsumerWarps, u1 = (w + 1) * U / kConsumerWarps;
+    if (u1 > u0 && u1 > lo && u0 < hi) {
+      wf = min(wf, w);
+      wl = w;
+    }
+  }
+  nw = wl - wf + 1;
+}
+
+FB_DEV bool reduce_coords(const ReduceArgs& r, int64_t e, int& i, int& pc, int& orow, int& ocol) {
+  const int n0 = r.da * r.da;
+  int j;
   if (e < n0) {
     i = static_cast<int>(e / r.da);
     j = static_cast<int>(e % r.da);
-    if (i > j) return;
+    if (i > j) return false;
     pc = j;
     orow = r.off0 + i;
     ocol = r.off0 + j;
@@ -282,11 +357,22 @@ __global__ void cp_reduce_kernel(ReduceArgs r) {
     orow = r.off0 + i;
     ocol = r.off1 + j;
   }
-  const double* p = r.partials + static_cast<size_t>(i) * r.cw + pc;
+  return true;
+}
+
+__global__ void cp_reduce_kernel(ReduceArgs r) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= static_cast<int64_t>(r.da) * (r.da + r.db)) return;
+  int i, pc, orow, ocol, wf, nw;
+  if (!reduce_coords(r, e, i, pc, orow, ocol)) return;
+  tile_writers(r, i, pc, wf, nw);
   const size_t stride = static_cast<size_t>(r.ra) * r.cw;
+  const double* p = r.partials + static_cast<size_t>(i) * r.cw + pc + wf * stride;
   double s = 0.0;
-#pragma unroll 8
-  for (int q = 0; q < r.nparts; ++q) s += p[q * stride];
+  for (int x = 0; x < r.gridx; ++x) {
+    for (int w = 0; w < nw; ++w) s += p[w * stride];
+    p += kConsumerWarps * stride;
+  }
   r.out[orow * r.ldo + ocol] = s;
   r.out[ocol * r.ldo + orow] = s;
 }
@@ -294,28 +380,14 @@ __global__ void cp_reduce_kernel(ReduceArgs r) {
 // Small outputs (e.g. WᵀW with r = 5) over many partials: one CTA per element, a fixed
 // strided split over the partials and a fixed shared-memory tree (deterministic).
 __global__ void cp_reduce_small_kernel(ReduceArgs r) {
-  const int e = blockIdx.x;
-  const int n0 = r.da * r.da;
-  int i, j, pc, orow, ocol;
-  if (e < n0) {
-    i = e / r.da;
-    j = e % r.da;
-    if (i > j) return;
-    pc = j;
-    orow = r.off0 + i;
-    ocol = r.off0 + j;
-  } else {
-    const int f = e - n0;
-    i = f / r.db;
-    j = f % r.db;
-    pc = r.w1_col0 + j;
-    orow = r.off0 + i;
-    ocol = r.off1 + j;
-  }
-  const double* p = r.partials + static_cast<size_t>(i) * r.cw + pc;
+  int i, pc, orow, ocol, wf, nw;
+  if (!reduce_coords(r, blockIdx.x, i, pc, orow, ocol)) return;
+  tile_writers(r, i, pc, wf, nw);
   const size_t stride = static_cast<size_t>(r.ra) * r.cw;
+  const double* p = r.partials + static_cast<size_t>(i) * r.cw + pc + wf * stride;
   double s = 0.0;
-  for (int q = threadIdx.x; q < r.nparts; q += blockDim.x) s += p[q * stride];
+  const int nq = r.gridx * nw;
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) s += p[(static_cast<size_t>(q / nw) * kConsumerWarps + q % nw) * stride];
   __shared__ double red[256];
   red[threadIdx.x] = s;
   __syncthreads();
@@ -331,7 +403,7 @@ __global__ void cp_reduce_small_kernel(ReduceArgs r) {
 
 static void launch_reduce(const ReduceArgs& r, cudaStream_t st) {
   const int n = r.da * r.da + r.da * r.db;
-  if (n <= 2048 && r.nparts >= 64) {
+  if (n <= 2048 && r.gridx >= 32) {
     cp_reduce_small_kernel<<<n, 256, 0, st>>>(r);
   } else {
     cp_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(r);
@@ -342,10 +414,9 @@ static void launch_reduce(const ReduceArgs& r, cudaStream_t st) {
 // ------------------------------------------------------------------ host side
 namespace {
 
-// Upper-triangle block tiles of a T2a × T2a gram, plus a full T2a × T2b rectangle (region 1).
-// With `reserve_set0` the first set of warps (consumer warps 0..ks-1, which run the
-// segmented KᵀS walk in the S pass) gets no block tiles when that keeps the others <= kMaxBPW.
-bool build_block_jobs(int T2a, int T2b, BlockJobs& J, bool reserve_set0 = false, int bpw_max = kMaxBPW) {
+// Upper-triangle block tiles of a T2a × T2a gram, plus a full T2a × T2b rectangle (region 1),
+// in row-major order (tile_writers depends on it), cut into ngroups equal groups of <= kMaxBTG.
+bool build_block_jobs(int T2a, int T2b, BlockJobs& J) {
   std::vector<uint16_t> list;
   for (int bi = 0; bi < T2a; ++bi) {
     for (int bj = bi; bj < T2a; ++bj) list.push_back(static_cast<uint16_t>(bi | (bj << 6)));
@@ -353,32 +424,17 @@ bool build_block_jobs(int T2a, int T2b, BlockJobs& J, bool reserve_set0 = false,
   }
   const int bt = static_cast<int>(list.size());
   J = BlockJobs{};
-  J.ks = 1;
   J.ngroups = 1;
+  J.per_group = 1;
+  J.total = bt;
   if (bt == 0) return true;
   if (T2a > 63 || T2b > 63) return false;
-  const int cap = kConsumerWarps * bpw_max;  // block tiles one group can hold
-  J.ngroups = (bt + cap - 1) / cap;
+  J.ngroups = (bt + kMaxBTG - 1) / kMaxBTG;
   if (J.ngroups > kMaxGroups) return false;
-  const int per_group = (bt + J.ngroups - 1) / J.ngroups;
-  // sets per group: the smallest power of two with sets · kMaxBPW >= per_group
-  int sets = 1;
-  while (sets * bpw_max < per_group) sets *= 2;
-  int first = 0;
-  if (reserve_set0 && J.ngroups == 1) {
-    while (sets < kConsumerWarps && (sets - 1) * bpw_max < per_group) sets *= 2;
-    if (sets > 1 && (sets - 1) * bpw_max >= per_group) first = 1;
-  }
-  J.ks = kConsumerWarps / sets;
-  for (int gi = 0; gi < J.ngroups; ++gi) {
-    const int b0 = gi * per_group, b1 = std::min(bt, b0 + per_group);
-    for (int b = b0; b < b1; ++b) {
-      const int set = first + (b - b0) % (sets - first);
-      for (int k = 0; k < J.ks; ++k) {  // every warp of the set carries the same tiles
-        const int w = set * J.ks + k;
-        J.bt[gi][w][J.nbt[gi][w]++] = list[b];
-      }
-    }
+  J.per_group = (bt + J.ngroups - 1) / J.ngroups;
+  for (int b = 0; b < bt; ++b) {
+    const int gi = b / J.per_group;
+    J.code[gi][J.nbt[gi]++] = list[b];
   }
   return true;
 }
@@ -391,65 +447,59 @@ int gram_grid(int64_t n, int tile_rows, int ngroups, int num_sms) {
   return grid_for(ntiles, 1, 1, per);
 }
 
-int gram_tile_rows(uint32_t row_bytes, int ks, bool gather) {
+int gram_tile_rows(uint32_t row_bytes, bool gather) {
   int rows = static_cast<int>((48u * 1024u) / (row_bytes > 0 ? row_bytes : 1));
-  const int unit = 4 * ks;
+  const int unit = 32;  // 8 k-steps: one per consumer warp
   if (rows > (gather ? 128 : 256)) rows = gather ? 128 : 256;
   rows = (rows / unit) * unit;
   if (rows < unit) rows = unit;
   return rows;
 }
 
-// Launch one pass; *nparts = partials written (grid.x · ks).
+// Launch one pass; *gridx = CTAs per group (each wrote kConsumerWarps partial slots).
 cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_rows, cudaStream_t st, int num_sms,
-                     int* nparts, int bs) {
+                     int* gridx, int bs) {
   stream_layout(ss, tile_rows, a.n);
   int stages = static_cast<int>((200 * 1024 - kRingHeader - 256) / ss.stage_bytes);
   if (stages > 6) stages = 6;
   if (stages < 2) return cudaErrorNotSupported;
-  // + slack: fragment loads of a padded 16-column block read up to 15 doubles past a row,
+  // + slack: fragment loads of a padded block read up to 8·BS - 1 doubles past a row,
   // so the last row of the last stage must not sit at the end of the allocation
   const size_t smem = kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes + 256;
   if (const char* dbg = getenv("FB_CP_DEBUG")) a.debug = atoi(dbg);
-  int bpw = 0;
-  for (int gi = 0; gi < J.ngroups; ++gi)
-    for (int w = 0; w < kConsumerWarps; ++w) bpw = std::max(bpw, static_cast<int>(J.nbt[gi][w]));
   dim3 gdim(gram_grid(a.n, tile_rows, J.ngroups, num_sms), J.ngroups);
-  *nparts = static_cast<int>(gdim.x) * J.ks;
+  *gridx = static_cast<int>(gdim.x);
   if (getenv("FB_DEBUG_SYNC"))
-    fprintf(stderr, "[fb] gram pass n=%lld tile_rows=%d stages=%d grid=%dx%d ks=%d bpw=%d seg=%d gidx=%d\n",
-            (long long)a.n, tile_rows, stages, gdim.x, gdim.y, J.ks, bpw, a.seg, ss.gidx != nullptr);
+    fprintf(stderr, "[fb] gram pass n=%lld tile_rows=%d stages=%d grid=%dx%d bt=%d/group bs=%d seg=%d gidx=%d\n",
+            (long long)a.n, tile_rows, stages, gdim.x, gdim.y, J.per_group, bs, a.seg, ss.gidx != nullptr);
   cudaError_t e;
-#define FB_GRAM_CASE(B, S)                                                                                      \
-  if (bpw <= B && bs == S) {                                                                                    \
-    auto kern = a.cnt_stream >= 0 ? cp_gram_kernel<B, S, true> : cp_gram_kernel<B, S, false>;                  \
+#define FB_GRAM_CASE(S)                                                                                         \
+  if (bs == S) {                                                                                                \
+    auto kern = a.cnt_stream >= 0 ? cp_gram_kernel<S, true> : cp_gram_kernel<S, false>;                        \
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));        \
     if (e != cudaSuccess) return e;                                                                             \
     kern<<<gdim, kRingThreads, smem, st>>>(J, a, ss, stages, tile_rows);                                        \
     FB_LAUNCHED();                                                                                              \
     return cudaGetLastError();                                                                                  \
   }
-  FB_GRAM_CASE(1, 1)
-  FB_GRAM_CASE(2, 1)
-  FB_GRAM_CASE(4, 1)
-  FB_GRAM_CASE(1, 2)
-  FB_GRAM_CASE(2, 2)
-  FB_GRAM_CASE(4, 2)
-  FB_GRAM_CASE(1, 4)
+  FB_GRAM_CASE(1)
+  FB_GRAM_CASE(2)
+  FB_GRAM_CASE(4)
 #undef FB_GRAM_CASE
   return cudaErrorNotSupported;
 }
 
 size_t partial_doubles(int T2a, int T2b, int num_sms, int bs) {
-  // worst case: one group with ks = kConsumerWarps (several groups share the SMs)
+  // one slot per (CTA, consumer warp); all groups together use at most num_sms CTAs per row
   return static_cast<size_t>(num_sms) * kConsumerWarps * (8 * bs * T2a) * (8 * bs * (T2a + T2b));
 }
 
 // Block size (8-column blocks per side) of a pass over widths da (A) and db (region 1): large
 // blocks reuse fragments (4 + 4 loads per 16 DMMAs) at the cost of triangle padding.
-int block_size(int da) { return da <= 8 ? 1 : (da <= 40 ? 2 : 4); }
-
-int bpw_for(int bs) { return bs == 4 ? 1 : kMaxBPW; }
+int block_size(int da) {
+  if (const char* e = getenv("FB_CP_BS")) return atoi(e);  // development override (1, 2 or 4)
+  return da <= 8 ? 1 : (da <= 40 ? 2 : 4);
+}
 
 }  // namespace
 
@@ -532,7 +582,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
   // ---- S pass: SᵀS (+ KᵀS when q = 1)
   if (c.d_s > 0 && c.n_s > 0) {
     BlockJobs JS;
-    if (!build_block_jobs(t2s, 0, JS, q != 0, bpw_for(bs_s))) return cudaErrorNotSupported;
+    if (!build_block_jobs(t2s, 0, JS)) return cudaErrorNotSupported;
     GramArgs a{};
     a.n = c.n_s;
     a.p0 = a.p1 = c.d_s;
@@ -557,16 +607,17 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
       a.carry_key = ckey;
       a.carry_val = cval;
     }
-    const int tr = gram_tile_rows(ss.row_bytes[0] + (q ? 4u : 0u), JS.ks, q != 0);
-    int nparts = 0;
-    e = run_gram(JS, a, ss, tr, st, num_sms, &nparts, bs_s);
+    const int tr = gram_tile_rows(ss.row_bytes[0] + (q ? 4u : 0u), q != 0);
+    int gridx = 0;
+    e = run_gram(JS, a, ss, tr, st, num_sms, &gridx, bs_s);
     if (e != cudaSuccess) return e;
     if (q) {
-      const int grid = nparts / JS.ks;
+      const int grid = gridx;
       cp_carry_fixup_kernel<<<1, ((c.d_s + 31) / 32) * 32, 0, st>>>(ckey, cval, 2 * grid, c.d_s, bins, c.n_r);
       FB_LAUNCHED();
     }
-    ReduceArgs r{sp, nparts, a.ra, a.cw, a.w1_col0, c.d_s, 0, 0, 0, c.out, d};
+    ReduceArgs r{sp, gridx, a.ra, a.cw, a.w1_col0, c.d_s, 0, 0, 0, c.out, d, 8 * bs_s, t2s, 0, JS.per_group, JS.total, tr / 4,
+                 bs_s == 4 ? 1 : 2};
     launch_reduce(r, st);
   } else if (q && c.d_s > 0) {
     e = cudaMemsetAsync(bins, 0, static_cast<size_t>(c.n_r) * c.d_s * 8, st);  // no rows: KᵀS = 0
@@ -576,7 +627,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
   // ---- R pass: Rᵀ diag(c) R (upper) and RᵀB
   if (q && c.d_r > 0 && c.n_r > 0) {
     BlockJobs JR;
-    if (!build_block_jobs(t2r, t2b, JR, false, bpw_for(bs_r))) return cudaErrorNotSupported;
+    if (!build_block_jobs(t2r, t2b, JR)) return cudaErrorNotSupported;
     GramArgs a{};
     a.n = c.n_r;
     // pitch ≡ 4 (mod 8) doubles keeps the 8-row fragment loads bank-conflict free
@@ -598,11 +649,12 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     ss.base[2] = reinterpret_cast<const char*>(c.counts);
     ss.row_bytes[2] = 8u;
     ss.count = 3;
-    const int tr = gram_tile_rows(pr * 8u + c.d_s * 8u + 8u, JR.ks, false);
-    int nparts = 0;
-    e = run_gram(JR, a, ss, tr, st, num_sms, &nparts, bs_r);
+    const int tr = gram_tile_rows(pr * 8u + c.d_s * 8u + 8u, false);
+    int gridx = 0;
+    e = run_gram(JR, a, ss, tr, st, num_sms, &gridx, bs_r);
     if (e != cudaSuccess) return e;
-    ReduceArgs r{rp, nparts, a.ra, a.cw, a.w1_col0, c.d_r, c.d_s, c.d_s, 0, c.out, d};
+    ReduceArgs r{rp, gridx, a.ra, a.cw, a.w1_col0, c.d_r, c.d_s, c.d_s, 0, c.out, d, 8 * bs_r, t2r, t2b, JR.per_group,
+                 JR.total, tr / 4, bs_r == 4 ? 1 : 2};
     launch_reduce(r, st);
   }
   return cudaGetLastError();
