@@ -36,16 +36,23 @@
 
 namespace fb {
 
-constexpr int kMaxBTG = 8;      // block tiles per job group (a warp's unit range then spans <= 2 of them)
+constexpr int kNB = 4;          // block tiles one warp may touch (BS = 2: 4 × 16 accumulator registers)
 constexpr int kMaxGroups = 16;  // gridDim.y job groups
+constexpr int kMaxBT = 256;     // block tiles per pass
 
 // block tile code: bits 0-5 A block bi, bits 6-11 W block bj, bit 12 W from region 1.
-// Within a group, the (block tile, k-step) units of a tile are split evenly over the 8
-// consumer warps (block-tile major), so every SM sub-partition gets the same DMMA work
-// whatever the block-tile count; warp w takes units [w·U/8, (w+1)·U/8), U = nbt · tile_rows/4.
+// Host-built assignment (build_block_jobs): the (block tile, k-step) units of a tile are
+// laid out block-tile major and cut into one contiguous range per consumer warp, sized so
+// every SM sub-partition (warp slot mod 4: one DMMA pipe each) gets the same share; warps
+// that run the KᵀS walk get none. A warp's range covers <= kNB block tiles, each with a
+// k-step interval [ka, kb) of every full tile.
+struct WarpJob {
+  uint16_t code[kNB];
+  uint8_t ka[kNB], kb[kNB];
+  uint8_t nb;
+};
 struct BlockJobs {
-  uint16_t code[kMaxGroups][kMaxBTG];
-  uint8_t nbt[kMaxGroups];
+  WarpJob w[kMaxGroups][kConsumerWarps];
   int ngroups;
   int per_group;  // block tiles per group (the last may hold fewer)
   int total;      // block tiles of the pass
@@ -113,37 +120,15 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
   const int lane = lane_id();
   const int g = lane >> 2, t = lane & 3;
 
-  // this warp's units: NB = 2 (BS < 4): the (block tile, k-step) units of a tile are split
-  // evenly over the 8 warps, block-tile major, so a warp meets at most two block tiles.
-  // NB = 1 (BS = 4: a 32×32 accumulator is 64 registers): block tile i gets warps
-  // [8i/nbt, 8(i+1)/nbt), which split its k-steps evenly.
-  constexpr int NB = BS == 4 ? 1 : 2;
-  const int nks = tile_rows >> 2;
-  const int nbtg = (a.debug & 2) ? 0 : jobs.nbt[grp];
-  int nb = 0, ka[2] = {0, 0}, kb[2] = {0, 0}, code[2] = {0, 0};
-  if (NB == 2) {
-    const int U = nbtg * nks;
-    const int u0 = warp * U / kConsumerWarps, u1 = (warp + 1) * U / kConsumerWarps;
-    if (u1 > u0) {
-      const int b0 = u0 / nks;
-      code[0] = jobs.code[grp][b0];
-      ka[0] = u0 - b0 * nks;
-      kb[0] = min(nks, u1 - b0 * nks);
-      nb = 1;
-      if (u1 > (b0 + 1) * nks) {
-        code[1] = jobs.code[grp][b0 + 1];
-        kb[1] = u1 - (b0 + 1) * nks;
-        nb = 2;
-      }
-    }
-  } else if (nbtg > 0) {
-    int b = 0;
-    while ((b + 1) * kConsumerWarps / nbtg <= warp) ++b;
-    const int w0 = b * kConsumerWarps / nbtg, m = (b + 1) * kConsumerWarps / nbtg - w0;
-    code[0] = jobs.code[grp][b];
-    ka[0] = (warp - w0) * nks / m;
-    kb[0] = (warp - w0 + 1) * nks / m;
-    nb = kb[0] > ka[0] ? 1 : 0;
+  const WarpJob& wj = jobs.w[grp][warp];
+  const int nb = (a.debug & 2) ? 0 : wj.nb;
+  constexpr int NB = kNB;
+  int ka[NB], kb[NB], code[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    code[b] = wj.code[b];
+    ka[b] = wj.ka[b];
+    kb[b] = wj.kb[b];
   }
   // per block tile: A column offset and W column offset (this lane's row of the fragments)
   int aoff[NB], woff[NB];
@@ -177,35 +162,53 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
     for (int b = 0; b < NB; ++b) {
       if (b < nb) {
         // one k-step of block tile b: rows k0..k0+3 (lane t takes row k0 + t)
-        auto kstep = [&](const double* r0, const double* r1, double c, bool live) {
-          double av[BS], wv[BS];
-          const double* wr = reg1[b] ? r1 : r0;
+        // one k-step of block tile b: rows k0..k0+3 (lane t takes row k0 + t). Operands of
+        // step k+1 are loaded before the DMMAs of step k are issued (a lone warp on an SM
+        // sub-partition otherwise waits out the shared-memory latency every step); the
+        // count scaling is applied at use so it does not force that wait early.
+        const double* wbase = reg1[b] ? R1 : R0;
+        const int wp = reg1[b] ? a.p1 : a.p0;
+        auto load = [&](int kr, bool live, double (&av)[BS], double (&wv)[BS], double& c) {
 #pragma unroll
           for (int u = 0; u < BS; ++u) {
-            av[u] = live ? r0[aoff[b] + 8 * u] : 0.0;
-            wv[u] = wr[woff[b] + 8 * u];
-            if (SCALE && !reg1[b]) wv[u] *= c;
+            av[u] = live ? R0[kr * a.p0 + aoff[b] + 8 * u] : 0.0;
+            wv[u] = wbase[kr * wp + woff[b] + 8 * u];
           }
+          c = SCALE && !reg1[b] ? cnt[kr] : 1.0;
+        };
+        auto mma = [&](const double (&av)[BS], const double (&wv)[BS], double c) {
 #pragma unroll
-          for (int u = 0; u < BS; ++u)
+          for (int v = 0; v < BS; ++v) {
+            const double w = SCALE ? wv[v] * c : wv[v];
 #pragma unroll
-            for (int v = 0; v < BS; ++v) dmma_8x8x4(acc[b][u * BS + v][0], acc[b][u * BS + v][1], av[u], wv[v]);
+            for (int u = 0; u < BS; ++u) dmma_8x8x4(acc[b][u * BS + v][0], acc[b][u * BS + v][1], av[u], w);
+          }
         };
         const int kend = min(kb[b], full);
-        const double* r0 = R0 + (4 * ka[b] + t) * a.p0;
-        const double* r1 = R1 + (4 * ka[b] + t) * a.p1;
-        const double* cp = SCALE ? cnt + 4 * ka[b] + t : nullptr;
-#pragma unroll 1
-        for (int k = ka[b]; k < kend; ++k) {
-          kstep(r0, r1, SCALE ? *cp : 1.0, true);
-          r0 += 4 * a.p0;
-          r1 += 4 * a.p1;
-          if (SCALE) cp += 4;
+        if (ka[b] < kend) {
+          double av[BS], wv[BS], c;
+          int kr = 4 * ka[b] + t;
+          load(kr, true, av, wv, c);
+#pragma unroll 2
+          for (int k = ka[b] + 1; k < kend; ++k) {
+            kr += 4;
+            double an[BS], wn[BS], cn;
+            load(kr, true, an, wn, cn);
+            mma(av, wv, c);
+#pragma unroll
+            for (int u = 0; u < BS; ++u) {
+              av[u] = an[u];
+              wv[u] = wn[u];
+            }
+            c = cn;
+          }
+          mma(av, wv, c);
         }
         if ((rows & 3) && full >= ka[b] && full < kb[b]) {  // ragged last k-step of the last tile
           const bool live = 4 * full + t < rows;
-          const int kr = live ? 4 * full + t : 0;
-          kstep(R0 + kr * a.p0, R1 + kr * a.p1, SCALE ? cnt[kr] : 1.0, live);
+          double av[BS], wv[BS], c;
+          load(live ? 4 * full + t : 0, live, av, wv, c);
+          mma(av, wv, c);
         }
       }
     }
@@ -309,34 +312,16 @@ struct ReduceArgs {
   int off0, off1;   // output offsets
   double* out;
   int64_t ldo;
-  int bsz, t2a, t2b, per_group, total, nks;  // the job layout of the pass (BlockJobs, build_block_jobs)
-  int nb;                                     // block tiles per warp: 2 (linear unit split) or 1 (BS = 4)
+  int bsz, t2a, t2b;  // block layout of the pass (build_block_jobs enumeration order)
+  uint8_t wmask[kMaxBT];  // per block tile: the consumer warps that wrote it
 };
 
-// Partial element (i, pc) -> its block tile -> the consumer warps [wf, wf + nw) that wrote it.
-FB_DEV void tile_writers(const ReduceArgs& r, int i, int pc, int& wf, int& nw) {
+// Partial element (i, pc) -> its block tile -> the mask of consumer warps that wrote it.
+FB_DEV uint32_t tile_writers(const ReduceArgs& r, int i, int pc) {
   const int bi = i / r.bsz;
   int idx = bi * (r.t2a + r.t2b) - bi * (bi - 1) / 2;
   idx += pc < r.w1_col0 ? pc / r.bsz - bi : (r.t2a - bi) + (pc - r.w1_col0) / r.bsz;
-  const int gi = idx / r.per_group, lb = idx - gi * r.per_group;
-  const int nbtg = min(r.per_group, r.total - gi * r.per_group);
-  if (r.nb == 1) {  // proportional warp sets (cp_gram_kernel, NB = 1)
-    wf = lb * kConsumerWarps / nbtg;
-    nw = (lb + 1) * kConsumerWarps / nbtg - wf;
-    return;
-  }
-  const int U = nbtg * r.nks;
-  const int lo = lb * r.nks, hi = lo + r.nks;
-  wf = kConsumerWarps;
-  int wl = -1;
-  for (int w = 0; w < kConsumerWarps; ++w) {
-    const int u0 = w * U / kConsumerWarps, u1 = (w + 1) * U / kConsumerWarps;
-    if (u1 > u0 && u1 > lo && u0 < hi) {
-      wf = min(wf, w);
-      wl = w;
-    }
-  }
-  nw = wl - wf + 1;
+  return r.wmask[idx];
 }
 
 FB_DEV bool reduce_coords(const ReduceArgs& r, int64_t e, int& i, int& pc, int& orow, int& ocol) {
@@ -363,14 +348,14 @@ FB_DEV bool reduce_coords(const ReduceArgs& r, int64_t e, int& i, int& pc, int& 
 __global__ void cp_reduce_kernel(ReduceArgs r) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (e >= static_cast<int64_t>(r.da) * (r.da + r.db)) return;
-  int i, pc, orow, ocol, wf, nw;
+  int i, pc, orow, ocol;
   if (!reduce_coords(r, e, i, pc, orow, ocol)) return;
-  tile_writers(r, i, pc, wf, nw);
+  const uint32_t mask = tile_writers(r, i, pc);
   const size_t stride = static_cast<size_t>(r.ra) * r.cw;
-  const double* p = r.partials + static_cast<size_t>(i) * r.cw + pc + wf * stride;
+  const double* p = r.partials + static_cast<size_t>(i) * r.cw + pc;
   double s = 0.0;
   for (int x = 0; x < r.gridx; ++x) {
-    for (int w = 0; w < nw; ++w) s += p[w * stride];
+    for (uint32_t m = mask; m; m &= m - 1) s += p[(__ffs(m) - 1) * stride];
     p += kConsumerWarps * stride;
   }
   r.out[orow * r.ldo + ocol] = s;
@@ -380,14 +365,14 @@ __global__ void cp_reduce_kernel(ReduceArgs r) {
 // Small outputs (e.g. WᵀW with r = 5) over many partials: one CTA per element, a fixed
 // strided split over the partials and a fixed shared-memory tree (deterministic).
 __global__ void cp_reduce_small_kernel(ReduceArgs r) {
-  int i, pc, orow, ocol, wf, nw;
+  int i, pc, orow, ocol;
   if (!reduce_coords(r, blockIdx.x, i, pc, orow, ocol)) return;
-  tile_writers(r, i, pc, wf, nw);
+  const uint32_t mask = tile_writers(r, i, pc);
   const size_t stride = static_cast<size_t>(r.ra) * r.cw;
-  const double* p = r.partials + static_cast<size_t>(i) * r.cw + pc + wf * stride;
+  const double* p = r.partials + static_cast<size_t>(i) * r.cw + pc;
   double s = 0.0;
-  const int nq = r.gridx * nw;
-  for (int q = threadIdx.x; q < nq; q += blockDim.x) s += p[(static_cast<size_t>(q / nw) * kConsumerWarps + q % nw) * stride];
+  for (int x = threadIdx.x; x < r.gridx; x += blockDim.x)
+    for (uint32_t m = mask; m; m &= m - 1) s += p[(static_cast<size_t>(x) * kConsumerWarps + __ffs(m) - 1) * stride];
   __shared__ double red[256];
   red[threadIdx.x] = s;
   __syncthreads();
@@ -415,8 +400,11 @@ static void launch_reduce(const ReduceArgs& r, cudaStream_t st) {
 namespace {
 
 // Upper-triangle block tiles of a T2a × T2a gram, plus a full T2a × T2b rectangle (region 1),
-// in row-major order (tile_writers depends on it), cut into ngroups equal groups of <= kMaxBTG.
-bool build_block_jobs(int T2a, int T2b, BlockJobs& J) {
+// in row-major order (tile_writers depends on it), cut into ngroups equal groups; in each
+// group the units are split over the consumer warps as described at WarpJob. The first
+// `walkers` consumer warps of group 0 run the KᵀS walk and get no units. wmask receives,
+// per block tile, the warps that hold units of it.
+bool build_block_jobs(int T2a, int T2b, int nks, int walkers, BlockJobs& J, uint8_t* wmask) {
   std::vector<uint16_t> list;
   for (int bi = 0; bi < T2a; ++bi) {
     for (int bj = bi; bj < T2a; ++bj) list.push_back(static_cast<uint16_t>(bi | (bj << 6)));
@@ -428,15 +416,50 @@ bool build_block_jobs(int T2a, int T2b, BlockJobs& J) {
   J.per_group = 1;
   J.total = bt;
   if (bt == 0) return true;
-  if (T2a > 63 || T2b > 63) return false;
-  J.ngroups = (bt + kMaxBTG - 1) / kMaxBTG;
-  if (J.ngroups > kMaxGroups) return false;
-  J.per_group = (bt + J.ngroups - 1) / J.ngroups;
-  for (int b = 0; b < bt; ++b) {
-    const int gi = b / J.per_group;
-    J.code[gi][J.nbt[gi]++] = list[b];
+  if (T2a > 63 || T2b > 63 || bt > kMaxBT || nks > 255) return false;
+  for (int ng = 1; ng <= kMaxGroups; ++ng) {
+    J = BlockJobs{};
+    J.ngroups = ng;
+    J.per_group = (bt + ng - 1) / ng;
+    J.total = bt;
+    std::fill(wmask, wmask + kMaxBT, 0);
+    bool ok = true;
+    for (int gi = 0; gi < ng && ok; ++gi) {
+      const int b0 = gi * J.per_group, nbtg = std::min(J.per_group, bt - b0);
+      if (nbtg <= 0) break;
+      const int first = gi == 0 ? walkers : 0;
+      // sub-partition of consumer warp w: its hardware warp slot mod 4
+      int m[4] = {0, 0, 0, 0};
+      for (int w = first; w < kConsumerWarps; ++w) ++m[(kServiceWarps + w) % 4];
+      int nsp = 0;
+      for (int q = 0; q < 4; ++q) nsp += m[q] > 0;
+      const int64_t U = static_cast<int64_t>(nbtg) * nks;
+      double cum = 0.0;
+      int64_t u0 = 0;
+      for (int w = first; w < kConsumerWarps && ok; ++w) {
+        cum += 1.0 / (m[(kServiceWarps + w) % 4] * nsp);
+        int64_t u1 = w == kConsumerWarps - 1 ? U : static_cast<int64_t>(cum * U + 0.5);
+        if (u1 > U) u1 = U;
+        WarpJob& wj = J.w[gi][w];
+        while (u0 < u1) {
+          const int b = static_cast<int>(u0 / nks);
+          const int64_t e = std::min<int64_t>(u1, static_cast<int64_t>(b + 1) * nks);
+          if (wj.nb == kNB) {
+            ok = false;
+            break;
+          }
+          wj.code[wj.nb] = list[b0 + b];
+          wj.ka[wj.nb] = static_cast<uint8_t>(u0 - static_cast<int64_t>(b) * nks);
+          wj.kb[wj.nb] = static_cast<uint8_t>(e - static_cast<int64_t>(b) * nks);
+          ++wj.nb;
+          wmask[b0 + b] |= static_cast<uint8_t>(1u << w);
+          u0 = e;
+        }
+      }
+    }
+    if (ok) return true;
   }
-  return true;
+  return false;
 }
 
 size_t al(size_t b) { return (b + 255) & ~size_t(255); }
@@ -462,6 +485,7 @@ cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_ro
   stream_layout(ss, tile_rows, a.n);
   int stages = static_cast<int>((200 * 1024 - kRingHeader - 256) / ss.stage_bytes);
   if (stages > 6) stages = 6;
+  if (const char* e = getenv("FB_CP_STAGES")) stages = std::min(stages, atoi(e));  // development override
   if (stages < 2) return cudaErrorNotSupported;
   // + slack: fragment loads of a padded block read up to 8·BS - 1 doubles past a row,
   // so the last row of the last stage must not sit at the end of the allocation
@@ -484,7 +508,6 @@ cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_ro
   }
   FB_GRAM_CASE(1)
   FB_GRAM_CASE(2)
-  FB_GRAM_CASE(4)
 #undef FB_GRAM_CASE
   return cudaErrorNotSupported;
 }
@@ -498,7 +521,7 @@ size_t partial_doubles(int T2a, int T2b, int num_sms, int bs) {
 // blocks reuse fragments (4 + 4 loads per 16 DMMAs) at the cost of triangle padding.
 int block_size(int da) {
   if (const char* e = getenv("FB_CP_BS")) return atoi(e);  // development override (1, 2 or 4)
-  return da <= 8 ? 1 : (da <= 40 ? 2 : 4);
+  return da <= 8 ? 1 : 2;
 }
 
 }  // namespace
@@ -581,8 +604,6 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
 
   // ---- S pass: SᵀS (+ KᵀS when q = 1)
   if (c.d_s > 0 && c.n_s > 0) {
-    BlockJobs JS;
-    if (!build_block_jobs(t2s, 0, JS)) return cudaErrorNotSupported;
     GramArgs a{};
     a.n = c.n_s;
     a.p0 = a.p1 = c.d_s;
@@ -608,16 +629,20 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
       a.carry_val = cval;
     }
     const int tr = gram_tile_rows(ss.row_bytes[0] + (q ? 4u : 0u), q != 0);
+    ReduceArgs r{sp, 0, a.ra, a.cw, a.w1_col0, c.d_s, 0, 0, 0, c.out, d, 8 * bs_s, t2s, 0, {}};
+    BlockJobs JS;
+    // consumer warps 0..walkers-1 run the KᵀS walk (d_S columns, one per thread) and get no DMMA units
+    const int walkers = q ? (c.d_s + 31) / 32 : 0;
+    if (!build_block_jobs(t2s, 0, tr / 4, walkers, JS, r.wmask)) return cudaErrorNotSupported;
     int gridx = 0;
     e = run_gram(JS, a, ss, tr, st, num_sms, &gridx, bs_s);
+    r.gridx = gridx;
     if (e != cudaSuccess) return e;
     if (q) {
       const int grid = gridx;
       cp_carry_fixup_kernel<<<1, ((c.d_s + 31) / 32) * 32, 0, st>>>(ckey, cval, 2 * grid, c.d_s, bins, c.n_r);
       FB_LAUNCHED();
     }
-    ReduceArgs r{sp, gridx, a.ra, a.cw, a.w1_col0, c.d_s, 0, 0, 0, c.out, d, 8 * bs_s, t2s, 0, JS.per_group, JS.total, tr / 4,
-                 bs_s == 4 ? 1 : 2};
     launch_reduce(r, st);
   } else if (q && c.d_s > 0) {
     e = cudaMemsetAsync(bins, 0, static_cast<size_t>(c.n_r) * c.d_s * 8, st);  // no rows: KᵀS = 0
@@ -626,8 +651,6 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
 
   // ---- R pass: Rᵀ diag(c) R (upper) and RᵀB
   if (q && c.d_r > 0 && c.n_r > 0) {
-    BlockJobs JR;
-    if (!build_block_jobs(t2r, t2b, JR)) return cudaErrorNotSupported;
     GramArgs a{};
     a.n = c.n_r;
     // pitch ≡ 4 (mod 8) doubles keeps the 8-row fragment loads bank-conflict free
@@ -650,11 +673,13 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     ss.row_bytes[2] = 8u;
     ss.count = 3;
     const int tr = gram_tile_rows(pr * 8u + c.d_s * 8u + 8u, false);
+    ReduceArgs r{rp, 0, a.ra, a.cw, a.w1_col0, c.d_r, c.d_s, c.d_s, 0, c.out, d, 8 * bs_r, t2r, t2b, {}};
+    BlockJobs JR;
+    if (!build_block_jobs(t2r, t2b, tr / 4, 0, JR, r.wmask)) return cudaErrorNotSupported;
     int gridx = 0;
     e = run_gram(JR, a, ss, tr, st, num_sms, &gridx, bs_r);
+    r.gridx = gridx;
     if (e != cudaSuccess) return e;
-    ReduceArgs r{rp, gridx, a.ra, a.cw, a.w1_col0, c.d_r, c.d_s, c.d_s, 0, c.out, d, 8 * bs_r, t2r, t2b, JR.per_group,
-                 JR.total, tr / 4, bs_r == 4 ? 1 : 2};
     launch_reduce(r, st);
   }
   return cudaGetLastError();
