@@ -277,27 +277,41 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
 // (first run, last run) pairs per CTA; interior gaps were zeroed by the walker.
 __global__ void cp_carry_fixup_kernel(const int* carry_key, const double* carry_val, int nslots, int cols,
                                       double* bins, int64_t n_bins) {
-  const int c = threadIdx.x;
-  if (c >= cols) return;
-  int cur = -1, prev = -1;
-  double sum = 0.0;
-  for (int i = 0; i < nslots; ++i) {
-    const int k = carry_key[i];
-    if (k < 0) continue;
-    const double v = carry_val[static_cast<size_t>(i) * cols + c];
-    if (k == cur) {
-      sum += v;
-      continue;
+  // one CTA per carry slot (threads over columns): the slot that starts a key's run of slots
+  // sums that run in slot order and writes the bins row; slots of a CTA's first run also
+  // zero the keys between the previous run and theirs (a CTA seam), the last run the tail
+  const int i = blockIdx.x;
+  const int k = carry_key[i];
+  if (k < 0) return;
+  int prev = -1;  // key of the previous valid slot
+  for (int j = i - 1; j >= 0; --j)
+    if (carry_key[j] >= 0) {
+      prev = carry_key[j];
+      break;
     }
-    if (cur >= 0) bins[static_cast<int64_t>(cur) * cols + c] = sum;
+  if (prev == k) return;  // not the head of its run of slots
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    double sum = 0.0;
+    int last = i;
+    for (int j = i; j < nslots; ++j) {
+      const int kj = carry_key[j];
+      if (kj < 0) continue;
+      if (kj != k) break;
+      sum += carry_val[static_cast<size_t>(j) * cols + c];
+      last = j;
+    }
+    bins[static_cast<int64_t>(k) * cols + c] = sum;
     if ((i & 1) == 0)
       for (int z = prev + 1; z < k; ++z) bins[static_cast<int64_t>(z) * cols + c] = 0.0;
-    cur = k;
-    sum = v;
-    prev = k;
+    bool tail = true;  // no valid slot after this run: zero the keys above it
+    for (int j = last + 1; j < nslots; ++j)
+      if (carry_key[j] >= 0) {
+        tail = false;
+        break;
+      }
+    if (tail)
+      for (int64_t z = k + 1; z < n_bins; ++z) bins[z * cols + c] = 0.0;
   }
-  if (cur >= 0) bins[static_cast<int64_t>(cur) * cols + c] = sum;
-  for (int64_t z = prev + 1; z < n_bins; ++z) bins[z * cols + c] = 0.0;
 }
 
 // Final assembly of one pass: element (i, j) of the pass = Σ over CTAs x, then over the
@@ -345,8 +359,11 @@ FB_DEV bool reduce_coords(const ReduceArgs& r, int64_t e, int& i, int& pc, int& 
   return true;
 }
 
+// One warp per output element: lanes stride over the CTAs, then a fixed butterfly
+// (deterministic); the per-element serial loop was latency bound (~100 us per pass).
 __global__ void cp_reduce_kernel(ReduceArgs r) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t e = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (e >= static_cast<int64_t>(r.da) * (r.da + r.db)) return;
   int i, pc, orow, ocol;
   if (!reduce_coords(r, e, i, pc, orow, ocol)) return;
@@ -354,45 +371,18 @@ __global__ void cp_reduce_kernel(ReduceArgs r) {
   const size_t stride = static_cast<size_t>(r.ra) * r.cw;
   const double* p = r.partials + static_cast<size_t>(i) * r.cw + pc;
   double s = 0.0;
-  for (int x = 0; x < r.gridx; ++x) {
-    for (uint32_t m = mask; m; m &= m - 1) s += p[(__ffs(m) - 1) * stride];
-    p += kConsumerWarps * stride;
-  }
-  r.out[orow * r.ldo + ocol] = s;
-  r.out[ocol * r.ldo + orow] = s;
-}
-
-// Small outputs (e.g. WᵀW with r = 5) over many partials: one CTA per element, a fixed
-// strided split over the partials and a fixed shared-memory tree (deterministic).
-__global__ void cp_reduce_small_kernel(ReduceArgs r) {
-  int i, pc, orow, ocol;
-  if (!reduce_coords(r, blockIdx.x, i, pc, orow, ocol)) return;
-  const uint32_t mask = tile_writers(r, i, pc);
-  const size_t stride = static_cast<size_t>(r.ra) * r.cw;
-  const double* p = r.partials + static_cast<size_t>(i) * r.cw + pc;
-  double s = 0.0;
-  for (int x = threadIdx.x; x < r.gridx; x += blockDim.x)
+  for (int x = lane; x < r.gridx; x += 32)
     for (uint32_t m = mask; m; m &= m - 1) s += p[(static_cast<size_t>(x) * kConsumerWarps + __ffs(m) - 1) * stride];
-  __shared__ double red[256];
-  red[threadIdx.x] = s;
-  __syncthreads();
-  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
-    if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    r.out[orow * r.ldo + ocol] = red[0];
-    r.out[ocol * r.ldo + orow] = red[0];
+  s = warp_sum(s);
+  if (lane == 0) {
+    r.out[orow * r.ldo + ocol] = s;
+    r.out[ocol * r.ldo + orow] = s;
   }
 }
 
 static void launch_reduce(const ReduceArgs& r, cudaStream_t st) {
-  const int n = r.da * r.da + r.da * r.db;
-  if (n <= 2048 && r.gridx >= 32) {
-    cp_reduce_small_kernel<<<n, 256, 0, st>>>(r);
-  } else {
-    cp_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(r);
-  }
+  const int64_t n = static_cast<int64_t>(r.da) * (r.da + r.db);
+  cp_reduce_kernel<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, st>>>(r);
   FB_LAUNCHED();
 }
 
@@ -640,7 +630,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     if (e != cudaSuccess) return e;
     if (q) {
       const int grid = gridx;
-      cp_carry_fixup_kernel<<<1, ((c.d_s + 31) / 32) * 32, 0, st>>>(ckey, cval, 2 * grid, c.d_s, bins, c.n_r);
+      cp_carry_fixup_kernel<<<2 * grid, ((c.d_s + 31) / 32) * 32, 0, st>>>(ckey, cval, 2 * grid, c.d_s, bins, c.n_r);
       FB_LAUNCHED();
     }
     launch_reduce(r, st);
