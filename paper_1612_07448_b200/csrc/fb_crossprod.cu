@@ -643,8 +643,11 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
   if (q && c.d_r > 0 && c.n_r > 0) {
     GramArgs a{};
     a.n = c.n_r;
-    // pitch ≡ 4 (mod 8) doubles keeps the 8-row fragment loads bank-conflict free
-    const int pr = (c.d_r % 8 == 0) ? c.d_r + 4 : c.d_r;
+    // Fragment loads read 8 consecutive doubles from each of 4 rows: conflict free unless
+    // the row pitch is a multiple of 16 doubles (then all 4 rows hit the same 16 banks).
+    // Only that case gets 4 doubles of padding — an unpadded R streams with bulk copies,
+    // a padded one needs the producer's per-chunk cp.async.
+    const int pr = (c.d_r % 16 == 0) ? c.d_r + 4 : c.d_r;
     a.p0 = pr;
     a.p1 = c.d_s > 0 ? c.d_s : 1;
     a.s1 = c.d_s > 0 ? 1 : -1;
