@@ -270,24 +270,19 @@ struct TileRing {
   }
 
   // Gatherer warps body. A stage's gathers start as soon as the stage is free (its
-  // "empty" phase), in parallel with the producer's stream copies. The keys come from
-  // global memory and are loaded kKeyAhead tiles ahead into rotating register sets (the
-  // tile loop is unrolled by kKeyAhead so every set is named statically; a one-tile
-  // lookahead left one HBM latency per tile exposed: 1.8 TB/s on an HBM-resident gather).
-  // Gatherer warp gw owns ring rows r ≡ gw (mod kGatherWarps) (<= 64 of them: tiles of at
-  // most 256 rows).
+  // "empty" phase), in parallel with the producer's stream copies: the keys come from
+  // global memory, loaded one tile ahead, so a gathered tile costs max(stream, key +
+  // gather) latency rather than their sum. Gatherer warp gw owns ring rows
+  // r ≡ gw (mod kGatherWarps) (<= 64 of them: tiles of at most 256 rows).
   FB_DEV void gather(const StreamSet& s) const {
-    constexpr int kKeyAhead = 3;
-    using Keys = int32_t[kMaxGather + 1][2];
     const int lane = threadIdx.x & 31;
     const int gw = (static_cast<int>(threadIdx.x) >> 5) - 1;
     int st = 0;
     uint32_t ph = 0;
     const int64_t n = count();
     // keys / gidx of this warp's rows gw + kGatherWarps·(lane + 32 j), j < 2
-    auto load_keys = [&](Keys& kn, int64_t k) {
-      if (k >= n) return;
-      const int64_t tile = tile_begin + k;
+    int32_t kc[kMaxGather + 1][2], kn[kMaxGather + 1][2];
+    auto load_keys = [&](int64_t tile) {
       const int rows = rows_of(tile);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
@@ -299,16 +294,23 @@ struct TileRing {
         kn[kMaxGather][j] = (s.gidx && live) ? __ldg(s.gidx + tile * tile_rows + r) : 0;
       }
     };
-    auto body = [&](int64_t k, Keys& kc) {
-      // key of this warp's row index ri (warp-uniform call; ri may differ per lane)
-      auto key_of = [&](int g, int ri) {
-        const int v0 = __shfl_sync(0xffffffffu, kc[g][0], ri & 31);
-        const int v1 = __shfl_sync(0xffffffffu, kc[g][1], ri & 31);
-        return ri < 32 ? v0 : v1;
-      };
+    // key of this warp's row index ri (warp-uniform call; ri may differ per lane)
+    auto key_of = [&](int g, int ri) {
+      const int v0 = __shfl_sync(0xffffffffu, kc[g][0], ri & 31);
+      const int v1 = __shfl_sync(0xffffffffu, kc[g][1], ri & 31);
+      return ri < 32 ? v0 : v1;
+    };
+    if (n > 0) load_keys(tile_begin);
+    for (int64_t k = 0; k < n; ++k) {
       const int64_t tile = tile_begin + k;
       const int rows = rows_of(tile);
       const int rows_w = rows > gw ? (rows - gw + kGatherWarps - 1) / kGatherWarps : 0;  // rows of this warp
+#pragma unroll
+      for (int g = 0; g <= kMaxGather; ++g) {
+        kc[g][0] = kn[g][0];
+        kc[g][1] = kn[g][1];
+      }
+      if (k + 1 < n) load_keys(tile + 1);  // latency overlaps this stage's wait and copies
       if (k >= stages) mbar_wait(&empty[st], ph ^ 1u);  // the stage is free again
       if (s.gidx && bulk_ok(s, tile)) {
         // stream 0 rows in gidx order: one row per instruction, lanes over 16-byte chunks
@@ -372,23 +374,6 @@ struct TileRing {
       if (++st == stages) {
         st = 0;
         ph ^= 1u;
-      }
-    };
-    Keys k0, k1, k2;
-    static_assert(kKeyAhead == 3, "three named key sets");
-    load_keys(k0, 0);
-    load_keys(k1, 1);
-    load_keys(k2, 2);
-    for (int64_t k = 0; k < n; k += kKeyAhead) {
-      body(k, k0);
-      load_keys(k0, k + 3);
-      if (k + 1 < n) {
-        body(k + 1, k1);
-        load_keys(k1, k + 4);
-      }
-      if (k + 2 < n) {
-        body(k + 2, k2);
-        load_keys(k2, k + 5);
       }
     }
     // do not retire the warp with copies (and their barrier arrivals) still in flight
