@@ -28,13 +28,7 @@ void count_launch(const char* file, int line) {
     if (err != cudaSuccess) fprintf(stderr, "[fb] kernel launched at %s:%d failed: %s\n", file, line, cudaGetErrorString(err));
   }
 }
-}  // namespace fb
-
 namespace {
-
-thread_local char g_err[512] = "";
-int g_num_sms = 148;
-
 // Fork/join onto a library-owned side stream so independent passes of one operator overlap
 // (stream-ordered and CUDA-graph capturable: record → wait → launch → record → wait).
 struct SideStream {
@@ -43,6 +37,8 @@ struct SideStream {
   int device = -1;
 };
 thread_local SideStream g_side;
+}  // namespace
+
 
 cudaError_t side_fork(cudaStream_t main, cudaStream_t* side) {
   int dev = 0;
@@ -65,6 +61,13 @@ cudaError_t side_join(cudaStream_t main) {
   if (e == cudaSuccess) e = cudaStreamWaitEvent(main, g_side.join, 0);
   return e;
 }
+
+}  // namespace fb
+
+namespace {
+
+thread_local char g_err[512] = "";
+int g_num_sms = 148;
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -322,7 +325,7 @@ static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_
         // X·K_i as segmented sums over the FK-sorted order (few atomics, no hot-line
         // contention), on the side stream so they overlap the S pass
         if (!forked) {
-          cudaError_t e = side_fork(cs(stream), &side);
+          cudaError_t e = fb::side_fork(cs(stream), &side);
           if (e != cudaSuccess) return cuda_status(e, "wt(fork)");
           forked = true;
         }
@@ -350,7 +353,7 @@ static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_
     cudaError_t e = fb::launch_colreduce(c, cs(stream), g_num_sms);
     if (e != cudaSuccess) return cuda_status(e, "wt(S)");
     if (forked) {
-      e = side_join(cs(stream));  // the R passes below read the segmented bins
+      e = fb::side_join(cs(stream));  // the R passes below read the segmented bins
       if (e != cudaSuccess) return cuda_status(e, "wt(join)");
     }
     int64_t off = nm->d_s;

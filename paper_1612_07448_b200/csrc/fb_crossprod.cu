@@ -66,45 +66,99 @@ struct GramArgs {
   int ra, cw;           // partial matrix: ra rows (8·BS·T2a) × cw cols (8·BS·(T2a + T2b))
   int w1_col0;          // first partial column of region 1 (8·BS·T2a)
   double* partials;     // [gridDim.x · 8 warps][ra][cw] (a warp writes only its block tiles)
-  // S pass only: segmented KᵀS
-  int seg;              // 1: run the segmented walk (stream 1 = sorted keys, int32)
-  int seg_cols;         // d_S
-  double* bins;         // n_R × d_S
-  int* carry_key;       // [gridDim.x][2]
-  double* carry_val;    // [gridDim.x][2][d_S]
   int debug;            // development bisection bits (FB_CP_DEBUG): 1 no walk, 2 no DMMA
 };
 
-// Segmented column sums over FK-sorted rows (thread c < d_S owns column c).
-struct SegState {
-  int key;     // current run key (-1: none yet)
-  double sum;
-  bool first;  // the current run is this CTA's first (may continue from the previous CTA)
-};
-
-FB_DEV void seg_flush(const GramArgs& a, SegState& st, int col, int slot) {
-  if (st.key < 0) return;
-  if (st.first) {
-    a.carry_val[(static_cast<size_t>(blockIdx.x) * 2 + slot) * a.seg_cols + col] = st.sum;
-    if (col == 0) a.carry_key[blockIdx.x * 2 + slot] = st.key;
-  } else {
-    a.bins[static_cast<int64_t>(st.key) * a.seg_cols + col] = st.sum;
+// KᵀS (B = group-by-key column sums of S, rewrite.py:260-270 via indicator.py:130-141) as
+// a segmented reduction over the FK-sorted rows, in its own pass on a side stream beside the
+// S gram (which then streams S in storage order with bulk copies). Warp w owns a contiguous
+// range of sorted positions; lanes own columns (lane + 32 j); rows are gathered through the
+// cached permutation 8 at a time (loads in flight together) and walked in order: a key
+// change closes the run (its bins row written once, keys without rows in between zeroed).
+// The first and last run of a warp's range may continue in the neighbouring ranges: they go
+// to a carry table that cp_carry_fixup_kernel combines in order (deterministic, no atomics).
+// Many resident warps hide the walk's dependency chains (a walker inside the gram CTA had
+// two warps for the whole SM and bounded the S pass).
+template <int CJ>
+__global__ void __launch_bounds__(256, 4) kts_walk_kernel(const int32_t* __restrict__ perm,
+                                                       const int32_t* __restrict__ keys, int64_t n,
+                                                       const double* __restrict__ S, int d, double* __restrict__ bins,
+                                                       int* __restrict__ carry_key, double* __restrict__ carry_val) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t wid = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t lo = n * wid / nwarps, hi = n * (wid + 1) / nwarps;
+  int key = -1;
+  bool first = true;  // the open run is this range's first
+  double sum[CJ];
+#pragma unroll
+  for (int j = 0; j < CJ; ++j) sum[j] = 0.0;
+  auto close_open = [&](int next) {  // close the open run (if any) before key `next`
+    if (key >= 0) {
+      if (first) {
+#pragma unroll
+        for (int j = 0; j < CJ; ++j)
+          if (lane + 32 * j < d) carry_val[static_cast<size_t>(2 * wid) * d + lane + 32 * j] = sum[j];
+        if (lane == 0) carry_key[2 * wid] = key;
+        first = false;
+      } else {
+#pragma unroll
+        for (int j = 0; j < CJ; ++j)
+          if (lane + 32 * j < d) bins[static_cast<int64_t>(key) * d + lane + 32 * j] = sum[j];
+      }
+      for (int z = key + 1; z < next; ++z)
+#pragma unroll
+        for (int j = 0; j < CJ; ++j)
+          if (lane + 32 * j < d) bins[static_cast<int64_t>(z) * d + lane + 32 * j] = 0.0;
+    }
+    key = next;
+#pragma unroll
+    for (int j = 0; j < CJ; ++j) sum[j] = 0.0;
+  };
+  for (int64_t b0 = lo; b0 < hi; b0 += 32) {
+    const int cnt = static_cast<int>(hi - b0 < 32 ? hi - b0 : 32);
+    const int kl = lane < cnt ? keys[b0 + lane] : 0;
+    const int rl = lane < cnt ? perm[b0 + lane] : 0;
+    for (int j0 = 0; j0 < cnt; j0 += 8) {
+      int kk[8];
+      double vv[8][CJ];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = j0 + u;
+        kk[u] = __shfl_sync(full, kl, r & 31);
+        const int row = __shfl_sync(full, rl, r & 31);
+#pragma unroll
+        for (int j = 0; j < CJ; ++j)
+          vv[u][j] = (r < cnt && lane + 32 * j < d) ? __ldcs(S + static_cast<int64_t>(row) * d + lane + 32 * j) : 0.0;
+      }
+      if (j0 + 8 <= cnt && kk[7] == key) {  // the batch continues the open run (keys are sorted)
+#pragma unroll
+        for (int j = 0; j < CJ; ++j)
+          sum[j] += ((vv[0][j] + vv[1][j]) + (vv[2][j] + vv[3][j])) + ((vv[4][j] + vv[5][j]) + (vv[6][j] + vv[7][j]));
+        continue;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (j0 + u < cnt) {
+          if (kk[u] != key) close_open(kk[u]);
+#pragma unroll
+          for (int j = 0; j < CJ; ++j) sum[j] += vv[u][j];
+        }
+      }
+    }
   }
-}
-
-// one row of the walk: extend the current run or close it and open the run of `key`
-FB_DEV void seg_row(const GramArgs& a, SegState& st, int col, int key, double v) {
-  if (key == st.key) {
-    st.sum += v;
-    return;
+  // the open run may continue in the next range: slot 1 (slot 0 if it is also the first run)
+  const int slot = first ? 0 : 1;
+  if (key >= 0) {
+#pragma unroll
+    for (int j = 0; j < CJ; ++j)
+      if (lane + 32 * j < d) carry_val[static_cast<size_t>(2 * wid + slot) * d + lane + 32 * j] = sum[j];
   }
-  seg_flush(a, st, col, 0);
-  if (st.key >= 0) {
-    st.first = false;
-    for (int z = st.key + 1; z < key; ++z) a.bins[static_cast<int64_t>(z) * a.seg_cols + col] = 0.0;
+  if (lane == 0) {
+    carry_key[2 * wid + slot] = key;  // -1: an empty range
+    if (first) carry_key[2 * wid + 1] = -1;
   }
-  st.key = key;
-  st.sum = v;
 }
 
 template <int BS, bool SCALE>
@@ -144,10 +198,6 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
   for (int b = 0; b < NB; ++b)
 #pragma unroll
     for (int u = 0; u < BS * BS; ++u) acc[b][u][0] = acc[b][u][1] = 0.0;
-
-  const int tid = consumer_tid();
-  const bool seg = a.seg && grp == 0 && tid < a.seg_cols && !(a.debug & 1);
-  SegState sst{-1, 0.0, true};
 
   for (int64_t kt = 0; kt < ring.count(); ++kt) {
     const int stage = ring.acquire(ss, kt);
@@ -212,46 +262,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_c
         }
       }
     }
-    if (seg) {
-      const double* S = R0;
-      const int32_t* keys = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, 1));
-      const int p = a.p0;
-      int r = 0;
-      // batches of 8 rows: loads issued together; keys are sorted, so the batch lies
-      // inside the current run iff its last key equals the run's key
-      for (; r + 8 <= rows; r += 8) {
-        int kk[8];
-        double vv[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          kk[j] = keys[r + j];
-          vv[j] = S[(r + j) * p + tid];
-        }
-        if (kk[7] == sst.key) {
-          sst.sum += ((vv[0] + vv[1]) + (vv[2] + vv[3])) + ((vv[4] + vv[5]) + (vv[6] + vv[7]));
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) seg_row(a, sst, tid, kk[j], vv[j]);
-        }
-      }
-      for (; r < rows; ++r) seg_row(a, sst, tid, keys[r], S[r * p + tid]);
-    }
     ring.release();
-  }
-  if (seg) {
-    // the last run may continue into the next CTA: carry slot 1 (slot 0 if it is also the
-    // first run, in which case slot 1 is marked empty)
-    if (sst.first) {
-      seg_flush(a, sst, tid, 0);
-      if (tid == 0) a.carry_key[blockIdx.x * 2 + 1] = -1;
-    } else {
-      a.carry_val[(static_cast<size_t>(blockIdx.x) * 2 + 1) * a.seg_cols + tid] = sst.sum;
-      if (tid == 0) a.carry_key[blockIdx.x * 2 + 1] = sst.key;
-    }
-    if (sst.key < 0 && tid == 0) {  // empty CTA
-      a.carry_key[blockIdx.x * 2] = -1;
-      a.carry_key[blockIdx.x * 2 + 1] = -1;
-    }
   }
   // this (CTA, warp) partial: block tile b covers rows 8·BS·bi + 8u + g, cols 8·BS·bj + 8v + 2t
   double* part = a.partials + static_cast<size_t>(blockIdx.x * kConsumerWarps + warp) * a.ra * a.cw;
@@ -484,8 +495,8 @@ cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_ro
   dim3 gdim(gram_grid(a.n, tile_rows, J.ngroups, num_sms), J.ngroups);
   *gridx = static_cast<int>(gdim.x);
   if (getenv("FB_DEBUG_SYNC"))
-    fprintf(stderr, "[fb] gram pass n=%lld tile_rows=%d stages=%d grid=%dx%d bt=%d/group bs=%d seg=%d gidx=%d\n",
-            (long long)a.n, tile_rows, stages, gdim.x, gdim.y, J.per_group, bs, a.seg, ss.gidx != nullptr);
+    fprintf(stderr, "[fb] gram pass n=%lld tile_rows=%d stages=%d grid=%dx%d bt=%d/group bs=%d\n", (long long)a.n,
+            tile_rows, stages, gdim.x, gdim.y, J.per_group, bs);
   cudaError_t e;
 #define FB_GRAM_CASE(S)                                                                                         \
   if (bs == S) {                                                                                                \
@@ -509,6 +520,32 @@ size_t partial_doubles(int T2a, int T2b, int num_sms, int bs) {
 
 // Block size (8-column blocks per side) of a pass over widths da (A) and db (region 1): large
 // blocks reuse fragments (4 + 4 loads per 16 DMMAs) at the cost of triangle padding.
+// KᵀS walk: warps (8 per CTA, 4 CTAs per SM) and the launch (+ the ordered carry fixup).
+int kts_warps(int num_sms) { return num_sms * 4 * 8; }
+
+cudaError_t launch_kts(const CrossArgs& c, double* bins, int* ckey, double* cval, cudaStream_t st, int num_sms) {
+  const int grid = num_sms * 4;
+  const int cj = (c.d_s + 31) / 32;
+#define FB_KTS_CASE(J)                                                                                        \
+  case J:                                                                                                     \
+    kts_walk_kernel<J><<<grid, 256, 0, st>>>(c.perm, c.fk_sorted, c.n_s, c.s, c.d_s, bins, ckey, cval);      \
+    break;
+  switch (cj) {
+    FB_KTS_CASE(1)
+    FB_KTS_CASE(2)
+    FB_KTS_CASE(3)
+    FB_KTS_CASE(4)
+    default:
+      return cudaErrorNotSupported;
+  }
+#undef FB_KTS_CASE
+  FB_LAUNCHED();
+  const int slots = 2 * kts_warps(num_sms);
+  cp_carry_fixup_kernel<<<slots, ((c.d_s + 31) / 32) * 32, 0, st>>>(ckey, cval, slots, c.d_s, bins, c.n_r);
+  FB_LAUNCHED();
+  return cudaGetLastError();
+}
+
 int block_size(int da) {
   if (const char* e = getenv("FB_CP_BS")) return atoi(e);  // development override (1, 2 or 4)
   return da <= 8 ? 1 : 2;
@@ -558,9 +595,10 @@ size_t crossprod_workspace_bytes(int64_t n_s, int d_s, int64_t n_r, int d_r, int
   size_t b = al(partial_doubles(t2s, 0, num_sms, bs_s) * 8);
   b += al(partial_doubles(t2r, t2b, num_sms, bs_r) * 8);
   if (q > 0) {
-    b += al(static_cast<size_t>(n_r) * d_s * 8);                          // B = KᵀS
-    b += al(static_cast<size_t>(num_sms) * 2 * sizeof(int));              // carry keys
-    b += al(static_cast<size_t>(num_sms) * 2 * (d_s > 0 ? d_s : 1) * 8);  // carry values
+    const size_t slots = 2 * kts_warps(num_sms);
+    b += al(static_cast<size_t>(n_r) * d_s * 8);               // B = KᵀS
+    b += al(slots * sizeof(int));                               // carry keys
+    b += al(slots * static_cast<size_t>(d_s > 0 ? d_s : 1) * 8);  // carry values
   }
   (void)n_s;
   return b + 1024;
@@ -583,16 +621,26 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
   double* bins = nullptr;
   int* ckey = nullptr;
   double* cval = nullptr;
+  const size_t slots = 2 * kts_warps(num_sms);
   if (q) {
     bins = reinterpret_cast<double*>(take(static_cast<size_t>(c.n_r) * c.d_s * 8));
-    ckey = reinterpret_cast<int*>(take(static_cast<size_t>(num_sms) * 2 * sizeof(int)));
-    cval = reinterpret_cast<double*>(take(static_cast<size_t>(num_sms) * 2 * (c.d_s > 0 ? c.d_s : 1) * 8));
+    ckey = reinterpret_cast<int*>(take(slots * sizeof(int)));
+    cval = reinterpret_cast<double*>(take(slots * (c.d_s > 0 ? c.d_s : 1) * 8));
   }
   if (static_cast<size_t>(p - static_cast<char*>(ws)) > ws_bytes) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(c.out, 0, static_cast<size_t>(d) * d * 8, st);
   if (e != cudaSuccess) return e;
 
-  // ---- S pass: SᵀS (+ KᵀS when q = 1)
+  // ---- S pass: SᵀS on the main stream; KᵀS (q = 1) on the side stream, joined before the R pass
+  bool forked = false;
+  if (q && c.d_s > 0 && c.n_s > 0) {
+    cudaStream_t side = nullptr;
+    e = side_fork(st, &side);
+    if (e != cudaSuccess) return e;
+    forked = true;
+    e = launch_kts(c, bins, ckey, cval, side, num_sms);
+    if (e != cudaSuccess) return e;
+  }
   if (c.d_s > 0 && c.n_s > 0) {
     GramArgs a{};
     a.n = c.n_s;
@@ -607,35 +655,21 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     ss.base[0] = reinterpret_cast<const char*>(c.s);
     ss.row_bytes[0] = static_cast<uint32_t>(c.d_s) * 8u;
     ss.count = 1;
-    if (q) {
-      ss.gidx = c.perm;
-      ss.base[1] = reinterpret_cast<const char*>(c.fk_sorted);
-      ss.row_bytes[1] = 4u;
-      ss.count = 2;
-      a.seg = 1;
-      a.seg_cols = c.d_s;
-      a.bins = bins;
-      a.carry_key = ckey;
-      a.carry_val = cval;
-    }
-    const int tr = gram_tile_rows(ss.row_bytes[0] + (q ? 4u : 0u), q != 0);
+    const int tr = gram_tile_rows(ss.row_bytes[0], false);
     ReduceArgs r{sp, 0, a.ra, a.cw, a.w1_col0, c.d_s, 0, 0, 0, c.out, d, 8 * bs_s, t2s, 0, {}};
     BlockJobs JS;
-    // consumer warps 0..walkers-1 run the KᵀS walk (d_S columns, one per thread) and get no DMMA units
-    const int walkers = q ? (c.d_s + 31) / 32 : 0;
-    if (!build_block_jobs(t2s, 0, tr / 4, walkers, JS, r.wmask)) return cudaErrorNotSupported;
+    if (!build_block_jobs(t2s, 0, tr / 4, 0, JS, r.wmask)) return cudaErrorNotSupported;
     int gridx = 0;
     e = run_gram(JS, a, ss, tr, st, num_sms, &gridx, bs_s);
     r.gridx = gridx;
     if (e != cudaSuccess) return e;
-    if (q) {
-      const int grid = gridx;
-      cp_carry_fixup_kernel<<<2 * grid, ((c.d_s + 31) / 32) * 32, 0, st>>>(ckey, cval, 2 * grid, c.d_s, bins, c.n_r);
-      FB_LAUNCHED();
-    }
     launch_reduce(r, st);
   } else if (q && c.d_s > 0) {
     e = cudaMemsetAsync(bins, 0, static_cast<size_t>(c.n_r) * c.d_s * 8, st);  // no rows: KᵀS = 0
+    if (e != cudaSuccess) return e;
+  }
+  if (forked) {
+    e = side_join(st);  // the R pass reads B
     if (e != cudaSuccess) return e;
   }
 

@@ -88,6 +88,10 @@ struct CrossArgs {
 size_t fk_sort_workspace_bytes(int64_t n);
 cudaError_t launch_fk_sort(const int32_t* fk, int64_t n, int64_t n_r, int32_t* perm, int32_t* fk_sorted, void* ws,
                            size_t ws_bytes, cudaStream_t st, int num_sms);
+// Library-owned side stream (fb_capi.cu): fork from / join back into `main` (graph-capturable).
+cudaError_t side_fork(cudaStream_t main, cudaStream_t* side);
+cudaError_t side_join(cudaStream_t main);
+
 size_t crossprod_workspace_bytes(int64_t n_s, int d_s, int64_t n_r, int d_r, int q, int num_sms);
 cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cudaStream_t st, int num_sms);
 
