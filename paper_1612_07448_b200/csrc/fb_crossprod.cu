@@ -80,7 +80,7 @@ struct GramArgs {
 // Many resident warps hide the walk's dependency chains (a walker inside the gram CTA had
 // two warps for the whole SM and bounded the S pass).
 template <int CJ>
-__global__ void __launch_bounds__(256, 4) kts_walk_kernel(const int32_t* __restrict__ perm,
+__global__ void __launch_bounds__(256, CJ <= 2 ? 4 : 2) kts_walk_kernel(const int32_t* __restrict__ perm,
                                                        const int32_t* __restrict__ keys, int64_t n,
                                                        const double* __restrict__ S, int d, double* __restrict__ bins,
                                                        int* __restrict__ carry_key, double* __restrict__ carry_val) {
