@@ -155,6 +155,16 @@ int fb_glm_eval(const fb_normalized* nm, const double* y, const double* w, int32
  * iteration whose weights are not finite (ml.py:190-192; *diverged starts at -1). */
 int fb_glm_step(const fb_normalized* nm, const double* y, double* w, int32_t mode, double alpha, int32_t it,
                 double* trace, int32_t* diverged, void* ws, size_t ws_bytes, fb_stream_t stream);
+/* A whole GD run (iters steps of fb_glm_step: ml.py:199-215 / 239-254). When the factors are
+   L2-resident it runs as ONE cooperative launch (three grid barriers per iteration), else as
+   iters fused steps. w, trace[iters] and *diverged (= -1) are initialised by the caller;
+   results match fb_glm_step's up to the order of the Kᵀp atomics.
+   Replaces the reference's driver loop ml.py:205-214 / 245-253. */
+size_t fb_glm_run_workspace_bytes(const fb_normalized* nm);
+/* 1 when fb_glm_run takes the single cooperative launch for this matrix (not graph-captured). */
+int fb_glm_run_fused(const fb_normalized* nm);
+int fb_glm_run(const fb_normalized* nm, const double* y, double* w, int32_t mode, double alpha, int32_t iters,
+               double* trace, int32_t* diverged, void* ws, size_t ws_bytes, fb_stream_t stream);
 
 /* One K-Means iteration (ml.py:275-283) on an untransposed T with k <= 16 clusters:
  * c is the d × k centroid matrix (updated in place; empty clusters keep theirs), cc[j] =

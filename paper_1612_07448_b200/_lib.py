@@ -85,6 +85,9 @@ _SIGS = {
     "fb_glm_workspace_bytes": (c_size, [_P]),
     "fb_glm_eval": (c_i32, [_P, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_size, c_vp]),
     "fb_glm_step": (c_i32, [_P, c_vp, c_vp, c_i32, c_f64, c_i32, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "fb_glm_run_workspace_bytes": (c_size, [_P]),
+    "fb_glm_run_fused": (c_i32, [_P]),
+    "fb_glm_run": (c_i32, [_P, c_vp, c_vp, c_i32, c_f64, c_i32, c_vp, c_vp, c_vp, c_size, c_vp]),
     "fb_kmeans_workspace_bytes": (c_size, [_P, c_i32]),
     "fb_kmeans_step": (c_i32, [_P, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "fb_gnmf_workspace_bytes": (c_size, [_P, c_i32]),

@@ -595,6 +595,62 @@ int fb_glm_step(const fb_normalized* nm, const double* y, double* w, int32_t mod
                      "glm(update)");
 }
 
+// Whole GD run: one cooperative launch when the factors are L2-resident (fb_glm_run.cu),
+// else `iters` fused steps. The caller initialises w, trace and *diverged (= -1).
+size_t fb_glm_run_workspace_bytes(const fb_normalized* nm) {
+  if (!nm) return 0;
+  int64_t nr[FB_MAX_PARTS] = {};
+  for (int i = 0; i < nm->q; ++i) nr[i] = nm->part[i].n_r;
+  return std::max(fb_glm_workspace_bytes(nm),
+                  fb::glm_run_workspace_bytes(static_cast<int>(total_cols(nm)), nr, nm->q, g_num_sms));
+}
+
+int fb_glm_run_fused(const fb_normalized* nm) {
+  if (!nm || check_nm(nm)) return 0;
+  if (getenv("FB_GLM_STEPWISE")) return 0;  // force the per-iteration path (tests, comparisons)
+  int dr[FB_MAX_PARTS] = {};
+  for (int i = 0; i < nm->q; ++i) dr[i] = nm->part[i].d_r;
+  return fb::glm_run_eligible(nm->n_s, nm->d_s, nm->q, dr, g_num_sms) ? 1 : 0;
+}
+
+int fb_glm_run(const fb_normalized* nm, const double* y, double* w, int32_t mode, double alpha, int32_t iters,
+               double* trace, int32_t* diverged, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (mode != 0 && mode != 1) return fail(FB_ERR_ARG, "glm: unknown mode %d", mode);
+  if ((!y && nm->n_s > 0) || !w || !trace || !diverged || iters < 0) return fail(FB_ERR_ARG, "glm: bad argument");
+  if (nm->d_s > 256 || max_width(nm) > 256) return fail(FB_ERR_ARG, "glm: factor widths above 256 are not supported");
+  if (ws_bytes < fb_glm_run_workspace_bytes(nm)) return fail(FB_ERR_ARG, "glm: workspace too small");
+  int dr[FB_MAX_PARTS] = {};
+  for (int i = 0; i < nm->q; ++i) dr[i] = nm->part[i].d_r;
+  if (iters > 0 && fb_glm_run_fused(nm)) {
+    fb::GlmRunIn in{};
+    in.s = nm->s;
+    in.n = nm->n_s;
+    in.ds = nm->d_s;
+    in.y = y;
+    in.mode = mode;
+    in.alpha = alpha;
+    in.q = nm->q;
+    for (int i = 0; i < nm->q; ++i) {
+      in.fk[i] = nm->part[i].fk;
+      in.r[i] = nm->part[i].r;
+      in.nr[i] = nm->part[i].n_r;
+      in.dr[i] = nm->part[i].d_r;
+    }
+    in.w = w;
+    in.iters = iters;
+    in.trace = trace;
+    in.diverged = diverged;
+    return cuda_status(fb::launch_glm_run(in, ws, ws_bytes, cs(stream), g_num_sms), "glm_run");
+  }
+  for (int it = 0; it < iters; ++it) {
+    st = fb_glm_step(nm, y, w, mode, alpha, it, trace, diverged, ws, ws_bytes, stream);
+    if (st) return st;
+  }
+  return FB_OK;
+}
+
 // ------------------------------------------------------------------ K-Means / GNMF steps
 size_t fb_kmeans_workspace_bytes(const fb_normalized* nm, int32_t k) {
   if (!nm || k < 1) return 0;

@@ -113,6 +113,28 @@ struct GlmArgs {
   unsigned* counter;           // one zeroed word
 };
 size_t glm_partials_doubles(int d, int num_sms);
+
+// Whole GD run in one cooperative launch (fb_glm_run.cu), for L2-resident problems.
+struct GlmRunIn {
+  const double* s;
+  int64_t n;
+  int ds;
+  const double* y;
+  int mode;
+  double alpha;  // the step size (sign applied per mode)
+  int q;
+  const int32_t* fk[kMaxParts];
+  const double* r[kMaxParts];
+  int64_t nr[kMaxParts];
+  int dr[kMaxParts];
+  double* w;
+  int iters;
+  double* trace;
+  int* diverged;
+};
+bool glm_run_eligible(int64_t n, int ds, int q, const int* dr, int num_sms);
+size_t glm_run_workspace_bytes(int d, const int64_t* nr, int q, int num_sms);
+cudaError_t launch_glm_run(const GlmRunIn& in, void* ws, size_t ws_bytes, cudaStream_t st, int num_sms);
 cudaError_t launch_glm_spass(const GlmArgs& g, cudaStream_t st, int num_sms);
 cudaError_t launch_glm_update(double* w, const double* g, int d, double alpha, const double* loss, double* trace,
                               int it, int* diverged, cudaStream_t st);

@@ -161,14 +161,14 @@ def _glm_run(so, cs, yd, w, trace, diverged, ws, mode, cfg, st):
     w.zero_()
     trace.zero_()
     diverged.fill_(-1)
-    for it in range(cfg.iterations):
-        _lib.check(so.fb_glm_step(cs, D.ptr(yd), D.ptr(w), mode, float(cfg.step_size), it, D.ptr(trace),
-                                  D.ptr(diverged), ws.data_ptr(), ws.numel(), st))
+    _lib.check(so.fb_glm_run(cs, D.ptr(yd), D.ptr(w), mode, float(cfg.step_size), cfg.iterations, D.ptr(trace),
+                             D.ptr(diverged), ws.data_ptr(), ws.numel(), st))
 
 
 def _glm_gd(m, y, cfg, mode, name):
-    """GD loop; each iteration is one fused pass (fb_glm_step). The whole run is captured once
-    into a CUDA graph and replayed (c1 is launch-latency bound: ~5 kernels per iteration)."""
+    """GD loop (fb_glm_run). L2-resident problems (c1) run the whole loop as ONE cooperative
+    launch; larger ones run one fused pass per iteration (fb_glm_step), captured once into a
+    CUDA graph and replayed."""
     nm = _matrix(m)
     n, d = nm.shape
     yd = _column(y, n)
@@ -184,9 +184,9 @@ def _glm_gd(m, y, cfg, mode, name):
         w = torch.zeros(d, dtype=torch.float64, device=dev)
         trace = torch.zeros(cfg.iterations, dtype=torch.float64, device=dev)
         diverged = torch.full((1,), -1, dtype=torch.int32, device=dev)
-        ws = torch.empty(max(int(so.fb_glm_workspace_bytes(cs)), 256), dtype=torch.uint8, device=dev)
+        ws = torch.empty(max(int(so.fb_glm_run_workspace_bytes(cs)), 256), dtype=torch.uint8, device=dev)
         _glm_run(so, cs, yd, w, trace, diverged, ws, mode, cfg, D.stream_handle())  # eager run (and warm-up)
-        if os.environ.get("FB_NO_GRAPHS") is None:
+        if os.environ.get("FB_NO_GRAPHS") is None and not so.fb_glm_run_fused(cs):
             graph = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream(device=dev)
             side.wait_stream(torch.cuda.current_stream())

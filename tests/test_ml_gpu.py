@@ -184,3 +184,31 @@ def test_logreg_graph_replay_matches_eager(monkeypatch):
     w, obj = O.logistic_gd(ref, y, 6, 1e-3)
     _close(again.weights, w)
     _close(again.objective, obj)
+
+
+def test_logreg_fused_run_matches_stepwise(monkeypatch):
+    """The single cooperative GD launch (L2-resident problems) and the per-iteration fused
+    steps (CUDA graph) agree to rounding (the Kᵀp scatter uses atomics) and with the oracle."""
+    fb = _fb()
+    rng, s, parts = _c1_like(22, n_s=50_000, n_r=4000)
+    nm, ref = _both(s, parts)
+    y = np.where(O.lmm(ref, rng.standard_normal((ref.d, 1))) >= 0, 1.0, -1.0)
+    yd = torch.from_numpy(y).cuda()
+    cfg = fb.TrainConfig(iterations=8, step_size=1e-3)
+    fused = fb.logistic_gd(nm, yd, cfg)
+    monkeypatch.setenv("FB_GLM_STEPWISE", "1")
+    steps = fb.logistic_gd(nm, yd, cfg)
+    _close(fused.weights, steps.weights, 1e-12)
+    _close(fused.objective, steps.objective, 1e-12)
+    w, obj = O.logistic_gd(ref, y, 8, 1e-3)
+    _close(fused.weights, w)
+    _close(fused.objective, obj)
+    yl = O.lmm(ref, rng.standard_normal((ref.d, 1)))
+    lcfg = fb.TrainConfig(iterations=5, step_size=1e-7)
+    lin_steps = fb.linreg_gd(nm, yl, lcfg)
+    monkeypatch.delenv("FB_GLM_STEPWISE")
+    lin_fused = fb.linreg_gd(nm, yl, lcfg)
+    _close(lin_fused.weights, lin_steps.weights, 1e-12)
+    w, obj = O.linreg_gd(ref, yl, 5, 1e-7)
+    _close(lin_fused.weights, w)
+    _close(lin_fused.objective, obj)
