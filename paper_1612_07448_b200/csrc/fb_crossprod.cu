@@ -1,30 +1,22 @@
 // fb_crossprod.cu — factorized crossprod TᵀT for T = [S, K·R] (rewrite.py:245-298,
-// Algorithm 2 of the paper), on the FP64 tensor cores.
+// Algorithm 2 of the paper).
 //
 //   TᵀT = [[ SᵀS,        (KᵀS)ᵀR       ],
 //          [ Rᵀ(KᵀS),    Rᵀ diag(c) R  ]]        c = colSums(K) (indicator.py:61-66)
 //
-// Two streaming passes, each a DMMA "gram" over row tiles staged by the tile ring:
-//   S pass  rows of S in FK-sorted order (a cached stable permutation — the GPU analogue of
-//           the reference's _csr_t, indicator.py:78-86 — gathered by the ring's gatherer
-//           warps). Every tile feeds (a) the upper triangle of SᵀS and (b) the segmented
-//           column sums B = KᵀS: each of d_S threads walks the sorted rows and emits one row
-//           of B per key run, so S is read once and KᵀS needs no atomics. Runs cut by a CTA
-//           boundary go to a carry table that a one-CTA fixup combines in CTA order.
-//   R pass  rows of R with B and c alongside: the upper triangle of Rᵀ diag(c) R (W
-//           fragments scaled by c on the fly) and the full RᵀB block.
+//   KᵀS     kts_walk_kernel: a segmented reduction over the cached FK-sorted order (the GPU
+//           analogue of the reference's _csr_t, indicator.py:78-86) on the side stream.
+//   S pass  cp_gram_kernel over S in storage order (bulk copies): the upper triangle of SᵀS.
+//   R pass  cp_gram_kernel over R with B = KᵀS and c alongside: the upper triangle of
+//           Rᵀ diag(c) R (W fragments scaled by c) and the full RᵀB block.
 //
-// Work unit: a 16×16 "block tile" = 2×2 DMMA tiles (mma.sync m8n8k4 f64 → DMMA.8x8x4;
-// tcgen05 has no f64 kind). Per k-step a block tile costs 4 shared loads and 4 DMMAs, so
-// the tensor pipe, not instruction issue, bounds the pass (the first design decoded one
-// 8×8 tile per slot and issued ~68 instructions per DMMA, ncu profile r01). The upper
-// triangle of a gram is covered by diagonal + off-diagonal block tiles (the strictly-lower
-// 8×8 quarter of a diagonal block tile is the only waste). Each consumer warp owns up to
-// kMaxBPW block tiles (accumulators in registers for the whole pass); with few block
-// tiles, warps split the k-steps instead (ks ways); with many, they are spread over
-// gridDim.y groups. Each (CTA, k-split) writes a dense partial; cp_reduce_kernel sums the
-// partials in a fixed order and writes the exact mirror (lower = upperᵀ, rewrite.py:298 /
-// kernel.py:132-135).
+// Gram work unit: an 8·BS × 8·BS "block tile" of BS × BS DMMA accumulators (mma.sync m8n8k4
+// f64 → DMMA.8x8x4; tcgen05 has no f64 kind); BS = 2 costs 4 shared loads per 4 DMMAs. The
+// (block tile, k-step) units of a tile are cut by a host-built table into one contiguous range
+// per consumer warp, balanced across the 4 SM sub-partitions (one DMMA pipe each); a warp's
+// accumulators stay in registers for the whole pass. Each (CTA, warp) writes its block tiles
+// into a dense partial; cp_reduce_kernel sums the writers of every element in a fixed order
+// and writes the exact mirror (lower = upperᵀ, rewrite.py:298 / kernel.py:132-135).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
