@@ -281,12 +281,16 @@ def run_gpu(args, rank, world, local_rank):
     # e2e: the public API with host operands (pinned), result read back to host each step
     pin = lambda a: a.cpu().pin_memory()
     hx1, hx16, hxr = pin(x1), pin(x16), pin(xr)
+    # rowSums of a device-resident T returns a device vector: read it back into page-locked
+    # memory (a pageable .cpu() of 160 MB costs ~75 ms of first-touch faults, not PCIe time)
+    hrs = torch.empty((n_s, 1), dtype=torch.float64, pin_memory=True)
     e2e_ops = {
         "lmm_x1": lambda: fb.lmm(nm, hx1),
         "lmm_x16": lambda: fb.lmm(nm, hx16),
         "rmm_x1": lambda: _host_allreduce(fb.rmm(hxr, nm), world, dev),
-        "row_sums": lambda: fb.row_sums(nm).cpu(),
-        "col_sums": lambda: _host_allreduce(fb.col_sums(nm), world, dev),
+        "row_sums": lambda: (hrs.copy_(fb.row_sums(nm).reshape(n_s, 1), non_blocking=True),
+                             torch.cuda.current_stream().synchronize()),
+        "col_sums": lambda: _host_allreduce(fb.col_sums(nm).cpu(), world, dev),
     }
     h2d = 8 * (x1.numel() + x16.numel() + xr.numel())
     d2h = 8 * (n_s * 1 + n_s * 16 + d + n_s + d)
