@@ -664,9 +664,12 @@ size_t fb_kmeans_workspace_bytes(const fb_normalized* nm, int32_t k) {
   b += align256(fb::onehot_partials_doubles(nm->d_s > 0 ? nm->d_s : 1, k, g_num_sms) * 8);
   b += align256(fb::colreduce_workspace_doubles(0, static_cast<int>(max_width(nm)), k, g_num_sms) * 8);
   b += 3 * 256;                                             // counters
-  for (int i = 0; i < nm->q; ++i) b += align256(static_cast<size_t>(nm->part[i].n_r) * k * 4) +
-                                       align256(static_cast<size_t>(nm->part[i].n_r) * k * 8);
-  return b + fb_lmm_workspace_bytes(nm, k) + 256;
+  size_t rtx = 0;
+  for (int i = 0; i < nm->q; ++i) {
+    b += align256(static_cast<size_t>(nm->part[i].n_r) * k * 4) + align256(static_cast<size_t>(nm->part[i].n_r) * k * 8);
+    if (fb::rtx_supported(nm->part[i].d_r, k)) rtx = std::max(rtx, fb::rtx_workspace_bytes(nm->part[i].d_r, k, g_num_sms));
+  }
+  return b + align256(rtx) + fb_lmm_workspace_bytes(nm, k) + 256;
 }
 
 static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const double* c, const double* cc,
@@ -728,11 +731,15 @@ static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const
   fb::KmFk fks{};
   fks.nfk = nm->q;
   double* fbins[FB_MAX_PARTS] = {};
+  size_t rtx_bytes = 0;
   for (int i = 0; i < nm->q; ++i) {
     fks.fk[i] = nm->part[i].fk;
     fks.bins[i] = cv.take<int32_t>(static_cast<size_t>(nm->part[i].n_r) * k);
     fbins[i] = cv.take<double>(static_cast<size_t>(nm->part[i].n_r) * k);
+    if (fb::rtx_supported(nm->part[i].d_r, k))
+      rtx_bytes = std::max(rtx_bytes, fb::rtx_workspace_bytes(nm->part[i].d_r, k, g_num_sms));
   }
+  char* rtx_ws = rtx_bytes ? cv.take<char>(rtx_bytes) : nullptr;
   // tc = (2T)·C computed as T·(2C): scaling by two is exact, so the products match bit for bit
   cudaError_t e = fb::launch_scalar_map(c, c2, d * k, fb::kMul, 2.0, s, g_num_sms);
   if (e != cudaSuccess) return cuda_status(e, "kmeans(2c)");
@@ -755,6 +762,12 @@ static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const
     const fb_part& p = nm->part[i];
     e = fb::launch_i32_to_f64(fks.bins[i], fbins[i], p.n_r * k, s, g_num_sms);
     if (e != cudaSuccess) return cuda_status(e, "kmeans(bins)");
+    if (rtx_ws && fb::rtx_supported(p.d_r, k)) {  // R_qᵀ H_q on the tensor cores
+      e = fb::launch_rtx(p.r, p.n_r, p.d_r, fbins[i], k, tta + off * k, k, 1, rtx_ws, rtx_bytes, s, g_num_sms);
+      if (e != cudaSuccess) return cuda_status(e, "kmeans(R pass)");
+      off += p.d_r;
+      continue;
+    }
     fb::ColReduce r{};
     r.a = p.r;
     r.n = p.n_r;

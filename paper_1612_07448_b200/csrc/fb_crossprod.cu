@@ -331,18 +331,21 @@ struct ReduceArgs {
   int64_t ldo;
   int bsz, t2a, t2b;  // block layout of the pass (build_block_jobs enumeration order)
   uint8_t wmask[kMaxBT];  // per block tile: the consumer warps that wrote it
+  int r1only;         // 1: region 1 only (Rᵀ·X, launch_rtx): no gram triangle, no mirror
+  int64_t o_cs;       // r1only: output column stride (element (i, j) at out[(off0+i)·ldo + (off1+j)·o_cs])
 };
 
 // Partial element (i, pc) -> its block tile -> the mask of consumer warps that wrote it.
 FB_DEV uint32_t tile_writers(const ReduceArgs& r, int i, int pc) {
   const int bi = i / r.bsz;
+  if (r.r1only) return r.wmask[bi * r.t2b + (pc - r.w1_col0) / r.bsz];
   int idx = bi * (r.t2a + r.t2b) - bi * (bi - 1) / 2;
   idx += pc < r.w1_col0 ? pc / r.bsz - bi : (r.t2a - bi) + (pc - r.w1_col0) / r.bsz;
   return r.wmask[idx];
 }
 
 FB_DEV bool reduce_coords(const ReduceArgs& r, int64_t e, int& i, int& pc, int& orow, int& ocol) {
-  const int n0 = r.da * r.da;
+  const int n0 = r.r1only ? 0 : r.da * r.da;
   int j;
   if (e < n0) {
     i = static_cast<int>(e / r.da);
@@ -378,13 +381,17 @@ __global__ void cp_reduce_kernel(ReduceArgs r) {
     for (uint32_t m = mask; m; m &= m - 1) s += p[(static_cast<size_t>(x) * kConsumerWarps + __ffs(m) - 1) * stride];
   s = warp_sum(s);
   if (lane == 0) {
-    r.out[orow * r.ldo + ocol] = s;
-    r.out[ocol * r.ldo + orow] = s;
+    if (r.r1only) {
+      r.out[orow * r.ldo + ocol * r.o_cs] = s;
+    } else {
+      r.out[orow * r.ldo + ocol] = s;
+      r.out[ocol * r.ldo + orow] = s;
+    }
   }
 }
 
 static void launch_reduce(const ReduceArgs& r, cudaStream_t st) {
-  const int64_t n = static_cast<int64_t>(r.da) * (r.da + r.db);
+  const int64_t n = static_cast<int64_t>(r.da) * ((r.r1only ? 0 : r.da) + r.db);
   cp_reduce_kernel<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, st>>>(r);
   FB_LAUNCHED();
 }
@@ -397,10 +404,11 @@ namespace {
 // group the units are split over the consumer warps as described at WarpJob. The first
 // `walkers` consumer warps of group 0 run the KᵀS walk and get no units. wmask receives,
 // per block tile, the warps that hold units of it.
-bool build_block_jobs(int T2a, int T2b, int nks, int walkers, BlockJobs& J, uint8_t* wmask) {
+bool build_block_jobs(int T2a, int T2b, int nks, int walkers, BlockJobs& J, uint8_t* wmask, bool r1only = false) {
   std::vector<uint16_t> list;
   for (int bi = 0; bi < T2a; ++bi) {
-    for (int bj = bi; bj < T2a; ++bj) list.push_back(static_cast<uint16_t>(bi | (bj << 6)));
+    if (!r1only)
+      for (int bj = bi; bj < T2a; ++bj) list.push_back(static_cast<uint16_t>(bi | (bj << 6)));
     for (int bj = 0; bj < T2b; ++bj) list.push_back(static_cast<uint16_t>(bi | (bj << 6) | (1 << 12)));
   }
   const int bt = static_cast<int>(list.size());
@@ -704,4 +712,78 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------ Rᵀ·X on the tensor cores
+// out(c, j) = Σ_r R(r, c)·X(r, j): the R-side contraction of Tᵀ·X-shaped products (K-Means
+// R_qᵀ(AᵀK_q)ᵀ, RMM/Tᵀ·X bins passes) as the crossprod R pass restricted to its region 1.
+// X rows must be 16-byte multiples (even nx) so both streams move with bulk copies.
+static void rtx_layout(int d_r, int nx, int& bs, int& t2a, int& t2b) {
+  bs = block_size(d_r > nx ? d_r : nx);
+  t2a = (d_r + 8 * bs - 1) / (8 * bs);
+  t2b = (nx + 8 * bs - 1) / (8 * bs);
+}
+
+size_t rtx_workspace_bytes(int d_r, int nx, int num_sms) {
+  int bs, t2a, t2b;
+  rtx_layout(d_r, nx, bs, t2a, t2b);
+  return static_cast<size_t>(num_sms) * kConsumerWarps * (8 * bs * t2a) * (8 * bs * t2b) * 8 + 256;
+}
+
+bool rtx_supported(int d_r, int nx) { return d_r > 0 && nx >= 2 && nx % 2 == 0 && nx <= 128 && d_r <= 512; }
+
+cudaError_t launch_rtx(const double* r, int64_t n_r, int d_r, const double* x, int nx, double* out, int64_t o_rs,
+                       int64_t o_cs, void* ws, size_t ws_bytes, cudaStream_t st, int num_sms) {
+  if (!rtx_supported(d_r, nx)) return cudaErrorNotSupported;
+  if (ws_bytes < rtx_workspace_bytes(d_r, nx, num_sms)) return cudaErrorInvalidValue;
+  if (n_r <= 0) {
+    for (int c = 0; c < d_r; ++c) {
+      cudaError_t e = cudaMemset2DAsync(out + c * o_rs, static_cast<size_t>(o_cs) * 8, 0, 8, nx, st);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  int bs, t2a, t2b;
+  rtx_layout(d_r, nx, bs, t2a, t2b);
+  GramArgs a{};
+  a.n = n_r;
+  const int pr = (d_r % 16 == 0) ? d_r + 4 : d_r;  // see the crossprod R pass
+  a.p0 = pr;
+  a.p1 = nx;
+  a.s1 = 1;
+  a.cnt_stream = -1;
+  a.ra = 8 * bs * t2a;
+  a.cw = 8 * bs * t2b;
+  a.w1_col0 = 0;
+  a.partials = static_cast<double*>(ws);
+  StreamSet ss{};
+  ss.base[0] = reinterpret_cast<const char*>(r);
+  ss.row_bytes[0] = static_cast<uint32_t>(d_r) * 8u;
+  ss.pitch[0] = static_cast<uint32_t>(pr) * 8u;
+  ss.base[1] = reinterpret_cast<const char*>(x);
+  ss.row_bytes[1] = static_cast<uint32_t>(nx) * 8u;
+  ss.count = 2;
+  const int tr = gram_tile_rows(pr * 8u + nx * 8u, false);
+  ReduceArgs ra{};
+  ra.partials = a.partials;
+  ra.ra = a.ra;
+  ra.cw = a.cw;
+  ra.w1_col0 = 0;
+  ra.da = d_r;
+  ra.db = nx;
+  ra.out = out;
+  ra.ldo = o_rs;
+  ra.o_cs = o_cs;
+  ra.bsz = 8 * bs;
+  ra.t2a = t2a;
+  ra.t2b = t2b;
+  ra.r1only = 1;
+  BlockJobs J;
+  if (!build_block_jobs(t2a, t2b, tr / 4, 0, J, ra.wmask, true)) return cudaErrorNotSupported;
+  int gridx = 0;
+  cudaError_t e = run_gram(J, a, ss, tr, st, num_sms, &gridx, bs);
+  if (e != cudaSuccess) return e;
+  ra.gridx = gridx;
+  launch_reduce(ra, st);
+  return cudaGetLastError();
+}
 }  // namespace fb

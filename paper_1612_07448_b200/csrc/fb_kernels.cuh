@@ -92,6 +92,12 @@ cudaError_t launch_fk_sort(const int32_t* fk, int64_t n, int64_t n_r, int32_t* p
 cudaError_t side_fork(cudaStream_t main, cudaStream_t* side);
 cudaError_t side_join(cudaStream_t main);
 
+// out(c, j) = Σ_r R(r, c)·X(r, j) on the FP64 tensor cores (fb_crossprod.cu); nx even.
+bool rtx_supported(int d_r, int nx);
+size_t rtx_workspace_bytes(int d_r, int nx, int num_sms);
+cudaError_t launch_rtx(const double* r, int64_t n_r, int d_r, const double* x, int nx, double* out, int64_t o_rs,
+                       int64_t o_cs, void* ws, size_t ws_bytes, cudaStream_t st, int num_sms);
+
 size_t crossprod_workspace_bytes(int64_t n_s, int d_s, int64_t n_r, int d_r, int q, int num_sms);
 cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cudaStream_t st, int num_sms);
 
