@@ -135,18 +135,21 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_rowdot_kernel(LmmArgs p, 
 }
 
 // ------------------------------------------------------------------ DMMA (5 <= d_x <= 16)
-template <int NT>
-FB_DEV int xs_ld() {
-  return 8 * NT + 4;  // bank skew for the B-fragment loads (see conflict_free_pitch)
-}
-
-template <int NT, int MT>
+// KS = number of 4-wide k-steps when known at compile time (narrow factors: the whole
+// k-loop unrolls into KS·MT·NT DMMAs with constant shared-memory offsets), 0 = runtime.
+// The ncu source view of the runtime-loop version at c2 (d = 20, d_x = 16) showed ~480
+// issued instructions per warp per 128-row tile for 20 DMMAs (row/k predicates, per-column
+// bounds checks, address arithmetic): the SM issue slots, not HBM, bounded the pass.
+// Rows past the end of a partial tile are computed on stale shared memory and simply not
+// stored (DMMA row g of C depends only on row g of A), so the k-loop carries no row
+// predicate; only the last k-step of a width that is not a multiple of 4 masks k >= d.
+template <int NT, int MT, int KS>
 __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, StreamSet ss, int stages,
                                                                int tile_rows) {
   extern __shared__ __align__(128) char smem[];
   const int d = p.d;
-  const int dpad = (d + 3) & ~3;
-  const int ldxs = xs_ld<NT>();
+  const int dpad = KS > 0 ? 4 * KS : (d + 3) & ~3;
+  constexpr int ldxs = 8 * NT + 4;  // bank skew for the B-fragment loads (see conflict_free_pitch)
   double* xs = reinterpret_cast<double*>(smem);
   const size_t xs_bytes = (static_cast<size_t>(dpad > 0 ? dpad : 4) * ldxs * sizeof(double) + 127) & ~size_t(127);
   char* buf = smem + xs_bytes;
@@ -167,13 +170,18 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, St
   const int pitch = p.pitch;
   const int wrow = warp * (8 * MT);
   const uint64_t pol = p.nfk == 0 ? policy_evict_last() : policy_evict_first();
+  const bool ragged_k = (d & 3) != 0;
+  // every output column pair present and 16-byte aligned: one v2 store per pair
+  const bool full_cols = p.dx == 8 * NT && (p.ldo & 1) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15u) == 0;
+  const double* xb = xs + t * ldxs + g;  // this lane's B-fragment column
+  const int zst = p.zstride;
 
   for (int64_t kt = 0; kt < ring.count(); ++kt) {
     const int cur = ring.acquire(ss, kt);
     const int64_t tile = ring.tile_begin + kt;
     const int rows = ring.rows_of(tile);
     const int64_t r0 = tile * tile_rows;
-    const double* A = reinterpret_cast<const double*>(ring.stage_ptr(cur, ss, 0));
+    const double* A = reinterpret_cast<const double*>(ring.stage_ptr(cur, ss, 0)) + (wrow + g) * pitch + t;
 
     __syncwarp();  // mma.sync.aligned needs the whole warp converged (after the barrier spin)
     if (wrow < rows) {
@@ -183,25 +191,24 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, St
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
 
-      const double* arow[MT];
-      bool rlive[MT];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const int r = wrow + 8 * mt + g;
-        rlive[mt] = r < rows;
-        arow[mt] = A + static_cast<size_t>(rlive[mt] ? r : 0) * pitch;
-      }
-      for (int k0 = 0; k0 < dpad; k0 += 4) {
-        const int k = k0 + t;
+      auto kstep = [&](int k0, bool mask) {
         double b[NT];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) b[nt] = xs[k * ldxs + 8 * nt + g];
+        for (int nt = 0; nt < NT; ++nt) b[nt] = xb[k0 * ldxs + 8 * nt];
+        const bool on = !mask || k0 + t < d;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          const double a = (rlive[mt] && k < d) ? arow[mt][k] : 0.0;
+          const double a = on ? A[8 * mt * pitch + k0] : 0.0;
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a, b[nt]);
         }
+      };
+      if constexpr (KS > 0) {
+#pragma unroll
+        for (int s = 0; s < KS - 1; ++s) kstep(4 * s, false);
+        kstep(4 * (KS - 1), ragged_k);
+      } else {
+        for (int k0 = 0; k0 < dpad; k0 += 4) kstep(k0, ragged_k && k0 + 4 > d);
       }
 
       // epilogue: + z_0 + z_1 ... in part order (rewrite.py:186-190), then store
@@ -209,8 +216,23 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, St
       for (int mt = 0; mt < MT; ++mt) {
         const int r = wrow + 8 * mt + g;
         if (r >= rows) continue;
+        double* o = p.out + (r0 + r) * p.ldo;
+        if (full_cols) {
+          for (int q = 0; q < p.nfk; ++q) {
+            const double* zr = reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, q)) + r * zst + 2 * t;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const double2 zv = *reinterpret_cast<const double2*>(zr + 8 * nt);
+              acc[mt][nt][0] += zv.x;
+              acc[mt][nt][1] += zv.y;
+            }
+          }
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) st_hint2(o + 8 * nt + 2 * t, acc[mt][nt][0], acc[mt][nt][1], pol);
+          continue;
+        }
         for (int q = 0; q < p.nfk; ++q) {
-          const double* zr = reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, q)) + r * p.zstride;
+          const double* zr = reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, q)) + r * zst;
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             const int c = 8 * nt + 2 * t;
@@ -218,7 +240,6 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, St
             if (c + 1 < p.dx) acc[mt][nt][1] += zr[c + 1];
           }
         }
-        double* o = p.out + (r0 + r) * p.ldo;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int c = 8 * nt + 2 * t;
@@ -300,7 +321,7 @@ static cudaError_t launch_rowdot(LmmArgs p, cudaStream_t st, int num_sms) {
   return launch_ring(lmm_rowdot_kernel<NX, 8>, p, ss, fixed, rw * kConsumerWarps, st, num_sms);
 }
 
-template <int NT, int MT>
+template <int NT, int MT, int KS>
 static cudaError_t launch_dmma_cfg(LmmArgs p, cudaStream_t st, int num_sms) {
   const int tile_rows = kConsumerWarps * 8 * MT;
   // dense rows (one bulk copy per tile): a padded pitch needs one copy per row, which costs
@@ -310,16 +331,33 @@ static cudaError_t launch_dmma_cfg(LmmArgs p, cudaStream_t st, int num_sms) {
   fill_streams(p, ss, p.pitch);
   const int dpad = (p.d + 3) & ~3;
   const size_t fixed = (static_cast<size_t>(dpad > 0 ? dpad : 4) * (8 * NT + 4) * 8 + 127) & ~size_t(127);
-  return launch_ring(lmm_dmma_kernel<NT, MT>, p, ss, fixed, tile_rows, st, num_sms);
+  return launch_ring(lmm_dmma_kernel<NT, MT, KS>, p, ss, fixed, tile_rows, st, num_sms);
+}
+
+// narrow factors (d <= 32, the multi-row tile configurations): the k-step count is a
+// template parameter so the k-loop unrolls completely
+template <int NT, int MT>
+static cudaError_t launch_dmma_ks(const LmmArgs& p, cudaStream_t st, int num_sms) {
+  switch ((p.d + 3) / 4) {
+    case 1: return launch_dmma_cfg<NT, MT, 1>(p, st, num_sms);
+    case 2: return launch_dmma_cfg<NT, MT, 2>(p, st, num_sms);
+    case 3: return launch_dmma_cfg<NT, MT, 3>(p, st, num_sms);
+    case 4: return launch_dmma_cfg<NT, MT, 4>(p, st, num_sms);
+    case 5: return launch_dmma_cfg<NT, MT, 5>(p, st, num_sms);
+    case 6: return launch_dmma_cfg<NT, MT, 6>(p, st, num_sms);
+    case 7: return launch_dmma_cfg<NT, MT, 7>(p, st, num_sms);
+    case 8: return launch_dmma_cfg<NT, MT, 8>(p, st, num_sms);
+    default: return launch_dmma_cfg<NT, MT, 0>(p, st, num_sms);
+  }
 }
 
 template <int NT>
 static cudaError_t launch_dmma(const LmmArgs& p, cudaStream_t st, int num_sms) {
   const size_t row_bytes = static_cast<size_t>(p.d) * 8 + 8 * static_cast<size_t>(p.zstride) * p.nfk;
   // stage <= ~48 KB
-  if (row_bytes * 256 <= 48 * 1024) return launch_dmma_cfg<NT, 4>(p, st, num_sms);
-  if (row_bytes * 128 <= 48 * 1024) return launch_dmma_cfg<NT, 2>(p, st, num_sms);
-  return launch_dmma_cfg<NT, 1>(p, st, num_sms);
+  if (row_bytes * 256 <= 48 * 1024) return launch_dmma_ks<NT, 4>(p, st, num_sms);
+  if (row_bytes * 128 <= 48 * 1024) return launch_dmma_ks<NT, 2>(p, st, num_sms);
+  return launch_dmma_cfg<NT, 1, 0>(p, st, num_sms);
 }
 
 cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, int dx, int64_t ldx,
