@@ -31,6 +31,7 @@ namespace fb {
 constexpr int kNB = 4;          // block tiles one warp may touch (BS = 2: 4 × 16 accumulator registers)
 constexpr int kMaxGroups = 16;  // gridDim.y job groups
 constexpr int kMaxBT = 256;     // block tiles per pass
+constexpr int kWalkers = 3;     // KᵀS walker warps of the fused S pass (416 + 96 threads: 128 registers each)
 
 // block tile code: bits 0-5 A block bi, bits 6-11 W block bj, bit 12 W from region 1.
 // Host-built assignment (build_block_jobs): the (block tile, k-step) units of a tile are
@@ -59,6 +60,15 @@ struct GramArgs {
   int w1_col0;          // first partial column of region 1 (8·BS·T2a)
   double* partials;     // [gridDim.x · 8 warps][ra][cw] (a warp writes only its block tiles)
   int debug;            // development bisection bits (FB_CP_DEBUG): 1 no walk, 2 no DMMA
+  // fused KᵀS walk (S pass in FK-sorted order; cp_gram_kernel<BS, false, CJ > 0>)
+  const int32_t* perm;       // sorted position -> S row
+  const int32_t* keys;       // FK-sorted keys (ring stream `key_stream` carries the tile's keys)
+  const double* s;           // S in global memory (rows of a tile the ring could not bulk-copy)
+  int d;                     // S width
+  int key_stream;
+  double* bins;              // n_r × d, B = KᵀS
+  int* carry_key;            // 2 slots per CTA (first run, last run)
+  double* carry_val;
 };
 
 // KᵀS (B = group-by-key column sums of S, rewrite.py:260-270 via indicator.py:130-141) as
@@ -153,13 +163,164 @@ __global__ void __launch_bounds__(256, CJ <= 2 ? 4 : 2) kts_walk_kernel(const in
   }
 }
 
-template <int BS, bool SCALE>
-__global__ void __launch_bounds__(kRingThreads, 1) cp_gram_kernel(const __grid_constant__ BlockJobs jobs, GramArgs a,
-                                                                  StreamSet ss, int stages, int tile_rows) {
+// KᵀS walker warps of the fused S pass. The ring streams S in FK-sorted order (rows gathered
+// through the cached permutation) with the sorted keys alongside, so the walk reads every
+// tile from shared memory while the consumer warps run the SᵀS DMMAs on the same tile: S
+// crosses HBM once for both products. NW walker warps take whole tiles round-robin (tile kt
+// of the CTA -> walker kt mod NW), lanes own columns (lane + 32 j). Within a tile, a key change
+// closes the run: interior runs write their bins row once (keys without rows in between are
+// zeroed); the tile's first and last runs, which may continue in the neighbouring tiles, go to
+// the tile's two carry slots, combined in tile order by cp_carry_fixup_kernel — deterministic,
+// no atomics (the contract of kts_walk_kernel, with tiles for warp ranges). A single walker
+// per CTA walking every tile in order was the pass's bottleneck (one warp's dependent DADD
+// and loop chains at IPC ~0.15 against ~4 spinning warps per SM sub-partition), hence several
+// walkers on independent tiles. The walker of a tile releases its stage with one extra arrival
+// on the stage's "empty" barrier.
+template <int CJ>
+FB_DEV void kts_walk_tiles(TileRing& ring, const StreamSet& ss, const GramArgs& a, int w, int nw) {
+  const unsigned full = 0xffffffffu;
+  const int lane = lane_id();
+  const int d = a.d;
+  const int pitch = static_cast<int>(ss.pitch[0] >> 3);
+  bool on[CJ];  // this lane's columns lane + 32 j
+  int lcol[CJ];  // lanes past the last column read a valid column (never stored): loads carry no predicate
+#pragma unroll
+  for (int j = 0; j < CJ; ++j) {
+    on[j] = lane + 32 * j < d;
+    lcol[j] = on[j] ? lane + 32 * j : d - 1;
+  }
+  int key;
+  bool first;
+  int64_t slot0;  // carry slots of the current tile
+  double sum[CJ];
+  auto close_open = [&](int next) {
+    if (key >= 0) {
+      double* dst = first ? a.carry_val + slot0 * d : a.bins + static_cast<int64_t>(key) * d;
+#pragma unroll
+      for (int j = 0; j < CJ; ++j)
+        if (on[j]) dst[lane + 32 * j] = sum[j];
+      if (first && lane == 0) a.carry_key[slot0] = key;
+      first = false;
+      for (int z = key + 1; z < next; ++z)
+#pragma unroll
+        for (int j = 0; j < CJ; ++j)
+          if (on[j]) a.bins[static_cast<int64_t>(z) * d + lane + 32 * j] = 0.0;
+    }
+    key = next;
+#pragma unroll
+    for (int j = 0; j < CJ; ++j) sum[j] = 0.0;
+  };
+  auto add_rows = [&](const double* base, int stride, int lo, int hi) {  // rows [lo, hi)
+    int u = lo;
+    // 8-row blocks: independent loads, a pairwise tree, one add on the run's chain
+    for (; u + 8 <= hi; u += 8) {
+      double t[8][CJ];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < CJ; ++j) t[i][j] = base[(u + i) * stride + lcol[j]];
+#pragma unroll
+      for (int j = 0; j < CJ; ++j)
+        sum[j] += ((t[0][j] + t[1][j]) + (t[2][j] + t[3][j])) + ((t[4][j] + t[5][j]) + (t[6][j] + t[7][j]));
+    }
+    if (u + 4 <= hi) {
+      double t[4][CJ];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < CJ; ++j) t[i][j] = base[(u + i) * stride + lcol[j]];
+#pragma unroll
+      for (int j = 0; j < CJ; ++j) sum[j] += (t[0][j] + t[1][j]) + (t[2][j] + t[3][j]);
+      u += 4;
+    }
+    for (; u < hi; ++u)
+#pragma unroll
+      for (int j = 0; j < CJ; ++j) sum[j] += base[u * stride + lcol[j]];
+  };
+  // A chunk of up to 32 rows: lane u < cnt holds the key of row u (kl); starts = rows whose key
+  // differs from the previous row's (row 0: from the open run). Each run's rows are summed in
+  // row order straight from shared memory; a run boundary closes the open run.
+  auto fold = [&](const double* base, int stride, int kl, int cnt) {
+    const int kprev0 = __shfl_up_sync(full, kl, 1);
+    const int kprev = lane == 0 ? key : kprev0;
+    unsigned starts = __ballot_sync(full, lane < cnt && kl != kprev);
+    int pos = 0;
+    while (starts) {
+      const int b = __ffs(starts) - 1;
+      starts &= starts - 1;
+      add_rows(base, stride, pos, b);
+      close_open(__shfl_sync(full, kl, b));
+      pos = b;
+    }
+    add_rows(base, stride, pos, cnt);
+  };
+  const bool active = blockIdx.y == 0 && !(a.debug & 1);  // job groups > 0 stream the same rows: release only
+  int st = w % ring.stages;
+  uint32_t ph = (w / ring.stages) & 1u;
+  for (int64_t kt = w; kt < ring.count(); kt += nw) {
+    const int64_t tile = ring.tile_begin + kt;
+    const int rows = active ? ring.rows_of(tile) : 0;
+    mbar_wait(&ring.full[st], ph);
+    mbar_wait(&ring.gfull[st], ph);
+    key = -1;
+    first = true;
+    slot0 = 2 * tile;
+#pragma unroll
+    for (int j = 0; j < CJ; ++j) sum[j] = 0.0;
+    if (ring.bulk_ok(ss, tile)) {
+      const double* A = reinterpret_cast<const double*>(ring.stage_ptr(st, ss, 0));
+      const int32_t* K = reinterpret_cast<const int32_t*>(ring.stage_ptr(st, ss, a.key_stream));
+      for (int r0 = 0; r0 < rows; r0 += 32) {
+        const int cnt = rows - r0 < 32 ? rows - r0 : 32;
+        fold(A + r0 * pitch, pitch, lane < cnt ? K[r0 + lane] : -1, cnt);
+      }
+    } else {
+      // a tile the ring could not bulk-copy is filled by the consumers: read it from global,
+      // one row at a time
+      const int64_t p0 = tile * ring.tile_rows;
+      for (int r = 0; r < rows; ++r) {
+        const double* row = a.s + static_cast<int64_t>(a.perm[p0 + r]) * d;
+        fold(row, 0, lane == 0 ? a.keys[p0 + r] : -1, 1);
+      }
+    }
+    __syncwarp(full);
+    if (lane == 0) mbar_arrive(&ring.empty[st]);
+    if (active) {
+      // the open run may continue in the next tile: slot 1 (slot 0 if it is also the first run)
+      const int64_t slot = slot0 + (first ? 0 : 1);
+      if (key >= 0) {
+#pragma unroll
+        for (int j = 0; j < CJ; ++j)
+          if (on[j]) a.carry_val[slot * d + lane + 32 * j] = sum[j];
+      }
+      if (lane == 0) {
+        a.carry_key[slot] = key;  // -1: an empty tile
+        if (first) a.carry_key[slot0 + 1] = -1;
+      }
+    }
+    st += nw;
+    while (st >= ring.stages) {
+      st -= ring.stages;
+      ph ^= 1u;
+    }
+  }
+}
+
+// NW > 0: fused KᵀS walk (see kts_walk_tiles) on NW extra warps, CJ = ceil(d_S / 32) columns
+// per lane.
+template <int BS, bool SCALE, int NW = 0, int CJ = 1>
+__global__ void __launch_bounds__(kRingThreads + 32 * NW, 1)
+    cp_gram_kernel(const __grid_constant__ BlockJobs jobs, GramArgs a, StreamSet ss, int stages, int tile_rows) {
   extern __shared__ __align__(128) char smem[];
   TileRing ring;
   ring.init(smem, stages, tile_rows, a.n);
-  ring.start(ss);
+  ring.start(ss, NW > 0 ? 1 : 0);  // one walker releases each stage
+  if constexpr (NW > 0) {
+    if (threadIdx.x >= kRingThreads) {
+      kts_walk_tiles<CJ>(ring, ss, a, (static_cast<int>(threadIdx.x) - kRingThreads) >> 5, NW);
+      return;
+    }
+  }
   if (ring.service(ss)) return;
   const int warp = consumer_warp();
   const int grp = blockIdx.y;
@@ -482,11 +643,15 @@ int gram_tile_rows(uint32_t row_bytes, bool gather) {
 
 // Launch one pass; *gridx = CTAs per group (each wrote kConsumerWarps partial slots).
 cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_rows, cudaStream_t st, int num_sms,
-                     int* gridx, int bs) {
+                     int* gridx, int bs, int walk_cj = 0) {
   stream_layout(ss, tile_rows, a.n);
   int stages = static_cast<int>((200 * 1024 - kRingHeader - 256) / ss.stage_bytes);
   if (stages > 6) stages = 6;
   if (const char* e = getenv("FB_CP_STAGES")) stages = std::min(stages, atoi(e));  // development override
+  // fused walk: walker w takes tiles w, w + kWalkers, ...; with a stage count that is a multiple
+  // of kWalkers, the previous tile on a walker's stage is its own, so its parity wait can never
+  // see a fill one round old as the one it wants (mbarrier parity aliases phases two apart)
+  if (walk_cj > 0) stages = (stages / kWalkers) * kWalkers;
   if (stages < 2) return cudaErrorNotSupported;
   // + slack: fragment loads of a padded block read up to 8·BS - 1 doubles past a row,
   // so the last row of the last stage must not sit at the end of the allocation
@@ -498,6 +663,24 @@ cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_ro
     fprintf(stderr, "[fb] gram pass n=%lld tile_rows=%d stages=%d grid=%dx%d bt=%d/group bs=%d\n", (long long)a.n,
             tile_rows, stages, gdim.x, gdim.y, J.per_group, bs);
   cudaError_t e;
+#define FB_WALK_CASE(S, CJ)                                                                                     \
+  if (bs == S && walk_cj == CJ) {                                                                               \
+    auto kern = cp_gram_kernel<S, false, kWalkers, CJ>;                                                         \
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));        \
+    if (e != cudaSuccess) return e;                                                                             \
+    kern<<<gdim, kRingThreads + 32 * kWalkers, smem, st>>>(J, a, ss, stages, tile_rows);                         \
+    FB_LAUNCHED();                                                                                              \
+    return cudaGetLastError();                                                                                  \
+  }
+  if (walk_cj > 0) {
+    FB_WALK_CASE(1, 1)
+    FB_WALK_CASE(2, 1)
+    FB_WALK_CASE(2, 2)
+    FB_WALK_CASE(2, 3)
+    FB_WALK_CASE(2, 4)
+    return cudaErrorNotSupported;
+  }
+#undef FB_WALK_CASE
 #define FB_GRAM_CASE(S)                                                                                         \
   if (bs == S) {                                                                                                \
     auto kern = a.cnt_stream >= 0 ? cp_gram_kernel<S, true> : cp_gram_kernel<S, false>;                        \
@@ -544,6 +727,23 @@ cudaError_t launch_kts(const CrossArgs& c, double* bins, int* ckey, double* cval
   cp_carry_fixup_kernel<<<slots, ((c.d_s + 31) / 32) * 32, 0, st>>>(ckey, cval, slots, c.d_s, bins, c.n_r);
   FB_LAUNCHED();
   return cudaGetLastError();
+}
+
+// Fused S pass tiles: ~32 KB stages (6 in flight). A stage stays busy for its gather latency
+// plus the walk of that tile (a walker's per-tile latency exceeds the DMMA time of a tile), so
+// the ring needs more, smaller stages than a pass whose stages turn over at consumer speed.
+int fused_tile_rows(int d_s) {
+  if (const char* e = getenv("FB_CP_FUSED_ROWS")) return atoi(e);  // development override
+  int rows = static_cast<int>((32u * 1024u) / (static_cast<uint32_t>(d_s) * 8u + 4u));
+  rows = (rows / 32) * 32;
+  if (rows > 128) rows = 128;
+  return rows < 32 ? 32 : rows;
+}
+
+// Carry slots: two per walker warp range (kts_walk_kernel) or per tile of the fused S pass.
+size_t carry_slots(int64_t n_s, int d_s, int num_sms) {
+  const int64_t tr = 32;  // the smallest fused tile (FB_CP_FUSED_ROWS may pick any multiple of 32)
+  return std::max<size_t>(2 * static_cast<size_t>(kts_warps(num_sms)), 2 * static_cast<size_t>((n_s + tr - 1) / tr));
 }
 
 int block_size(int da) {
@@ -595,12 +795,11 @@ size_t crossprod_workspace_bytes(int64_t n_s, int d_s, int64_t n_r, int d_r, int
   size_t b = al(partial_doubles(t2s, 0, num_sms, bs_s) * 8);
   b += al(partial_doubles(t2r, t2b, num_sms, bs_r) * 8);
   if (q > 0) {
-    const size_t slots = 2 * kts_warps(num_sms);
+    const size_t slots = carry_slots(n_s, d_s, num_sms);
     b += al(static_cast<size_t>(n_r) * d_s * 8);               // B = KᵀS
     b += al(slots * sizeof(int));                               // carry keys
     b += al(slots * static_cast<size_t>(d_s > 0 ? d_s : 1) * 8);  // carry values
   }
-  (void)n_s;
   return b + 1024;
 }
 
@@ -621,7 +820,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
   double* bins = nullptr;
   int* ckey = nullptr;
   double* cval = nullptr;
-  const size_t slots = 2 * kts_warps(num_sms);
+  const size_t slots = carry_slots(c.n_s, c.d_s, num_sms);
   if (q) {
     bins = reinterpret_cast<double*>(take(static_cast<size_t>(c.n_r) * c.d_s * 8));
     ckey = reinterpret_cast<int*>(take(slots * sizeof(int)));
@@ -631,9 +830,51 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
   cudaError_t e = cudaMemsetAsync(c.out, 0, static_cast<size_t>(d) * d * 8, st);
   if (e != cudaSuccess) return e;
 
-  // ---- S pass: SᵀS on the main stream; KᵀS (q = 1) on the side stream, joined before the R pass
+  // ---- S pass. Fused (q = 1, even d_S <= 128): one pass over S in FK-sorted order computes
+  // SᵀS on the consumer warps and KᵀS on the walker warp. Otherwise SᵀS streams S in storage
+  // order on the main stream and kts_walk_kernel runs KᵀS on the side stream.
+  const bool fused = q && c.d_s > 0 && c.n_s > 0 && c.d_s <= 128 && (c.d_s % 2) == 0 && c.n_s <= INT32_MAX &&
+                     !getenv("FB_CP_UNFUSED");
+  if (fused) {
+    GramArgs a{};
+    a.n = c.n_s;
+    a.p0 = a.p1 = c.d_s;
+    a.s1 = -1;
+    a.cnt_stream = -1;
+    a.ra = 8 * bs_s * t2s;
+    a.cw = 8 * bs_s * t2s;
+    a.w1_col0 = 8 * bs_s * t2s;
+    a.partials = sp;
+    a.perm = c.perm;
+    a.keys = c.fk_sorted;
+    a.s = c.s;
+    a.d = c.d_s;
+    a.key_stream = 1;
+    a.bins = bins;
+    a.carry_key = ckey;
+    a.carry_val = cval;
+    StreamSet ss{};
+    ss.base[0] = reinterpret_cast<const char*>(c.s);
+    ss.row_bytes[0] = static_cast<uint32_t>(c.d_s) * 8u;
+    ss.gidx = c.perm;
+    ss.base[1] = reinterpret_cast<const char*>(c.fk_sorted);
+    ss.row_bytes[1] = 4u;
+    ss.count = 2;
+    const int tr = fused_tile_rows(c.d_s);
+    ReduceArgs r{sp, 0, a.ra, a.cw, a.w1_col0, c.d_s, 0, 0, 0, c.out, d, 8 * bs_s, t2s, 0, {}};
+    BlockJobs JS;
+    if (!build_block_jobs(t2s, 0, tr / 4, 0, JS, r.wmask)) return cudaErrorNotSupported;
+    int gridx = 0;
+    e = run_gram(JS, a, ss, tr, st, num_sms, &gridx, bs_s, (c.d_s + 31) / 32);
+    if (e != cudaSuccess) return e;
+    r.gridx = gridx;
+    launch_reduce(r, st);
+    const int nslots = static_cast<int>(2 * ((c.n_s + tr - 1) / tr));  // two carry slots per tile
+    cp_carry_fixup_kernel<<<nslots, ((c.d_s + 31) / 32) * 32, 0, st>>>(ckey, cval, nslots, c.d_s, bins, c.n_r);
+    FB_LAUNCHED();
+  }
   bool forked = false;
-  if (q && c.d_s > 0 && c.n_s > 0) {
+  if (!fused && q && c.d_s > 0 && c.n_s > 0) {
     cudaStream_t side = nullptr;
     e = side_fork(st, &side);
     if (e != cudaSuccess) return e;
@@ -641,7 +882,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     e = launch_kts(c, bins, ckey, cval, side, num_sms);
     if (e != cudaSuccess) return e;
   }
-  if (c.d_s > 0 && c.n_s > 0) {
+  if (!fused && c.d_s > 0 && c.n_s > 0) {
     GramArgs a{};
     a.n = c.n_s;
     a.p0 = a.p1 = c.d_s;
@@ -664,7 +905,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     r.gridx = gridx;
     if (e != cudaSuccess) return e;
     launch_reduce(r, st);
-  } else if (q && c.d_s > 0) {
+  } else if (!fused && q && c.d_s > 0) {
     e = cudaMemsetAsync(bins, 0, static_cast<size_t>(c.n_r) * c.d_s * 8, st);  // no rows: KᵀS = 0
     if (e != cudaSuccess) return e;
   }

@@ -175,7 +175,8 @@ struct TileRing {
   }
 
   // Barrier setup; call from all threads before the role split (contains __syncthreads).
-  FB_DEV void start(const StreamSet& s) {
+  // extra_empty: additional warps (beyond the consumers) that release every stage.
+  FB_DEV void start(const StreamSet& s, int extra_empty = 0) {
     stage = 0;
     phase = 0;
     rstage = 0;
@@ -183,7 +184,7 @@ struct TileRing {
     if (threadIdx.x == 0) {
       for (int i = 0; i < stages; ++i) {
         mbar_init(&full[i], has_pitched(s) ? 33 : 1);
-        mbar_init(&empty[i], kConsumerWarps);
+        mbar_init(&empty[i], kConsumerWarps + extra_empty);
         mbar_init(&gfull[i], 32 * kGatherWarps);
       }
       fence_mbar_init();

@@ -1,0 +1,21 @@
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_1612_07448_b200 as fb
+from paper_1612_07448_b200.crossprod_impl import fk_sorted_order
+dev = torch.device("cuda", 0)
+for (n_s, d_s, n_r, d_r) in [(4, 2, 2, 2), (40, 2, 5, 2), (1000, 6, 50, 4)]:
+    g = torch.Generator(device=dev).manual_seed(1)
+    s = torch.rand(n_s, d_s, dtype=torch.float64, device=dev, generator=g)
+    r = torch.rand(n_r, d_r, dtype=torch.float64, device=dev, generator=g)
+    key = torch.randint(1, n_r + 1, (n_s,), device=dev, generator=g)
+    nm = fb.build_pkfk(s, key, r)
+    perm, fks = fk_sorted_order(nm.k)
+    ks = nm.k.target.long()
+    B = torch.zeros(nm.k.cols, d_s, dtype=torch.float64, device=dev).index_add_(0, ks, s)
+    P = nm.r.t() @ B
+    os.environ["FB_CP_UNFUSED"] = "1"; a = fb.crossprod(nm)
+    os.environ.pop("FB_CP_UNFUSED"); b = fb.crossprod(nm)
+    torch.cuda.synchronize()
+    print(n_s, "unfused P err", (a[d_s:, :d_s] - P).abs().max().item(), "fused P err", (b[d_s:, :d_s] - P).abs().max().item())
+    print("  fused P", b[d_s:, :d_s][:2].tolist(), "ref", P[:2].tolist(), "upper", b[:d_s, d_s:].t()[:2].tolist())
