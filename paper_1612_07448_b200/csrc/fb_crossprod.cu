@@ -746,6 +746,19 @@ size_t carry_slots(int64_t n_s, int d_s, int num_sms) {
   return std::max<size_t>(2 * static_cast<size_t>(kts_warps(num_sms)), 2 * static_cast<size_t>((n_s + tr - 1) / tr));
 }
 
+// Shared-memory row pitch (doubles) for the DMMA fragment loads of a gram pass: a half-warp
+// of an LDS.64 covers rows t = 0..3 × 4 consecutive doubles g, i.e. banks 2(t·p + g) (+1) mod 32;
+// they are distinct for p ≡ 4 or 12 (mod 16). Even widths are padded up to the next such
+// pitch (the padded rows stream with one bulk copy per row, StreamSet::row_bulk); odd widths
+// (whose rows cannot be bulk-copied) keep their width. d_r = 120 (≡ 8): 2-way conflicts on
+// every fragment load held the c3 R pass at ~55% of the DMMA rate.
+int frag_pitch(int d) {
+  if (d & 1) return d;
+  int p = d;
+  while (p % 16 != 4 && p % 16 != 12) p += 2;
+  return p;
+}
+
 int block_size(int da) {
   if (const char* e = getenv("FB_CP_BS")) return atoi(e);  // development override (1, 2 or 4)
   return da <= 8 ? 1 : 2;
@@ -918,11 +931,8 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
   if (q && c.d_r > 0 && c.n_r > 0) {
     GramArgs a{};
     a.n = c.n_r;
-    // Fragment loads read 8 consecutive doubles from each of 4 rows: conflict free unless
-    // the row pitch is a multiple of 16 doubles (then all 4 rows hit the same 16 banks).
-    // Only that case gets 4 doubles of padding — an unpadded R streams with bulk copies,
-    // a padded one needs the producer's per-chunk cp.async.
-    const int pr = (c.d_r % 16 == 0) ? c.d_r + 4 : c.d_r;
+    // R rows padded to a bank-conflict-free pitch (frag_pitch), one bulk copy per row
+    const int pr = frag_pitch(c.d_r);
     a.p0 = pr;
     a.p1 = c.d_s > 0 ? c.d_s : 1;
     a.s1 = c.d_s > 0 ? 1 : -1;
@@ -940,6 +950,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     ss.base[2] = reinterpret_cast<const char*>(c.counts);
     ss.row_bytes[2] = 8u;
     ss.count = 3;
+    ss.row_bulk = true;
     const int tr = gram_tile_rows(pr * 8u + c.d_s * 8u + 8u, false);
     ReduceArgs r{rp, 0, a.ra, a.cw, a.w1_col0, c.d_r, c.d_s, c.d_s, 0, c.out, d, 8 * bs_r, t2r, t2b, {}};
     BlockJobs JR;
@@ -987,7 +998,7 @@ cudaError_t launch_rtx(const double* r, int64_t n_r, int d_r, const double* x, i
   rtx_layout(d_r, nx, bs, t2a, t2b);
   GramArgs a{};
   a.n = n_r;
-  const int pr = (d_r % 16 == 0) ? d_r + 4 : d_r;  // see the crossprod R pass
+  const int pr = frag_pitch(d_r);  // see the crossprod R pass
   a.p0 = pr;
   a.p1 = nx;
   a.s1 = 1;
@@ -1003,6 +1014,7 @@ cudaError_t launch_rtx(const double* r, int64_t n_r, int d_r, const double* x, i
   ss.base[1] = reinterpret_cast<const char*>(x);
   ss.row_bytes[1] = static_cast<uint32_t>(nx) * 8u;
   ss.count = 2;
+  ss.row_bulk = true;
   const int tr = gram_tile_rows(pr * 8u + nx * 8u, false);
   ReduceArgs ra{};
   ra.partials = a.partials;

@@ -62,6 +62,8 @@ struct StreamSet {
   uint32_t tile_tx;      // transaction bytes of a full tile
   bool bulk_full;        // full tiles can use bulk copies
   bool bulk_last;        // the final (possibly partial) tile can use bulk copies
+  bool row_bulk;         // padded-pitch streams: one bulk copy per row (instead of 16-byte
+                         // cp.async chunks) — for tiles of few, long rows
   const int32_t* gidx;   // optional: stream 0 row r of the ring is source row gidx[r]
                          // (a gathered stream, e.g. rows in FK-sorted order); <= 128 rows/tile
   // keyed gathers: row r of gather g = gbase[g] + key * grow_bytes[g], key = gkeys[g][row]
@@ -195,6 +197,7 @@ struct TileRing {
   // Streams copied with cp.async by the producer (padded pitch): its 32 lanes then arrive
   // on "full" as well.
   FB_DEV static bool has_pitched(const StreamSet& s) {
+    if (s.row_bulk) return false;
     bool p = false;
 #pragma unroll
     for (int i = 0; i < kMaxStreams; ++i)
@@ -232,7 +235,7 @@ struct TileRing {
           uint32_t tx = 0;
 #pragma unroll
           for (int i = 0; i < kMaxStreams; ++i)
-            if (i < s.count && !(i == 0 && s.gidx) && s.pitch[i] == s.row_bytes[i])
+            if (i < s.count && !(i == 0 && s.gidx) && (s.pitch[i] == s.row_bytes[i] || s.row_bulk))
               tx += s.row_bytes[i] * static_cast<uint32_t>(rows);
           mbar_arrive_expect_tx(&full[st], tx);
         }
@@ -245,6 +248,10 @@ struct TileRing {
           if (s.pitch[i] == s.row_bytes[i]) {
             if (lane == 0)
               bulk_g2s_stream(dst, src, s.row_bytes[i] * static_cast<uint32_t>(rows), &full[st], policy);
+          } else if (s.row_bulk) {
+            for (int r = lane; r < rows; r += 32)
+              bulk_g2s_stream(dst + r * s.pitch[i], src + static_cast<size_t>(r) * s.row_bytes[i], s.row_bytes[i],
+                              &full[st], policy);
           } else {
             // padded pitch: (row, 16-byte chunk) items over the lanes with cp.async — one warp
             // instruction moves 512 bytes (a per-row bulk copy costs ~60 issue cycles)
