@@ -60,6 +60,115 @@ def _fixtures():
     return fx
 
 
+def _mn_fixtures():
+    """M:N (normmat.py:240-285) and multi-table M:N (normmat.py:288-319) fixtures."""
+    rng = np.random.default_rng(1612)
+    fx = {}
+    # M:N, N(0,1): join values 0..14 on S, 3..19 on R (values outside the overlap and the rows
+    # holding them are dropped), duplicates on both sides
+    n_s, n_r = 90, 40
+    fx["mn_normal"] = dict(kind="mn", s=rng.standard_normal((n_s, 4)), j_s=rng.integers(0, 15, size=n_s),
+                           r=rng.standard_normal((n_r, 6)), j_r=rng.integers(3, 20, size=n_r))
+    # M:N over U[0,1) tables (GNMF needs non-negative T)
+    n_s, n_r = 70, 25
+    fx["mn_uniform"] = dict(kind="mn", s=rng.random((n_s, 5)), j_s=rng.integers(0, 9, size=n_s),
+                            r=rng.random((n_r, 3)), j_r=rng.integers(0, 12, size=n_r))
+    # multi-table M:N: three tables, an explicit row map with unreferenced rows
+    n_out = 150
+    tabs = [rng.standard_normal((30, 3)), rng.standard_normal((12, 4)), rng.standard_normal((50, 2))]
+    row_map = np.stack([rng.integers(0, 25, size=n_out), rng.integers(0, 12, size=n_out),
+                        rng.integers(5, 50, size=n_out)], axis=1)
+    fx["multimn_normal"] = dict(kind="multimn", tables=tabs, row_map=row_map)
+    return fx
+
+
+def _record_ops(rec, nm, rng, kernel, ml, normmat, rewrite, nonneg):
+    n, d = nm.shape
+    rec["materialize"] = normmat.materialize(nm)
+    x1 = rng.standard_normal((d, 1))
+    x3 = rng.standard_normal((d, 3))
+    p2 = rng.standard_normal((n, 2))
+    xr = rng.standard_normal((2, n))
+    xt = rng.standard_normal((3, d))
+    rec.update(x1=x1, x3=x3, p2=p2, xr=xr, xt=xt)
+    c = kernel.OpCounter()
+    rec["lmm_x1"] = rewrite.lmm(nm, x1, c)
+    rec["cnt_lmm_x1"] = np.array([c.multiplies, c.additions])
+    rec["lmm_x3"] = rewrite.lmm(nm, x3)
+    c = kernel.OpCounter()
+    rec["tmm_p2"] = rewrite.lmm(nm.T, p2, c)
+    rec["cnt_tmm_p2"] = np.array([c.multiplies, c.additions])
+    c = kernel.OpCounter()
+    rec["rmm_xr"] = rewrite.rmm(xr, nm, c)
+    rec["cnt_rmm_xr"] = np.array([c.multiplies, c.additions])
+    rec["rmm_t_xt"] = rewrite.rmm(xt, nm.T)
+    c = kernel.OpCounter()
+    rec["row_sums"] = rewrite.row_sums(nm, c)
+    rec["cnt_row_sums"] = np.array([c.multiplies, c.additions])
+    c = kernel.OpCounter()
+    rec["col_sums"] = rewrite.col_sums(nm, c)
+    rec["cnt_col_sums"] = np.array([c.multiplies, c.additions])
+    c = kernel.OpCounter()
+    rec["sum_all"] = np.array(rewrite.sum_all(nm, c))
+    rec["cnt_sum_all"] = np.array([c.multiplies, c.additions])
+    rec["row_sums_t"] = rewrite.row_sums(nm.T)
+    rec["col_sums_t"] = rewrite.col_sums(nm.T)
+    for op, x in (("mul", 2.0), ("add", 3.0), ("rsub", 1.5), ("div", 4.0), ("pow", 2.0)):
+        c = kernel.OpCounter()
+        rec[f"scalar_{op}"] = normmat.materialize(rewrite.scalar_op(nm, x, op, c))
+        rec[f"cnt_scalar_{op}"] = np.array([c.multiplies, c.additions])
+    rec["fn_exp"] = normmat.materialize(rewrite.scalar_fn(nm, np.exp))
+    c = kernel.OpCounter()
+    rec["crossprod"] = rewrite.crossprod(nm, counter=c)
+    rec["cnt_crossprod"] = np.array([c.multiplies, c.additions])
+    w_true = rng.standard_normal((d, 1))
+    t = normmat.materialize(nm)
+    y_lin = t @ w_true + 0.01 * rng.standard_normal((n, 1))
+    out = ml.linreg_normal(nm, y_lin)
+    rec.update(y_lin=y_lin, linreg_w=out.weights, linreg_obj=np.array(out.objective))
+    cfg = ml.TrainConfig(iterations=5, step_size=1e-3, k=3, r=2, rng_seed=3)
+    y_log = np.where(t @ w_true >= 0, 1.0, -1.0)
+    out = ml.logistic_gd(nm, y_log, cfg)
+    rec.update(y_log=y_log, logreg_w=out.weights, logreg_obj=np.array(out.objective))
+    out = ml.linreg_gd(nm, y_lin, cfg)
+    rec.update(linreg_gd_w=out.weights, linreg_gd_obj=np.array(out.objective))
+    out = ml.kmeans(nm, cfg)
+    rec.update(kmeans_c=out.centroids, kmeans_obj=np.array(out.objective))
+    if nonneg:
+        out = ml.gnmf(nm, cfg)
+        rec.update(gnmf_w=out.factors[0], gnmf_h=out.factors[1], gnmf_obj=np.array(out.objective))
+
+
+def main_mn():
+    sys.path.insert(0, REF)
+    os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    import factorla
+    from factorla import kernel, ml, normmat, rewrite
+
+    rng = np.random.default_rng(11)
+    for name, f in _mn_fixtures().items():
+        if f["kind"] == "mn":
+            nm = normmat.build_mn(f["s"], f["j_s"], f["r"], f["j_r"])
+            rec = {"kind": np.array("mn"), "s": f["s"], "j_s": f["j_s"], "r": f["r"], "j_r": f["j_r"]}
+            facs = [f["s"], f["r"]]
+        else:
+            nm = normmat.build_multimn(f["row_map"], f["tables"])
+            rec = {"kind": np.array("multimn"), "row_map": f["row_map"], "q": np.array(len(f["tables"]))}
+            for j, t in enumerate(f["tables"]):
+                rec[f"table{j}"] = t
+            facs = f["tables"]
+        for i, (e, fk) in enumerate(nm.blocks):
+            rec[f"target{i}"] = e.target
+            rec[f"used{i}"] = nm.source_rows[i]
+            rec[f"counts{i}"] = e.counts
+            rec[f"kept{i}"] = fk
+        nonneg = all(float(np.min(t)) >= 0 for t in facs)
+        _record_ops(rec, nm, rng, kernel, ml, normmat, rewrite, nonneg)
+        path = os.path.join(OUT, f"{name}.npz")
+        np.savez_compressed(path, **{k: np.asarray(v) for k, v in rec.items()})
+        print("wrote", path, os.path.getsize(path), "bytes", "factorla", getattr(factorla, "__version__", "?"))
+
+
 def main():
     sys.path.insert(0, REF)
     os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
@@ -145,4 +254,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "mn":
+        main_mn()
+    else:
+        main()
+        main_mn()

@@ -22,6 +22,8 @@ from .normmat import (
     NormalizedMatrix,
     ShapeStats,
     as_normalized,
+    build_mn,
+    build_multimn,
     build_pkfk,
     build_star,
     materialize,
@@ -46,6 +48,8 @@ __all__ = [
     "NormalizedMatrix",
     "ShapeStats",
     "as_normalized",
+    "build_mn",
+    "build_multimn",
     "build_pkfk",
     "build_star",
     "materialize",

@@ -67,11 +67,13 @@ def crossprod(nm, method="efficient", counter=None):
     so = _lib.lib()
     st = D.stream_handle()
     d = nm.base_cols
-    dev = nm.s.device
+    dev = nm.device
     out = torch.empty((d, d), dtype=torch.float64, device=dev)
     q = len(nm.blocks) - 1
     cs = nm.c_struct()
-    if q == 1 and nm.blocks[0][1].shape[1] > 128:
+    if nm.blocks[0][0] is not None:
+        _star_crossprod(nm, out, so, st)  # M:N: every block gathered (the fused passes need S = block 0)
+    elif q == 1 and nm.blocks[0][1].shape[1] > 128:
         _star_crossprod(nm, out, so, st)  # the fused segmented KᵀS covers d_S <= 128
     elif q <= 1:
         perm = fks = None

@@ -274,7 +274,7 @@ cudaError_t launch_glm_run(const GlmRunIn& in, void* ws, size_t ws_bytes, cudaSt
   while (L < 32 && in.ds > 8 * L) L *= 2;
   if (in.ds > 8 * L) return cudaErrorNotSupported;
   a.lanes = L;
-  const int C = (in.ds + L - 1) / L;
+  const int C = in.ds > 0 ? (in.ds + L - 1) / L : 1;  // d_S = 0 (M:N: every block keyed) runs the C = 1 kernel
   void* kern = nullptr;
   switch (C) {
 #define FB_RUN_CASE(N)                                       \
@@ -287,7 +287,6 @@ cudaError_t launch_glm_run(const GlmRunIn& in, void* ws, size_t ws_bytes, cudaSt
     default:
       return cudaErrorNotSupported;
   }
-  if (in.ds == 0) kern = reinterpret_cast<void*>(glm_run_kernel<1>);
   const size_t smem = (static_cast<size_t>((a.d + 2) & ~1) + static_cast<size_t>(kRunWarps) * (a.d + 1)) * 8;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;

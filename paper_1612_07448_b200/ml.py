@@ -174,9 +174,9 @@ def _glm_gd(m, y, cfg, mode, name):
     yd = _column(y, n)
     so = _lib.lib()
     cs = nm.c_struct()
-    dev = nm.s.device
+    dev = nm.device
     counter = OpCounter()
-    key = (id(nm._cache), nm.s.data_ptr(), yd.data_ptr(), cfg.iterations, float(cfg.step_size), mode, dev.index)
+    key = (id(nm._cache), nm.blocks[0][1].data_ptr(), yd.data_ptr(), cfg.iterations, float(cfg.step_size), mode, dev.index)
     entry = _GLM_GRAPHS.get(key) if os.environ.get("FB_NO_GRAPHS") is None else None
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -295,10 +295,10 @@ def _take_rows(nm, idx):
     """Dense copy of selected logical rows (ml.py:155-168), gathered on the device."""
     so = _lib.lib()
     st = D.stream_handle()
-    idx_t = torch.as_tensor(np.asarray(idx, dtype=np.int64), device=nm.s.device)
+    idx_t = torch.as_tensor(np.asarray(idx, dtype=np.int64), device=nm.device)
     k = idx_t.numel()
     d = nm.base_cols
-    out = torch.empty((k, d), dtype=torch.float64, device=nm.s.device)
+    out = torch.empty((k, d), dtype=torch.float64, device=nm.device)
     off = 0
     for e, f in nm.blocks:
         w = f.shape[1]
@@ -330,7 +330,7 @@ def kmeans(m, cfg):
     so = _lib.lib()
     st = D.stream_handle()
     cs = nm.c_struct()
-    dev = nm.s.device
+    dev = nm.device
     rng = np.random.default_rng(cfg.rng_seed)
     counter = OpCounter()
     torch.cuda.synchronize()
@@ -390,7 +390,7 @@ def gnmf(m, cfg):
     st = D.stream_handle()
     cs = nm.c_struct()
     nm.ensure_sorted()  # Tᵀ·W scatters as segmented sums over the cached FK-sorted order
-    dev = nm.s.device
+    dev = nm.device
     rng = np.random.default_rng(cfg.rng_seed)
     counter = OpCounter()
     torch.cuda.synchronize()

@@ -1,6 +1,7 @@
 """The normalized matrix on a B200: base-table factors resident in HBM.
 
-Mirrors ``factorla.normmat`` (normmat.py:1-375) for the PK-FK and star variants:
+Mirrors ``factorla.normmat`` (normmat.py:1-375) for the PK-FK, star, M:N and multi-table
+M:N variants:
 ``NormalizedMatrix`` keeps column blocks ``(indicator | None, factor)``, a logical
 transpose flag, and the kept source rows of every attribute table. The factors are
 float64 CUDA tensors (row-major, as the reference's C-contiguous arrays) and each
@@ -10,6 +11,11 @@ unreferenced-row drop and remap) runs in the library's kernels (fb_build.cu).
 HBM layout per matrix: S (n_S × d_S f64), per part: FK (n_S int32), R_kept
 (n_R' × d_R f64), counts (n_R' f64, cached), plus lazily built caches (the FK-sorted
 permutation used by the segmented reductions).
+
+M:N (normmat.py:240-285) and multi-table M:N (normmat.py:288-319) matrices have an
+indicator on every block, S included: T = [I_S·S, I_R·R]. The kernels see them as a
+zero-width entity table plus one attribute part per block (``fb_normalized`` with
+d_s = 0), so every operator and driver runs unchanged on the same gathers/scatters.
 """
 
 import ctypes
@@ -20,7 +26,7 @@ import torch
 
 from . import _device as D
 from . import _lib
-from .exceptions import DataError, ShapeError
+from .exceptions import DataError, EmptyJoinError, ShapeError
 
 __all__ = [
     "IndicatorMatrix",
@@ -28,6 +34,8 @@ __all__ = [
     "ShapeStats",
     "build_pkfk",
     "build_star",
+    "build_mn",
+    "build_multimn",
     "materialize",
     "transpose",
     "stats",
@@ -35,6 +43,8 @@ __all__ = [
 
 PKFK = "pkfk"
 STAR = "star"
+MN = "mn"
+MULTIMN = "multimn"
 DENSE = "dense"  # a regular matrix viewed as T = [S] (q = 0); used by the ML drivers
 
 
@@ -162,10 +172,10 @@ class NormalizedMatrix:
         for e, f in blocks:
             if e is not None and e.cols != f.shape[0]:
                 raise ShapeError(f"indicator cols {e.cols} != factor rows {f.shape[0]}")
-        if blocks[0][0] is not None:
-            raise ShapeError("the first block must be the entity table S (no indicator)")
-        if len(blocks) - 1 > _lib.FB_MAX_PARTS:
-            raise ShapeError(f"at most {_lib.FB_MAX_PARTS} attribute tables are supported")
+        if blocks[0][0] is not None and any(e is None for e, _ in blocks):
+            raise ShapeError("either only the first block (the entity table) or every block has no indicator")
+        if len(blocks) - (1 if blocks[0][0] is None else 0) > _lib.FB_MAX_PARTS:
+            raise ShapeError(f"at most {_lib.FB_MAX_PARTS} indicator blocks are supported")
         self.variant = variant
         self.blocks = blocks
         self.transposed = bool(transposed)
@@ -176,7 +186,17 @@ class NormalizedMatrix:
     # -- shape ------------------------------------------------------------
     @property
     def base_rows(self):
-        return self.blocks[0][1].shape[0]
+        e, f = self.blocks[0]
+        return e.rows if e is not None else f.shape[0]
+
+    @property
+    def device(self):
+        return self.blocks[0][1].device
+
+    @property
+    def indicator_blocks(self):
+        """The blocks the kernels see as attribute parts (all blocks of an M:N matrix)."""
+        return self.blocks[1:] if self.blocks[0][0] is None else self.blocks
 
     @property
     def base_cols(self):
@@ -194,6 +214,8 @@ class NormalizedMatrix:
     # -- accessors ---------------------------------------------------------
     @property
     def s(self):
+        if self.variant == MULTIMN:
+            raise ShapeError(f"{self.variant} variant has no entity block")
         return self.blocks[0][1]
 
     @property
@@ -204,7 +226,7 @@ class NormalizedMatrix:
 
     @property
     def r(self):
-        if self.variant != PKFK:
+        if self.variant not in (PKFK, MN):
             raise ShapeError("r accessor applies to single-attribute variants")
         return self.blocks[1][1]
 
@@ -241,12 +263,18 @@ class NormalizedMatrix:
         st = self._cache.get("c_struct")
         if st is None:
             st = _lib.FbNormalized()
-            s = self.blocks[0][1]
-            st.s = D.ptr(s)
-            st.n_s = s.shape[0]
-            st.d_s = s.shape[1]
-            st.q = len(self.blocks) - 1
-            for i, (e, f) in enumerate(self.blocks[1:]):
+            if self.blocks[0][0] is None:
+                s = self.blocks[0][1]
+                st.s = D.ptr(s)
+                st.n_s = s.shape[0]
+                st.d_s = s.shape[1]
+            else:  # M:N: a zero-width entity table, every block an attribute part
+                st.s = 0
+                st.n_s = self.base_rows
+                st.d_s = 0
+            parts = self.indicator_blocks
+            st.q = len(parts)
+            for i, (e, f) in enumerate(parts):
                 p = st.part[i]
                 p.fk = D.ptr(e.target)
                 p.r = D.ptr(f)
@@ -265,7 +293,7 @@ class NormalizedMatrix:
     def ensure_sorted(self):
         """Build (once) the FK-sorted order of every indicator and expose it to the kernels."""
         st = self._cache.get("c_struct")
-        for i, (e, _) in enumerate(self.blocks[1:]):
+        for i, (e, _) in enumerate(self.indicator_blocks):
             perm, fks = e.sorted_order()
             if st is not None:
                 st.part[i].perm, st.part[i].fk_sorted = D.ptr(perm), D.ptr(fks)
@@ -296,7 +324,7 @@ def materialize(nm):
     """
     so = _lib.lib()
     n, d = nm.base_rows, nm.base_cols
-    out = torch.empty((n, d), dtype=torch.float64, device=nm.s.device)
+    out = torch.empty((n, d), dtype=torch.float64, device=nm.device)
     offs = nm.col_offsets()
     st = D.stream_handle()
     for (e, f), c0, c1 in zip(nm.blocks, offs[:-1], offs[1:]):
@@ -397,6 +425,90 @@ def build_star(s, parts):
     return NormalizedMatrix(STAR, blocks, source_rows=source, host_io=host)
 
 
+def build_mn(s, j_s, r, j_r):
+    """M:N normalized matrix from join columns of equal values (normmat.py:240-285).
+
+    Output rows are enumerated in lexicographic (S-row, R-row) order; rows of either table
+    that match nothing are dropped before the indicators are built. The join planning runs
+    on the device: join values coded through the sorted common values, R rows grouped by
+    code with a stable sort, then per S row its group expanded into consecutive output rows.
+    """
+    host = D.is_host(s)
+    s = D.as_matrix(s)
+    r = D.as_matrix(r)
+    dev = s.device
+    js = D.as_vector_i64(j_s)
+    jr = D.as_vector_i64(j_r)
+    if js.dtype != jr.dtype:
+        js, jr = js.to(torch.float64), jr.to(torch.float64)
+    if js.numel() != s.shape[0]:
+        raise ShapeError(f"join column length {js.numel()} != S rows {s.shape[0]}")
+    if jr.numel() != r.shape[0]:
+        raise ShapeError(f"join column length {jr.numel()} != R rows {r.shape[0]}")
+    common = torch.unique(js)
+    common = common[torch.isin(common, jr)]  # np.intersect1d: sorted unique common values
+    if common.numel() == 0:
+        raise EmptyJoinError("M:N join is empty: the join columns share no values")
+    s_keep = torch.nonzero(torch.isin(js, common)).reshape(-1)
+    r_keep = torch.nonzero(torch.isin(jr, common)).reshape(-1)
+    s_code = torch.searchsorted(common, js.index_select(0, s_keep))
+    r_code = torch.searchsorted(common, jr.index_select(0, r_keep))
+    r_order = torch.sort(r_code, stable=True).indices  # groups of kept R rows, ascending within
+    group_sizes = torch.bincount(r_code, minlength=common.numel())
+    group_starts = torch.cumsum(group_sizes, 0) - group_sizes
+    match = group_sizes.index_select(0, s_code)
+    n_out = int(match.sum().item())
+    if n_out >= 2**31:
+        raise ShapeError(f"M:N join output has {n_out} rows; the device indicators are int32")
+    i_s = torch.repeat_interleave(torch.arange(s_keep.numel(), device=dev), match)
+    out_starts = torch.cumsum(match, 0) - match
+    within = torch.arange(n_out, device=dev) - torch.repeat_interleave(out_starts, match)
+    i_r = r_order.index_select(0, torch.repeat_interleave(group_starts.index_select(0, s_code), match) + within)
+    s_kept = _take(s, s_keep)
+    r_kept = _take(r, r_keep)
+    ind_s = IndicatorMatrix(i_s.to(torch.int32), s_keep.numel())
+    ind_r = IndicatorMatrix(i_r.to(torch.int32), r_keep.numel())
+    return NormalizedMatrix(MN, [(ind_s, s_kept), (ind_r, r_kept)], source_rows=[s_keep, r_keep], host_io=host)
+
+
+def build_multimn(row_map, tables):
+    """Multi-table M:N normalized matrix from an explicit row mapping (normmat.py:288-319).
+
+    ``row_map`` is an (n_out, q) integer array whose column j holds the 0-based row of
+    ``tables[j]`` feeding each output row. Unreferenced table rows are dropped and indices
+    compacted (the remap kernels of build_pkfk, on 1-based keys).
+    """
+    host = D.is_host(tables[0]) if len(tables) else True
+    rm = row_map if isinstance(row_map, torch.Tensor) else torch.from_numpy(np.asarray(row_map, dtype=np.int64))
+    if rm.dim() != 2:
+        raise ShapeError("row_map must be 2-D (output rows x tables)")
+    if rm.shape[0] < 1:
+        raise EmptyJoinError("row mapping has no output rows")
+    if rm.shape[1] != len(tables):
+        raise ShapeError(f"row_map has {rm.shape[1]} columns but {len(tables)} tables given")
+    blocks, source = [], []
+    for j, t in enumerate(tables):
+        t = D.as_matrix(t)
+        refs = rm[:, j].to(device=t.device, dtype=torch.int64).contiguous()
+        lo, hi = int(refs.min().item()), int(refs.max().item())
+        if lo < 0 or hi >= t.shape[0]:
+            raise DataError(f"row_map column {j} references nonexistent rows")
+        ind, kept, used = _remap_part((refs + 1).contiguous(), t, part_label=f" (table {j})")
+        blocks.append((ind, kept))
+        source.append(used)
+    return NormalizedMatrix(MULTIMN, blocks, source_rows=source, host_io=host)
+
+
+def _take(f, rows):
+    """f[rows] with the library's row gather (rows: int64 device indices)."""
+    out = torch.empty((rows.numel(), f.shape[1]), dtype=torch.float64, device=f.device)
+    if rows.numel() and f.shape[1]:
+        so = _lib.lib()
+        _lib.check(so.fb_gather_rows(D.ptr(f), f.shape[1], D.ptr(rows.contiguous()), rows.numel(), f.shape[1],
+                                     D.ptr(out), f.shape[1], D.stream_handle()))
+    return out
+
+
 # ---------------------------------------------------------------------------
 # shape statistics
 
@@ -421,11 +533,19 @@ class ShapeStats:
 
 
 def stats(nm):
+    """Shape statistics (normmat.py:340-375; transpose flag ignored)."""
     base = nm.untransposed()
     n_log, d_log = base.shape
-    n_s, d_s = base.s.shape
-    n_r = tuple(f.shape[0] for _, f in base.blocks[1:])
-    d_r = tuple(f.shape[1] for _, f in base.blocks[1:])
-    tr = n_s / max(n_r) if n_r else 1.0
-    fr = (sum(d_r) / d_s) if d_s > 0 else float("inf")
+    if nm.variant == MULTIMN:  # no entity table
+        n_s, d_s = 0, 0
+        n_r = tuple(f.shape[0] for _, f in base.blocks)
+        d_r = tuple(f.shape[1] for _, f in base.blocks)
+        tr = n_log / max(n_r)
+        fr = float("inf")
+    else:
+        n_s, d_s = base.blocks[0][1].shape
+        n_r = tuple(f.shape[0] for _, f in base.blocks[1:])
+        d_r = tuple(f.shape[1] for _, f in base.blocks[1:])
+        tr = n_s / max(n_r) if n_r else 1.0
+        fr = (sum(d_r) / d_s) if d_s > 0 else float("inf")
     return ShapeStats(nm.variant, n_s, d_s, n_r, d_r, n_log, d_log, float(tr), float(fr))

@@ -140,7 +140,7 @@ def row_sums(nm, counter=None):
         return D.to_like(_as_dev(r).t().contiguous(), nm.host_io)
     so = _lib.lib()
     n = nm.base_rows
-    out = torch.empty((n, 1), dtype=torch.float64, device=nm.s.device)
+    out = torch.empty((n, 1), dtype=torch.float64, device=nm.device)
     cs = nm.c_struct()
     ws = D.workspace(so.fb_row_sums_workspace_bytes(cs))
     _lib.check(so.fb_row_sums(cs, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
@@ -159,7 +159,7 @@ def col_sums(nm, counter=None):
         r = row_sums(nm.T, counter)
         return D.to_like(_as_dev(r).t().contiguous(), nm.host_io)
     so = _lib.lib()
-    out = torch.empty((1, nm.base_cols), dtype=torch.float64, device=nm.s.device)
+    out = torch.empty((1, nm.base_cols), dtype=torch.float64, device=nm.device)
     cs = nm.c_struct()
     ws = D.workspace(so.fb_col_sums_workspace_bytes(cs))
     _lib.check(so.fb_col_sums(cs, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
@@ -179,7 +179,7 @@ def sum_all(nm, counter=None):
     base = nm.untransposed()
     so = _lib.lib()
     cs = base.c_struct()
-    out = torch.empty(1, dtype=torch.float64, device=base.s.device)
+    out = torch.empty(1, dtype=torch.float64, device=base.device)
     d = base.base_cols
     ws = D.workspace(so.fb_col_sums_workspace_bytes(cs) + 8 * d + 512)
     _lib.check(so.fb_sum_all(cs, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))

@@ -7,8 +7,18 @@ import numpy as np
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
-def names():
+def _all():
     return sorted(os.path.splitext(os.path.basename(p))[0] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+
+
+def names():
+    """PK-FK / star fixtures (S plus keyed attribute tables)."""
+    return [n for n in _all() if not n.startswith(("mn_", "multimn_"))]
+
+
+def mn_names():
+    """M:N and multi-table M:N fixtures (normmat.py:240-319)."""
+    return [n for n in _all() if n.startswith(("mn_", "multimn_"))]
 
 
 def load(name):
