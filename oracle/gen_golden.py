@@ -169,6 +169,59 @@ def main_mn():
         print("wrote", path, os.path.getsize(path), "bytes", "factorla", getattr(factorla, "__version__", "?"))
 
 
+def main_products():
+    """gram_transposed / ginv / dmm / dmm_gram / pair_product / elementwise (rewrite.py:301-470)."""
+    sys.path.insert(0, REF)
+    os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    import warnings
+
+    from factorla import indicator, kernel, normmat, rewrite
+
+    rng = np.random.default_rng(301)
+    rec = {}
+
+    def pk(prefix, n_s, d_s, n_r, d_r):
+        s = rng.standard_normal((n_s, d_s))
+        k = rng.integers(1, n_r + 1, size=n_s)
+        r = rng.standard_normal((n_r, d_r))
+        rec.update({f"{prefix}_s": s, f"{prefix}_k": k, f"{prefix}_r": r})
+        return normmat.build_pkfk(s, k, r)
+
+    def cnt(name, fn):
+        c = kernel.OpCounter()
+        out = fn(c)
+        rec[name] = out.toarray() if hasattr(out, "toarray") else np.asarray(out)
+        rec["cnt_" + name] = np.array([c.multiplies, c.additions])
+
+    a = pk("a", 120, 5, 17, 7)        # A: 120 x 12 (tall)
+    w = pk("w", 6, 4, 3, 5)           # W: 6 x 9 (wide)
+    cnt("gram_t_a", lambda c: rewrite.gram_transposed(a, c))
+    cnt("gram_t_w", lambda c: rewrite.gram_transposed(w.T, c))
+    cnt("ginv_a", lambda c: rewrite.ginv(a, c))
+    cnt("ginv_at", lambda c: rewrite.ginv(a.T, c))
+    cnt("ginv_w", lambda c: rewrite.ginv(w, c))
+    cnt("ginv_wt", lambda c: rewrite.ginv(w.T, c))
+    b = pk("b", 12, 3, 5, 4)          # B: 12 x 7 (rows = A's columns)
+    cnt("dmm_ab", lambda c: rewrite.dmm(a, b, c))
+    b2 = pk("b2", 120, 2, 9, 3)       # same rows as A: A'B2 (atb)
+    cnt("dmm_atb", lambda c: rewrite.dmm(a.T, b2, c))
+    for tag, ds in (("lt", 3), ("eq", 5), ("gt", 8)):  # d_S of B3 below / equal / above A's
+        b3 = pk(f"b3{tag}", 40, ds, 11, 12 - ds)
+        cnt(f"dmm_abt_{tag}", lambda c, b3=b3: rewrite.dmm(a, b3.T, c))
+    b4 = pk("b4", 9, 2, 4, 10)        # B4 (9 x 12): A'' B4' = (B4 A)'... dmm(A.T, B4.T) = (B4 A)'
+    cnt("dmm_atbt", lambda c: rewrite.dmm(b4.T, pk("c", 12, 2, 3, 7).T, c))
+    cnt("pair_ab2", lambda c: indicator.pair_product(a.k, b2.k, c))
+    x = rng.standard_normal(a.shape)
+    rec["ew_x"] = x
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for op in ("add", "sub", "rsub", "mul", "div", "rdiv"):
+            cnt(f"ew_{op}", lambda c, op=op: rewrite.elementwise_matrix_op(a, x, op, c))
+    path = os.path.join(OUT, "products.npz")
+    np.savez_compressed(path, **{k: np.asarray(v) for k, v in rec.items()})
+    print("wrote", path, os.path.getsize(path), "bytes")
+
+
 def main():
     sys.path.insert(0, REF)
     os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
@@ -256,6 +309,9 @@ def main():
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "mn":
         main_mn()
+    elif len(sys.argv) > 1 and sys.argv[1] == "products":
+        main_products()
     else:
         main()
         main_mn()
+        main_products()

@@ -31,6 +31,15 @@ from .normmat import (
     transpose,
 )
 from .rewrite import col_sums, crossprod, lmm, rmm, row_sums, scalar_fn, scalar_op, sum_all
+from .products import (
+    MaterializationWarning,
+    dmm,
+    dmm_gram,
+    elementwise_matrix_op,
+    ginv,
+    gram_transposed,
+    pair_product,
+)
 from .ml import ModelOutput, TrainConfig, gnmf, kmeans, linreg_gd, linreg_normal, logistic_gd
 
 __version__ = "0.1.0"
@@ -63,6 +72,13 @@ __all__ = [
     "scalar_fn",
     "scalar_op",
     "sum_all",
+    "gram_transposed",
+    "ginv",
+    "dmm",
+    "dmm_gram",
+    "elementwise_matrix_op",
+    "pair_product",
+    "MaterializationWarning",
     "launch_count",
     "ModelOutput",
     "TrainConfig",

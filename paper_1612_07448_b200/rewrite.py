@@ -39,6 +39,12 @@ __all__ = [
     "lmm",
     "rmm",
     "crossprod",
+    "gram_transposed",
+    "ginv",
+    "dmm",
+    "dmm_gram",
+    "elementwise_matrix_op",
+    "MaterializationWarning",
 ]
 
 _SCALAR_OPS = {"add": 0, "radd": 1, "sub": 2, "rsub": 3, "mul": 4, "rmul": 5, "div": 6, "rdiv": 7, "pow": 8, "rpow": 9}
@@ -280,3 +286,13 @@ def crossprod(nm, method="efficient", counter=None):
     from .crossprod_impl import crossprod as _cp
 
     return _cp(nm, method=method, counter=counter)
+
+
+from .products import (  # noqa: E402  (rewrite.py:301-470: the rest of the operator surface)
+    MaterializationWarning,
+    dmm,
+    dmm_gram,
+    elementwise_matrix_op,
+    ginv,
+    gram_transposed,
+)

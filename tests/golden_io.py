@@ -13,7 +13,7 @@ def _all():
 
 def names():
     """PK-FK / star fixtures (S plus keyed attribute tables)."""
-    return [n for n in _all() if not n.startswith(("mn_", "multimn_"))]
+    return [n for n in _all() if not n.startswith(("mn_", "multimn_")) and n != "products"]
 
 
 def mn_names():
