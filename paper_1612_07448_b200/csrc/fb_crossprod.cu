@@ -31,7 +31,9 @@ namespace fb {
 constexpr int kNB = 4;          // block tiles one warp may touch (BS = 2: 4 × 16 accumulator registers)
 constexpr int kMaxGroups = 16;  // gridDim.y job groups
 constexpr int kMaxBT = 256;     // block tiles per pass
-constexpr int kWalkers = 3;     // KᵀS walker warps of the fused S pass (416 + 96 threads: 128 registers each)
+constexpr int kWalkers = 3;     // KᵀS walker warps of the fused S pass (416 + 96 threads: 128 registers each;
+                                // a fourth walker caps registers at 96 and the consumers spill)
+constexpr int kWalkNB = kNB;    // block tiles per consumer warp in the fused pass
 
 // block tile code: bits 0-5 A block bi, bits 6-11 W block bj, bit 12 W from region 1.
 // Host-built assignment (build_block_jobs): the (block tile, k-step) units of a tile are
@@ -308,7 +310,7 @@ FB_DEV void kts_walk_tiles(TileRing& ring, const StreamSet& ss, const GramArgs& 
 
 // NW > 0: fused KᵀS walk (see kts_walk_tiles) on NW extra warps, CJ = ceil(d_S / 32) columns
 // per lane.
-template <int BS, bool SCALE, int NW = 0, int CJ = 1>
+template <int BS, bool SCALE, int NW = 0, int CJ = 1, int NB = kNB>
 __global__ void __launch_bounds__(kRingThreads + 32 * NW, 1)
     cp_gram_kernel(const __grid_constant__ BlockJobs jobs, GramArgs a, StreamSet ss, int stages, int tile_rows) {
   extern __shared__ __align__(128) char smem[];
@@ -329,7 +331,6 @@ __global__ void __launch_bounds__(kRingThreads + 32 * NW, 1)
 
   const WarpJob& wj = jobs.w[grp][warp];
   const int nb = (a.debug & 2) ? 0 : wj.nb;
-  constexpr int NB = kNB;
   int ka[NB], kb[NB], code[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
@@ -565,7 +566,8 @@ namespace {
 // group the units are split over the consumer warps as described at WarpJob. The first
 // `walkers` consumer warps of group 0 run the KᵀS walk and get no units. wmask receives,
 // per block tile, the warps that hold units of it.
-bool build_block_jobs(int T2a, int T2b, int nks, int walkers, BlockJobs& J, uint8_t* wmask, bool r1only = false) {
+bool build_block_jobs(int T2a, int T2b, int nks, int walkers, BlockJobs& J, uint8_t* wmask, bool r1only = false,
+                      int nb_max = kNB) {
   std::vector<uint16_t> list;
   for (int bi = 0; bi < T2a; ++bi) {
     if (!r1only)
@@ -606,7 +608,7 @@ bool build_block_jobs(int T2a, int T2b, int nks, int walkers, BlockJobs& J, uint
         while (u0 < u1) {
           const int b = static_cast<int>(u0 / nks);
           const int64_t e = std::min<int64_t>(u1, static_cast<int64_t>(b + 1) * nks);
-          if (wj.nb == kNB) {
+          if (wj.nb == nb_max) {
             ok = false;
             break;
           }
@@ -665,7 +667,7 @@ cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_ro
   cudaError_t e;
 #define FB_WALK_CASE(S, CJ)                                                                                     \
   if (bs == S && walk_cj == CJ) {                                                                               \
-    auto kern = cp_gram_kernel<S, false, kWalkers, CJ>;                                                         \
+    auto kern = cp_gram_kernel<S, false, kWalkers, CJ, kWalkNB>;                                                \
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));        \
     if (e != cudaSuccess) return e;                                                                             \
     kern<<<gdim, kRingThreads + 32 * kWalkers, smem, st>>>(J, a, ss, stages, tile_rows);                         \
@@ -876,7 +878,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     const int tr = fused_tile_rows(c.d_s);
     ReduceArgs r{sp, 0, a.ra, a.cw, a.w1_col0, c.d_s, 0, 0, 0, c.out, d, 8 * bs_s, t2s, 0, {}};
     BlockJobs JS;
-    if (!build_block_jobs(t2s, 0, tr / 4, 0, JS, r.wmask)) return cudaErrorNotSupported;
+    if (!build_block_jobs(t2s, 0, tr / 4, 0, JS, r.wmask, false, kWalkNB)) return cudaErrorNotSupported;
     int gridx = 0;
     e = run_gram(JS, a, ss, tr, st, num_sms, &gridx, bs_s, (c.d_s + 31) / 32);
     if (e != cudaSuccess) return e;
