@@ -437,15 +437,17 @@ __global__ void __launch_bounds__(kRingThreads + 32 * NW, 1)
   }
 }
 
-// Combine the CTA-boundary runs in CTA order and zero the bins no row maps to at the
-// CTA seams and at both ends (one CTA; thread c owns column c). Carry slots come in
-// (first run, last run) pairs per CTA; interior gaps were zeroed by the walker.
-__global__ void cp_carry_fixup_kernel(const int* carry_key, const double* carry_val, int nslots, int cols,
-                                      double* bins, int64_t n_bins) {
-  // one CTA per carry slot (threads over columns): the slot that starts a key's run of slots
-  // sums that run in slot order and writes the bins row; slots of a CTA's first run also
-  // zero the keys between the previous run and theirs (a CTA seam), the last run the tail
-  const int i = blockIdx.x;
+// Combine the boundary runs in slot order and zero the bins no row maps to at the seams and
+// at both ends. Carry slots come in (first run, last run) pairs per walker range / per fused
+// tile; interior gaps were zeroed by the walkers. One warp per slot (lanes over columns): the
+// slot that starts a key's run of slots sums that run in slot order and writes the bins row;
+// an even slot (a range's first run) also zeroes the keys between the previous run and its
+// own (a seam), the last run the tail. (One CTA per slot cost ~160 us at c3's 312k slots.)
+__global__ void cp_carry_fixup_kernel(const int* __restrict__ carry_key, const double* __restrict__ carry_val,
+                                      int nslots, int cols, double* __restrict__ bins, int64_t n_bins) {
+  const int i = static_cast<int>((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= nslots) return;
   const int k = carry_key[i];
   if (k < 0) return;
   int prev = -1;  // key of the previous valid slot
@@ -455,28 +457,36 @@ __global__ void cp_carry_fixup_kernel(const int* carry_key, const double* carry_
       break;
     }
   if (prev == k) return;  // not the head of its run of slots
-  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
-    double sum = 0.0;
-    int last = i;
-    for (int j = i; j < nslots; ++j) {
-      const int kj = carry_key[j];
-      if (kj < 0) continue;
-      if (kj != k) break;
-      sum += carry_val[static_cast<size_t>(j) * cols + c];
-      last = j;
+  int last = i;
+  for (int j = i + 1; j < nslots; ++j) {
+    const int kj = carry_key[j];
+    if (kj < 0) continue;
+    if (kj != k) break;
+    last = j;
+  }
+  bool tail = true;  // no valid slot after this run: zero the keys above it
+  for (int j = last + 1; j < nslots; ++j)
+    if (carry_key[j] >= 0) {
+      tail = false;
+      break;
     }
+  for (int c = lane; c < cols; c += 32) {
+    double sum = 0.0;
+    for (int j = i; j <= last; ++j)
+      if (carry_key[j] >= 0) sum += carry_val[static_cast<size_t>(j) * cols + c];
     bins[static_cast<int64_t>(k) * cols + c] = sum;
     if ((i & 1) == 0)
       for (int z = prev + 1; z < k; ++z) bins[static_cast<int64_t>(z) * cols + c] = 0.0;
-    bool tail = true;  // no valid slot after this run: zero the keys above it
-    for (int j = last + 1; j < nslots; ++j)
-      if (carry_key[j] >= 0) {
-        tail = false;
-        break;
-      }
     if (tail)
       for (int64_t z = k + 1; z < n_bins; ++z) bins[z * cols + c] = 0.0;
   }
+}
+
+static void launch_carry_fixup(const int* ckey, const double* cval, int nslots, int cols, double* bins,
+                               int64_t n_bins, cudaStream_t st) {
+  if (nslots <= 0) return;
+  cp_carry_fixup_kernel<<<(nslots + 7) / 8, 256, 0, st>>>(ckey, cval, nslots, cols, bins, n_bins);
+  FB_LAUNCHED();
 }
 
 // Final assembly of one pass: element (i, j) of the pass = Σ over CTAs x, then over the
@@ -726,8 +736,7 @@ cudaError_t launch_kts(const CrossArgs& c, double* bins, int* ckey, double* cval
 #undef FB_KTS_CASE
   FB_LAUNCHED();
   const int slots = 2 * kts_warps(num_sms);
-  cp_carry_fixup_kernel<<<slots, ((c.d_s + 31) / 32) * 32, 0, st>>>(ckey, cval, slots, c.d_s, bins, c.n_r);
-  FB_LAUNCHED();
+  launch_carry_fixup(ckey, cval, slots, c.d_s, bins, c.n_r, st);
   return cudaGetLastError();
 }
 
@@ -885,8 +894,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     r.gridx = gridx;
     launch_reduce(r, st);
     const int nslots = static_cast<int>(2 * ((c.n_s + tr - 1) / tr));  // two carry slots per tile
-    cp_carry_fixup_kernel<<<nslots, ((c.d_s + 31) / 32) * 32, 0, st>>>(ckey, cval, nslots, c.d_s, bins, c.n_r);
-    FB_LAUNCHED();
+    launch_carry_fixup(ckey, cval, nslots, c.d_s, bins, c.n_r, st);
   }
   bool forked = false;
   if (!fused && q && c.d_s > 0 && c.n_s > 0) {
