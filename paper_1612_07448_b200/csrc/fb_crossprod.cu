@@ -650,6 +650,10 @@ int gram_tile_rows(uint32_t row_bytes, bool gather) {
   if (rows > (gather ? 128 : 256)) rows = gather ? 128 : 256;
   rows = (rows / unit) * unit;
   if (rows < unit) rows = unit;
+  // long rows (the c3 R pass: 1480 B): 64-row tiles in two ~95 KB stages beat 32-row tiles in
+  // four — a warp's per-tile overhead (ring wait, job loop, pipeline prologue) is paid over 16
+  // k-steps instead of 8 (R pass 0.83 -> 0.74 ms)
+  if (!gather && rows < 64 && 2u * 64u * row_bytes + 2048u <= 200u * 1024u) rows = 64;
   return rows;
 }
 
