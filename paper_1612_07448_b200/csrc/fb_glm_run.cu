@@ -2,16 +2,20 @@
 // ml.py:239-254) in ONE cooperative launch, for problems whose factors sit in L2 (c1:
 // S 100k×20, R 10k×40 — 24 MB). Per-iteration launches (z-pass, fused S pass, R-side
 // reduction, update: fb_glm_step) are latency bound there (~60 µs per iteration even as a
-// CUDA graph); here an iteration is three grid barriers:
-//   phase 1  z_q = R_q·w_q (one warp per R row, lanes over columns), bins_q = 0
-//   phase 2  t_i = S_i·w_S + Σ_q z_q[fk_q,i] (L lanes per S row, 32/L rows per warp step);
-//            p_i / loss_i as in fb_ml.cu; Kᵀp scattered into bins_q (atomics, as the
-//            per-iteration path); g_S += p_i S_i in registers → per-CTA partials
-//   phase 3  g_q = bins_qᵀ R_q per CTA slice → per-CTA partials
-//   phase 4  every CTA sums the partials in CTA order (identical, deterministic) and
-//            applies w ± α·g to its own shared-memory copy of w — no fourth barrier.
-// z / bins / partials are double-buffered by iteration parity, so phase 1 of the next
-// iteration never races phase 3/4 readers of this one.
+// CUDA graph); here an iteration is two grid barriers:
+//   phase 2  t_i = S_i·w_S + Σ_q R_q[fk_q,i]·w_q (the R rows are dotted in place: at c1 the
+//            extra 0.2 µs of FP64 work replaces a z-pass and its grid barrier); p_i / loss_i
+//            as in fb_ml.cu; Kᵀp scattered into bins_q (atomics, as the per-iteration path);
+//            g_S += p_i S_i in registers → per-warp shared partials
+//   -- barrier --
+//   phase 3  g_q = bins_qᵀ R_q per CTA slice → per-CTA partials; the next iteration's bins
+//            zeroed
+//   -- barrier --
+//   phase 4  every CTA sums the partials in CTA order itself (identical in every CTA,
+//            deterministic) and applies w ± α·g to its own shared-memory copy of w.
+// bins / partials are double-buffered by iteration parity, so a CTA racing ahead into the
+// next iteration never touches buffers a slower CTA still reads. (Four barriers per
+// iteration — a separate z-pass and a grid-distributed g — cost ~34 µs per c1 iteration.)
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
@@ -24,6 +28,8 @@ namespace fb {
 
 constexpr int kRunThreads = 512;
 constexpr int kRunWarps = kRunThreads / 32;
+constexpr int kRunRCols = 8;      // R columns per lane loaded together in the S phase
+constexpr int kRunMaxCtas = 320;  // co-resident CTAs the phase-4 sum unrolls for (2 per SM × 148 = 296)
 
 struct GlmRunArgs {
   const double* s;
@@ -71,34 +77,14 @@ __global__ void __launch_bounds__(kRunThreads, 2) glm_run_kernel(GlmRunArgs a) {
   const bool logistic = a.mode == 0;
   const int W = a.d + 1;
   for (int j = tid; j < a.d; j += kRunThreads) sw[j] = a.w[j];
-  __syncthreads();
+  for (int q = 0; q < a.q; ++q)  // iteration 0's bins
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * kRunThreads + tid; j < a.nr[q];
+         j += static_cast<int64_t>(gridDim.x) * kRunThreads)
+      a.bins[0][q][j] = 0.0;
+  grid.sync();
 
   for (int it = 0; it < a.iters; ++it) {
     const int b = it & 1;
-    // ---- phase 1: z_q = R_q w_q (8 lanes per R row, 4 rows per warp step), bins_q = 0
-    for (int q = 0; q < a.q; ++q) {
-      const double* R = a.r[q];
-      const int dr = a.dr[q];
-      const double* wq = sw + a.off[q];
-      const int zs = lane & 7, zr = lane >> 3;
-      for (int64_t j0 = gwarp * 4; j0 < a.nr[q]; j0 += nwarps * 4) {
-        const int64_t j = j0 + zr;
-        double acc = 0.0;
-        if (j < a.nr[q])
-          for (int c = zs; c < dr; c += 8) acc = fma(R[j * dr + c], wq[c], acc);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (zs == 0 && j < a.nr[q]) {
-          a.z[b][q][j] = acc;
-          a.bins[b][q][j] = 0.0;
-        }
-      }
-    }
-    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[it * 5 + 0] = gtimer();
-    grid.sync();
-    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[it * 5 + 1] = gtimer();
-
     // ---- phase 2: the S pass, two row steps in flight per warp
     double gs[C];
 #pragma unroll
@@ -117,7 +103,29 @@ __global__ void __launch_bounds__(kRunThreads, 2) glm_run_kernel(GlmRunArgs a) {
         const int64_t i = live[h] ? ii[h] : 0;
         yv[h] = a.y[i];
         zsum[h] = 0.0;
-        for (int q = 0; q < a.q; ++q) zsum[h] += a.z[b][q][a.fk[q][i]];  // part order
+        for (int q = 0; q < a.q; ++q) {  // Σ_q R_q[fk]·w_q in part order (rewrite.py:186-190)
+          const double* rrow = a.r[q] + static_cast<int64_t>(a.fk[q][i]) * a.dr[q];
+          const double* wq = sw + a.off[q];
+          // all of the lane's R loads issued together (a runtime-bound loop issued them one
+          // L2 round trip at a time: ~8 µs per row step at c1)
+          const int dr = a.dr[q];
+          double zq = 0.0;
+          for (int c0 = 0; c0 < dr; c0 += kRunRCols * L) {
+            double rv[kRunRCols];
+#pragma unroll
+            for (int m = 0; m < kRunRCols; ++m) {
+              const int c = c0 + sub + m * L;
+              rv[m] = c < dr ? rrow[c] : 0.0;
+            }
+#pragma unroll
+            for (int m = 0; m < kRunRCols; ++m) {
+              const int c = c0 + sub + m * L;
+              if (c < dr) zq = fma(rv[m], wq[c], zq);
+            }
+          }
+          for (int o = L >> 1; o > 0; o >>= 1) zq += __shfl_xor_sync(0xffffffffu, zq, o);
+          zsum[h] += zq;
+        }
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -172,6 +180,10 @@ __global__ void __launch_bounds__(kRunThreads, 2) glm_run_kernel(GlmRunArgs a) {
     // ---- phase 3 needs every CTA's bins: barrier, then g_q = bins_qᵀ R_q over this CTA's rows
     if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[it * 5 + 2] = gtimer();
     grid.sync();
+    for (int q = 0; q < a.q; ++q)  // the next iteration's bins (its atomics start after the next barrier)
+      for (int64_t j = static_cast<int64_t>(blockIdx.x) * kRunThreads + tid; j < a.nr[q];
+           j += static_cast<int64_t>(gridDim.x) * kRunThreads)
+        a.bins[b ^ 1][q][j] = 0.0;
     for (int q = 0; q < a.q; ++q) {
       const double* R = a.r[q];
       const int dr = a.dr[q];
@@ -200,31 +212,41 @@ __global__ void __launch_bounds__(kRunThreads, 2) glm_run_kernel(GlmRunArgs a) {
     if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[it * 5 + 3] = gtimer();
     grid.sync();
 
-    // ---- phase 4: g (and the objective) in CTA order, one warp per column
+    // ---- phase 4: g (and the objective) in CTA order, summed by every CTA itself (warp per
+    // column, lanes strided over CTAs, fixed butterfly: identical in every CTA), then w ± α·g
     {
       const double* P = a.partials[b];
-      for (int64_t c = gwarp; c < W; c += nwarps) {
+      double* gsm = red;  // the warp partials are consumed: reuse the space for g
+      __syncthreads();
+      for (int c = warp; c < W; c += kRunWarps) {
+        // the lane's partials loaded together, then summed in CTA order
+        double pv[kRunMaxCtas / 32];
+#pragma unroll
+        for (int k = 0; k < kRunMaxCtas / 32; ++k) {
+          const int x = lane + 32 * k;
+          pv[k] = x < static_cast<int>(gridDim.x) ? P[static_cast<size_t>(x) * W + c] : 0.0;
+        }
         double sum = 0.0;
-        for (int x = lane; x < static_cast<int>(gridDim.x); x += 32) sum += P[static_cast<size_t>(x) * W + c];
+#pragma unroll
+        for (int k = 0; k < kRunMaxCtas / 32; ++k) sum += pv[k];
         sum = warp_sum(sum);
-        if (lane == 0) a.g[b][c] = sum;
+        if (lane == 0) gsm[c] = sum;
       }
-    }
-    if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[it * 5 + 4] = gtimer();
-    grid.sync();
-    // ---- phase 5: w ± α·g in every CTA's copy
-    __shared__ int bad;
-    if (tid == 0) bad = 0;
-    __syncthreads();
-    for (int c = tid; c < a.d; c += kRunThreads) {
-      const double v = sw[c] + a.alpha * a.g[b][c];
-      sw[c] = v;
-      if (!isfinite(v)) bad = 1;
-    }
-    __syncthreads();
-    if (blockIdx.x == 0 && tid == 0) {
-      a.trace[it] = a.g[b][a.d];
-      if (bad && *a.diverged < 0) *a.diverged = it;
+      __syncthreads();
+      __shared__ int bad;
+      if (tid == 0) bad = 0;
+      __syncthreads();
+      for (int c = tid; c < a.d; c += kRunThreads) {
+        const double v = sw[c] + a.alpha * gsm[c];
+        sw[c] = v;
+        if (!isfinite(v)) bad = 1;
+      }
+      __syncthreads();
+      if (blockIdx.x == 0 && tid == 0) {
+        a.trace[it] = gsm[a.d];
+        if (bad && *a.diverged < 0) *a.diverged = it;
+      }
+      if (a.prof && blockIdx.x == 0 && tid == 0) a.prof[it * 5 + 4] = gtimer();
     }
   }
   if (blockIdx.x == 0)
@@ -235,8 +257,8 @@ bool glm_run_eligible(int64_t n, int ds, int q, const int* dr, int num_sms) {
   if (ds > 256 || q > kMaxParts) return false;
   for (int i = 0; i < q; ++i)
     if (dr[i] > 128) return false;
+  if (2 * num_sms > kRunMaxCtas) return false;  // the phase-4 sum is unrolled for <= kRunMaxCtas CTAs
   // factors small enough to stay in L2 between phases
-  (void)num_sms;
   return static_cast<double>(n) * (ds + 2) * 8 <= 48.0 * 1024 * 1024;
 }
 
@@ -322,11 +344,10 @@ cudaError_t launch_glm_run(const GlmRunIn& in, void* ws, size_t ws_bytes, cudaSt
     unsigned long long h[64 * 5];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, a.prof, sizeof(unsigned long long) * 5 * in.iters, cudaMemcpyDeviceToHost);
-    for (int it = 0; it + 1 < in.iters && it < 4; ++it)
-      fprintf(stderr, "[glm_run] it %d: upd+z %.1f us, sync %.1f, S %.1f, sync+R+part %.1f, sync+g %.1f, sync+upd %.1f\n", it,
-              (h[it * 5 + 0] - (it ? h[it * 5 - 1] : h[0])) / 1e3, (h[it * 5 + 1] - h[it * 5]) / 1e3,
-              (h[it * 5 + 2] - h[it * 5 + 1]) / 1e3, (h[it * 5 + 3] - h[it * 5 + 2]) / 1e3,
-              (h[it * 5 + 4] - h[it * 5 + 3]) / 1e3, (h[it * 5 + 5] - h[it * 5 + 4]) / 1e3);
+    for (int it = 1; it + 1 < in.iters && it < 5; ++it)
+      fprintf(stderr, "[glm_run] it %d: S phase %.1f us, sync+R+partials %.1f, sync+g+update %.1f\n", it,
+              (h[it * 5 + 2] - h[(it - 1) * 5 + 4]) / 1e3, (h[it * 5 + 3] - h[it * 5 + 2]) / 1e3,
+              (h[it * 5 + 4] - h[it * 5 + 3]) / 1e3);
   }
   return e;
 }
