@@ -217,6 +217,24 @@ def main_products():
         warnings.simplefilter("ignore")
         for op in ("add", "sub", "rsub", "mul", "div", "rdiv"):
             cnt(f"ew_{op}", lambda c, op=op: rewrite.elementwise_matrix_op(a, x, op, c))
+    # drivers on a transposed normalized matrix (ml.py: _mm / _tmm / _crossprod dispatch on the
+    # flag; kmeans refuses it in _take_rows)
+    from factorla import ml
+    u = normmat.build_pkfk(rng.random((40, 3)), rng.integers(1, 9, size=40), rng.random((8, 4)))
+    rec.update(u_s=u.s, u_k=np.asarray(u.k.target) + 1, u_r=u.r)
+    n_t = u.T.shape[0]
+    y_lin = rng.standard_normal((n_t, 1))
+    y_log = np.where(rng.standard_normal((n_t, 1)) >= 0, 1.0, -1.0)
+    cfg = ml.TrainConfig(iterations=4, step_size=1e-2, r=2, rng_seed=5)
+    rec.update(ut_y_lin=y_lin, ut_y_log=y_log)
+    out = ml.logistic_gd(u.T, y_log, cfg)
+    rec.update(ut_logreg_w=out.weights, ut_logreg_obj=np.array(out.objective))
+    out = ml.linreg_gd(u.T, y_lin, cfg)
+    rec.update(ut_linreg_gd_w=out.weights, ut_linreg_gd_obj=np.array(out.objective))
+    out = ml.linreg_normal(u.T, y_lin)
+    rec.update(ut_linreg_w=out.weights, ut_linreg_obj=np.array(out.objective))
+    out = ml.gnmf(u.T, cfg)
+    rec.update(ut_gnmf_w=out.factors[0], ut_gnmf_h=out.factors[1], ut_gnmf_obj=np.array(out.objective))
     path = os.path.join(OUT, "products.npz")
     np.savez_compressed(path, **{k: np.asarray(v) for k, v in rec.items()})
     print("wrote", path, os.path.getsize(path), "bytes")

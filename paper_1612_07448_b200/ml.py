@@ -110,8 +110,107 @@ def _matrix(m):
     """Untransposed NormalizedMatrix view of the training input, device results."""
     nm = as_normalized(m)
     if nm.transposed:
-        raise ShapeError("the device drivers expect an untransposed matrix (train on nm, not nm.T)")
+        raise ShapeError("row sampling expects an untransposed matrix")  # ml.py:160-161 (kmeans)
     return nm.device_view()
+
+
+def _transposed(m):
+    return isinstance(m, NormalizedMatrix) and m.transposed
+
+
+# ---------------------------------------------------------------------------
+# drivers on a transposed normalized matrix: the reference's loops (ml.py:199-317) composed
+# from the device operators, whose flag dispatch (rewrite.py:182-183, 204-205) turns T·w into
+# Wᵀ·T scatters and Tᵀ·p into LMM gathers; the n_base-long weight vectors stay on the device
+
+
+def _t_glm(m, y, cfg, mode, name):
+    from .rewrite import lmm
+
+    mt = m.device_view()
+    n, d = mt.shape
+    yd = _column(y, n)
+    counter = OpCounter()
+    w = torch.zeros((d, 1), dtype=torch.float64, device=yd.device)
+    trace = []
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for it in range(cfg.iterations):
+        tw = lmm(mt, w, counter)
+        if mode == 0:
+            p = yd / (1.0 + torch.exp(tw))
+            trace.append(float(torch.sum(torch.log1p(torch.exp(-torch.abs(yd * tw))) + torch.clamp(-yd * tw, min=0.0))))
+            w = w + cfg.step_size * lmm(mt.T, p, counter)
+        else:
+            resid = tw - yd
+            trace.append(float(torch.sum(resid**2)))
+            w = w - cfg.step_size * lmm(mt.T, resid, counter)
+        if not bool(torch.isfinite(w).all()):
+            raise DivergenceError(it)
+    wall = time.perf_counter() - t0
+    return ModelOutput(name, (n, d), cfg, trace, weights=_np(w), wall_time_s=wall, counts=counter)
+
+
+def _t_linreg_normal(m, y):
+    from .products import gram_transposed
+    from .rewrite import lmm
+
+    mt = m.device_view()
+    n, d = mt.shape
+    yd = _column(y, n)
+    counter = OpCounter()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g = _np(gram_transposed(mt.T, counter))  # _crossprod of a transposed matrix (ml.py:148-150)
+    tty = _np(lmm(mt.T, yd, counter))
+    w = _pinv_dense(g, counter) @ tty
+    K.tally_matmul(counter, d, d, 1)
+    resid = lmm(mt, torch.from_numpy(w).to(yd.device), counter) - yd
+    wall = time.perf_counter() - t0
+    out = ModelOutput("linreg_normal", (n, d), None, [float(torch.sum(resid**2))], weights=w)
+    out.wall_time_s = wall
+    out.counts = counter
+    return out
+
+
+def _t_gnmf(m, cfg):
+    from .rewrite import lmm, scalar_fn, sum_all
+
+    mt = m.device_view()
+    n, d = mt.shape
+    if _min_value(mt) < 0:
+        warnings.warn("input has negative entries; GNMF semantics assume non-negative data")
+    rng = np.random.default_rng(cfg.rng_seed)
+    counter = OpCounter()
+    dev = mt.device
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    w = torch.from_numpy(1.0 - rng.random((n, cfg.r))).to(dev)
+    h = torch.from_numpy(1.0 - rng.random((d, cfg.r))).to(dev)
+    sum_t2 = sum_all(scalar_fn(mt, np.square, counter), counter)
+    eps = 1e-12
+    trace = []
+    cpw = _mirror_gram(w, counter)
+    for _ in range(cfg.iterations):
+        ttw = lmm(mt.T, w, counter)
+        h = h * ttw / (h @ cpw + eps)
+        cph = _mirror_gram(h, counter)
+        th = lmm(mt, h, counter)
+        w = w * th / (w @ cph + eps)
+        ttw_now = lmm(mt.T, w, counter)
+        cpw = _mirror_gram(w, counter)
+        sq = sum_t2 - 2.0 * float(torch.sum(ttw_now * h)) + float(torch.sum(cpw * cph))
+        trace.append(float(np.sqrt(max(sq, 0.0))))
+    wall = time.perf_counter() - t0
+    return ModelOutput("gnmf", (n, d), cfg, trace, factors=(_np(w), _np(h)), wall_time_s=wall, counts=counter)
+
+
+def _mirror_gram(f, counter):
+    """kernel.crossprod of a small dense factor: fᵀf with the upper triangle mirrored (kernel.py:138-154)."""
+    g = f.t() @ f
+    g = torch.triu(g) + torch.triu(g, 1).t()
+    K.tally_crossprod(counter, f.shape[0], f.shape[1])
+    return g
 
 
 def _column(y, n, what="y"):
@@ -221,11 +320,15 @@ def logistic_gd(m, y, cfg):
 
     Per iteration: w += α·Tᵀ(y / (1 + exp(T w))); the objective is the stable log-loss.
     """
+    if _transposed(m):
+        return _t_glm(m, y, cfg, 0, "logistic_gd")
     return _glm_gd(m, y, cfg, 0, "logistic_gd")
 
 
 def linreg_gd(m, y, cfg):
     """Least squares by gradient descent: w -= α·Tᵀ(T w - y) (ml.py:239-254)."""
+    if _transposed(m):
+        return _t_glm(m, y, cfg, 1, "linreg_gd")
     return _glm_gd(m, y, cfg, 1, "linreg_gd")
 
 
@@ -254,6 +357,8 @@ def linreg_normal(m, y):
     TᵀT (factorized crossprod, DMMA) and Tᵀy run on the device; the d × d pseudo-inverse
     is the reference's host SVD; the residual objective ‖Tw − y‖² is one fused device pass.
     """
+    if _transposed(m):
+        return _t_linreg_normal(m, y)
     nm = _matrix(m)
     n, d = nm.shape
     yd = _column(y, n)
@@ -379,6 +484,8 @@ def gnmf(m, cfg):
     objective ‖T − W Hᵀ‖ is tracked without materializing T. Tᵀ W of the updated W is
     reused as the next iteration's Tᵀ W (the reference recomputes the same product).
     """
+    if _transposed(m):
+        return _t_gnmf(m, cfg)
     nm = _matrix(m)
     n, d = nm.shape
     r = cfg.r

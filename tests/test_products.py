@@ -105,3 +105,30 @@ def test_device_elementwise_matrix_op_warns_and_matches():
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
             fb.elementwise_matrix_op(a, np.ones((2, 2)), "add")
+
+
+@pytest.mark.gpu
+def test_device_drivers_on_transposed_matrix():
+    """logistic_gd / linreg_gd / linreg_normal / gnmf on nm.T (ml.py dispatches on the flag);
+    kmeans refuses it like the reference's _take_rows."""
+    import paper_1612_07448_b200 as fb
+
+    u = _d("u")
+    cfg = fb.TrainConfig(iterations=4, step_size=1e-2, r=2, rng_seed=5)
+    out = fb.logistic_gd(u.T, G["ut_y_log"], cfg)
+    _close(out.weights, G["ut_logreg_w"])
+    _close(out.objective, G["ut_logreg_obj"])
+    out = fb.linreg_gd(u.T, G["ut_y_lin"], cfg)
+    _close(out.weights, G["ut_linreg_gd_w"])
+    _close(out.objective, G["ut_linreg_gd_obj"])
+    out = fb.linreg_normal(u.T, G["ut_y_lin"])
+    _close(out.weights, G["ut_linreg_w"])
+    # 7 rows, 40 columns: an exact minimum-norm fit, the objective is rounding noise — compared
+    # against ‖y‖² (as the PK-FK exact-fit cases in test_ml_gpu.py)
+    assert abs(out.objective[0] - float(G["ut_linreg_obj"][0])) <= 1e-9 * float(np.sum(G["ut_y_lin"] ** 2))
+    out = fb.gnmf(u.T, cfg)
+    _close(out.factors[0], G["ut_gnmf_w"])
+    _close(out.factors[1], G["ut_gnmf_h"])
+    _close(out.objective, G["ut_gnmf_obj"])
+    with pytest.raises(fb.ShapeError):
+        fb.kmeans(u.T, fb.TrainConfig(iterations=1, k=2))
