@@ -235,6 +235,22 @@ def main_products():
     rec.update(ut_linreg_w=out.weights, ut_linreg_obj=np.array(out.objective))
     out = ml.gnmf(u.T, cfg)
     rec.update(ut_gnmf_w=out.factors[0], ut_gnmf_h=out.factors[1], ut_gnmf_obj=np.array(out.objective))
+    # cost model (costmodel.py:75-134): predicted counts and plans on a few shapes
+    from factorla import costmodel
+    st_mats = {"a": a, "u": u, "w": w}
+    mnm = normmat.build_mn(rng.random((30, 2)), rng.integers(0, 6, size=30), rng.random((12, 3)),
+                           rng.integers(0, 6, size=12))
+    rec.update(mn_s=np.asarray(mnm.blocks[0][1]), mn_r=np.asarray(mnm.blocks[1][1]))
+    rec["mn_ts"] = np.asarray(mnm.blocks[0][0].target)
+    rec["mn_tr"] = np.asarray(mnm.blocks[1][0].target)
+    st_mats["mn"] = mnm
+    for key, nmx in st_mats.items():
+        st = normmat.stats(nmx)
+        for op in costmodel.KNOWN_OPS:
+            pc = costmodel.predict_counts(op, st, d_x=3, n_x=2)
+            rec[f"cm_{key}_{op}"] = np.array([pc.standard, pc.factorized])
+        rec[f"cm_{key}_plan_default"] = np.array(costmodel.decide(st).value)
+        rec[f"cm_{key}_plan_loose"] = np.array(costmodel.decide(st, costmodel.DecisionThresholds(1.0, 0.1)).value)
     path = os.path.join(OUT, "products.npz")
     np.savez_compressed(path, **{k: np.asarray(v) for k, v in rec.items()})
     print("wrote", path, os.path.getsize(path), "bytes")

@@ -41,6 +41,8 @@ from .products import (
     pair_product,
 )
 from .ml import ModelOutput, TrainConfig, gnmf, kmeans, linreg_gd, linreg_normal, logistic_gd
+from . import costmodel
+from .costmodel import auto_dispatch
 
 __version__ = "0.1.0"
 
@@ -80,6 +82,8 @@ __all__ = [
     "pair_product",
     "MaterializationWarning",
     "launch_count",
+    "costmodel",
+    "auto_dispatch",
     "ModelOutput",
     "TrainConfig",
     "gnmf",
