@@ -220,6 +220,9 @@ CP_CASES = [
     (12_345, 0, [(300, 9)], "uniform", 6),     # no entity features
     (40_001, 5, [(97, 6), (1000, 3)], "uniform", 7),  # star: block-column path
     (1, 3, [(1, 2)], "uniform", 8),
+    (30_001, 72, [(2000, 16)], "uniform", 9),   # fused S pass, 3 columns per walker lane
+    (20_000, 100, [(500, 10)], "zipf", 10),     # fused S pass, 4 columns per walker lane
+    (10_000, 130, [(100, 4)], "uniform", 11),   # d_S > 128: the block-column path
 ]
 
 
@@ -274,3 +277,24 @@ def test_crossprod_dense_narrow(n, d):
     cp = fb.crossprod(fb.as_normalized(torch.from_numpy(a).cuda()))
     _close(cp, a.T @ a)
     assert torch.equal(cp, cp.t())
+
+
+def test_crossprod_fused_with_unreferenced_keys():
+    """An indicator whose targets skip some R rows (row-sharded builds keep every R row, so a
+    shard's FK leaves gaps): KᵀS bins without rows are zeroed inside tiles, at tile seams and at
+    both ends, in the fused S pass."""
+    fb = _fb()
+    from paper_1612_07448_b200.normmat import PKFK, IndicatorMatrix, NormalizedMatrix
+
+    rng = np.random.default_rng(12)
+    n_s, d_s, n_r, d_r = 150_001, 12, 4000, 6
+    used = np.sort(rng.choice(np.arange(3, n_r - 5), size=900, replace=False))  # rows 0-2, tail unused
+    target = rng.choice(used, size=n_s)
+    s = rng.random((n_s, d_s))
+    r = rng.random((n_r, d_r))
+    ind = IndicatorMatrix(torch.from_numpy(target.astype(np.int32)).cuda(), n_r)
+    nm = NormalizedMatrix(PKFK, [(None, torch.from_numpy(s).cuda()), (ind, torch.from_numpy(r).cuda())])
+    cp = fb.crossprod(nm).cpu().numpy()
+    t = np.hstack([s, r[target]])
+    _close(cp, t.T @ t)
+    np.testing.assert_array_equal(cp, cp.T)
