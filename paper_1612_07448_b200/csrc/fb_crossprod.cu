@@ -831,9 +831,95 @@ size_t crossprod_workspace_bytes(int64_t n_s, int d_s, int64_t n_r, int d_r, int
   return b + 1024;
 }
 
+// SᵀS of a narrow plain matrix (q = 0, d <= 8: GNMF's WᵀW, 5M × 5 at c5): a thread per row
+// (a warp reads 32 consecutive rows), the d(d+1)/2 upper products in registers, warp
+// butterflies, per-CTA partials in warp order, the last CTA sums the partials in CTA order and
+// writes both triangles (exactly symmetric). The DMMA gram pass costs ~100 µs of tile and job
+// overhead for these 200 MB; this one streams them.
+template <int R>
+__global__ void __launch_bounds__(256) narrow_gram_kernel(const double* __restrict__ f, int64_t n,
+                                                          double* __restrict__ partials, unsigned* counter,
+                                                          double* __restrict__ out, int64_t ldo) {
+  constexpr int P = R * (R + 1) / 2;
+  double acc[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) acc[i] = 0.0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    double v[R];
+#pragma unroll
+    for (int a = 0; a < R; ++a) v[a] = __ldcs(f + i * R + a);
+    int k = 0;
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = a; b < R; ++b, ++k) acc[k] = fma(v[a], v[b], acc[k]);
+  }
+  __shared__ double wpart[8][P];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const double v = warp_sum(acc[k]);
+    if (lane == 0) wpart[warp][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < P) {
+    double v = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) v += wpart[w][threadIdx.x];
+    partials[static_cast<size_t>(blockIdx.x) * P + threadIdx.x] = v;
+  }
+  __threadfence();
+  __shared__ unsigned ticket;
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(counter, 1u);
+  __syncthreads();
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  for (int k = warp; k < P; k += blockDim.x >> 5) {
+    const double v = warp_sum_strided(partials + k, gridDim.x, P);
+    if (lane == 0) {
+      int a = 0, rem = k;
+      while (rem >= R - a) {
+        rem -= R - a;
+        ++a;
+      }
+      const int b = a + rem;
+      out[a * ldo + b] = v;
+      out[b * ldo + a] = v;
+    }
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+static cudaError_t launch_narrow_gram(const double* f, int64_t n, int d, double* partials, unsigned* counter,
+                                      double* out, cudaStream_t st, int num_sms) {
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  const int grid = grid_for(n, 256 * 4, 4, num_sms);
+  switch (d) {
+#define FB_NG_CASE(R)                                                                       \
+  case R:                                                                                   \
+    narrow_gram_kernel<R><<<grid, 256, 0, st>>>(f, n, partials, counter, out, d);           \
+    break;
+    FB_NG_CASE(1) FB_NG_CASE(2) FB_NG_CASE(3) FB_NG_CASE(4) FB_NG_CASE(5) FB_NG_CASE(6) FB_NG_CASE(7) FB_NG_CASE(8)
+#undef FB_NG_CASE
+    default:
+      return cudaErrorNotSupported;
+  }
+  FB_LAUNCHED();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cudaStream_t st, int num_sms) {
   const int d = c.d_s + c.d_r;
   const int q = c.r ? 1 : 0;
+  if (!q && c.d_s >= 1 && c.d_s <= 8 && c.n_s > 0 && !getenv("FB_CP_NO_NARROW")) {
+    // partials (grid × d(d+1)/2 doubles) + counter inside the workspace's first partial slot
+    double* partials = static_cast<double*>(ws);
+    unsigned* counter = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + al(static_cast<size_t>(num_sms) * 4 * 36 * 8));
+    if (al(static_cast<size_t>(num_sms) * 4 * 36 * 8) + 256 > ws_bytes) return cudaErrorInvalidValue;
+    return launch_narrow_gram(c.s, c.n_s, c.d_s, partials, counter, c.out, st, num_sms);
+  }
   const int bs_s = block_size(c.d_s), bs_r = block_size(c.d_r);
   const int t2s = (c.d_s + 8 * bs_s - 1) / (8 * bs_s), t2r = (c.d_r + 8 * bs_r - 1) / (8 * bs_r);
   const int t2b = q && c.d_s > 0 ? (c.d_s + 8 * bs_r - 1) / (8 * bs_r) : 0;

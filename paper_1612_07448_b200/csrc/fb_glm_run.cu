@@ -49,10 +49,8 @@ struct GlmRunArgs {
   int iters;
   double* trace;       // iters
   int* diverged;       // first iteration with a non-finite w (-1 otherwise)
-  double* z[2][kMaxParts];
   double* bins[2][kMaxParts];
   double* partials[2];  // [gridDim.x][d + 1]
-  double* g[2];         // d + 1: the gradient and the objective of an iteration
   int lanes;            // lanes per S row (power of two)
   unsigned long long* prof;  // development: CTA 0's globaltimer at each phase end (FB_GLM_PROF)
   int debug;                 // development bisection (FB_GLM_RUN_DEBUG): 1 no Kᵀp atomics
@@ -264,8 +262,7 @@ bool glm_run_eligible(int64_t n, int ds, int q, const int* dr, int num_sms) {
 
 size_t glm_run_workspace_bytes(int d, const int64_t* nr, int q, int num_sms) {
   size_t b = 2 * ((static_cast<size_t>(2 * num_sms) * (d + 1) * 8 + 255) & ~size_t(255));
-  b += 2 * ((static_cast<size_t>(d + 1) * 8 + 255) & ~size_t(255));
-  for (int i = 0; i < q; ++i) b += 4 * ((static_cast<size_t>(nr[i]) * 8 + 255) & ~size_t(255));
+  for (int i = 0; i < q; ++i) b += 2 * ((static_cast<size_t>(nr[i]) * 8 + 255) & ~size_t(255));
   return b + 256;
 }
 
@@ -324,12 +321,8 @@ cudaError_t launch_glm_run(const GlmRunIn& in, void* ws, size_t ws_bytes, cudaSt
     return reinterpret_cast<double*>(r);
   };
   for (int b = 0; b < 2; ++b) a.partials[b] = take(static_cast<size_t>(grid) * (a.d + 1) * 8);
-  for (int b = 0; b < 2; ++b) a.g[b] = take(static_cast<size_t>(a.d + 1) * 8);
   for (int i = 0; i < in.q; ++i)
-    for (int b = 0; b < 2; ++b) {
-      a.z[b][i] = take(static_cast<size_t>(in.nr[i]) * 8);
-      a.bins[b][i] = take(static_cast<size_t>(in.nr[i]) * 8);
-    }
+    for (int b = 0; b < 2; ++b) a.bins[b][i] = take(static_cast<size_t>(in.nr[i]) * 8);
   if (static_cast<size_t>(p - static_cast<char*>(ws)) > ws_bytes) return cudaErrorInvalidValue;
   static unsigned long long* prof = nullptr;
   if (getenv("FB_GLM_PROF") && in.iters <= 64) {
