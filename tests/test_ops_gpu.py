@@ -298,3 +298,26 @@ def test_crossprod_fused_with_unreferenced_keys():
     t = np.hstack([s, r[target]])
     _close(cp, t.T @ t)
     np.testing.assert_array_equal(cp, cp.T)
+
+
+def test_crossprod_fused_and_unfused_s_pass_agree(monkeypatch):
+    """The fused S pass (SᵀS + KᵀS from one FK-sorted stream) and the two-kernel path
+    (storage-order SᵀS gram + kts_walk_kernel) agree to rounding; so do the narrow-matrix gram
+    and the DMMA gram for a plain d <= 8 matrix."""
+    fb = _fb()
+    rng = np.random.default_rng(13)
+    n_s, d_s, n_r, d_r = 80_001, 30, 3000, 12
+    s = rng.random((n_s, d_s))
+    keys = rng.integers(1, n_r + 1, size=n_s)
+    r = rng.random((n_r, d_r))
+    nm = fb.build_pkfk(s, keys, r)
+    fused = fb.crossprod(nm)
+    monkeypatch.setenv("FB_CP_UNFUSED", "1")
+    unfused = fb.crossprod(nm)
+    _close(fused, unfused, 1e-13)
+    np.testing.assert_array_equal(unfused, unfused.T)
+    w = torch.from_numpy(rng.random((200_003, 6))).cuda()
+    narrow = fb.crossprod(fb.as_normalized(w))
+    monkeypatch.setenv("FB_CP_NO_NARROW", "1")
+    dmma = fb.crossprod(fb.as_normalized(w))
+    _close(narrow, dmma.cpu().numpy(), 1e-13)
