@@ -373,11 +373,77 @@ __global__ void onehot_colsum_kernel(const double* __restrict__ s, int64_t n, in
   if (tid == 0) *counter = 0u;
 }
 
+// Narrow S (d <= 32): lanes over columns, rows in contiguous per-warp ranges, 16 rows' loads
+// in flight per warp, then each row added into the warp's own shared accumulator row
+// acc[a_i][c] (consecutive lanes, consecutive banks). Warps folded in warp order, CTAs in CTA
+// order (deterministic). The per-thread private accumulators above (stride k + 1) ran at half
+// of HBM bandwidth at c4 (0.50 ms for 1.6 GB).
+constexpr int kOhThreads = 512;
+__global__ void __launch_bounds__(kOhThreads) onehot_colsum_lanes_kernel(const double* __restrict__ s, int64_t n, int d,
+                                                                        const int32_t* __restrict__ assign, int k,
+                                                                        double* partials, unsigned* counter, double* out) {
+  extern __shared__ double wacc[];  // [2][warps][k][d]: even / odd rows (two independent RMW chains)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kOhThreads / 32;
+  const int kd = k * d;
+  for (int e = threadIdx.x; e < 2 * nw * kd; e += kOhThreads) wacc[e] = 0.0;
+  __syncthreads();
+  double* acc0 = wacc + warp * kd;
+  double* acc1 = wacc + (nw + warp) * kd;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * nw + warp, nwarps = static_cast<int64_t>(gridDim.x) * nw;
+  const int64_t lo = n * gw / nwarps, hi = n * (gw + 1) / nwarps;
+  const bool on = lane < d;
+  constexpr int U = 16;
+  for (int64_t r0 = lo; r0 < hi; r0 += U) {
+    const int cnt = hi - r0 < U ? static_cast<int>(hi - r0) : U;
+    const int al = lane < cnt ? __ldg(assign + r0 + lane) : 0;
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = (on && u < cnt) ? __ldcs(s + (r0 + u) * d + lane) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int a = __shfl_sync(0xffffffffu, al, u);
+      if (on && u < cnt) ((u & 1) ? acc1 : acc0)[a * d + lane] += v[u];
+    }
+  }
+  __syncthreads();
+  double* part = partials + static_cast<size_t>(blockIdx.x) * kd;  // layout [c][j]
+  for (int e = threadIdx.x; e < kd; e += kOhThreads) {
+    const int j = e / d, c = e % d;
+    double v = 0.0;
+    for (int w = 0; w < 2 * nw; ++w) v += wacc[w * kd + e];
+    part[c * k + j] = v;
+  }
+  __threadfence();
+  __shared__ unsigned ticket;
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(counter, 1u);
+  __syncthreads();
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  for (int e = warp; e < kd; e += nw) {  // one warp per output, CTAs in a fixed order
+    const double v = warp_sum_strided(partials + e, gridDim.x, static_cast<size_t>(kd));
+    if (lane == 0) out[e] = v;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
 size_t onehot_partials_doubles(int d, int k, int num_sms) { return static_cast<size_t>(num_sms) * 2 * d * k; }
 
 cudaError_t launch_onehot_colsum(const double* s, int64_t n, int d, const int32_t* assign, int k, double* partials,
                                  unsigned* counter, double* out, cudaStream_t st, int num_sms) {
   if (d < 1) return cudaSuccess;
+  const size_t lane_smem = 2 * static_cast<size_t>(kOhThreads / 32) * k * d * 8;
+  if (d <= 32 && lane_smem <= 100 * 1024 && !getenv("FB_KM_ONEHOT_OLD")) {
+    cudaError_t e = cudaFuncSetAttribute(onehot_colsum_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(lane_smem));
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    const int grid = grid_for(n, 16 * 256, 2, num_sms);  // <= 2 CTAs per SM: the partials slots
+    onehot_colsum_lanes_kernel<<<grid, kOhThreads, lane_smem, st>>>(s, n, d, assign, k, partials, counter, out);
+    FB_LAUNCHED();
+    return cudaGetLastError();
+  }
   if (d > 256 || k > 64) return cudaErrorNotSupported;
   int threads = 256;
   const size_t smem = static_cast<size_t>(threads) * (k + 1) * 8;
