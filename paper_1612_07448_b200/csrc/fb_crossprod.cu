@@ -974,6 +974,7 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     ss.base[1] = reinterpret_cast<const char*>(c.fk_sorted);
     ss.row_bytes[1] = 4u;
     ss.count = 2;
+    ss.gidx_bulk = !getenv("FB_CP_GIDX_CHUNKS");
     const int tr = fused_tile_rows(c.d_s);
     ReduceArgs r{sp, 0, a.ra, a.cw, a.w1_col0, c.d_s, 0, 0, 0, c.out, d, 8 * bs_s, t2s, 0, {}};
     BlockJobs JS;

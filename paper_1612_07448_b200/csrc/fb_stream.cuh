@@ -64,6 +64,10 @@ struct StreamSet {
   bool bulk_last;        // the final (possibly partial) tile can use bulk copies
   bool row_bulk;         // padded-pitch streams: one bulk copy per row (instead of 16-byte
                          // cp.async chunks) — for tiles of few, long rows
+  bool gidx_bulk;        // gidx rows moved with one bulk copy per row (long rows, no keyed
+                         // gathers in the same ring): the gatherer lanes arrive on "gfull"
+                         // themselves (lane 0 with the warp's byte count) and the copies
+                         // complete it
   const int32_t* gidx;   // optional: stream 0 row r of the ring is source row gidx[r]
                          // (a gathered stream, e.g. rows in FK-sorted order); <= 128 rows/tile
   // keyed gathers: row r of gather g = gbase[g] + key * grow_bytes[g], key = gkeys[g][row]
@@ -320,6 +324,29 @@ struct TileRing {
       }
       if (k + 1 < n) load_keys(tile + 1);  // latency overlaps this stage's wait and copies
       if (k >= stages) mbar_wait(&empty[st], ph ^ 1u);  // the stage is free again
+      if (s.gidx && s.gidx_bulk && bulk_ok(s, tile)) {
+        // one bulk copy per row, lane i moving the warp's row i (its own gidx register): the
+        // copy engine takes a 480-byte row as one request where 16-byte cp.async took 30
+        const uint32_t rb = s.row_bytes[0];
+        char* dst = stage_ptr(st, s, 0);
+        if (lane == 0)
+          mbar_arrive_expect_tx(&gfull[st], static_cast<uint32_t>(rows_w) * rb);
+        else
+          mbar_arrive(&gfull[st]);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = lane + 32 * j;
+          if (i < rows_w)
+            bulk_g2s(dst + static_cast<uint32_t>(gw + kGatherWarps * i) * s.pitch[0],
+                     s.base[0] + static_cast<size_t>(kc[kMaxGather][j]) * rb, rb, &gfull[st]);
+        }
+        if (++st == stages) {
+          st = 0;
+          ph ^= 1u;
+        }
+        continue;
+      }
       if (s.gidx && bulk_ok(s, tile)) {
         // stream 0 rows in gidx order: one row per instruction, lanes over 16-byte chunks
         char* dst = stage_ptr(st, s, 0);
