@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kRingThreads + 32 * NW, 1)
       return;
     }
   }
-  if (ring.service(ss)) return;
+  if (ring.template service<(NW > 0)>(ss)) return;
   const int warp = consumer_warp();
   const int grp = blockIdx.y;
   const int lane = lane_id();

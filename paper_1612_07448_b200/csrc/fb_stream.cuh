@@ -209,14 +209,18 @@ struct TileRing {
     return p;
   }
 
-  // Service warps run their loop and return true; consumers get false.
+  // Service warps run their loop and return true; consumers get false. GIDX_BULK: a ring whose
+  // gidx rows move with one bulk copy each (StreamSet::gidx_bulk) — a separate instantiation
+  // used only by the kernels that need it (a runtime branch, or a second gather loop in every
+  // kernel, slowed the LMM gathers by 2-15%).
+  template <bool GIDX_BULK = false>
   FB_DEV bool service(const StreamSet& s) const {
     if (is_producer_warp()) {
       produce(s);
       return true;
     }
     if (is_gather_warp()) {
-      if (s.ngather > 0 || s.gidx) gather(s);
+      if (s.ngather > 0 || s.gidx) gather<GIDX_BULK>(s);
       return true;
     }
     return false;
@@ -286,6 +290,7 @@ struct TileRing {
   // global memory, loaded one tile ahead, so a gathered tile costs max(stream, key +
   // gather) latency rather than their sum. Gatherer warp gw owns ring rows
   // r ≡ gw (mod kGatherWarps) (<= 64 of them: tiles of at most 256 rows).
+  template <bool GIDX_BULK>
   FB_DEV void gather(const StreamSet& s) const {
     const int lane = threadIdx.x & 31;
     const int gw = (static_cast<int>(threadIdx.x) >> 5) - 1;
@@ -324,7 +329,7 @@ struct TileRing {
       }
       if (k + 1 < n) load_keys(tile + 1);  // latency overlaps this stage's wait and copies
       if (k >= stages) mbar_wait(&empty[st], ph ^ 1u);  // the stage is free again
-      if (s.gidx && s.gidx_bulk && bulk_ok(s, tile)) {
+      if (GIDX_BULK && s.gidx && s.gidx_bulk && bulk_ok(s, tile)) {
         // one bulk copy per row, lane i moving the warp's row i (its own gidx register): the
         // copy engine takes a 480-byte row as one request where 16-byte cp.async took 30
         const uint32_t rb = s.row_bytes[0];
