@@ -339,9 +339,13 @@ def sum_all(sm):
 
 
 def crossprod(sm):
-    """TᵀT: per-rank factorized crossprod partials (each exactly symmetric) summed over ranks
-    in rank order, so the result stays exactly symmetric."""
-    return _allreduce(sm.backend.crossprod(sm.local), sm.group)
+    """TᵀT: per-rank factorized crossprod partials summed over ranks, then the upper triangle
+    mirrored (rewrite.py:298): an all-reduce may sum element (i, j) and its mirror (j, i) in
+    different orders (NCCL rings chunk the buffer), so symmetry is restored explicitly."""
+    g = _allreduce(sm.backend.crossprod(sm.local), sm.group)
+    if _world(sm.group) > 1:
+        g = torch.triu(g) + torch.triu(g, 1).t()
+    return g
 
 
 # ---------------------------------------------------------------------------
