@@ -390,14 +390,30 @@ __global__ void __launch_bounds__(kRingThreads + 32 * NW, 1)
         };
         const int kend = min(kb[b], full);
         if (ka[b] < kend) {
+          // operand pointers advanced by one k-step (4 rows) per iteration instead of an index
+          // product per load (the R pass issued 1.5 IMAD per DMMA; ncu source view)
+          const int kr0 = 4 * ka[b] + t;
+          const double* pa = R0 + kr0 * a.p0 + aoff[b];
+          const double* pw = wbase + kr0 * wp + woff[b];
+          const double* pc = SCALE ? cnt + kr0 : nullptr;
+          const int sa = 4 * a.p0, sw = 4 * wp;
+          auto loadp = [&](double (&av)[BS], double (&wv)[BS], double& c) {
+#pragma unroll
+            for (int u = 0; u < BS; ++u) {
+              av[u] = pa[8 * u];
+              wv[u] = pw[8 * u];
+            }
+            c = SCALE && !reg1[b] ? *pc : 1.0;
+            pa += sa;
+            pw += sw;
+            if (SCALE) pc += 4;
+          };
           double av[BS], wv[BS], c;
-          int kr = 4 * ka[b] + t;
-          load(kr, true, av, wv, c);
+          loadp(av, wv, c);
 #pragma unroll 2
           for (int k = ka[b] + 1; k < kend; ++k) {
-            kr += 4;
             double an[BS], wn[BS], cn;
-            load(kr, true, an, wn, cn);
+            loadp(an, wn, cn);
             mma(av, wv, c);
 #pragma unroll
             for (int u = 0; u < BS; ++u) {
