@@ -100,6 +100,11 @@ int fb_gather_rows(const double* in, int64_t ld_in, const int64_t* idx, int64_t 
 int fb_gather_rows_i32(const double* in, int64_t ld_in, const int32_t* idx, int64_t nrows,
                        int32_t d, double* out, int64_t ld_out, fb_stream_t stream);
 int fb_i32_to_f64(const int32_t* in, double* out, int64_t n, fb_stream_t stream);
+/* Sparse factor matrix ingestion (kernel.py:110-121 stores factors as scipy CSR; dataio.py:208-214
+ * picks CSR at density <= 5%): canonical CSR (sorted, duplicate-free; indptr int64[nrows+1],
+ * indices int32[nnz], data f64[nnz]) expanded into the dense row-major layout (ld_out >= ncols). */
+int fb_csr_expand(const int64_t* indptr, const int32_t* indices, const double* data, int64_t nrows,
+                  int32_t ncols, double* out, int64_t ld_out, fb_stream_t stream);
 
 /* ---- operators (rewrite.py) ------------------------------------------------------ */
 /* LMM T·X (rewrite.py:172-191). x: d x d_x row-major, d = d_s + sum d_r; out: n_s x d_x. */

@@ -43,6 +43,7 @@ from .products import (
 from .ml import ModelOutput, TrainConfig, gnmf, kmeans, linreg_gd, linreg_normal, logistic_gd
 from . import costmodel
 from .costmodel import auto_dispatch
+from . import dataio
 
 __version__ = "0.1.0"
 
@@ -84,6 +85,7 @@ __all__ = [
     "launch_count",
     "costmodel",
     "auto_dispatch",
+    "dataio",
     "ModelOutput",
     "TrainConfig",
     "gnmf",

@@ -30,8 +30,42 @@ def is_host(a):
     return not (isinstance(a, torch.Tensor) and a.is_cuda)
 
 
+def _is_scipy_sparse(a):
+    mod = type(a).__module__
+    return mod.startswith("scipy.sparse") and hasattr(a, "tocsr")
+
+
+def _csr_to_device(a):
+    """A scipy sparse factor matrix expanded into the dense device layout (fb_csr_expand).
+
+    The reference keeps sparse factors as CSR (kernel.py:110-121); here every operator reads
+    row-major f64 rows, so the CSR arrays travel to HBM (nnz-sized copies) and one kernel
+    writes the dense rows. Duplicates are summed first, as scipy does on conversion.
+    """
+    from . import _lib
+
+    m = a.tocsr(copy=True)
+    m.sum_duplicates()
+    n, d = m.shape
+    dev = device()
+    out = torch.empty((n, d), dtype=torch.float64, device=dev)
+    if n and d:
+        indptr = torch.from_numpy(m.indptr.astype(np.int64)).to(dev, non_blocking=True)
+        indices = torch.from_numpy(m.indices.astype(np.int32)).to(dev, non_blocking=True)
+        data = torch.from_numpy(np.ascontiguousarray(m.data, dtype=np.float64)).to(dev, non_blocking=True)
+        _lib.check(_lib.lib().fb_csr_expand(indptr.data_ptr(), ptr(indices), ptr(data), n, d,
+                                            out.data_ptr(), d, stream_handle()))
+    return out
+
+
 def as_matrix(a, dtype=torch.float64):
-    """2-D contiguous float64 CUDA tensor (kernel.as_matrix semantics)."""
+    """2-D contiguous float64 CUDA tensor (kernel.as_matrix semantics).
+
+    scipy sparse inputs are accepted (the reference's CSR factor matrices) and expanded on
+    the device.
+    """
+    if _is_scipy_sparse(a):
+        return _csr_to_device(a)
     if isinstance(a, torch.Tensor):
         t = a
     else:

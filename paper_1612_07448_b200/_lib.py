@@ -68,6 +68,7 @@ _SIGS = {
     "fb_fk_counts": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp]),
     "fb_gather_rows": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),
     "fb_gather_rows_i32": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),
+    "fb_csr_expand": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),
     "fb_i32_to_f64": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "fb_lmm_workspace_bytes": (c_size, [_P, c_i32]),
     "fb_lmm": (c_i32, [_P, c_vp, c_i32, c_vp, c_vp, c_size, c_vp]),

@@ -228,4 +228,31 @@ cudaError_t launch_i32_to_f64(const int32_t* in, double* out, int64_t n, cudaStr
   return cudaGetLastError();
 }
 
+// CSR -> dense rows (a sparse factor matrix of the reference, kernel.py:110-121, expanded into
+// the row-major HBM layout every operator reads). Canonical CSR: no duplicate (row, col) entries,
+// so each output cell has at most one writer. A warp per row; the zero fill is a memset.
+__global__ void csr_expand_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                                  const double* __restrict__ data, int64_t nrows, double* __restrict__ out,
+                                  int64_t ld_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < nrows; r += warps) {
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    double* row = out + r * ld_out;
+    for (int64_t k = b + lane; k < e; k += 32) row[indices[k]] = data[k];
+  }
+}
+
+cudaError_t launch_csr_expand(const int64_t* indptr, const int32_t* indices, const double* data,
+                              int64_t nrows, int32_t ncols, double* out, int64_t ld_out,
+                              cudaStream_t st, int num_sms) {
+  if (nrows <= 0 || ncols <= 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(out, 0, static_cast<size_t>(nrows) * ld_out * sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  csr_expand_kernel<<<grid_for(nrows, 8, 8, num_sms), 256, 0, st>>>(indptr, indices, data, nrows, out, ld_out);
+  FB_LAUNCHED();
+  return cudaGetLastError();
+}
+
 }  // namespace fb
+

@@ -220,6 +220,13 @@ int fb_i32_to_f64(const int32_t* in, double* out, int64_t n, fb_stream_t stream)
   return cuda_status(fb::launch_i32_to_f64(in, out, n, cs(stream), g_num_sms), "i32_to_f64");
 }
 
+int fb_csr_expand(const int64_t* indptr, const int32_t* indices, const double* data, int64_t nrows,
+                  int32_t ncols, double* out, int64_t ld_out, fb_stream_t stream) {
+  if (nrows < 0 || ncols < 0 || ld_out < ncols) return fail(FB_ERR_SHAPE, "csr_expand: bad shape");
+  return cuda_status(fb::launch_csr_expand(indptr, indices, data, nrows, ncols, out, ld_out, cs(stream), g_num_sms),
+                     "csr_expand");
+}
+
 // ------------------------------------------------------------------ LMM / rowSums
 size_t fb_lmm_workspace_bytes(const fb_normalized* nm, int32_t d_x) {
   if (!nm) return 0;

@@ -70,6 +70,9 @@ cudaError_t launch_gather_rows(const double* in, int64_t ld_in, const int64_t* i
                                int64_t ld_out, cudaStream_t st, int num_sms);
 cudaError_t launch_i32_to_f64(const int32_t* in, double* out, int64_t n, cudaStream_t st,
                               int num_sms);
+cudaError_t launch_csr_expand(const int64_t* indptr, const int32_t* indices, const double* data,
+                              int64_t nrows, int32_t ncols, double* out, int64_t ld_out,
+                              cudaStream_t st, int num_sms);
 
 // fb_crossprod.cu --------------------------------------------------------------------
 // Crossprod of a PK-FK (q = 1) or dense (q = 0) normalized matrix.
