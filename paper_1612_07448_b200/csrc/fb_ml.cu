@@ -1,3 +1,4 @@
+#include <algorithm>
 // fb_ml.cu — fused iteration kernels of the ML drivers (ml.py).
 //
 // GLM step (logistic_gd ml.py:199-215, linreg_gd ml.py:239-254), one pass over S per
@@ -427,12 +428,113 @@ __global__ void __launch_bounds__(kOhThreads) onehot_colsum_lanes_kernel(const d
   if (threadIdx.x == 0) *counter = 0u;
 }
 
+// Bulk-staged variant for even d: each warp streams its contiguous row range through its own
+// ring of `stages` shared-memory buffers, 16 rows (16·d·8 bytes, one cp.async.bulk) per buffer,
+// so ~stages·16 rows per warp stay in flight without holding them in registers; the warp's
+// assignments for the next batch are prefetched one batch ahead. The shared accumulators and
+// the deterministic fold are those of onehot_colsum_lanes_kernel.
+constexpr int kOhBatch = 16;
+__global__ void __launch_bounds__(kOhThreads, 1) onehot_colsum_bulk_kernel(const double* __restrict__ s, int64_t n,
+                                                                           int d, const int32_t* __restrict__ assign,
+                                                                           int k, int stages, double* partials,
+                                                                           unsigned* counter, double* out) {
+  extern __shared__ __align__(16) double oh_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kOhThreads / 32;
+  const int kd = k * d;
+  double* wacc = oh_smem;                               // [2][warps][k][d]
+  double* ring = wacc + 2 * nw * kd;                    // [warps][stages][16][d]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(nw) * stages * kOhBatch * d);
+  for (int e = threadIdx.x; e < 2 * nw * kd; e += kOhThreads) wacc[e] = 0.0;
+  uint64_t* mb = bars + warp * stages;
+  if (lane == 0) {
+    for (int st = 0; st < stages; ++st) mbar_init(&mb[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  double* acc0 = wacc + warp * kd;
+  double* acc1 = wacc + (nw + warp) * kd;
+  double* my = ring + static_cast<size_t>(warp) * stages * kOhBatch * d;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * nw + warp, nwarps = static_cast<int64_t>(gridDim.x) * nw;
+  const int64_t lo = n * gw / nwarps, hi = n * (gw + 1) / nwarps;
+  const int64_t nb = (hi - lo + kOhBatch - 1) / kOhBatch;
+  auto issue = [&](int64_t b, int st) {
+    const int64_t r0 = lo + b * kOhBatch;
+    const int cnt = hi - r0 < kOhBatch ? static_cast<int>(hi - r0) : kOhBatch;
+    const uint32_t bytes = static_cast<uint32_t>(cnt) * d * 8u;
+    mbar_arrive_expect_tx(&mb[st], bytes);
+    bulk_g2s(my + st * kOhBatch * d, s + r0 * d, bytes, &mb[st]);
+  };
+  if (lane == 0)
+    for (int b = 0; b < stages && b < nb; ++b) issue(b, b);
+  const bool on = lane < d;
+  int al_next = (nb > 0 && lane < hi - lo) ? __ldg(assign + lo + lane) : 0;
+  int st = 0;
+  uint32_t phase = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t r0 = lo + b * kOhBatch;
+    const int cnt = hi - r0 < kOhBatch ? static_cast<int>(hi - r0) : kOhBatch;
+    const int al = al_next;
+    if (b + 1 < nb) al_next = (lane < hi - r0 - kOhBatch) && lane < kOhBatch ? __ldg(assign + r0 + kOhBatch + lane) : 0;
+    mbar_wait(&mb[st], phase);
+    const double* buf = my + st * kOhBatch * d;
+#pragma unroll
+    for (int u = 0; u < kOhBatch; ++u) {
+      const int a = __shfl_sync(0xffffffffu, al, u);
+      if (on && u < cnt) ((u & 1) ? acc1 : acc0)[a * d + lane] += buf[u * d + lane];
+    }
+    __syncwarp();
+    if (lane == 0 && b + stages < nb) {
+      fence_proxy_async();
+      issue(b + stages, st);
+    }
+    if (++st == stages) {
+      st = 0;
+      phase ^= 1u;
+    }
+  }
+  __syncthreads();
+  double* part = partials + static_cast<size_t>(blockIdx.x) * kd;  // layout [c][j]
+  for (int e = threadIdx.x; e < kd; e += kOhThreads) {
+    const int j = e / d, c = e % d;
+    double v = 0.0;
+    for (int w = 0; w < 2 * nw; ++w) v += wacc[w * kd + e];
+    part[c * k + j] = v;
+  }
+  __threadfence();
+  __shared__ unsigned ticket;
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(counter, 1u);
+  __syncthreads();
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  for (int e = warp; e < kd; e += nw) {
+    const double v = warp_sum_strided(partials + e, gridDim.x, static_cast<size_t>(kd));
+    if (lane == 0) out[e] = v;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
 size_t onehot_partials_doubles(int d, int k, int num_sms) { return static_cast<size_t>(num_sms) * 2 * d * k; }
 
 cudaError_t launch_onehot_colsum(const double* s, int64_t n, int d, const int32_t* assign, int k, double* partials,
                                  unsigned* counter, double* out, cudaStream_t st, int num_sms) {
   if (d < 1) return cudaSuccess;
   const size_t lane_smem = 2 * static_cast<size_t>(kOhThreads / 32) * k * d * 8;
+  const size_t stage_bytes = static_cast<size_t>(kOhThreads / 32) * kOhBatch * d * 8;
+  const int stages = lane_smem < 200 * 1024 ? static_cast<int>(std::min<size_t>(4, (200 * 1024 - lane_smem) / stage_bytes)) : 0;
+  if (d <= 32 && d % 2 == 0 && stages >= 2 && (reinterpret_cast<uintptr_t>(s) & 15) == 0 && !getenv("FB_KM_ONEHOT_LANES") &&
+      !getenv("FB_KM_ONEHOT_OLD")) {
+    const size_t smem = lane_smem + static_cast<size_t>(stages) * stage_bytes + (kOhThreads / 32) * stages * 8;
+    cudaError_t e = cudaFuncSetAttribute(onehot_colsum_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    const int grid = grid_for(n, 16 * kOhBatch, 1, num_sms);
+    onehot_colsum_bulk_kernel<<<grid, kOhThreads, smem, st>>>(s, n, d, assign, k, stages, partials, counter, out);
+    FB_LAUNCHED();
+    return cudaGetLastError();
+  }
   if (d <= 32 && lane_smem <= 100 * 1024 && !getenv("FB_KM_ONEHOT_OLD")) {
     cudaError_t e = cudaFuncSetAttribute(onehot_colsum_lanes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(lane_smem));
