@@ -389,6 +389,17 @@ def zipf_keys_dev(n, n_r, s, gen, dev):
     return torch.clamp(torch.searchsorted(cdf, u, right=True), max=n_r - 1) + 1
 
 
+def _slope(run, trials=3):
+    """Per-iteration wall time of a driver: median over trials of (wall(20) - wall(1)) / 19."""
+    pers, last = [], None
+    for _ in range(trials):
+        r1 = run(1)
+        last = run(20)
+        pers.append((last.wall_time_s - r1.wall_time_s) / 19)
+    pers.sort()
+    return pers[len(pers) // 2], last
+
+
 def run_extras(dev, cpu=True):
     """c3 crossprod + LinReg normal, c1 LogReg iter/s, c4 K-Means, c5 GNMF (BASELINE.json configs)."""
     import torch
@@ -463,12 +474,10 @@ def run_extras(dev, cpu=True):
     nm = fb.build_star(s, [(k1t, r1t), (k2t, r2t)])
     del k1t, k2t
     fb.kmeans(nm, fb.TrainConfig(iterations=2, k=10, rng_seed=0))  # warm: workspaces, kernel attributes
-    res1 = fb.kmeans(nm, fb.TrainConfig(iterations=1, k=10, rng_seed=0))
-    res = fb.kmeans(nm, fb.TrainConfig(iterations=20, k=10, rng_seed=0))
-    per = (res.wall_time_s - res1.wall_time_s) / 19
+    per, res = _slope(lambda it: fb.kmeans(nm, fb.TrainConfig(iterations=it, k=10, rng_seed=0)))
     out["c4_kmeans"] = {"iter_per_s": round(1 / per, 1), "ms_per_iter": round(1e3 * per, 3),
                         "s_total_20_iters": round(res.wall_time_s, 4),
-                        "timing": "per iteration = (wall(20 iters) - wall(1 iter)) / 19; total incl. seeding and rowSums(T²)"}
+                        "timing": "per iteration = median over 3 trials of (wall(20 iters) - wall(1 iter)) / 19; total incl. seeding and rowSums(T²)"}
     del nm, s, r1t, r2t
     torch.cuda.empty_cache()
     # ---- c5: GNMF r=5, 20 iterations, Zipf(1.2) FK (S 5M×10, R 50k×40 U[0,1))
@@ -478,12 +487,10 @@ def run_extras(dev, cpu=True):
     key = zipf_keys_dev(n_s, n_r, 1.2, g, dev)
     nm = fb.build_pkfk(s, key, r)
     fb.gnmf(nm, fb.TrainConfig(iterations=2, r=5, rng_seed=0))  # warm: workspaces, sorted order, attributes
-    res1 = fb.gnmf(nm, fb.TrainConfig(iterations=1, r=5, rng_seed=0))
-    res = fb.gnmf(nm, fb.TrainConfig(iterations=20, r=5, rng_seed=0))
-    per = (res.wall_time_s - res1.wall_time_s) / 19
+    per, res = _slope(lambda it: fb.gnmf(nm, fb.TrainConfig(iterations=it, r=5, rng_seed=0)))
     out["c5_gnmf"] = {"iter_per_s": round(1 / per, 1), "ms_per_iter": round(1e3 * per, 3),
                       "s_total_20_iters": round(res.wall_time_s, 4), "kept_r_rows": int(nm.r.shape[0]),
-                      "timing": "per iteration = (wall(20 iters) - wall(1 iter)) / 19; total incl. the host "
+                      "timing": "per iteration = median over 3 trials of (wall(20 iters) - wall(1 iter)) / 19; total incl. the host "
                                 "RNG draw of W (5M×5, the reference's default_rng call) and its upload"}
     del nm, s, r, key
     torch.cuda.empty_cache()
