@@ -239,3 +239,19 @@ def test_sparse_factors_through_builders():
     x = rng.standard_normal((80, 3))
     np.testing.assert_array_equal(fb.lmm(nm_sp, x), fb.lmm(nm_d, x))
     np.testing.assert_array_equal(fb.crossprod(nm_sp), fb.crossprod(nm_d))
+
+
+def test_sparse_input_fails_loudly_without_gpu():
+    """No CPU fallback: a CSR factor needs the device expansion kernel."""
+    import torch
+    from scipy import sparse
+
+    from paper_1612_07448_b200 import _device as D
+    from paper_1612_07448_b200.exceptions import ExtensionMissingError
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by test_csr_expand_bit_exact")
+    with pytest.raises(ExtensionMissingError):
+        D.as_matrix(sparse.eye(3, format="csr"))
+    with pytest.raises(ExtensionMissingError):
+        dataio.load(os.path.join(DIR, "pkfk_sparse", "schema.json"))
