@@ -23,7 +23,7 @@ __global__ void key_check_hist_kernel(const int64_t* __restrict__ key, int64_t n
     if (k < 1 || k > n_r) {
       atomicMin(first_bad, static_cast<unsigned long long>(i));
     } else {
-      atomicAdd(counts + (k - 1), 1);
+      red_add(counts + (k - 1), 1);
     }
   }
 }
@@ -31,7 +31,7 @@ __global__ void key_check_hist_kernel(const int64_t* __restrict__ key, int64_t n
 __global__ void fk_hist_kernel(const int32_t* __restrict__ fk, int64_t n, int32_t* __restrict__ counts) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
-    atomicAdd(counts + fk[i], 1);
+    red_add(counts + fk[i], 1);
 }
 
 // ---- exclusive scan of used flags (counts > 0) in three phases

@@ -301,6 +301,21 @@ size_t fb_wt_workspace_bytes(const fb_normalized* nm, int32_t n_w) {
   return b;
 }
 
+// X·K for a uniform FK: one RED per row fused into the S pass (the bins — n_R·n_x doubles, 8 MB at
+// c2 — stay L2-resident, and the weights are read in storage order with the S tiles). Skewed FKs
+// (a hot target holding > 1/256 of the rows) take the segmented sums over the cached FK-sorted
+// order instead. FB_WT_SCATTER=seg|atomic overrides the choice (measurement only).
+static bool use_segsum(const fb_part& pt) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("FB_WT_SCATTER");
+    mode = (e && e[0] == 's') ? 1 : (e && e[0] == 'a') ? 2 : 0;
+  }
+  if (mode == 1) return true;
+  if (mode == 2) return false;
+  return pt.skewed != 0;
+}
+
 static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_t w_rs, int64_t w_cs,
                    const double* const* part_weights, double* out, int64_t o_js, int64_t o_cs, void* ws,
                    size_t ws_bytes, fb_stream_t stream) {
@@ -328,7 +343,7 @@ static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_
     c.nfk = 0;
     for (int i = 0; !part_weights && i < nm->q; ++i) {
       const fb_part& pt = nm->part[i];
-      if (pt.perm && pt.fk_sorted && nm->n_s > 0) {
+      if (pt.perm && pt.fk_sorted && nm->n_s > 0 && use_segsum(pt)) {
         // X·K_i as segmented sums over the FK-sorted order (few atomics, no hot-line
         // contention), on the side stream so they overlap the S pass
         if (!forked) {

@@ -112,6 +112,24 @@ FB_DEV uint64_t policy_evict_last() {
   return p;
 }
 
+// A fraction `f` of the addresses (a fixed hash subset) evict_last, the rest evict_first: a
+// lookup table larger than L2 keeps a stable resident subset instead of thrashing.
+FB_DEV uint64_t policy_evict_last_frac(float f) {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;\n" : "=l"(p) : "f"(f));
+  return p;
+}
+
+// Fire-and-forget global reductions (SASS REDG). atomicAdd with an unused result may still
+// compile to ATOMG, which holds a return slot until L2 answers: in the RMM S pass that cost
+// 0.67 ms for 20M adds that a plain REDG loop issues in 0.13 ms (tools/red_probe.cu).
+FB_DEV void red_add(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+}
+FB_DEV void red_add(int* p, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
 // Streaming 128-bit global loads that skip L1 allocation.
 FB_DEV double2 ld_stream_d2(const double2* p) {
   double2 r;

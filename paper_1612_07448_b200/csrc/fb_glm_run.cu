@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kRunThreads, 2) glm_run_kernel(GlmRunArgs a) {
             if (sub == 0) lacc += pv[h] * pv[h];
           }
           if (sub == 0 && !(a.debug & 1))
-            for (int q = 0; q < a.q; ++q) atomicAdd(a.bins[b][q] + a.fk[q][i], pv[h]);
+            for (int q = 0; q < a.q; ++q) red_add(a.bins[b][q] + a.fk[q][i], pv[h]);
         }
       }
 #pragma unroll

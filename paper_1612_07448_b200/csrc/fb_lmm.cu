@@ -41,6 +41,7 @@ struct LmmArgs {
   int zstride;                 // doubles per z row (even: gathered rows are 16-byte bulk copies)
   int lanes;                   // rowdot: lanes per row (power of two)
   int cols;                    // rowdot: columns per lane (d / lanes)
+  float zfrac;                 // z-pass (nfk == 0): evict_last fraction of the stored z rows
 };
 
 // ------------------------------------------------------------------ rowdot (d_x <= 4)
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_rowdot_kernel(LmmArgs p, 
   const int sub = lane % L, rsub = lane / L;
   const int src = (lane % rpi) * L;           // lane k takes row k: iteration k / rpi, group k % rpi
   const int myit = lane / rpi;
-  const uint64_t pol = p.nfk == 0 ? policy_evict_last() : policy_evict_first();  // z stays in L2
+  const uint64_t pol = p.nfk == 0 ? policy_evict_last_frac(p.zfrac) : policy_evict_first();  // z stays in L2
   const double* xc = xs + sub * NX;
 
   for (int64_t kt = 0; kt < ring.count(); ++kt) {
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, St
   const int warp = consumer_warp();
   const int pitch = p.pitch;
   const int wrow = warp * (8 * MT);
-  const uint64_t pol = p.nfk == 0 ? policy_evict_last() : policy_evict_first();
+  const uint64_t pol = p.nfk == 0 ? policy_evict_last_frac(p.zfrac) : policy_evict_first();
   const bool ragged_k = (d & 3) != 0;
   // every output column pair present and 16-byte aligned: one v2 store per pair
   const bool full_cols = p.dx == 8 * NT && (p.ldo & 1) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 15u) == 0;
@@ -283,6 +284,17 @@ static cudaError_t launch_ring(K kern, const LmmArgs& p, StreamSet& ss, size_t f
   return cudaGetLastError();
 }
 
+// z-pass stores: evict_last for this fraction of the z lines (FB_ZSTORE_FRAC overrides it,
+// measurement only: fractions 0.5-1.0, with or without evict_last gathers, all timed the c2
+// X100x16 S pass within 2% of each other)
+static float z_store_frac() {
+  static float f = [] {
+    const char* e = getenv("FB_ZSTORE_FRAC");
+    return e ? static_cast<float>(atof(e)) : 1.0f;
+  }();
+  return f;
+}
+
 // The ring carries the factor rows; the FK columns are read by the gatherer warps only
 // (keys straight from global memory), which copy z[fk] rows into the stage.
 static void fill_streams(const LmmArgs& p, StreamSet& ss, int pitch) {
@@ -381,6 +393,7 @@ cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, 
   if (nfk > 0 && (zstride < dx || (zstride & 1))) return cudaErrorInvalidValue;
   p.out = out;
   p.ldo = ldo;
+  p.zfrac = z_store_frac();
   switch (dx) {
     case 1:
       return launch_rowdot<1>(p, st, num_sms);

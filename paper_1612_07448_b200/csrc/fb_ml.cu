@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) glm_spass_kernel(GlmDev p, St
         const bool act = live && sub == 0;
         if (act && !(p.debug & 1)) {
           const double pv = ptile[r];
-          atomicAdd(p.g.bins[q] + fkt[r], pv);
+          red_add(p.g.bins[q] + fkt[r], pv);
         }
       }
     }
@@ -280,11 +280,11 @@ __global__ void kmeans_assign_kernel(const double* __restrict__ tc, const double
     assign[i] = best;
     acc += bv;
     atomicAdd(&ssz[best], 1);
-    for (int q = 0; q < fks.nfk; ++q) atomicAdd(fks.bins[q] + static_cast<int64_t>(fks.fk[q][i]) * k + best, 1);
+    for (int q = 0; q < fks.nfk; ++q) red_add(fks.bins[q] + static_cast<int64_t>(fks.fk[q][i]) * k + best, 1);
   }
   __syncthreads();
   for (int j = threadIdx.x; j < k; j += blockDim.x)
-    if (ssz[j]) atomicAdd(sizes + j, ssz[j]);
+    if (ssz[j]) red_add(sizes + j, ssz[j]);
   // deterministic objective: warp tree, block in warp order, CTAs in order by the last CTA
   acc = warp_sum_d(acc);
   if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;

@@ -23,6 +23,7 @@ struct ColRedDev {
   int wmode;
   int w_stream0;  // first stream index holding weights
   int fk_stream0;
+  int svc_scatter;  // the Kᵀ scatter runs on the (otherwise idle) gatherer warps
 };
 
 template <int NX>
@@ -50,7 +51,7 @@ FB_DEV void scatter_add(double* bins, int key, const double (&vals)[NX], bool ac
     if (active) {
       double* b = bins + static_cast<int64_t>(key) * NX;
 #pragma unroll
-      for (int j = 0; j < NX; ++j) atomicAdd(b + j, vals[j]);
+      for (int j = 0; j < NX; ++j) red_add(b + j, vals[j]);
     }
     return;
   }
@@ -75,7 +76,7 @@ FB_DEV void scatter_add(double* bins, int key, const double (&vals)[NX], bool ac
   if (active && lane == leader) {
     double* b = bins + static_cast<int64_t>(key) * NX;
 #pragma unroll
-    for (int j = 0; j < NX; ++j) atomicAdd(b + j, acc[j]);
+    for (int j = 0; j < NX; ++j) red_add(b + j, acc[j]);
   }
 }
 
@@ -92,7 +93,7 @@ FB_DEV void scatter_hot(double* bins, double* whot, int key, int slot, const dou
   if (active && !hot) {
     double* b = bins + static_cast<int64_t>(key) * NX;
 #pragma unroll
-    for (int j = 0; j < NX; ++j) atomicAdd(b + j, vals[j]);
+    for (int j = 0; j < NX; ++j) red_add(b + j, vals[j]);
   }
   if (!__any_sync(full, hot)) return;
   const int k = hot ? slot : -1 - lane;  // non-hot lanes get keys no hot lane has
@@ -119,6 +120,51 @@ FB_DEV void scatter_hot(double* bins, double* whot, int key, int slot, const dou
   __syncwarp();
 }
 
+// Uniform-FK scatter on the gatherer warps (no keyed gathers in this ring): they wait for
+// each stage like the consumers, RED every row's weights into bins[fk] (fire-and-forget
+// REDG: the 8 MB c2 bins stay in L2) and release the stage. The consumers keep only the
+// column sums, so the scatter costs no consumer issue slots. Tiles the producer could not
+// bulk-copy are filled by the consumers after the "full" wait, so for those the keys and
+// weights come from global memory.
+template <int NX>
+FB_DEV void service_scatter(const ColRedDev& p, const TileRing& ring, const StreamSet& ss) {
+  const int lane = lane_id();
+  const int gw = (static_cast<int>(threadIdx.x) >> 5) - 1;
+  int st = 0;
+  uint32_t ph = 0;
+  const int64_t n = ring.count();
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t tile = ring.tile_begin + k;
+    const int rows = ring.rows_of(tile);
+    const int64_t r0 = tile * ring.tile_rows;
+    mbar_wait(&ring.full[st], ph);
+    const bool staged = ring.bulk_ok(ss, tile);
+    for (int q = 0; q < p.c.nfk; ++q) {
+      const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(st, ss, p.fk_stream0 + q));
+      for (int r = gw * 32 + lane; r < rows; r += 32 * kGatherWarps) {
+        const int key = staged ? fkt[r] : p.c.fk[q][r0 + r];
+        double v[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j)
+          v[j] = (staged || p.wmode == kWOnes || p.wmode == kWGlobal)
+                     ? wval<NX>(p, ring, ss, st, r0, r, j)
+                     : p.c.w[(r0 + r) * p.c.w_rs + j * p.c.w_cs];
+        double* b = p.c.bins[q] + static_cast<int64_t>(key) * NX;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) red_add(b + j, v[j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[st]);
+    if (++st == ring.stages) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+  // the consumers fold their partials into the ring buffers once every stage is read
+  asm volatile("bar.arrive 2, %0;\n" ::"n"(kConsumerThreads + 32 * kGatherWarps) : "memory");
+}
+
 template <int NX>
 __global__ void __launch_bounds__(kRingThreads, 1) colreduce_kernel(ColRedDev p, StreamSet ss, int stages,
                                                                  int tile_rows) {
@@ -134,7 +180,11 @@ __global__ void __launch_bounds__(kRingThreads, 1) colreduce_kernel(ColRedDev p,
   for (int i = threadIdx.x; i < hot_per_warp * kConsumerWarps; i += blockDim.x) hotbins[i] = 0.0;
   TileRing ring;
   ring.init(smem, stages, tile_rows, p.c.n);
-  ring.start(ss);  // __syncthreads: hot bins zeroed
+  ring.start(ss, p.svc_scatter ? kGatherWarps : 0);  // __syncthreads: hot bins zeroed
+  if (p.svc_scatter && is_gather_warp()) {
+    service_scatter<NX>(p, ring, ss);
+    return;
+  }
   if (ring.service(ss)) return;
   const int tid = consumer_tid();
   const int groups = d > 0 ? kConsumerThreads / d : 0;
@@ -160,7 +210,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) colreduce_kernel(ColRedDev p,
       }
     }
     // fused Kᵀ scatter of the same weights (row-per-thread)
-    for (int q = 0; q < p.c.nfk; ++q) {
+    for (int q = 0; q < (p.svc_scatter ? 0 : p.c.nfk); ++q) {
       const int32_t* fkt = reinterpret_cast<const int32_t*>(ring.stage_ptr(stage, ss, p.fk_stream0 + q));
       for (int rb = 0; rb < rows; rb += kConsumerThreads) {
         const int r = rb + tid;
@@ -188,10 +238,11 @@ __global__ void __launch_bounds__(kRingThreads, 1) colreduce_kernel(ColRedDev p,
     const int slot = (i - hot_off[q]) / NX, j = (i - hot_off[q]) % NX;
     double s = 0.0;
     for (int w = 0; w < kConsumerWarps; ++w) s += hotbins[w * hot_per_warp + i];
-    atomicAdd(p.c.bins[q] + static_cast<int64_t>(p.c.hot_key[q][slot]) * NX + j, s);
+    red_add(p.c.bins[q] + static_cast<int64_t>(p.c.hot_key[q][slot]) * NX + j, s);
   }
-  // fold row groups: red[g][j][c] (the ring buffers are idle now)
+  // fold row groups: red[g][j][c] (the ring buffers are idle now — the scatter warps too)
   double* red = reinterpret_cast<double*>(ring.buf);
+  if (p.svc_scatter) asm volatile("bar.sync 2, %0;\n" ::"n"(kConsumerThreads + 32 * kGatherWarps) : "memory");
   consumer_sync();
   if (colthread) {
 #pragma unroll
@@ -259,7 +310,7 @@ __global__ void segsum_kernel(const int32_t* __restrict__ perm, const int32_t* _
 #pragma unroll
         for (int j = 0; j < NX; ++j) {
           if (cfirst)
-            atomicAdd(b + j, csum[j]);
+            red_add(b + j, csum[j]);
           else
             b[j] = csum[j];
         }
@@ -286,7 +337,7 @@ __global__ void segsum_kernel(const int32_t* __restrict__ perm, const int32_t* _
       double* b = bins + static_cast<int64_t>(key) * NX;
       if (key == first_key && cfirst) {
 #pragma unroll
-        for (int j = 0; j < NX; ++j) atomicAdd(b + j, v[j]);
+        for (int j = 0; j < NX; ++j) red_add(b + j, v[j]);
       } else {
 #pragma unroll
         for (int j = 0; j < NX; ++j) b[j] = v[j];  // complete run inside the range
@@ -301,7 +352,7 @@ __global__ void segsum_kernel(const int32_t* __restrict__ perm, const int32_t* _
   if (lane == 0 && ckey >= 0) {
     double* b = bins + static_cast<int64_t>(ckey) * NX;
 #pragma unroll
-    for (int j = 0; j < NX; ++j) atomicAdd(b + j, csum[j]);
+    for (int j = 0; j < NX; ++j) red_add(b + j, csum[j]);
   }
 }
 
@@ -367,6 +418,10 @@ static cudaError_t launch_colreduce_nx(const ColReduce& c, cudaStream_t st, int 
     p.wmode = kWGlobal;
   }
   p.fk_stream0 = ns;
+  p.svc_scatter = c.nfk > 0 ? 1 : 0;
+  for (int q = 0; q < c.nfk; ++q)
+    if (c.nhot[q] > 0 || c.aggregate[q]) p.svc_scatter = 0;  // skewed keys: consumer path
+  if (const char* e = getenv("FB_SVC_SCATTER")) p.svc_scatter = p.svc_scatter && e[0] == '1';
   for (int q = 0; q < c.nfk; ++q) {
     ss.base[ns] = reinterpret_cast<const char*>(c.fk[q]);
     ss.row_bytes[ns++] = 4u;
