@@ -13,7 +13,7 @@ import threading
 from .exceptions import DataError, ExtensionMissingError, NumericError, ShapeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfactorla_b200.so")
+LIB_PATH = os.environ.get("FB_LIB_PATH") or os.path.join(_HERE, "libfactorla_b200.so")  # override: A/B builds
 
 FB_MAX_PARTS = 4
 

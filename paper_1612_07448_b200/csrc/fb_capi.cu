@@ -250,6 +250,7 @@ int fb_lmm(const fb_normalized* nm, const double* x, int32_t d_x, double* out, v
     Carver cv{static_cast<char*>(ws), ws_bytes};
     const int32_t* fks[FB_MAX_PARTS];
     const double* zs[FB_MAX_PARTS];
+    int64_t zrows[FB_MAX_PARTS];
     int64_t off = nm->d_s;
     for (int i = 0; i < nm->q; ++i) {
       const fb_part& p = nm->part[i];
@@ -261,11 +262,12 @@ int fb_lmm(const fb_normalized* nm, const double* x, int32_t d_x, double* out, v
       if (e != cudaSuccess) return cuda_status(e, "lmm(z)");
       fks[i] = p.fk;
       zs[i] = z;
+      zrows[i] = p.n_r;
       off += p.d_r;
     }
     // out = S · X[0:d_s, c0:c0+w] + Σ z_i[fk_i]   (rewrite.py:186-190)
     cudaError_t e = fb::launch_lmm_rows(nm->s, nm->n_s, nm->d_s, x + c0, w, d_x, nm->q, fks, zs,
-                                        fb::z_stride(w), out + c0, d_x, cs(stream), g_num_sms);
+                                        fb::z_stride(w), out + c0, d_x, cs(stream), g_num_sms, zrows);
     if (e != cudaSuccess) return cuda_status(e, "lmm(S)");
     c0 += w;
   }

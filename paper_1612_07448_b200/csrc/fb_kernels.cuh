@@ -12,7 +12,7 @@ constexpr int kMaxParts = 4;  // attribute tables per star schema handled in one
 inline int z_stride(int dx) { return dx < 2 ? 2 : (dx + 1) & ~1; }
 cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, int dx, int64_t ldx,
                             int nfk, const int32_t* const* fk, const double* const* z, int zstride, double* out,
-                            int64_t ldo, cudaStream_t st, int num_sms);
+                            int64_t ldo, cudaStream_t st, int num_sms, const int64_t* z_rows = nullptr);
 
 // fb_reduce.cu ---------------------------------------------------------------------
 struct ColReduce {

@@ -42,6 +42,8 @@ struct LmmArgs {
   int lanes;                   // rowdot: lanes per row (power of two)
   int cols;                    // rowdot: columns per lane (d / lanes)
   float zfrac;                 // z-pass (nfk == 0): evict_last fraction of the stored z rows
+  int debug;                   // FB_LMM_DEBUG (measurement only): 1 skip stores, 4 plain stores
+  size_t ztable_bytes[kMaxParts];  // bytes of each z table (host side: gather cache choice)
 };
 
 // ------------------------------------------------------------------ rowdot (d_x <= 4)
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_rowdot_kernel(LmmArgs p, 
 // Rows past the end of a partial tile are computed on stale shared memory and simply not
 // stored (DMMA row g of C depends only on row g of A), so the k-loop carries no row
 // predicate; only the last k-step of a width that is not a multiple of 4 masks k >= d.
-template <int NT, int MT, int KS>
+template <int NT, int MT, int KS, bool CG>
 __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, StreamSet ss, int stages,
                                                                int tile_rows) {
   extern __shared__ __align__(128) char smem[];
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, St
   TileRing ring;
   ring.init(buf, stages, tile_rows, p.n);
   ring.start(ss);  // contains __syncthreads (xs visible after it)
-  if (ring.service(ss)) return;
+  if (ring.service<false, CG>(ss)) return;
 
   const int lane = lane_id();
   const int g = lane >> 2, t = lane & 3;
@@ -228,6 +230,13 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, St
               acc[mt][nt][1] += zv.y;
             }
           }
+          if (p.debug & 1) continue;
+          if (p.debug & 4) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              *reinterpret_cast<double2*>(o + 8 * nt + 2 * t) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+            continue;
+          }
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) st_hint2(o + 8 * nt + 2 * t, acc[mt][nt][0], acc[mt][nt][1], pol);
           continue;
@@ -258,8 +267,15 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, St
 }
 
 // ------------------------------------------------------------------ host launchers
-static int stages_for(size_t fixed, uint32_t stage_bytes, int max_stages) {
-  const size_t budget = 200 * 1024;
+static size_t ring_budget() {
+  static size_t b = [] {
+    const char* e = getenv("FB_RING_BUDGET_KB");
+    return static_cast<size_t>(e ? atoi(e) : 200) * 1024;
+  }();
+  return b;
+}
+
+static int stages_for(size_t fixed, uint32_t stage_bytes, int max_stages, size_t budget) {
   if (fixed + kRingHeader + 2 * static_cast<size_t>(stage_bytes) > budget) return 0;
   int st = static_cast<int>((budget - fixed - kRingHeader) / stage_bytes);
   return st > max_stages ? max_stages : st;
@@ -267,9 +283,9 @@ static int stages_for(size_t fixed, uint32_t stage_bytes, int max_stages) {
 
 template <class K>
 static cudaError_t launch_ring(K kern, const LmmArgs& p, StreamSet& ss, size_t fixed, int tile_rows,
-                               cudaStream_t st, int num_sms) {
+                               cudaStream_t st, int num_sms, size_t budget = 0) {
   stream_layout(ss, tile_rows, p.n);
-  const int stages = stages_for(fixed, ss.stage_bytes, 8);
+  const int stages = stages_for(fixed, ss.stage_bytes, 8, budget ? budget : ring_budget());
   if (stages < 2) return cudaErrorNotSupported;
   const size_t smem = fixed + kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -308,7 +324,7 @@ static void fill_streams(const LmmArgs& p, StreamSet& ss, int pitch) {
     ss.gbase[q] = reinterpret_cast<const char*>(p.z[q]);
     ss.grow_bytes[q] = static_cast<uint32_t>(p.zstride) * 8u;
   }
-  ss.ngather = p.nfk;
+  ss.ngather = (p.debug & 2) ? 0 : p.nfk;
 }
 
 template <int NX>
@@ -334,7 +350,11 @@ static cudaError_t launch_rowdot(LmmArgs p, cudaStream_t st, int num_sms) {
 }
 
 template <int NT, int MT, int KS>
-static cudaError_t launch_dmma_cfg(LmmArgs p, cudaStream_t st, int num_sms) {
+static cudaError_t launch_dmma_cfg(LmmArgs p, cudaStream_t st, int num_sms, size_t budget = 0) {
+  // uniform keys into a table far beyond L1 (largest z > 32 MB): L1-bypassing gathers
+  size_t zmax = 0;
+  for (int q = 0; q < p.nfk; ++q) zmax = p.ztable_bytes[q] > zmax ? p.ztable_bytes[q] : zmax;
+  const bool cg = zmax > (32u << 20);
   const int tile_rows = kConsumerWarps * 8 * MT;
   // dense rows (one bulk copy per tile): a padded pitch needs one copy per row, which costs
   // more than the 8-way A-fragment bank conflicts of a width ≡ 0 (mod 16)
@@ -343,38 +363,48 @@ static cudaError_t launch_dmma_cfg(LmmArgs p, cudaStream_t st, int num_sms) {
   fill_streams(p, ss, p.pitch);
   const int dpad = (p.d + 3) & ~3;
   const size_t fixed = (static_cast<size_t>(dpad > 0 ? dpad : 4) * (8 * NT + 4) * 8 + 127) & ~size_t(127);
-  return launch_ring(lmm_dmma_kernel<NT, MT, KS>, p, ss, fixed, tile_rows, st, num_sms);
+  if (cg) return launch_ring(lmm_dmma_kernel<NT, MT, KS, true>, p, ss, fixed, tile_rows, st, num_sms, budget);
+  return launch_ring(lmm_dmma_kernel<NT, MT, KS, false>, p, ss, fixed, tile_rows, st, num_sms, budget);
 }
 
 // narrow factors (d <= 32, the multi-row tile configurations): the k-step count is a
 // template parameter so the k-loop unrolls completely
 template <int NT, int MT>
-static cudaError_t launch_dmma_ks(const LmmArgs& p, cudaStream_t st, int num_sms) {
+static cudaError_t launch_dmma_ks(const LmmArgs& p, cudaStream_t st, int num_sms, size_t budget = 0) {
   switch ((p.d + 3) / 4) {
-    case 1: return launch_dmma_cfg<NT, MT, 1>(p, st, num_sms);
-    case 2: return launch_dmma_cfg<NT, MT, 2>(p, st, num_sms);
-    case 3: return launch_dmma_cfg<NT, MT, 3>(p, st, num_sms);
-    case 4: return launch_dmma_cfg<NT, MT, 4>(p, st, num_sms);
-    case 5: return launch_dmma_cfg<NT, MT, 5>(p, st, num_sms);
-    case 6: return launch_dmma_cfg<NT, MT, 6>(p, st, num_sms);
-    case 7: return launch_dmma_cfg<NT, MT, 7>(p, st, num_sms);
-    case 8: return launch_dmma_cfg<NT, MT, 8>(p, st, num_sms);
-    default: return launch_dmma_cfg<NT, MT, 0>(p, st, num_sms);
+    case 1: return launch_dmma_cfg<NT, MT, 1>(p, st, num_sms, budget);
+    case 2: return launch_dmma_cfg<NT, MT, 2>(p, st, num_sms, budget);
+    case 3: return launch_dmma_cfg<NT, MT, 3>(p, st, num_sms, budget);
+    case 4: return launch_dmma_cfg<NT, MT, 4>(p, st, num_sms, budget);
+    case 5: return launch_dmma_cfg<NT, MT, 5>(p, st, num_sms, budget);
+    case 6: return launch_dmma_cfg<NT, MT, 6>(p, st, num_sms, budget);
+    case 7: return launch_dmma_cfg<NT, MT, 7>(p, st, num_sms, budget);
+    case 8: return launch_dmma_cfg<NT, MT, 8>(p, st, num_sms, budget);
+    default: return launch_dmma_cfg<NT, MT, 0>(p, st, num_sms, budget);
   }
 }
 
 template <int NT>
 static cudaError_t launch_dmma(const LmmArgs& p, cudaStream_t st, int num_sms) {
   const size_t row_bytes = static_cast<size_t>(p.d) * 8 + 8 * static_cast<size_t>(p.zstride) * p.nfk;
-  // stage <= ~48 KB
+  // The consumers are latency-bound on the DMMA chains (c2 X100x16 with z L2-resident: 1.24 ms
+  // with 2 m-tiles per warp, 1.10 ms with 4; ncu: 'wait' / 'math' stalls in the k-loop), so
+  // prefer 4 m-tiles (8 independent accumulators per warp) even when that makes a stage
+  // ~74 KB (S rows + gathered z rows): three stages in a 224 KB ring.
+  static int mt = [] { const char* e = getenv("FB_LMM_MT"); return e ? atoi(e) : 0; }();
+  const size_t big = 224 * 1024;
+  if (mt == 4 && p.nfk > 0) return launch_dmma_ks<NT, 4>(p, st, num_sms, big);
+  if (mt == 2 && p.nfk > 0 && row_bytes * 128 <= 48 * 1024) return launch_dmma_ks<NT, 2>(p, st, num_sms);
+  if (mt == 1 && p.nfk > 0) return launch_dmma_ks<NT, 1>(p, st, num_sms);
   if (row_bytes * 256 <= 48 * 1024) return launch_dmma_ks<NT, 4>(p, st, num_sms);
+  if (mt == 0 && p.nfk > 0 && row_bytes * 256 <= 76 * 1024) return launch_dmma_ks<NT, 4>(p, st, num_sms, big);
   if (row_bytes * 128 <= 48 * 1024) return launch_dmma_ks<NT, 2>(p, st, num_sms);
   return launch_dmma_cfg<NT, 1, 0>(p, st, num_sms);
 }
 
 cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, int dx, int64_t ldx,
                             int nfk, const int32_t* const* fk, const double* const* z, int zstride, double* out,
-                            int64_t ldo, cudaStream_t st, int num_sms) {
+                            int64_t ldo, cudaStream_t st, int num_sms, const int64_t* z_rows) {
   if (n <= 0) return cudaSuccess;
   if (dx < 1 || dx > 16) return cudaErrorNotSupported;
   LmmArgs p{};
@@ -388,12 +418,15 @@ cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, 
   for (int q = 0; q < nfk; ++q) {
     p.fk[q] = fk[q];
     p.z[q] = z[q];
+    p.ztable_bytes[q] = z_rows ? static_cast<size_t>(z_rows[q]) * zstride * sizeof(double) : 0;
   }
   p.zstride = zstride;
   if (nfk > 0 && (zstride < dx || (zstride & 1))) return cudaErrorInvalidValue;
   p.out = out;
   p.ldo = ldo;
   p.zfrac = z_store_frac();
+  static int dbg = [] { const char* e = getenv("FB_LMM_DEBUG"); return e ? atoi(e) : 0; }();
+  p.debug = nfk > 0 ? dbg : 0;
   switch (dx) {
     case 1:
       return launch_rowdot<1>(p, st, num_sms);

@@ -213,14 +213,14 @@ struct TileRing {
   // gidx rows move with one bulk copy each (StreamSet::gidx_bulk) — a separate instantiation
   // used only by the kernels that need it (a runtime branch, or a second gather loop in every
   // kernel, slowed the LMM gathers by 2-15%).
-  template <bool GIDX_BULK = false>
+  template <bool GIDX_BULK = false, bool GATHER_CG = false>
   FB_DEV bool service(const StreamSet& s) const {
     if (is_producer_warp()) {
       produce(s);
       return true;
     }
     if (is_gather_warp()) {
-      if (s.ngather > 0 || s.gidx) gather<GIDX_BULK>(s);
+      if (s.ngather > 0 || s.gidx) gather<GIDX_BULK, GATHER_CG>(s);
       return true;
     }
     return false;
@@ -290,7 +290,7 @@ struct TileRing {
   // global memory, loaded one tile ahead, so a gathered tile costs max(stream, key +
   // gather) latency rather than their sum. Gatherer warp gw owns ring rows
   // r ≡ gw (mod kGatherWarps) (<= 64 of them: tiles of at most 256 rows).
-  template <bool GIDX_BULK>
+  template <bool GIDX_BULK, bool GATHER_CG>
   FB_DEV void gather(const StreamSet& s) const {
     const int lane = threadIdx.x & 31;
     const int gw = (static_cast<int>(threadIdx.x) >> 5) - 1;
@@ -397,7 +397,7 @@ struct TileRing {
             const int32_t key = key_of(g, ri);
             if (ri < rows_w && c < nch) {
               const uint32_t r = gw + kGatherWarps * ri;
-              cp_async16_ca(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c);
+              cp_async16_gather<GATHER_CG>(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c);
             }
           }
         } else {
@@ -405,7 +405,7 @@ struct TileRing {
             const int32_t key = key_of(g, ri);
             const uint32_t r = gw + kGatherWarps * ri;
             for (uint32_t c = lane; c < nch; c += 32)
-              cp_async16_ca(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c);
+              cp_async16_gather<GATHER_CG>(dst + r * rb + 16u * c, s.gbase[g] + static_cast<size_t>(key) * rb + 16u * c);
           }
         }
       }
