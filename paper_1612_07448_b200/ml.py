@@ -459,7 +459,9 @@ def kmeans(m, cfg):
     wall = time.perf_counter() - t0
     if bad != -1:
         raise NumericError(f"row_min_mask: NaN in row {bad}")
-    return ModelOutput("kmeans", (n, d), cfg, _np(trace).tolist(), centroids=_np(c), wall_time_s=wall, counts=counter)
+    out = ModelOutput("kmeans", (n, d), cfg, _np(trace).tolist(), centroids=_np(c), wall_time_s=wall, counts=counter)
+    out.assignment = assign  # last iteration's argmin cluster per row (int32, device): parity checks
+    return out
 
 
 def _col_sq_sums(c):
