@@ -424,10 +424,15 @@ def kmeans(sm, cfg):
         _allreduce(tta, sm.group)
         _allreduce(sizes, sm.group)
         be.kmeans_update(c, tta, sizes, cc)
-    bad = int(nan_row[0])
-    if bad != -1:
-        raise NumericError(f"row_min_mask: NaN in row {sm.row0 + bad}")
+    # every rank takes the same path: the trace and the first NaN row (global index, MIN over
+    # ranks) are all-reduced before anyone raises, so no rank is left waiting in a collective
     _allreduce(trace, sm.group)
+    bad = int(nan_row[0])
+    none = np.iinfo(np.int64).max
+    first = be.tensor([sm.row0 + bad if bad != -1 else none], dtype=torch.int64)
+    _allreduce(first, sm.group, op=dist.ReduceOp.MIN if _world(sm.group) > 1 else None)
+    if int(first[0]) != none:
+        raise NumericError(f"row_min_mask: NaN in row {int(first[0])}")
     return ModelOutput("kmeans", (n, d), cfg, be.to_numpy(trace).tolist(), centroids=be.to_numpy(c))
 
 

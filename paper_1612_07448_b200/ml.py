@@ -276,7 +276,12 @@ def _glm_gd(m, y, cfg, mode, name):
     dev = nm.device
     counter = OpCounter()
     key = (id(nm._cache), nm.blocks[0][1].data_ptr(), yd.data_ptr(), cfg.iterations, float(cfg.step_size), mode, dev.index)
-    entry = _GLM_GRAPHS.get(key) if os.environ.get("FB_NO_GRAPHS") is None else None
+    # graphs are cached only for caller-owned device operands: host y (or a host-built matrix)
+    # means fresh device copies every call, whose key never repeats — capturing and pinning
+    # them would only hold HBM
+    cacheable = os.environ.get("FB_NO_GRAPHS") is None and isinstance(y, torch.Tensor) and y.is_cuda \
+        and not nm.host_io
+    entry = _GLM_GRAPHS.get(key) if cacheable else None
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     if entry is None:
@@ -285,7 +290,7 @@ def _glm_gd(m, y, cfg, mode, name):
         diverged = torch.full((1,), -1, dtype=torch.int32, device=dev)
         ws = torch.empty(max(int(so.fb_glm_run_workspace_bytes(cs)), 256), dtype=torch.uint8, device=dev)
         _glm_run(so, cs, yd, w, trace, diverged, ws, mode, cfg, D.stream_handle())  # eager run (and warm-up)
-        if os.environ.get("FB_NO_GRAPHS") is None and not so.fb_glm_run_fused(cs):
+        if cacheable and not so.fb_glm_run_fused(cs):
             graph = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream(device=dev)
             side.wait_stream(torch.cuda.current_stream())

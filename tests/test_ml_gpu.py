@@ -212,3 +212,24 @@ def test_logreg_fused_run_matches_stepwise(monkeypatch):
     w, obj = O.linreg_gd(ref, yl, 5, 1e-7)
     _close(lin_fused.weights, w)
     _close(lin_fused.objective, obj)
+
+
+def test_glm_host_inputs_do_not_pin_device_memory():
+    """Host y / host-built matrices: the per-iteration graph path must not cache (and so pin)
+    device copies made from host inputs (ml.py GLM graph cache key)."""
+    fb = _fb()
+    rng = np.random.default_rng(8)
+    n, n_r = 2_000_000, 20_000  # 320 MB of S: beyond L2, so fb_glm_run takes the per-iteration path
+    s = rng.standard_normal((n, 20))
+    r = rng.standard_normal((n_r, 10))
+    nm = fb.build_pkfk(s, rng.integers(1, n_r + 1, size=n), r)
+    y = np.where(rng.standard_normal((n, 1)) >= 0, 1.0, -1.0)
+    cfg = fb.TrainConfig(iterations=3, step_size=1e-4)
+    first = fb.logistic_gd(nm, y, cfg)
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    for _ in range(4):
+        out = fb.logistic_gd(nm, y, cfg)
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() <= base + (1 << 20)
+    assert O.max_rel_deviation(out.weights, first.weights) <= 1e-12  # Kᵀp scatter order (REDs) varies
