@@ -30,7 +30,7 @@ extern "C" {
 
 typedef struct CUstream_st* fb_stream_t; /* == cudaStream_t */
 
-#define FB_ABI_VERSION 3
+#define FB_ABI_VERSION 4
 #define FB_MAX_PARTS 4
 
 enum {
@@ -76,7 +76,7 @@ typedef struct fb_normalized {
 /* ---- library ---------------------------------------------------------------- */
 int fb_abi_version(void);
 const char* fb_last_error(void);
-/* Select the device and cache its SM count. */
+/* Cache the SM count of `device` (the caller's current device is not changed). */
 int fb_init(int device);
 /* Number of kernels this library has launched in this process (instrumentation). */
 uint64_t fb_launch_count(void);
@@ -151,6 +151,41 @@ size_t fb_crossprod_workspace_bytes(const fb_normalized* nm);
 int fb_crossprod(const fb_normalized* nm, const int32_t* perm, const int32_t* fk_sorted, double* out, void* ws,
                  size_t ws_bytes, fb_stream_t stream);
 
+/* ---- split passes: the R-row-sliced multi-GPU composition (dist.py) ----
+ * Each operator's S pass runs on a rank's own S rows; its R-side work runs on the rank's slice
+ * of R rows, joined by all-gather (z) / reduce-scatter (bins, KᵀS) / all-reduce (small results)
+ * in the caller. Single-GPU callers use the whole-operator entries above. */
+/* Doubles per z row for d_x <= 16 columns (even: gathered rows are 16-byte copies); 0 otherwise. */
+int fb_z_stride(int32_t d_x);
+/* z rows [row_lo, row_hi) of part `part`: z[r*zst + c] = (R_part · X[off_part : off_part + d_r, :])[r, c]
+ * (rewrite.py:187, "R·X before K"); z is the base of the whole n_r × zst table. d_x <= 16. */
+int fb_lmm_zpass(const fb_normalized* nm, const double* x, int32_t d_x, int32_t part, int64_t row_lo, int64_t row_hi,
+                 double* z, fb_stream_t stream);
+/* out = S·X[0:d_s] + Σ_i z_i[fk_i] with caller z tables (n_r,i × fb_z_stride(d_x)); d_x <= 16
+ * (rewrite.py:186-190). */
+int fb_lmm_spass(const fb_normalized* nm, const double* x, int32_t d_x, const double* const* z, double* out,
+                 fb_stream_t stream);
+/* The S pass of fb_wt: out(j, c) = Σ_i w(i, j) S(i, c) for c < d_s (w = NULL: all-ones weights,
+ * i.e. colSums(S)), and bins[i] (n_r,i × n_w row-major, zeroed here) = X·K_i (indicator.py:130-141)
+ * for every part whose bins[i] is not NULL (bins = NULL: none). n_w <= 16. */
+size_t fb_wt_spass_workspace_bytes(const fb_normalized* nm, int32_t n_w);
+int fb_wt_spass(const fb_normalized* nm, const double* w, int32_t n_w, int64_t w_rs, int64_t w_cs, double* out,
+                int64_t o_js, int64_t o_cs, double* const* bins, void* ws, size_t ws_bytes, fb_stream_t stream);
+/* Weighted column sums of dense rows: out(j, c) = Σ_i w(i, j) a(i, c) (the binsᵀ·R / counts·R
+ * pass of rmm / colSums on one R-row slice, rewrite.py:131-149, 194-212). */
+size_t fb_rows_wt_workspace_bytes(int32_t d, int32_t n_w);
+int fb_rows_wt(const double* a, int64_t n, int32_t d, const double* w, int32_t n_w, int64_t w_rs, int64_t w_cs,
+               double* out, int64_t o_js, int64_t o_cs, void* ws, size_t ws_bytes, fb_stream_t stream);
+/* The two halves of fb_crossprod (workspace: fb_crossprod_workspace_bytes). spass: out = the
+ * SᵀS block (rest zero) and kts (n_r × d_s) = KᵀS of this rank's rows. rpass: nm->part[0] is one
+ * R-row slice (r, n_r, counts of that slice) and kts its KᵀS rows: out = the blocks involving R
+ * ((KᵀS)ᵀR and Rᵀdiag(c)R, both triangles; rest zero). Summing the halves over ranks and slices
+ * gives TᵀT (rewrite.py:245-298). */
+int fb_crossprod_spass(const fb_normalized* nm, const int32_t* perm, const int32_t* fk_sorted, double* out,
+                       double* kts, void* ws, size_t ws_bytes, fb_stream_t stream);
+int fb_crossprod_rpass(const fb_normalized* nm, const double* kts, double* out, void* ws, size_t ws_bytes,
+                       fb_stream_t stream);
+
 /* ---- ML driver steps (ml.py) ------------------------------------------------------ */
 /* One fused GLM evaluation over T (d = d_s + Σ d_r, w a device d-vector, y n_s targets):
  *   mode 0 (logistic_gd, ml.py:207-213): p = y/(1+exp(T w)), loss = Σ log1p(exp(-|y·Tw|)) + max(-y·Tw, 0)
@@ -177,8 +212,9 @@ int fb_glm_run(const fb_normalized* nm, const double* y, double* w, int32_t mode
 /* One K-Means iteration (ml.py:275-283) on an untransposed T with k <= 16 clusters:
  * c is the d × k centroid matrix (updated in place; empty clusters keep theirs), cc[j] =
  * Σ c[:, j]² (in/out), d_t = rowSums(T²) (n_s), assign (n_s int32) the argmin cluster
- * (ties to the lowest index), trace[it] = Σ_i min_j dist, *nan_row = first row whose
- * distances hold a NaN (device; start at UINT64_MAX). */
+ * (ties to the lowest index), trace[it] = Σ_i min_j dist, *nan_row = (it << 40) | row for the
+ * first row whose distances hold a NaN in the first iteration that had one (device; start at
+ * UINT64_MAX; atomicMin keeps the earliest). */
 size_t fb_kmeans_workspace_bytes(const fb_normalized* nm, int32_t k);
 int fb_kmeans_step(const fb_normalized* nm, const double* d_t, double* c, double* cc, int32_t k, int32_t it,
                    double* trace, int32_t* assign, unsigned long long* nan_row, void* ws, size_t ws_bytes,

@@ -83,6 +83,15 @@ _SIGS = {
     "fb_fk_sort": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_size, c_vp]),
     "fb_crossprod_workspace_bytes": (c_size, [_P]),
     "fb_crossprod": (c_i32, [_P, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "fb_z_stride": (c_i32, [c_i32]),
+    "fb_lmm_zpass": (c_i32, [_P, c_vp, c_i32, c_i32, c_i64, c_i64, c_vp, c_vp]),
+    "fb_lmm_spass": (c_i32, [_P, c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "fb_wt_spass_workspace_bytes": (c_size, [_P, c_i32]),
+    "fb_wt_spass": (c_i32, [_P, c_vp, c_i32, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_size, c_vp]),
+    "fb_rows_wt_workspace_bytes": (c_size, [c_i32, c_i32]),
+    "fb_rows_wt": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i32, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_size, c_vp]),
+    "fb_crossprod_spass": (c_i32, [_P, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "fb_crossprod_rpass": (c_i32, [_P, c_vp, c_vp, c_vp, c_size, c_vp]),
     "fb_glm_workspace_bytes": (c_size, [_P]),
     "fb_glm_eval": (c_i32, [_P, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_size, c_vp]),
     "fb_glm_step": (c_i32, [_P, c_vp, c_vp, c_i32, c_f64, c_i32, c_vp, c_vp, c_vp, c_size, c_vp]),

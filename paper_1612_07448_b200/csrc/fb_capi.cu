@@ -36,29 +36,39 @@ struct SideStream {
   cudaEvent_t fork = nullptr, join = nullptr;
   int device = -1;
 };
-thread_local SideStream g_side;
+constexpr int kMaxDevices = 64;
+// one side stream (+ its fork/join events) per (thread, device): switching devices neither
+// recreates nor leaks them
+thread_local SideStream g_side[kMaxDevices];
+
+SideStream* side_for_current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return (dev >= 0 && dev < kMaxDevices) ? &g_side[dev] : nullptr;
+}
 }  // namespace
 
 
 cudaError_t side_fork(cudaStream_t main, cudaStream_t* side) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (g_side.side == nullptr || g_side.device != dev) {
-    cudaError_t e = cudaStreamCreateWithFlags(&g_side.side, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_side.join, cudaEventDisableTiming);
+  SideStream* ss = side_for_current_device();
+  if (!ss) return cudaErrorInvalidDevice;
+  if (ss->side == nullptr) {
+    cudaError_t e = cudaStreamCreateWithFlags(&ss->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss->fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss->join, cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
-    g_side.device = dev;
   }
-  cudaError_t e = cudaEventRecord(g_side.fork, main);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(g_side.side, g_side.fork, 0);
-  *side = g_side.side;
+  cudaError_t e = cudaEventRecord(ss->fork, main);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ss->side, ss->fork, 0);
+  *side = ss->side;
   return e;
 }
 
 cudaError_t side_join(cudaStream_t main) {
-  cudaError_t e = cudaEventRecord(g_side.join, g_side.side);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(main, g_side.join, 0);
+  SideStream* ss = side_for_current_device();
+  if (!ss || !ss->side) return cudaErrorInvalidResourceHandle;
+  cudaError_t e = cudaEventRecord(ss->join, ss->side);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(main, ss->join, 0);
   return e;
 }
 
@@ -67,7 +77,16 @@ cudaError_t side_join(cudaStream_t main) {
 namespace {
 
 thread_local char g_err[512] = "";
-int g_num_sms = 148;
+// SM count per device (fb_init fills it; 148 = B200 until then), read for the current device
+std::atomic<int> g_sms[64];
+
+int current_num_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int v = (dev >= 0 && dev < 64) ? g_sms[dev].load(std::memory_order_relaxed) : 0;
+  return v > 0 ? v : 148;
+}
+#define g_num_sms current_num_sms()
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -167,12 +186,12 @@ const char* fb_last_error(void) { return g_err; }
 uint64_t fb_launch_count(void) { return fb::g_launches.load(); }
 
 int fb_init(int device) {
-  cudaError_t e = cudaSetDevice(device);
-  if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+  // caches the device's SM count; the caller's current device is left as it was
+  if (device < 0 || device >= 64) return fail(FB_ERR_ARG, "fb_init: device %d out of range", device);
   int sms = 0;
-  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
-  g_num_sms = sms;
+  g_sms[device].store(sms, std::memory_order_relaxed);
   return FB_OK;
 }
 
@@ -320,14 +339,17 @@ static bool use_segsum(const fb_part& pt) {
 
 static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_t w_rs, int64_t w_cs,
                    const double* const* part_weights, double* out, int64_t o_js, int64_t o_cs, void* ws,
-                   size_t ws_bytes, fb_stream_t stream) {
+                   size_t ws_bytes, fb_stream_t stream, double* const* bins_out = nullptr, bool r_pass = true) {
   // part_weights != nullptr: colSums mode — S pass with implicit ones, R_i pass with counts_i.
+  // bins_out (n_w <= 16): the X·K bins go to the caller's buffers; r_pass = false stops after
+  // the S pass (the R-row-sliced multi-GPU composition runs the R passes itself).
   for (int j0 = 0; j0 < n_w;) {
     const int nx = chunk_width(n_w - j0);
     Carver cv{static_cast<char*>(ws), ws_bytes};
     double* bins[FB_MAX_PARTS] = {};
     if (!part_weights)
-      for (int i = 0; i < nm->q; ++i) bins[i] = cv.take<double>(static_cast<size_t>(nm->part[i].n_r) * nx);
+      for (int i = 0; i < nm->q; ++i)
+        bins[i] = bins_out ? bins_out[i] : cv.take<double>(static_cast<size_t>(nm->part[i].n_r) * nx);
     double* partials = cv.take<double>(fb::colreduce_workspace_doubles(0, static_cast<int>(max_width(nm)), nx, g_num_sms));
     unsigned int* counter = cv.take<unsigned int>(1);
     if (!partials || !counter) return fail(FB_ERR_ARG, "wt: workspace too small");
@@ -345,6 +367,7 @@ static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_
     c.nfk = 0;
     for (int i = 0; !part_weights && i < nm->q; ++i) {
       const fb_part& pt = nm->part[i];
+      if (!bins[i]) continue;  // no scatter wanted for this part
       if (pt.perm && pt.fk_sorted && nm->n_s > 0 && use_segsum(pt)) {
         // X·K_i as segmented sums over the FK-sorted order (few atomics, no hot-line
         // contention), on the side stream so they overlap the S pass
@@ -381,7 +404,7 @@ static int wt_impl(const fb_normalized* nm, const double* w, int32_t n_w, int64_
       if (e != cudaSuccess) return cuda_status(e, "wt(join)");
     }
     int64_t off = nm->d_s;
-    for (int i = 0; i < nm->q; ++i) {
+    for (int i = 0; r_pass && i < nm->q; ++i) {
       const fb_part& p = nm->part[i];
       fb::ColReduce r{};
       r.a = p.r;
@@ -464,6 +487,117 @@ int fb_sum_all(const fb_normalized* nm, double* out, void* ws, size_t ws_bytes, 
   return cuda_status(cudaGetLastError(), "sum_all");
 }
 
+// ------------------------------------------------------------------ split passes (multi-GPU)
+int fb_z_stride(int32_t d_x) { return d_x >= 1 && d_x <= 16 ? fb::z_stride(d_x) : 0; }
+
+int fb_lmm_zpass(const fb_normalized* nm, const double* x, int32_t d_x, int32_t part, int64_t row_lo, int64_t row_hi,
+                 double* z, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (d_x < 1 || d_x > 16) return fail(FB_ERR_ARG, "lmm_zpass: d_x=%d outside [1, 16]", d_x);
+  if (part < 0 || part >= nm->q) return fail(FB_ERR_ARG, "lmm_zpass: part %d of %d", part, nm->q);
+  const fb_part& p = nm->part[part];
+  if (row_lo < 0 || row_hi > p.n_r || row_lo > row_hi) return fail(FB_ERR_SHAPE, "lmm_zpass: rows [%lld, %lld) of %lld",
+                                                                  (long long)row_lo, (long long)row_hi, (long long)p.n_r);
+  if (!x || !z) return fail(FB_ERR_ARG, "lmm_zpass: NULL pointer");
+  if (max_width(nm) > 256) return fail(FB_ERR_ARG, "lmm_zpass: factor widths above 256 are not supported");
+  int64_t off = nm->d_s;
+  for (int i = 0; i < part; ++i) off += nm->part[i].d_r;
+  const int zst = fb::z_stride(d_x);
+  return cuda_status(fb::launch_lmm_rows(p.r + row_lo * p.d_r, row_hi - row_lo, p.d_r, x + off * d_x, d_x, d_x, 0,
+                                         nullptr, nullptr, 0, z + row_lo * zst, zst, cs(stream), g_num_sms),
+                     "lmm_zpass");
+}
+
+int fb_lmm_spass(const fb_normalized* nm, const double* x, int32_t d_x, const double* const* z, double* out,
+                 fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (d_x < 1 || d_x > 16) return fail(FB_ERR_ARG, "lmm_spass: d_x=%d outside [1, 16]", d_x);
+  if (!x || (!out && nm->n_s > 0) || (nm->q > 0 && !z)) return fail(FB_ERR_ARG, "lmm_spass: NULL pointer");
+  if (max_width(nm) > 256) return fail(FB_ERR_ARG, "lmm_spass: factor widths above 256 are not supported");
+  const int32_t* fks[FB_MAX_PARTS];
+  const double* zs[FB_MAX_PARTS];
+  int64_t zrows[FB_MAX_PARTS];
+  for (int i = 0; i < nm->q; ++i) {
+    if (!z[i]) return fail(FB_ERR_ARG, "lmm_spass: z[%d] is NULL", i);
+    fks[i] = nm->part[i].fk;
+    zs[i] = z[i];
+    zrows[i] = nm->part[i].n_r;
+  }
+  return cuda_status(fb::launch_lmm_rows(nm->s, nm->n_s, nm->d_s, x, d_x, d_x, nm->q, fks, zs, fb::z_stride(d_x), out,
+                                         d_x, cs(stream), g_num_sms, zrows),
+                     "lmm_spass");
+}
+
+size_t fb_wt_spass_workspace_bytes(const fb_normalized* nm, int32_t n_w) {
+  if (!nm) return 0;
+  const int w = n_w < 16 ? n_w : 16;
+  return align256(fb::colreduce_workspace_doubles(0, static_cast<int>(max_width(nm)), w, g_num_sms) * sizeof(double)) +
+         256;
+}
+
+int fb_wt_spass(const fb_normalized* nm, const double* w, int32_t n_w, int64_t w_rs, int64_t w_cs, double* out,
+                int64_t o_js, int64_t o_cs, double* const* bins, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (n_w < 1 || n_w > 16) return fail(FB_ERR_ARG, "wt_spass: n_w=%d outside [1, 16]", n_w);
+  if (!out) return fail(FB_ERR_ARG, "wt_spass: NULL output");
+  if (!w && bins) return fail(FB_ERR_ARG, "wt_spass: the X·K scatter needs explicit weights");
+  if (max_width(nm) > 256) return fail(FB_ERR_ARG, "wt_spass: factor widths above 256 are not supported");
+  if (ws_bytes < fb_wt_spass_workspace_bytes(nm, n_w)) return fail(FB_ERR_ARG, "wt_spass: workspace too small");
+  double* none[FB_MAX_PARTS] = {};
+  if (!w) {  // all-ones weights: colSums of S
+    fb_normalized s_only = *nm;
+    s_only.q = 0;
+    return wt_impl(&s_only, nullptr, 1, 1, 1, nullptr, out, o_js, o_cs, ws, ws_bytes, stream, none, false);
+  }
+  return wt_impl(nm, w, n_w, w_rs, w_cs, nullptr, out, o_js, o_cs, ws, ws_bytes, stream, bins ? bins : none, false);
+}
+
+size_t fb_rows_wt_workspace_bytes(int32_t d, int32_t n_w) {
+  const int w = n_w < 16 ? n_w : 16;
+  return align256(fb::colreduce_workspace_doubles(0, d > 0 ? d : 1, w > 0 ? w : 1, g_num_sms) * sizeof(double)) + 256;
+}
+
+int fb_rows_wt(const double* a, int64_t n, int32_t d, const double* w, int32_t n_w, int64_t w_rs, int64_t w_cs,
+               double* out, int64_t o_js, int64_t o_cs, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  if (n < 0 || d < 0 || n_w < 1) return fail(FB_ERR_SHAPE, "rows_wt: n=%lld d=%d n_w=%d", (long long)n, d, n_w);
+  if (d > 256) return fail(FB_ERR_ARG, "rows_wt: widths above 256 are not supported");
+  if ((n > 0 && (!a || !w)) || !out) return fail(FB_ERR_ARG, "rows_wt: NULL pointer");
+  if (ws_bytes < fb_rows_wt_workspace_bytes(d, n_w)) return fail(FB_ERR_ARG, "rows_wt: workspace too small");
+  for (int j0 = 0; j0 < n_w;) {
+    const int nx = chunk_width(n_w - j0);
+    Carver cv{static_cast<char*>(ws), ws_bytes};
+    double* partials = cv.take<double>(fb::colreduce_workspace_doubles(0, d > 0 ? d : 1, nx, g_num_sms));
+    unsigned int* counter = cv.take<unsigned int>(1);
+    fb::ColReduce r{};
+    r.a = a;
+    r.n = n;
+    r.d = d;
+    r.nx = nx;
+    r.w = w + j0 * w_cs;
+    r.w_rs = w_rs;
+    r.w_cs = w_cs;
+    r.out = out + j0 * o_js;
+    r.o_js = o_js;
+    r.o_cs = o_cs;
+    r.partials = partials;
+    r.counter = counter;
+    if (n == 0) {
+      for (int j = 0; j < nx; ++j) {  // empty slice: zero output (colreduce needs rows)
+        cudaError_t e = cudaMemset2DAsync(out + (j0 + j) * o_js, o_cs * sizeof(double), 0, sizeof(double), d, cs(stream));
+        if (e != cudaSuccess) return cuda_status(e, "rows_wt(empty)");
+      }
+    } else {
+      cudaError_t e = fb::launch_colreduce(r, cs(stream), g_num_sms);
+      if (e != cudaSuccess) return cuda_status(e, "rows_wt");
+    }
+    j0 += nx;
+  }
+  return FB_OK;
+}
+
 // ------------------------------------------------------------------ crossprod
 size_t fb_fk_sort_workspace_bytes(int64_t n) { return fb::fk_sort_workspace_bytes(n); }
 
@@ -482,8 +616,8 @@ size_t fb_crossprod_workspace_bytes(const fb_normalized* nm) {
                                        q ? 1 : 0, g_num_sms);
 }
 
-int fb_crossprod(const fb_normalized* nm, const int32_t* perm, const int32_t* fk_sorted, double* out, void* ws,
-                 size_t ws_bytes, fb_stream_t stream) {
+static int crossprod_impl(const fb_normalized* nm, const int32_t* perm, const int32_t* fk_sorted, double* out, void* ws,
+                          size_t ws_bytes, fb_stream_t stream, int mode, double* kts) {
   int st = check_nm(nm);
   if (st) return st;
   if (nm->q > 1) return fail(FB_ERR_ARG, "crossprod: star schemas (q=%d) are not supported by the device path", nm->q);
@@ -497,7 +631,7 @@ int fb_crossprod(const fb_normalized* nm, const int32_t* perm, const int32_t* fk
   c.d_s = nm->d_s;
   if (nm->q == 1) {
     const fb_part& p = nm->part[0];
-    if (nm->n_s > 0 && (!perm || !fk_sorted)) return fail(FB_ERR_ARG, "crossprod: FK-sorted order missing");
+    if (mode != 2 && nm->n_s > 0 && (!perm || !fk_sorted)) return fail(FB_ERR_ARG, "crossprod: FK-sorted order missing");
     if (!p.counts) return fail(FB_ERR_ARG, "crossprod: counts missing");
     c.perm = perm;
     c.fk_sorted = fk_sorted;
@@ -507,7 +641,26 @@ int fb_crossprod(const fb_normalized* nm, const int32_t* perm, const int32_t* fk
     c.counts = p.counts;
   }
   c.out = out;
+  c.mode = mode;
+  c.kts = kts;
+  if (mode != 0 && nm->q == 1 && !kts) return fail(FB_ERR_ARG, "crossprod: split passes need the KᵀS buffer");
   return cuda_status(fb::launch_crossprod(c, ws, ws_bytes, cs(stream), g_num_sms), "crossprod");
+}
+
+int fb_crossprod(const fb_normalized* nm, const int32_t* perm, const int32_t* fk_sorted, double* out, void* ws,
+                 size_t ws_bytes, fb_stream_t stream) {
+  return crossprod_impl(nm, perm, fk_sorted, out, ws, ws_bytes, stream, 0, nullptr);
+}
+
+int fb_crossprod_spass(const fb_normalized* nm, const int32_t* perm, const int32_t* fk_sorted, double* out,
+                       double* kts, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  return crossprod_impl(nm, perm, fk_sorted, out, ws, ws_bytes, stream, 1, kts);
+}
+
+int fb_crossprod_rpass(const fb_normalized* nm, const double* kts, double* out, void* ws, size_t ws_bytes,
+                       fb_stream_t stream) {
+  if (nm && nm->q != 1) return fail(FB_ERR_ARG, "crossprod_rpass: needs exactly one attribute block (q=%d)", nm->q);
+  return crossprod_impl(nm, nullptr, nullptr, out, ws, ws_bytes, stream, 2, const_cast<double*>(kts));
 }
 
 // ------------------------------------------------------------------ GLM steps

@@ -955,10 +955,13 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     bins = reinterpret_cast<double*>(take(static_cast<size_t>(c.n_r) * c.d_s * 8));
     ckey = reinterpret_cast<int*>(take(slots * sizeof(int)));
     cval = reinterpret_cast<double*>(take(slots * (c.d_s > 0 ? c.d_s : 1) * 8));
+    if (c.kts) bins = c.kts;  // split passes: KᵀS lives in the caller's buffer
   }
   if (static_cast<size_t>(p - static_cast<char*>(ws)) > ws_bytes) return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(c.out, 0, static_cast<size_t>(d) * d * 8, st);
   if (e != cudaSuccess) return e;
+  const bool do_s = c.mode != 2, do_r = c.mode != 1;
+  if (do_s) {
 
   // ---- S pass. Fused (q = 1, even d_S <= 128): one pass over S in FK-sorted order computes
   // SᵀS on the consumer warps and KᵀS on the walker warp. Otherwise SᵀS streams S in storage
@@ -1044,8 +1047,10 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     if (e != cudaSuccess) return e;
   }
 
+  }  // do_s
+
   // ---- R pass: Rᵀ diag(c) R (upper) and RᵀB
-  if (q && c.d_r > 0 && c.n_r > 0) {
+  if (do_r && q && c.d_r > 0 && c.n_r > 0) {
     GramArgs a{};
     a.n = c.n_r;
     // R rows padded to a bank-conflict-free pitch (frag_pitch), one bulk copy per row

@@ -87,6 +87,11 @@ struct CrossArgs {
   int d_r;
   const double* counts;      // f64 colSums(K)
   double* out;               // d × d, d = d_s + d_r
+  // split passes for R-row-sliced multi-GPU crossprod (dist.py): 0 = whole, 1 = S pass only
+  // (SᵀS block of out, KᵀS into kts), 2 = R pass only (r / n_r / counts / kts = one R slice;
+  // out gets only the blocks that involve R)
+  int mode;
+  double* kts;               // caller KᵀS (n_r × d_s): written in mode 1, read in mode 2
 };
 size_t fk_sort_workspace_bytes(int64_t n);
 cudaError_t launch_fk_sort(const int32_t* fk, int64_t n, int64_t n_r, int32_t* perm, int32_t* fk_sorted, void* ws,

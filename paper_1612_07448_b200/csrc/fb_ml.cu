@@ -276,7 +276,9 @@ __global__ void kmeans_assign_kernel(const double* __restrict__ tc, const double
         best = j;
       }
     }
-    if (nan) atomicMin(nan_row, static_cast<unsigned long long>(i));
+    // (iteration, row) packed: the smallest is the first NaN row of the FIRST iteration that
+    // saw one — the row the reference reports when row_min_mask raises (kernel.py:330-332)
+    if (nan) atomicMin(nan_row, (static_cast<unsigned long long>(it) << 40) | static_cast<unsigned long long>(i));
     assign[i] = best;
     acc += bv;
     atomicAdd(&ssz[best], 1);

@@ -2,22 +2,31 @@
 
 Partitioning (BASELINE.json north star): the rows of S, of every FK
 column and of every per-row vector (y, W, assignments) are split into contiguous blocks,
-one per rank; the attribute tables R_i are replicated. Consequences:
+one per rank; the attribute tables R_i are replicated — but the R-side *work* is split by
+R-row slice (with every rank reading all of R, c2 LMM would scale ~3.8x at
+N = 8). Rank g owns R rows [g·⌈n_R/N⌉, (g+1)·⌈n_R/N⌉) of every part:
 
-* row-local results — LMM T·X, rowSums, the K-Means argmin, the GNMF W update — need no
-  communication and stay sharded;
-* every Tᵀ-side result — Tᵀ·P, X·T, colSums, sum, crossprod, GLM gradients and losses,
-  K-Means cluster sums/sizes, GNMF Tᵀ·W and WᵀW — is a sum over rows: each rank computes its
-  shard's partial with the single-GPU kernels and one all-reduce (NCCL over NVLink /
-  NVSwitch) combines them. Integer partials (key histograms, cluster sizes) are reduced as
-  integers, so they stay bit-exact.
-* construction keeps the reference's global semantics (normmat.py:168-198): the key
-  histogram is all-reduced first, so every rank drops the same unreferenced R rows and
-  remaps keys identically.
+* LMM T·X / rowSums: each rank computes z = R_slice·X_R for its slice (``fb_lmm_zpass``),
+  one **all-gather** assembles the whole z, and the S pass runs on the rank's own rows
+  (``fb_lmm_spass``); the output stays row-sharded.
+* Tᵀ·P, X·T, colSums: the S pass (``fb_wt_spass``) gives this rank's SᵀW partial and its
+  X·K bins over all n_R rows; a **reduce-scatter** of the bins leaves each rank the summed
+  bins of its own slice, which it multiplies into its R slice (``fb_rows_wt``); one
+  **all-reduce** of the small n_w × d result combines everything. colSums needs no
+  reduce-scatter: its bins are the global key counts, known on every rank since the build.
+* crossprod: SᵀS and KᵀS of the rank's rows (``fb_crossprod_spass``), a reduce-scatter of
+  KᵀS (n_R × d_S), then (KᵀS)ᵀR and Rᵀdiag(c)R on the slice (``fb_crossprod_rpass``), one
+  all-reduce of the d × d result and an exact mirror.
+* GNMF composes the above (Tᵀ·W, T·H); the GLM and K-Means drivers keep their fused
+  single-GPU steps per rank (replicated R-side work) plus one all-reduce per iteration.
+* Integer partials (key histograms, cluster sizes) are reduced as integers, so they stay
+  bit-exact; construction keeps the reference's global semantics (normmat.py:168-198): the
+  key histogram is all-reduced first, so every rank drops the same unreferenced R rows.
 
 The local arithmetic goes through a *backend* (``DeviceBackend``: the sm_100a kernels of
 this package). The collective composition is backend-independent, which is what the
-world-size-2 ``gloo`` tests exercise on CPU with an oracle-backed backend.
+world-size-2 ``gloo`` tests exercise on CPU with an oracle-backed backend (and on one GPU
+with the device backend).
 """
 
 import numpy as np
@@ -65,19 +74,72 @@ def _rank(group):
 def _allreduce(t, group=None, op=None):
     """In-place sum (default) over the group; a no-op on one process."""
     if _world(group) > 1:
-        dist.all_reduce(t, op=op or dist.ReduceOp.SUM, group=group)
+        if t.is_cuda and dist.get_backend(group) != "nccl":  # gloo: reduce a host copy
+            h = t.cpu()
+            dist.all_reduce(h, op=op or dist.ReduceOp.SUM, group=group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=op or dist.ReduceOp.SUM, group=group)
     return t
 
 
-class ShardedMatrix:
-    """This rank's row block of a normalized matrix plus its place in the global one."""
+def _nccl(group):
+    return _world(group) > 1 and dist.get_backend(group) == "nccl"
 
-    def __init__(self, local, n_global, row0, group=None, backend=None):
+
+def _allgather_rows(buf, chunk, group):
+    """buf: (world·chunk, cols); this rank filled rows [rank·chunk, (rank+1)·chunk)."""
+    world, rank = _world(group), _rank(group)
+    if world == 1:
+        return buf
+    mine = buf[rank * chunk:(rank + 1) * chunk]
+    if _nccl(group):
+        dist.all_gather_into_tensor(buf, mine.contiguous(), group=group)
+    else:  # gloo (functional checks; its all-gather is host-only): list all-gather on host copies
+        host = mine.cpu()
+        parts = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(parts, host, group=group)
+        for g, t in enumerate(parts):
+            buf[g * chunk:(g + 1) * chunk] = t.to(buf.device)
+    return buf
+
+
+def _reduce_scatter_rows(buf, chunk, group):
+    """buf: (world·chunk, cols) partial sums on every rank -> this rank's summed row chunk."""
+    world, rank = _world(group), _rank(group)
+    if world == 1:
+        return buf[:chunk]
+    if _nccl(group):
+        out = torch.empty((chunk,) + tuple(buf.shape[1:]), dtype=buf.dtype, device=buf.device)
+        dist.reduce_scatter_tensor(out, buf, group=group)
+        return out
+    _allreduce(buf, group)  # gloo has no reduce-scatter: same sums, more traffic
+    return buf[rank * chunk:(rank + 1) * chunk]
+
+
+class ShardedMatrix:
+    """This rank's row block of a normalized matrix plus its place in the global one.
+
+    ``gcounts[i]``: global key counts (f64) of part i's kept R rows — colSums(K_i) of the whole
+    matrix, all-reduced at build time. ``r_slice(i)`` is this rank's R-row slice of part i.
+    """
+
+    def __init__(self, local, n_global, row0, group=None, backend=None, gcounts=None):
         self.local = local
         self.n_global = int(n_global)
         self.row0 = int(row0)
         self.group = group
         self.backend = backend or DeviceBackend()
+        self.gcounts = gcounts or []
+
+    def r_chunk(self, i):
+        n_r = self.backend.part_rows(self.local, i)
+        return -(-n_r // _world(self.group)), n_r
+
+    def r_slice(self, i):
+        chunk, n_r = self.r_chunk(i)
+        lo = min(n_r, _rank(self.group) * chunk)
+        return lo, min(n_r, lo + chunk)
 
     @property
     def n_local(self):
@@ -148,6 +210,105 @@ class DeviceBackend:
 
     def cols(self, nm):
         return nm.base_cols
+
+    def nparts(self, nm):
+        return len(nm.indicator_blocks)
+
+    def part_rows(self, nm, i):
+        return nm.indicator_blocks[i][1].shape[0]
+
+    def part_cols(self, nm, i):
+        return nm.indicator_blocks[i][1].shape[1]
+
+    def source_rows(self, nm, i):
+        return nm.source_rows[i + 1]
+
+    def splittable(self, nm):
+        return nm.blocks[0][0] is None  # PK-FK / star (M:N matrices keep the replicated path)
+
+    def zeros(self, *shape):
+        return torch.zeros(shape, dtype=torch.float64, device=D.device())
+
+    def z_cols(self, d_x):
+        return int(_lib.lib().fb_z_stride(d_x))
+
+    def lmm_zpass(self, nm, x, i, lo, hi, z):
+        xd = self.tensor(x).contiguous()
+        _lib.check(_lib.lib().fb_lmm_zpass(nm.c_struct(), D.ptr(xd), xd.shape[1], i, lo, hi, D.ptr(z),
+                                           D.stream_handle()))
+
+    def lmm_spass(self, nm, x, zs):
+        import ctypes
+
+        xd = self.tensor(x).contiguous()
+        out = torch.empty((nm.base_rows, xd.shape[1]), dtype=torch.float64, device=D.device())
+        arr = (ctypes.c_void_p * max(1, len(zs)))(*[z.data_ptr() for z in zs])
+        _lib.check(_lib.lib().fb_lmm_spass(nm.c_struct(), D.ptr(xd), xd.shape[1], arr, D.ptr(out),
+                                           D.stream_handle()))
+        return out
+
+    def wt_spass(self, nm, w, n_w, w_rs, w_cs, bins):
+        """(n_w × d) with this rank's SᵀW in the S columns (rest zero); bins[i][:n_r] = WᵀK_i."""
+        import ctypes
+
+        so = _lib.lib()
+        cs = nm.c_struct()
+        if any(b is not None for b in bins) and any(e.skewed for e, _ in nm.indicator_blocks):
+            nm.ensure_sorted()  # skewed keys scatter as segmented sums over the sorted order
+        out = torch.zeros((n_w, nm.base_cols), dtype=torch.float64, device=D.device())
+        ws = D.workspace(so.fb_wt_spass_workspace_bytes(cs, n_w))
+        arr = (ctypes.c_void_p * 4)(*[(b.data_ptr() if b is not None else None) for b in bins] + [None] * (4 - len(bins)))
+        _lib.check(so.fb_wt_spass(cs, D.ptr(w) if w is not None else None, n_w, w_rs, w_cs, D.ptr(out),
+                                  nm.base_cols, 1, arr if w is not None else None, ws.data_ptr(), ws.numel(),
+                                  D.stream_handle()))
+        return out
+
+    def rows_wt(self, nm, i, lo, hi, wts):
+        """(n_w × d_r) = wtsᵀ · R_i[lo:hi] (wts: (hi-lo) × n_w)."""
+        so = _lib.lib()
+        r = nm.indicator_blocks[i][1]
+        d_r = r.shape[1]
+        n_w = wts.shape[1]
+        out = torch.empty((n_w, d_r), dtype=torch.float64, device=D.device())
+        ws = D.workspace(so.fb_rows_wt_workspace_bytes(d_r, n_w))
+        wts = wts.contiguous()
+        _lib.check(so.fb_rows_wt(r.data_ptr() + 8 * lo * d_r, hi - lo, d_r, D.ptr(wts), n_w, n_w, 1, D.ptr(out), d_r,
+                                 1, ws.data_ptr(), ws.numel(), D.stream_handle()))
+        return out
+
+    def crossprod_spass(self, nm, kts):
+        so = _lib.lib()
+        cs = nm.c_struct()
+        perm, fks = nm.k.sorted_order()
+        d = nm.base_cols
+        out = torch.empty((d, d), dtype=torch.float64, device=D.device())
+        ws = D.workspace(so.fb_crossprod_workspace_bytes(cs))
+        _lib.check(so.fb_crossprod_spass(cs, D.ptr(perm), D.ptr(fks), D.ptr(out), D.ptr(kts), ws.data_ptr(),
+                                         ws.numel(), D.stream_handle()))
+        return out
+
+    def crossprod_rpass(self, nm, lo, hi, kts_slice, counts_slice):
+        so = _lib.lib()
+        d = nm.base_cols
+        out = torch.zeros((d, d), dtype=torch.float64, device=D.device())
+        if hi <= lo:
+            return out
+        r = nm.r
+        st = _lib.FbNormalized()
+        st.s, st.n_s, st.d_s, st.q = D.ptr(nm.blocks[0][1]), nm.base_rows, nm.blocks[0][1].shape[1], 1
+        p = st.part[0]
+        p.fk = D.ptr(nm.k.target)
+        p.r = r.data_ptr() + 8 * lo * r.shape[1]
+        p.n_r, p.d_r = hi - lo, r.shape[1]
+        cnt = counts_slice.contiguous()
+        p.counts = D.ptr(cnt)
+        kts_slice = kts_slice.contiguous()
+        import ctypes
+
+        ws = D.workspace(so.fb_crossprod_workspace_bytes(ctypes.byref(st)))
+        _lib.check(so.fb_crossprod_rpass(ctypes.byref(st), D.ptr(kts_slice), D.ptr(out), ws.data_ptr(), ws.numel(),
+                                         D.stream_handle()))
+        return out
 
     def lmm(self, nm, x):
         from .rewrite import lmm
@@ -299,7 +460,10 @@ def build_star(s_local, parts, n_global, group=None, backend=None):
     local = be.build(s_local, parts, global_counts)
     if be.rows(local) != r1 - r0:
         raise ShapeError(f"rank {rank} holds {be.rows(local)} rows, expected {r1 - r0} of {n_global}")
-    return ShardedMatrix(local, n_global, r0, group, be)
+    # global colSums(K_i) of the kept rows: the weights of colSums' R-slice pass
+    gcounts = [be.tensor(be.to_numpy(gc)[be.to_numpy(be.source_rows(local, i))].astype(np.float64))
+               for i, gc in enumerate(global_counts)]
+    return ShardedMatrix(local, n_global, r0, group, be, gcounts)
 
 
 def build_pkfk(s_local, key_local, r, n_global, group=None, backend=None):
@@ -311,38 +475,123 @@ def build_pkfk(s_local, key_local, r, n_global, group=None, backend=None):
 # operators
 
 
+def _split(sm, width=1):
+    """The R-row-sliced composition applies (multi-rank, PK-FK / star, <= 16 columns per pass)."""
+    return _world(sm.group) > 1 and width <= 16 and sm.backend.splittable(sm.local)
+
+
 def lmm(sm, x):
-    """T·X for this rank's rows (row-local: no communication)."""
-    return sm.backend.lmm(sm.local, x)
+    """T·X for this rank's rows: z slices (R_slice·X_R) all-gathered, then the S pass."""
+    be = sm.backend
+    x = be.tensor(x)
+    if x.dim() == 1:
+        x = x.reshape(-1, 1)
+    if not _split(sm, x.shape[1]):
+        return be.lmm(sm.local, x)
+    zc = be.z_cols(x.shape[1])
+    zs = []
+    for i in range(be.nparts(sm.local)):
+        chunk, n_r = sm.r_chunk(i)
+        lo, hi = sm.r_slice(i)
+        z = be.zeros(chunk * _world(sm.group), zc)
+        if hi > lo:
+            be.lmm_zpass(sm.local, x, i, lo, hi, z)
+        zs.append(_allgather_rows(z, chunk, sm.group))
+    return be.lmm_spass(sm.local, x, zs)
+
+
+def _wt(sm, w, n_w, w_rs, w_cs):
+    """out (n_w × d) = Σ_i w(i, ·)ᵀ T(i, ·) over all ranks' rows (w: this rank's rows)."""
+    be = sm.backend
+    nparts = be.nparts(sm.local)
+    world = _world(sm.group)
+    bins = []
+    for i in range(nparts):
+        chunk, n_r = sm.r_chunk(i)
+        bins.append(be.zeros(chunk * world, n_w))
+    out = be.wt_spass(sm.local, w, n_w, w_rs, w_cs, [b[:sm.r_chunk(i)[1]] for i, b in enumerate(bins)])
+    off = be.cols(sm.local) - sum(be.part_cols(sm.local, i) for i in range(nparts))
+    for i in range(nparts):
+        chunk, _ = sm.r_chunk(i)
+        lo, hi = sm.r_slice(i)
+        mine = _reduce_scatter_rows(bins[i], chunk, sm.group)  # summed X·K_i of my R slice
+        d_r = be.part_cols(sm.local, i)
+        if hi > lo and d_r:
+            out[:, off:off + d_r] = be.rows_wt(sm.local, i, lo, hi, mine[:hi - lo])
+        off += d_r
+    return _allreduce(out, sm.group)
 
 
 def tmm(sm, p_local):
     """Tᵀ·P (d × m) from this rank's rows of P, summed over ranks."""
-    return _allreduce(sm.backend.tmm(sm.local, p_local), sm.group)
+    be = sm.backend
+    p = be.tensor(p_local)
+    if p.dim() == 1:
+        p = p.reshape(-1, 1)
+    if not _split(sm, p.shape[1]):
+        return _allreduce(be.tmm(sm.local, p), sm.group)
+    p = p.contiguous()
+    m = p.shape[1]
+    return _wt(sm, p, m, m, 1).t().contiguous()
 
 
 def rmm(x_local, sm):
     """X·T (n_x × d) from this rank's columns of X, summed over ranks."""
-    return _allreduce(sm.backend.rmm(x_local, sm.local), sm.group)
+    be = sm.backend
+    x = be.tensor(x_local)
+    if not _split(sm, x.shape[0]):
+        return _allreduce(be.rmm(x, sm.local), sm.group)
+    x = x.contiguous()
+    return _wt(sm, x, x.shape[0], 1, x.shape[1])
 
 
 def row_sums(sm):
-    return sm.backend.row_sums(sm.local)
+    """rowSums(T) for this rank's rows (the LMM composition with X = 1, rewrite.py:118-128)."""
+    if not _split(sm):
+        return sm.backend.row_sums(sm.local)
+    return lmm(sm, np.ones((sm.shape[1], 1)))
 
 
 def col_sums(sm):
-    return _allreduce(sm.backend.col_sums(sm.local), sm.group)
+    """colSums(T) = [1ᵀS summed over ranks, global counts_i · R_i by R slice] (rewrite.py:131-149)."""
+    be = sm.backend
+    if not _split(sm):
+        return _allreduce(be.col_sums(sm.local), sm.group)
+    out = be.wt_spass(sm.local, None, 1, 1, 1, [None] * be.nparts(sm.local))
+    nparts = be.nparts(sm.local)
+    off = be.cols(sm.local) - sum(be.part_cols(sm.local, i) for i in range(nparts))
+    for i in range(nparts):
+        lo, hi = sm.r_slice(i)
+        d_r = be.part_cols(sm.local, i)
+        if hi > lo and d_r:
+            out[:, off:off + d_r] = be.rows_wt(sm.local, i, lo, hi, sm.gcounts[i][lo:hi].reshape(-1, 1))
+        off += d_r
+    return _allreduce(out, sm.group)
 
 
 def sum_all(sm):
-    return float(_allreduce(sm.backend.sum_all(sm.local), sm.group)[0])
+    if not _split(sm):
+        return float(_allreduce(sm.backend.sum_all(sm.local), sm.group)[0])
+    return float(col_sums(sm).sum())
 
 
 def crossprod(sm):
-    """TᵀT: per-rank factorized crossprod partials summed over ranks, then the upper triangle
-    mirrored (rewrite.py:298): an all-reduce may sum element (i, j) and its mirror (j, i) in
-    different orders (NCCL rings chunk the buffer), so symmetry is restored explicitly."""
-    g = _allreduce(sm.backend.crossprod(sm.local), sm.group)
+    """TᵀT: this rank's SᵀS + KᵀS; KᵀS reduce-scattered by R slice; (KᵀS)ᵀR and Rᵀdiag(c)R on
+    the slice; one all-reduce of the d × d sum, then the upper triangle mirrored
+    (rewrite.py:298): an all-reduce may sum element (i, j) and its mirror (j, i) in different
+    orders (NCCL rings chunk the buffer), so symmetry is restored explicitly."""
+    be = sm.backend
+    if _split(sm) and be.nparts(sm.local) == 1:
+        chunk, n_r = sm.r_chunk(0)
+        d_s = be.cols(sm.local) - be.part_cols(sm.local, 0)
+        kts = be.zeros(chunk * _world(sm.group), max(d_s, 1))
+        g = be.crossprod_spass(sm.local, kts[:n_r])
+        mine = _reduce_scatter_rows(kts, chunk, sm.group)
+        lo, hi = sm.r_slice(0)
+        g = g + be.crossprod_rpass(sm.local, lo, hi, mine[:hi - lo], sm.gcounts[0][lo:hi])
+        g = _allreduce(g, sm.group)
+    else:
+        g = _allreduce(be.crossprod(sm.local), sm.group)
     if _world(sm.group) > 1:
         g = torch.triu(g) + torch.triu(g, 1).t()
     return g
@@ -427,12 +676,13 @@ def kmeans(sm, cfg):
     # every rank takes the same path: the trace and the first NaN row (global index, MIN over
     # ranks) are all-reduced before anyone raises, so no rank is left waiting in a collective
     _allreduce(trace, sm.group)
-    bad = int(nan_row[0])
+    bad = int(nan_row[0])  # (iteration << 40) | local row, or -1
     none = np.iinfo(np.int64).max
-    first = be.tensor([sm.row0 + bad if bad != -1 else none], dtype=torch.int64)
+    low = (1 << 40) - 1
+    first = be.tensor([((bad >> 40) << 40) | (sm.row0 + (bad & low)) if bad != -1 else none], dtype=torch.int64)
     _allreduce(first, sm.group, op=dist.ReduceOp.MIN if _world(sm.group) > 1 else None)
     if int(first[0]) != none:
-        raise NumericError(f"row_min_mask: NaN in row {int(first[0])}")
+        raise NumericError(f"row_min_mask: NaN in row {int(first[0]) & low}")
     return ModelOutput("kmeans", (n, d), cfg, be.to_numpy(trace).tolist(), centroids=be.to_numpy(c))
 
 
@@ -451,14 +701,14 @@ def gnmf(sm, cfg):
     del w_full
     sum_t2 = _allreduce(be.square_sum(sm.local), sm.group)
     cpw = _allreduce(be.dense_crossprod(w), sm.group)
-    ttw = _allreduce(be.tmm(sm.local, w), sm.group)
+    ttw = tmm(sm, w)
     trace = be.tensor(np.zeros(cfg.iterations))
     for it in range(cfg.iterations):
         be.nmf_update(h, ttw, cpw)            # h = h ∘ TᵀW / (h·WᵀW + eps) (replicated)
         cph = be.small_gram(h)
-        th = be.lmm(sm.local, h)              # row-local
+        th = lmm(sm, h)                       # row-local S pass, R-sliced z
         be.nmf_update(w, th, cph)             # w = w ∘ T·h / (w·hᵀh + eps) (row-local)
-        ttw = _allreduce(be.tmm(sm.local, w), sm.group)
+        ttw = tmm(sm, w)                      # R-sliced Tᵀ·W
         cpw = _allreduce(be.dense_crossprod(w), sm.group)
         be.nmf_objective(sum_t2, ttw, h, cpw, cph, trace, it)
     return ModelOutput("gnmf", (n, d), cfg, be.to_numpy(trace).tolist(), factors=(be.to_numpy(w), be.to_numpy(h)))

@@ -462,8 +462,8 @@ def kmeans(m, cfg):
         _tally_tmm(counter, nm, k)
     bad = int(nan_row.item())
     wall = time.perf_counter() - t0
-    if bad != -1:
-        raise NumericError(f"row_min_mask: NaN in row {bad}")
+    if bad != -1:  # (iteration << 40) | row of the first NaN row of the first NaN iteration
+        raise NumericError(f"row_min_mask: NaN in row {bad & ((1 << 40) - 1)}")
     out = ModelOutput("kmeans", (n, d), cfg, _np(trace).tolist(), centroids=_np(c), wall_time_s=wall, counts=counter)
     out.assignment = assign  # last iteration's argmin cluster per row (int32, device): parity checks
     return out

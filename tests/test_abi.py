@@ -28,7 +28,7 @@ def test_abi_version_without_device():
     from paper_1612_07448_b200 import _lib
 
     so = _lib.load_library()
-    assert so.fb_abi_version() == 3
+    assert so.fb_abi_version() == 4
     assert so.fb_launch_count() >= 0
 
 

@@ -24,9 +24,17 @@ class OracleBackend:
     """Local arithmetic with the CPU oracle; tensors are CPU float64 (gloo)."""
 
     def __init__(self):
+        import collections
+
         import factorla_oracle as O
 
         self.O = O
+        self.calls = collections.Counter()
+
+    def __getattribute__(self, name):
+        if name in ("lmm_zpass", "wt_spass", "crossprod_rpass", "rows_wt"):
+            object.__getattribute__(self, "calls")[name] += 1
+        return object.__getattribute__(self, name)
 
     def tensor(self, a, dtype=torch.float64):
         return torch.as_tensor(np.asarray(a), dtype=dtype).clone()
@@ -53,6 +61,78 @@ class OracleBackend:
 
     def cols(self, nm):
         return nm.d
+
+    # ---- the R-row-sliced split passes (same contract as DeviceBackend)
+    def nparts(self, nm):
+        return len(nm.parts)
+
+    def part_rows(self, nm, i):
+        return nm.parts[i][1].shape[0]
+
+    def part_cols(self, nm, i):
+        return nm.parts[i][1].shape[1]
+
+    def source_rows(self, nm, i):
+        return nm.source_rows[i + 1]
+
+    def splittable(self, nm):
+        return True
+
+    def zeros(self, *shape):
+        return torch.zeros(shape, dtype=torch.float64)
+
+    def z_cols(self, d_x):
+        return d_x
+
+    def _off(self, nm, i):
+        return nm.s.shape[1] + sum(r.shape[1] for _, r in nm.parts[:i])
+
+    def lmm_zpass(self, nm, x, i, lo, hi, z):
+        r = nm.parts[i][1]
+        off = self._off(nm, i)
+        z[lo:hi] = self._t(r[lo:hi] @ x.numpy()[off:off + r.shape[1]])
+
+    def lmm_spass(self, nm, x, zs):
+        xn = x.numpy()
+        out = nm.s @ xn[:nm.s.shape[1]]
+        for (t, _), z in zip(nm.parts, zs):
+            out = out + z.numpy()[t]
+        return self._t(out)
+
+    def wt_spass(self, nm, w, n_w, w_rs, w_cs, bins):
+        n, d_s = nm.s.shape
+        wm = np.ones((n, 1)) if w is None else torch.as_strided(w, (n, n_w), (w_rs, w_cs)).numpy()
+        out = np.zeros((wm.shape[1], nm.d))
+        out[:, :d_s] = wm.T @ nm.s
+        for (t, r), b in zip(nm.parts, bins):
+            if b is not None:
+                acc = np.zeros((r.shape[0], wm.shape[1]))
+                np.add.at(acc, t, wm)
+                b.copy_(self._t(acc))
+        return self._t(out)
+
+    def rows_wt(self, nm, i, lo, hi, wts):
+        return self._t(wts.numpy().T @ nm.parts[i][1][lo:hi])
+
+    def crossprod_spass(self, nm, kts):
+        t, _ = nm.parts[0]
+        d_s = nm.s.shape[1]
+        g = np.zeros((nm.d, nm.d))
+        g[:d_s, :d_s] = nm.s.T @ nm.s
+        acc = np.zeros(tuple(kts.shape))
+        np.add.at(acc, t, nm.s)
+        kts.copy_(self._t(acc))
+        return self._t(g)
+
+    def crossprod_rpass(self, nm, lo, hi, kts_slice, counts_slice):
+        d_s = nm.s.shape[1]
+        g = np.zeros((nm.d, nm.d))
+        r = nm.parts[0][1][lo:hi]
+        p = r.T @ kts_slice.numpy()
+        g[d_s:, :d_s] = p
+        g[:d_s, d_s:] = p.T
+        g[d_s:, d_s:] = (r * counts_slice.numpy()[:, None]).T @ r
+        return self._t(g)
 
     def _t(self, a):
         return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64)))
@@ -218,6 +298,16 @@ def _worker(rank, world, port, q):
         close(out.factors[0], w[r0:r1])
         close(out.factors[1], h)
         close(out.objective, obj)
+        # a PK-FK matrix: the R-sliced crossprod (KᵀS reduce-scatter + R-slice pass)
+        pk = D.build_pkfk(s[r0:r1], parts[0][0][r0:r1], parts[0][1], n, backend=be)
+        rpk = O.build_pkfk(s, parts[0][0], parts[0][1])
+        cp = D.crossprod(pk)
+        close(cp, O.crossprod(rpk))
+        assert torch.equal(cp, cp.t())
+        close(D.col_sums(pk), O.col_sums(rpk))
+        close(D.lmm(pk, x[:rpk.d]), O.lmm(rpk, x[:rpk.d])[r0:r1])
+        # the split passes really ran (not the replicated fallback)
+        assert be.calls["lmm_zpass"] > 0 and be.calls["wt_spass"] > 0 and be.calls["crossprod_rpass"] > 0, be.calls
         dist.destroy_process_group()
         q.put((rank, "ok"))
     except Exception as e:  # noqa: BLE001
@@ -244,14 +334,16 @@ def test_shard_range_partitions_rows():
 
 
 @pytest.mark.timeout(300)
-def test_world2_gloo_matches_unsharded_oracle():
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_ranks_match_unsharded_oracle(world):
+    """world 3: R slices of unequal length (97 and 40 kept rows over 3 ranks)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=280) for _ in procs)
     for p in procs:
         p.join(timeout=30)
-    assert res == {0: "ok", 1: "ok"}, res
+    assert res == {r: "ok" for r in range(world)}, res
