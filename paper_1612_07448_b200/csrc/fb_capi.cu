@@ -841,6 +841,7 @@ size_t fb_kmeans_workspace_bytes(const fb_normalized* nm, int32_t k) {
   b += align256(fb::onehot_partials_doubles(nm->d_s > 0 ? nm->d_s : 1, k, g_num_sms) * 8);
   b += align256(fb::colreduce_workspace_doubles(0, static_cast<int>(max_width(nm)), k, g_num_sms) * 8);
   b += 3 * 256;                                             // counters
+  b += align256(std::max(fb::kmeans_pass_partials_doubles(g_num_sms), fb::rth_partials_doubles(g_num_sms)) * 8);
   size_t rtx = 0;
   for (int i = 0; i < nm->q; ++i) {
     b += align256(static_cast<size_t>(nm->part[i].n_r) * k * 4) + align256(static_cast<size_t>(nm->part[i].n_r) * k * 8);
@@ -917,26 +918,73 @@ static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const
       rtx_bytes = std::max(rtx_bytes, fb::rtx_workspace_bytes(nm->part[i].d_r, k, g_num_sms));
   }
   char* rtx_ws = rtx_bytes ? cv.take<char>(rtx_bytes) : nullptr;
+  double* kpart = cv.take<double>(std::max(fb::kmeans_pass_partials_doubles(g_num_sms), fb::rth_partials_doubles(g_num_sms)));
   // tc = (2T)·C computed as T·(2C): scaling by two is exact, so the products match bit for bit
   cudaError_t e = fb::launch_scalar_map(c, c2, d * k, fb::kMul, 2.0, s, g_num_sms);
   if (e != cudaSuccess) return cuda_status(e, "kmeans(2c)");
-  st = fb_lmm(nm, c2, k, tc, cv.p, cv.left, stream);
-  if (st) return st;
   for (int i = 0; i < nm->q; ++i) {
     e = cudaMemsetAsync(fks.bins[i], 0, static_cast<size_t>(nm->part[i].n_r) * k * 4, s);
     if (e != cudaSuccess) return cuda_status(e, "kmeans(memset)");
   }
-  e = fb::launch_kmeans_assign(tc, d_t, cc, nm->n_s, k, fks, assign, sizes, apart, cnt0, trace, it, nan_row, s,
-                               g_num_sms);
-  if (e != cudaSuccess) return cuda_status(e, "kmeans(assign)");
-  // TᵀA: S part by one-hot column sums, R parts as R_qᵀ (A_qᵀ K_q) from the integer histograms
-  if (nm->d_s > 0) {
-    e = fb::launch_onehot_colsum(nm->s, nm->n_s, nm->d_s, assign, k, opart, cnt1, tta, s, g_num_sms);
-    if (e != cudaSuccess) return cuda_status(e, "kmeans(onehot)");
+  static const bool fused_on = [] { const char* v = getenv("FB_KMEANS_FUSED"); return !(v && atoi(v) == 0); }();
+  if (fused_on && nm->n_s > 0 && fb::kmeans_pass_supported(nm->d_s, k, nm->q)) {
+    // one pass over S (fb_kmeans.cu) after the z-passes z_q = R_q · (2C)_q
+    fb::KmPass kp{};
+    kp.s = nm->s;
+    kp.n = nm->n_s;
+    kp.d = nm->d_s;
+    kp.d_t = d_t;
+    kp.c2s = c2;
+    kp.cc = cc;
+    kp.k = k;
+    kp.nfk = nm->q;
+    kp.zst = fb::z_stride(k);
+    int64_t zoff = nm->d_s;
+    for (int i = 0; i < nm->q; ++i) {
+      const fb_part& p = nm->part[i];
+      double* z = cv.take<double>(static_cast<size_t>(p.n_r) * kp.zst);
+      if (!z) return fail(FB_ERR_ARG, "kmeans: workspace too small");
+      e = fb::launch_lmm_rows(p.r, p.n_r, p.d_r, c2 + zoff * k, k, k, 0, nullptr, nullptr, 0, z, kp.zst, s, g_num_sms);
+      if (e != cudaSuccess) return cuda_status(e, "kmeans(z)");
+      kp.fk[i] = p.fk;
+      kp.z[i] = z;
+      kp.ztable_bytes[i] = static_cast<size_t>(p.n_r) * kp.zst * sizeof(double);
+      kp.bins[i] = fks.bins[i];
+      zoff += p.d_r;
+    }
+    kp.assign = assign;
+    kp.sizes = sizes;
+    kp.partials = kpart;
+    kp.counter = cnt0;
+    kp.trace = trace;
+    kp.it = it;
+    kp.nan_row = nan_row;
+    kp.sta = tta;
+    e = cudaMemsetAsync(sizes, 0, sizeof(int32_t) * k, s);
+    if (e != cudaSuccess) return cuda_status(e, "kmeans(sizes)");
+    e = fb::launch_kmeans_pass(kp, s, g_num_sms);
+    if (e != cudaSuccess) return cuda_status(e, "kmeans(pass)");
+  } else {
+    st = fb_lmm(nm, c2, k, tc, cv.p, cv.left, stream);
+    if (st) return st;
+    e = fb::launch_kmeans_assign(tc, d_t, cc, nm->n_s, k, fks, assign, sizes, apart, cnt0, trace, it, nan_row, s,
+                                 g_num_sms);
+    if (e != cudaSuccess) return cuda_status(e, "kmeans(assign)");
+    // TᵀA: S part by one-hot column sums, R parts as R_qᵀ (A_qᵀ K_q) from the integer histograms
+    if (nm->d_s > 0) {
+      e = fb::launch_onehot_colsum(nm->s, nm->n_s, nm->d_s, assign, k, opart, cnt1, tta, s, g_num_sms);
+      if (e != cudaSuccess) return cuda_status(e, "kmeans(onehot)");
+    }
   }
   int64_t off = nm->d_s;
   for (int i = 0; i < nm->q; ++i) {
     const fb_part& p = nm->part[i];
+    if (fb::rth_supported(p.d_r, k)) {  // R_qᵀ H_q straight from the integer histograms
+      e = fb::launch_rth(p.r, p.n_r, p.d_r, fks.bins[i], k, tta + off * k, k, 1, kpart, cnt2, s, g_num_sms);
+      if (e != cudaSuccess) return cuda_status(e, "kmeans(R pass)");
+      off += p.d_r;
+      continue;
+    }
     e = fb::launch_i32_to_f64(fks.bins[i], fbins[i], p.n_r * k, s, g_num_sms);
     if (e != cudaSuccess) return cuda_status(e, "kmeans(bins)");
     if (rtx_ws && fb::rtx_supported(p.d_r, k)) {  // R_qᵀ H_q on the tensor cores

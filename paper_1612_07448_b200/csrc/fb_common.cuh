@@ -98,6 +98,8 @@ FB_DEV void cp_async16_ca(void* dst, const void* src) {
 // Keyed gather of a lookup table far larger than L1 (uniform keys into a 100+ MB z): the
 // L1-bypassing form. With a 224 KB ring L1 is only 32 KB, and L1-allocating LDGSTS then
 // limit the gathers in flight (c2 X100x16: 1.575 -> 1.445 ms).
+// (An evict_last policy operand on these gathers — `cp.async.cg...L2::cache_hint [d], [s], 16,
+// 16, pol` — ran correctly but 2-3% slower at c2 X100x16 and did not raise the z hit rate.)
 template <bool CG>
 FB_DEV void cp_async16_gather(void* dst, const void* src) {
   if constexpr (CG)
@@ -195,6 +197,14 @@ FB_DEV void dmma_8x8x4(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
+}
+
+// Same, without `volatile`: the compiler may interleave these with independent loads and
+// stores (used by the LMM consumers, whose DMMA chains are latency-bound).
+FB_DEV void dmma_8x8x4_sched(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
 }
 
 // ---------------------------------------------------------------- launch accounting

@@ -161,6 +161,39 @@ struct KmFk {
 cudaError_t launch_kmeans_assign(const double* tc, const double* d_t, const double* cc, int64_t n, int k,
                                  const KmFk& fks, int32_t* assign, int32_t* sizes, double* partials, unsigned* counter,
                                  double* trace, int it, unsigned long long* nan_row, cudaStream_t st, int num_sms);
+// One fused pass over S per K-Means iteration (fb_kmeans.cu): T·(2C), argmin, objective,
+// sizes, K_qᵀA histograms and SᵀA.
+struct KmPass {
+  const double* s;  // n × d entity rows (d <= 32; d may be 0)
+  int64_t n;
+  int d;
+  const double* d_t;  // rowSums(T²)
+  const double* c2s;  // (2C)[0:d, :] row-major d × k
+  const double* cc;   // Σ_r c[r, j]²
+  int k;              // <= 16
+  int nfk;
+  const int32_t* fk[kMaxParts];
+  const double* z[kMaxParts];  // R_q·(2C)_q, n_R,q × zst
+  size_t ztable_bytes[kMaxParts];
+  int zst;
+  int32_t* bins[kMaxParts];  // n_R,q × k, zeroed by the caller
+  int32_t* assign;
+  int32_t* sizes;            // k, zeroed by the caller
+  double* partials;          // kmeans_pass_partials_doubles
+  unsigned* counter;         // one word (zeroed by the launcher)
+  double* trace;
+  int it;
+  unsigned long long* nan_row;
+  double* sta;               // SᵀA into tta[c*k + j], c < d
+};
+bool kmeans_pass_supported(int d_s, int k, int nfk);
+size_t kmeans_pass_partials_doubles(int num_sms);
+cudaError_t launch_kmeans_pass(const KmPass& p, cudaStream_t st, int num_sms);
+// out(c, j) = Σ_r R[r, c]·H[r, j], H int32 n × nx (d_r <= 64, nx <= 16), FP64 tensor cores
+bool rth_supported(int d_r, int nx);
+size_t rth_partials_doubles(int num_sms);
+cudaError_t launch_rth(const double* r, int64_t n, int d_r, const int32_t* h, int nx, double* out, int64_t o_rs,
+                       int64_t o_cs, double* partials, unsigned* counter, cudaStream_t st, int num_sms);
 size_t onehot_partials_doubles(int d, int k, int num_sms);
 cudaError_t launch_onehot_colsum(const double* s, int64_t n, int d, const int32_t* assign, int k, double* partials,
                                  unsigned* counter, double* out, cudaStream_t st, int num_sms);

@@ -266,6 +266,115 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_kernel(LmmArgs p, St
   }
 }
 
+// ------------------------------------------------------------------ DMMA, z-initialised accumulators
+// The common case of the S pass (every output column present and 16-byte aligned, d_x = 8·NT,
+// at least one keyed part, narrow S so the k-loop is unrolled): the accumulators start from the
+// gathered z rows (the C-fragment layout of m8n8k4 — lane (g, t) owns C[g][2t, 2t+1] — is
+// exactly a double2 of a z row), so the epilogue is the stores alone; the X fragments are
+// loaded once per CTA into registers; full tiles store without row predicates. ncu of the
+// generic body at c2 X100x16: ~420 issued instructions per warp per 256-row tile (z adds,
+// part loop, per-row bounds, debug switches) for 40 DMMAs, and the consumers' DADD chains on
+// the z loads sat on the critical path of every tile.
+// Parts after the first are added before the DMMAs (sum order z_0 + z_1 + ... then + S·X).
+template <int NT, int MT, int KS, bool CG>
+__global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_zinit_kernel(LmmArgs p, StreamSet ss, int stages,
+                                                                     int tile_rows) {
+  static_assert(KS > 0, "the z-initialised body needs a compile-time k-loop");
+  extern __shared__ __align__(128) char smem[];
+  const int d = p.d;
+  constexpr int dpad = 4 * KS;
+  constexpr int ldxs = 8 * NT + 4;
+  double* xs = reinterpret_cast<double*>(smem);
+  const size_t xs_bytes = (static_cast<size_t>(dpad) * ldxs * sizeof(double) + 127) & ~size_t(127);
+  char* buf = smem + xs_bytes;
+  for (int i = threadIdx.x; i < dpad * ldxs; i += blockDim.x) {
+    const int k = i / ldxs, n = i % ldxs;
+    xs[i] = (k < d && n < p.dx) ? p.x[k * p.ldx + n] : 0.0;
+  }
+
+  TileRing ring;
+  ring.init(buf, stages, tile_rows, p.n);
+  ring.start(ss);  // contains __syncthreads (xs visible after it)
+  if (ring.service<false, CG>(ss)) return;
+
+  const int lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int warp = consumer_warp();
+  const int pitch = p.pitch;
+  const int wrow = warp * (8 * MT);
+  const uint64_t pol = policy_evict_first();
+  const bool ragged_k = (d & 3) != 0;
+  const int zst = p.zstride;
+  const int nfk = p.nfk;
+  double bf[KS][NT];  // B fragments: X[4s + t][8nt + g], zero past d
+#pragma unroll
+  for (int s = 0; s < KS; ++s)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) bf[s][nt] = xs[(4 * s + t) * ldxs + 8 * nt + g];
+  const int a_off = (wrow + g) * pitch + t;
+  const int z_off = (wrow + g) * zst + 2 * t;
+
+  for (int64_t kt = 0; kt < ring.count(); ++kt) {
+    const int cur = ring.acquire(ss, kt);
+    const int64_t tile = ring.tile_begin + kt;
+    const int rows = ring.rows_of(tile);
+    const double* A = reinterpret_cast<const double*>(ring.stage_ptr(cur, ss, 0)) + a_off;
+    __syncwarp();  // mma.sync.aligned needs the whole warp converged (after the barrier spin)
+    if (wrow < rows) {
+      double acc[MT][NT][2];
+      {
+        const double* z0 = reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, 0)) + z_off;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const double2 zv = *reinterpret_cast<const double2*>(z0 + 8 * mt * zst + 8 * nt);
+            acc[mt][nt][0] = zv.x;
+            acc[mt][nt][1] = zv.y;
+          }
+      }
+      for (int q = 1; q < nfk; ++q) {
+        const double* zq = reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, q)) + z_off;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const double2 zv = *reinterpret_cast<const double2*>(zq + 8 * mt * zst + 8 * nt);
+            acc[mt][nt][0] += zv.x;
+            acc[mt][nt][1] += zv.y;
+          }
+      }
+#pragma unroll
+      for (int s = 0; s < KS; ++s) {
+        const bool on = !(s == KS - 1 && ragged_k) || 4 * s + t < d;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const double a = on ? A[8 * mt * pitch + 4 * s] : 0.0;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma_8x8x4_sched(acc[mt][nt][0], acc[mt][nt][1], a, bf[s][nt]);
+        }
+      }
+      double* o = p.out + (tile * tile_rows + wrow + g) * p.ldo + 2 * t;
+      if (rows == tile_rows) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            st_hint2(o + 8 * mt * p.ldo + 8 * nt, acc[mt][nt][0], acc[mt][nt][1], pol);
+      } else {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          if (wrow + 8 * mt + g >= rows) continue;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            st_hint2(o + 8 * mt * p.ldo + 8 * nt, acc[mt][nt][0], acc[mt][nt][1], pol);
+        }
+      }
+    }
+    ring.release();
+  }
+}
+
 // ------------------------------------------------------------------ host launchers
 static size_t ring_budget() {
   static size_t b = [] {
@@ -363,6 +472,13 @@ static cudaError_t launch_dmma_cfg(LmmArgs p, cudaStream_t st, int num_sms, size
   fill_streams(p, ss, p.pitch);
   const int dpad = (p.d + 3) & ~3;
   const size_t fixed = (static_cast<size_t>(dpad > 0 ? dpad : 4) * (8 * NT + 4) * 8 + 127) & ~size_t(127);
+  static const bool zinit_on = [] { const char* e = getenv("FB_LMM_ZINIT"); return !(e && atoi(e) == 0); }();
+  if constexpr (KS > 0) {
+    const bool zinit = zinit_on && p.nfk > 0 && p.dx == 8 * NT && p.zstride >= 8 * NT && (p.ldo & 1) == 0 &&
+                       (reinterpret_cast<uintptr_t>(p.out) & 15u) == 0 && p.debug == 0;
+    if (zinit && cg) return launch_ring(lmm_dmma_zinit_kernel<NT, MT, KS, true>, p, ss, fixed, tile_rows, st, num_sms, budget);
+    if (zinit) return launch_ring(lmm_dmma_zinit_kernel<NT, MT, KS, false>, p, ss, fixed, tile_rows, st, num_sms, budget);
+  }
   if (cg) return launch_ring(lmm_dmma_kernel<NT, MT, KS, true>, p, ss, fixed, tile_rows, st, num_sms, budget);
   return launch_ring(lmm_dmma_kernel<NT, MT, KS, false>, p, ss, fixed, tile_rows, st, num_sms, budget);
 }
