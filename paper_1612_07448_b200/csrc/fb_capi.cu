@@ -1021,7 +1021,9 @@ size_t fb_gnmf_workspace_bytes(const fb_normalized* nm, int32_t r) {
   size_t inner = fb_lmm_workspace_bytes(nm, r);
   inner = std::max(inner, fb_wt_workspace_bytes(nm, r));
   inner = std::max(inner, fb_crossprod_workspace_bytes(&wm));
-  return align256(static_cast<size_t>(nm->n_s) * r * 8) + align256(static_cast<size_t>(r) * r * 8) + inner + 256;
+  size_t fused = align256(std::max(fb::nmf_pass_partials_doubles(g_num_sms), fb::rth_partials_doubles(g_num_sms)) * 8) + 256;
+  for (int i = 0; i < nm->q; ++i) fused += align256(static_cast<size_t>(nm->part[i].n_r) * r * 8);
+  return align256(static_cast<size_t>(nm->n_s) * r * 8) + align256(static_cast<size_t>(r) * r * 8) + fused + inner + 256;
 }
 
 int fb_gnmf_step(const fb_normalized* nm, double* w, double* h, double* ttw, double* cpw, const double* sum_t2,
@@ -1041,6 +1043,78 @@ int fb_gnmf_step(const fb_normalized* nm, double* w, double* h, double* ttw, dou
   cudaError_t e = fb::launch_nmf_update(h, ttw, cpw, d, r, eps, s, g_num_sms);
   if (e == cudaSuccess) e = fb::launch_small_gram(h, d, r, cph, s);
   if (e != cudaSuccess) return cuda_status(e, "gnmf(h)");
+  double* npart = cv.take<double>(std::max(fb::nmf_pass_partials_doubles(g_num_sms), fb::rth_partials_doubles(g_num_sms)));
+  unsigned* ncnt = cv.take<unsigned>(1);
+  double* nbins[FB_MAX_PARTS] = {};
+  for (int i = 0; i < nm->q; ++i) nbins[i] = cv.take<double>(static_cast<size_t>(nm->part[i].n_r) * r);
+  static const bool fused_on = [] { const char* v = getenv("FB_GNMF_FUSED"); return !(v && atoi(v) == 0); }();
+  if (fused_on && nm->n_s > 0 && fb::nmf_pass_supported(nm->d_s, r, nm->q)) {
+    // one pass over S (fb_gnmf.cu): th, the W update, SᵀW, WᵀW and the K_qᵀW bins; then R_qᵀ bins_q
+    fb::NmfPass np{};
+    np.s = nm->s;
+    np.n = nm->n_s;
+    np.d = nm->d_s;
+    np.w = w;
+    np.r = r;
+    np.h = h;
+    np.cph = cph;
+    np.eps = eps;
+    np.nfk = nm->q;
+    np.zst = fb::z_stride(r);
+    int64_t off = nm->d_s;
+    for (int i = 0; i < nm->q; ++i) {
+      const fb_part& p = nm->part[i];
+      double* z = cv.take<double>(static_cast<size_t>(p.n_r) * np.zst);
+      if (!z) return fail(FB_ERR_ARG, "gnmf: workspace too small");
+      // z_q = R_q · H[off:off+d_r]   (rewrite.py:187)
+      e = fb::launch_lmm_rows(p.r, p.n_r, p.d_r, h + off * r, r, r, 0, nullptr, nullptr, 0, z, np.zst, s, g_num_sms);
+      if (e == cudaSuccess) e = cudaMemsetAsync(nbins[i], 0, static_cast<size_t>(p.n_r) * r * 8, s);
+      if (e != cudaSuccess) return cuda_status(e, "gnmf(z)");
+      np.fk[i] = p.fk;
+      np.z[i] = z;
+      np.ztable_bytes[i] = static_cast<size_t>(p.n_r) * np.zst * sizeof(double);
+      np.bins[i] = nbins[i];
+      if (p.nhot > 0 && p.hot_slot && p.hot_key) {
+        np.hot_slot[i] = p.hot_slot;
+        np.hot_key[i] = p.hot_key;
+        np.nhot[i] = p.nhot < 64 ? p.nhot : 64;
+      }
+      off += p.d_r;
+    }
+    np.partials = npart;
+    np.ttw_s = ttw;
+    np.cpw = cpw;
+    e = fb::launch_nmf_wpass(np, s, g_num_sms);
+    if (e != cudaSuccess) return cuda_status(e, "gnmf(W pass)");
+    off = nm->d_s;
+    for (int i = 0; i < nm->q; ++i) {  // ttw[off:off+d_r] = R_qᵀ (K_qᵀ W)
+      const fb_part& p = nm->part[i];
+      if (fb::rth_supported(p.d_r, r)) {
+        e = fb::launch_rth(p.r, p.n_r, p.d_r, static_cast<const double*>(nbins[i]), r, ttw + off * r, r, 1, npart,
+                           ncnt, s, g_num_sms);
+      } else {
+        fb::ColReduce c{};
+        c.a = p.r;
+        c.n = p.n_r;
+        c.d = p.d_r;
+        c.nx = r;
+        c.w = nbins[i];
+        c.w_rs = r;
+        c.w_cs = 1;
+        c.out = ttw + off * r;
+        c.o_js = 1;
+        c.o_cs = r;
+        c.partials = npart;
+        c.counter = ncnt;
+        e = cudaMemsetAsync(ncnt, 0, sizeof(unsigned), s);
+        if (e == cudaSuccess) e = fb::launch_colreduce(c, s, g_num_sms);
+      }
+      if (e != cudaSuccess) return cuda_status(e, "gnmf(R pass)");
+      off += p.d_r;
+    }
+    return cuda_status(fb::launch_nmf_objective(sum_t2, ttw, h, d * r, cpw, cph, r * r, trace, it, s),
+                       "gnmf(objective)");
+  }
   // th = T·h; w = w ∘ th / (w·cph + eps)
   st = fb_lmm(nm, h, r, th, cv.p, cv.left, stream);
   if (st) return st;

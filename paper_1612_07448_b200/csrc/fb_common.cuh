@@ -193,18 +193,12 @@ FB_DEV double warp_sum_strided(const double* p, int count, size_t stride) {
 // ---------------------------------------------------------------- FP64 tensor core
 // D(8x8) += A(8x4, row) * B(4x8, col). Fragment ownership (lane l, g = l>>2, t = l&3):
 //   a = A[g][t], b = B[t][g], c0/c1 = C[g][2t], C[g][2t+1].
+// `volatile` matters: a non-volatile mma.sync asm may be moved by the compiler into a divergent
+// region (a masked operand select for a ragged k-step made the fused GNMF pass hang).
 FB_DEV void dmma_8x8x4(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
-}
-
-// Same, without `volatile`: the compiler may interleave these with independent loads and
-// stores (used by the LMM consumers, whose DMMA chains are latency-bound).
-FB_DEV void dmma_8x8x4_sched(double& c0, double& c1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
-      : "+d"(c0), "+d"(c1)
-      : "d"(a), "d"(b));
 }
 
 // ---------------------------------------------------------------- launch accounting

@@ -1,0 +1,363 @@
+// fb_gnmf.cu — one fused pass over S per GNMF W step.
+//
+// Replaces, for the rows of S, the W half of the reference's multiplicative-update loop
+// (ml.py:309-313):
+//   th = T·H ;  W ← W ∘ th / (W·cph + eps) ;  ttw = Tᵀ·W ;  cpw = WᵀW
+// evaluated there as four whole-matrix steps (th written out, the update, another pass for
+// Tᵀ·W, another for WᵀW). One ring pass over S, W and the FK columns (fb_stream.cuh) does, per
+// 32-row share of a consumer warp:
+//   1. th = z_q[fk_q] (gathered R_q·H_q rows) + S·H_S on the FP64 tensor cores (DMMA);
+//   2. the fragments go through a per-warp shared tile so each lane owns one row: the row's
+//      update w_j ← w_j·th_j / (Σ_l w_l·cph[l][j] + eps) (the reference's operation order),
+//      written back in place (one coalesced 40·r-byte row per lane);
+//   3. SᵀW and WᵀW of the updated rows on the tensor cores from the same shared tiles;
+//   4. K_qᵀW: the updated row added to bins_q[fk_q] — hot Zipf targets (fb_part.hot_slot)
+//      into per-CTA shared bins flushed once, the rest as fire-and-forget REDG f64 adds
+//      (reordered atomics: rel ~1e-16 run to run, inside the 1e-9 parity bar).
+// Per-warp SᵀW / WᵀW partials are summed per CTA in warp order and across CTAs in CTA order
+// (nmf_reduce_kernel). The R side (R_qᵀ bins_q) runs after the pass (launch_rth).
+#include "fb_kernels.cuh"
+
+namespace fb {
+
+namespace {
+constexpr int kNmfMaxR = 16;
+constexpr int kNmfMaxD = 32;
+constexpr int kNmfPitch = 17;   // per-warp row tile pitch (doubles): conflict-free row-per-lane reads
+constexpr int kNmfSlots = kNmfMaxD * kNmfMaxR + kNmfMaxR * kNmfMaxR;  // SᵀW then WᵀW, per CTA
+constexpr int kNmfHot = 64;     // hot slots per part
+}  // namespace
+
+size_t nmf_pass_partials_doubles(int num_sms) { return static_cast<size_t>(num_sms) * kNmfSlots; }
+
+bool nmf_pass_supported(int d_s, int r, int nfk) {
+  return d_s >= 0 && d_s <= kNmfMaxD && r >= 1 && r <= kNmfMaxR && nfk >= 1 && nfk <= kMaxParts;
+}
+
+// shared memory ahead of the ring: H_S, cph, the per-warp row tiles, the hot bins
+__host__ __device__ inline size_t nmf_head_bytes(int ks, int nt, int nfk) {
+  const int dpad = ks > 0 ? 4 * ks : 4;
+  const size_t dbl = static_cast<size_t>(dpad) * (8 * nt + 4) + kNmfMaxR * kNmfMaxR +
+                     static_cast<size_t>(kConsumerWarps) * 32 * kNmfPitch + static_cast<size_t>(nfk) * kNmfHot * kNmfMaxR;
+  return (dbl * 8 + 127) & ~size_t(127);
+}
+
+template <int R, bool CG>
+__global__ void __launch_bounds__(kRingThreads, 1) nmf_wpass_kernel(NmfPass p, StreamSet ss, int stages,
+                                                                int tile_rows) {
+  constexpr int MT = 4;                // 32 rows per consumer warp
+  constexpr int NT = (R + 7) / 8;      // 8-column n-tiles of th / W
+  constexpr int ldxs = 8 * NT + 4;
+  constexpr int kMaxMts = kNmfMaxD / 8;  // SᵀW m-tiles (d_S <= 32)
+  extern __shared__ __align__(128) char smem[];
+  const int d = p.d;
+  const int ks = (d + 3) / 4, mts = (d + 7) / 8;
+  const int dpad = ks > 0 ? 4 * ks : 4;
+  double* xs = reinterpret_cast<double*>(smem);  // H_S, dpad × ldxs
+  double* cphs = xs + dpad * ldxs;              // cph, R × R (ld kNmfMaxR)
+  double* tiles = cphs + kNmfMaxR * kNmfMaxR;   // [warp][32][kNmfPitch]
+  double* hot = tiles + kConsumerWarps * 32 * kNmfPitch;  // [part][kNmfHot][kNmfMaxR]
+  char* buf = smem + nmf_head_bytes(ks, NT, p.nfk);
+  for (int i = threadIdx.x; i < dpad * ldxs; i += blockDim.x) {
+    const int k = i / ldxs, c = i % ldxs;
+    xs[i] = (k < d && c < R) ? p.h[k * R + c] : 0.0;
+  }
+  for (int i = threadIdx.x; i < kNmfMaxR * kNmfMaxR; i += blockDim.x) {
+    const int a = i / kNmfMaxR, b = i % kNmfMaxR;
+    cphs[i] = (a < R && b < R) ? p.cph[a * R + b] : 0.0;
+  }
+  for (int i = threadIdx.x; i < p.nfk * kNmfHot * kNmfMaxR; i += blockDim.x) hot[i] = 0.0;
+
+  TileRing ring;
+  ring.init(buf, stages, tile_rows, p.n);
+  ring.start(ss);  // __syncthreads
+  if (ring.service<false, CG>(ss)) return;
+
+  const int lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int warp = consumer_warp();
+  const int wrow = warp * 32;
+  const int zst = p.zst;
+  const bool ragged_k = (d & 3) != 0;
+  double* tile = tiles + warp * 32 * kNmfPitch;
+  double* trow = tile + lane * kNmfPitch;
+  double sw[kMaxMts][NT][2];  // SᵀW (S column m, W column n)
+  double ww[NT][NT][2];       // WᵀW
+#pragma unroll
+  for (int a = 0; a < kMaxMts; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b) sw[a][b][0] = sw[a][b][1] = 0.0;
+#pragma unroll
+  for (int a = 0; a < NT; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b) ww[a][b][0] = ww[a][b][1] = 0.0;
+
+  for (int64_t kt = 0; kt < ring.count(); ++kt) {
+    const int cur = ring.acquire(ss, kt);
+    const int64_t tl = ring.tile_begin + kt;
+    const int rows = ring.rows_of(tl);
+    const int64_t r0 = tl * tile_rows;
+    const double* S = reinterpret_cast<const double*>(ring.stage_ptr(cur, ss, 0));
+    const double* W = reinterpret_cast<const double*>(ring.stage_ptr(cur, ss, 1));
+    __syncwarp();
+    if (wrow < rows) {
+      // 1. th = Σ_q z_q[fk_q] (parts in order) + S·H_S
+      double acc[MT][NT][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+#pragma unroll
+      for (int q = 0; q < kMaxParts; ++q) {
+        if (q >= p.nfk) break;
+        const double* zq = reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, q)) + (wrow + g) * zst;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const int c = 8 * nt + 2 * t;
+            if (c < zst) {
+              const double2 zv = *reinterpret_cast<const double2*>(zq + 8 * mt * zst + c);
+              acc[mt][nt][0] += zv.x;
+              acc[mt][nt][1] += zv.y;
+            }
+          }
+      }
+      {
+        const double* A = S + (wrow + g) * d + t;
+        for (int s = 0; s < ks; ++s) {
+          const bool on = !(s == ks - 1 && ragged_k) || 4 * s + t < d;
+          double bk[NT];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) bk[nt] = xs[(4 * s + t) * ldxs + 8 * nt + g];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const double a = on ? A[8 * mt * d + 4 * s] : 0.0;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a, bk[nt]);
+          }
+        }
+      }
+      // 2. row per lane: w_j ← w_j·th_j / (Σ_l w_l·cph[l][j] + eps)   (ml.py:312)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          double* o = tile + (8 * mt + g) * kNmfPitch + 8 * nt + 2 * t;
+          o[0] = acc[mt][nt][0];
+          o[1] = acc[mt][nt][1];
+        }
+      __syncwarp();
+      const int rl = wrow + lane;
+      const bool live = rl < rows;
+      double wn[R];
+      if (live) {
+        const double* wr = W + static_cast<size_t>(rl) * R;
+        double wo[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) wo[j] = wr[j];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          double den = 0.0;
+#pragma unroll
+          for (int l = 0; l < R; ++l) den = fma(wo[l], cphs[l * kNmfMaxR + j], den);
+          wn[j] = wo[j] * trow[j] / (den + p.eps);
+        }
+        double* wg = p.w + (r0 + rl) * R;
+#pragma unroll
+        for (int j = 0; j < R; ++j) wg[j] = wn[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < R; ++j) wn[j] = 0.0;  // dead rows: zero B / WᵀW fragments
+      }
+#pragma unroll
+      for (int j = 0; j < 8 * NT; ++j) trow[j] = j < R ? wn[j] : 0.0;
+      __syncwarp();
+      // 4. K_qᵀW. Uniform keys: one REDG per row and column. Skewed keys: lanes holding the same
+      // key are combined first (the group's lowest lane sums the group's rows from the shared
+      // tile in lane order), then one add per key and column — into per-CTA shared bins for hot
+      // targets, a REDG otherwise (one atomic per row and column on the hottest slots: CAS
+      // retries, 0.78 ms at c5)
+#pragma unroll
+      for (int q = 0; q < kMaxParts; ++q) {
+        if (q >= p.nfk) break;
+        const int32_t key = live ? reinterpret_cast<const int32_t*>(ring.stage_ptr(cur, ss, 2 + q))[rl] : -1;
+        if (p.nhot[q] == 0) {
+          if (live) {
+            double* dst = p.bins[q] + static_cast<int64_t>(key) * R;
+#pragma unroll
+            for (int j = 0; j < R; ++j) red_add(dst + j, wn[j]);
+          }
+          continue;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (live && lane == __ffs(peers) - 1) {
+          double v[R];
+#pragma unroll
+          for (int j = 0; j < R; ++j) v[j] = wn[j];
+          for (unsigned m = peers & (peers - 1); m; m &= m - 1) {
+            const double* pr = tile + (__ffs(m) - 1) * kNmfPitch;
+#pragma unroll
+            for (int j = 0; j < R; ++j) v[j] += pr[j];
+          }
+          const int slot = p.hot_slot[q][key];
+          if (slot >= 0) {
+            double* dst = hot + (q * kNmfHot + slot) * kNmfMaxR;
+#pragma unroll
+            for (int j = 0; j < R; ++j) atomicAdd(dst + j, v[j]);
+          } else {
+            double* dst = p.bins[q] + static_cast<int64_t>(key) * R;
+#pragma unroll
+            for (int j = 0; j < R; ++j) red_add(dst + j, v[j]);
+          }
+        }
+      }
+      // 3. SᵀW and WᵀW of the updated rows (rows are the DMMA k dimension)
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int rr = 4 * s + t;  // row within the warp's share
+        const bool lv = wrow + rr < rows;
+        double b[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) b[nt] = tile[rr * kNmfPitch + 8 * nt + g];
+#pragma unroll
+        for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(ww[mt][nt][0], ww[mt][nt][1], b[mt], b[nt]);
+#pragma unroll
+        for (int mt = 0; mt < kMaxMts; ++mt) {
+          if (mt >= mts) break;
+          const int c = 8 * mt + g;
+          const double a = (lv && c < d) ? S[(wrow + rr) * d + c] : 0.0;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(sw[mt][nt][0], sw[mt][nt][1], a, b[nt]);
+        }
+      }
+    }
+    ring.release();
+  }
+
+  // per-warp partials -> per-CTA partial (warps in order); hot bins flushed once per CTA
+  consumer_sync();  // every consumer is past its last tile: the ring memory is free
+  double* red = reinterpret_cast<double*>(buf + kRingHeader);
+  double* mine = red + warp * kNmfSlots;
+#pragma unroll
+  for (int mt = 0; mt < kMaxMts; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) mine[(8 * mt + g) * kNmfMaxR + 8 * nt + 2 * t + e] = sw[mt][nt][e];
+#pragma unroll
+  for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        mine[kNmfMaxD * kNmfMaxR + (8 * mt + g) * kNmfMaxR + 8 * nt + 2 * t + e] = ww[mt][nt][e];
+  consumer_sync();
+  const int tid = consumer_tid();
+  for (int i = tid; i < kNmfSlots; i += kConsumerThreads) {
+    const bool is_sw = i < kNmfMaxD * kNmfMaxR;
+    const int a = is_sw ? i / kNmfMaxR : (i - kNmfMaxD * kNmfMaxR) / kNmfMaxR;
+    const int b = i % kNmfMaxR;
+    if ((is_sw && (a >= d || b >= R)) || (!is_sw && (a >= R || b >= R))) continue;
+    double v = 0.0;
+    for (int w = 0; w < kConsumerWarps; ++w) v += red[w * kNmfSlots + i];
+    p.partials[static_cast<size_t>(blockIdx.x) * kNmfSlots + i] = v;
+  }
+  for (int q = 0; q < p.nfk; ++q)
+    for (int i = tid; i < p.nhot[q] * R; i += kConsumerThreads) {
+      const int slot = i / R, j = i % R;
+      const double v = hot[(q * kNmfHot + slot) * kNmfMaxR + j];
+      if (v != 0.0) red_add(p.bins[q] + static_cast<int64_t>(p.hot_key[q][slot]) * R + j, v);
+    }
+}
+
+// ttw[c, j] (c < d_S) and cpw = WᵀW from the per-CTA partials, CTAs in order: a warp per
+// output (lanes over CTAs, fixed xor tree); WᵀW from its upper triangle, mirrored exactly.
+__global__ void nmf_reduce_kernel(const double* __restrict__ partials, int nb, int d, int r, double* ttw,
+                                  double* cpw) {
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nsw = d * r;
+  if (e < nsw) {
+    const int c = e / r, j = e % r;
+    const double v = warp_sum_strided(partials + c * kNmfMaxR + j, nb, kNmfSlots);
+    if ((threadIdx.x & 31) == 0) ttw[c * r + j] = v;
+  } else if (e < nsw + r * r) {
+    const int a = (e - nsw) / r, b = (e - nsw) % r;
+    if (a > b) return;
+    const double v = warp_sum_strided(partials + kNmfMaxD * kNmfMaxR + a * kNmfMaxR + b, nb, kNmfSlots);
+    if ((threadIdx.x & 31) == 0) {
+      cpw[a * r + b] = v;
+      cpw[b * r + a] = v;
+    }
+  }
+}
+
+template <int R, bool CG>
+static cudaError_t launch_nmf_cfg(const NmfPass& p, cudaStream_t st, int num_sms) {
+  constexpr int NT = (R + 7) / 8;
+  const int tile_rows = kConsumerWarps * 32;
+  StreamSet ss{};
+  ss.count = 2 + p.nfk;
+  ss.base[0] = reinterpret_cast<const char*>(p.s);
+  ss.row_bytes[0] = static_cast<uint32_t>(p.d) * 8u;
+  ss.base[1] = reinterpret_cast<const char*>(p.w);
+  ss.row_bytes[1] = static_cast<uint32_t>(R) * 8u;
+  for (int q = 0; q < p.nfk; ++q) {
+    ss.base[2 + q] = reinterpret_cast<const char*>(p.fk[q]);
+    ss.row_bytes[2 + q] = 4u;
+    ss.gkeys[q] = p.fk[q];
+    ss.gbase[q] = reinterpret_cast<const char*>(p.z[q]);
+    ss.grow_bytes[q] = static_cast<uint32_t>(p.zst) * 8u;
+  }
+  ss.ngather = p.nfk;
+  for (int i = 0; i < ss.count; ++i) ss.pitch[i] = ss.row_bytes[i];
+  stream_layout(ss, tile_rows, p.n);
+  const size_t head = nmf_head_bytes((p.d + 3) / 4, NT, p.nfk);
+  const size_t budget = 224 * 1024;
+  int stages = static_cast<int>((budget - head - kRingHeader) / ss.stage_bytes);
+  if (stages > 8) stages = 8;
+  if (stages < 2) return cudaErrorNotSupported;
+  // the per-CTA reduction reuses the ring memory
+  if (static_cast<size_t>(stages) * ss.stage_bytes < static_cast<size_t>(kConsumerWarps) * kNmfSlots * 8)
+    return cudaErrorNotSupported;
+  const size_t smem = head + kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes;
+  auto kern = nmf_wpass_kernel<R, CG>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (p.n + tile_rows - 1) / tile_rows;
+  const int grid = grid_for(ntiles, 1, 1, num_sms);
+  kern<<<grid, kRingThreads, smem, st>>>(p, ss, stages, tile_rows);
+  FB_LAUNCHED();
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int nout = p.d * R + R * R;
+  nmf_reduce_kernel<<<(nout + 7) / 8, 256, 0, st>>>(p.partials, grid, p.d, R, p.ttw_s, p.cpw);
+  FB_LAUNCHED();
+  return cudaGetLastError();
+}
+
+template <bool CG>
+static cudaError_t launch_nmf_r(const NmfPass& p, cudaStream_t st, int num_sms) {
+  switch (p.r) {
+#define FB_NMF_R(RR) \
+  case RR:           \
+    return launch_nmf_cfg<RR, CG>(p, st, num_sms);
+    FB_NMF_R(1) FB_NMF_R(2) FB_NMF_R(3) FB_NMF_R(4) FB_NMF_R(5) FB_NMF_R(6) FB_NMF_R(7) FB_NMF_R(8)
+    FB_NMF_R(9) FB_NMF_R(10) FB_NMF_R(11) FB_NMF_R(12) FB_NMF_R(13) FB_NMF_R(14) FB_NMF_R(15) FB_NMF_R(16)
+#undef FB_NMF_R
+    default:
+      return cudaErrorNotSupported;
+  }
+}
+
+cudaError_t launch_nmf_wpass(const NmfPass& p, cudaStream_t st, int num_sms) {
+  if (!nmf_pass_supported(p.d, p.r, p.nfk) || p.n <= 0) return cudaErrorNotSupported;
+  size_t zmax = 0;
+  for (int q = 0; q < p.nfk; ++q) zmax = p.ztable_bytes[q] > zmax ? p.ztable_bytes[q] : zmax;
+  return zmax > (32u << 20) ? launch_nmf_r<true>(p, st, num_sms) : launch_nmf_r<false>(p, st, num_sms);
+}
+
+}  // namespace fb

@@ -189,10 +189,40 @@ struct KmPass {
 bool kmeans_pass_supported(int d_s, int k, int nfk);
 size_t kmeans_pass_partials_doubles(int num_sms);
 cudaError_t launch_kmeans_pass(const KmPass& p, cudaStream_t st, int num_sms);
+// One fused pass over S per GNMF W step (fb_gnmf.cu): th = T·H, the W update in place,
+// SᵀW, WᵀW and the K_qᵀW bins of the updated W.
+struct NmfPass {
+  const double* s;  // n × d (d <= 32)
+  int64_t n;
+  int d;
+  double* w;          // n × r, updated in place
+  int r;              // <= 16
+  const double* h;    // H[0:d, :] (d × r)
+  const double* cph;  // HᵀH, r × r
+  double eps;
+  int nfk;            // >= 1
+  const int32_t* fk[kMaxParts];
+  const double* z[kMaxParts];  // R_q·H_q, n_R,q × zst
+  size_t ztable_bytes[kMaxParts];
+  int zst;
+  double* bins[kMaxParts];     // n_R,q × r, zeroed by the caller
+  const int16_t* hot_slot[kMaxParts];
+  const int32_t* hot_key[kMaxParts];
+  int nhot[kMaxParts];         // <= 64
+  double* partials;            // nmf_pass_partials_doubles
+  double* ttw_s;               // SᵀW (d × r)
+  double* cpw;                 // WᵀW (r × r)
+};
+bool nmf_pass_supported(int d_s, int r, int nfk);
+size_t nmf_pass_partials_doubles(int num_sms);
+cudaError_t launch_nmf_wpass(const NmfPass& p, cudaStream_t st, int num_sms);
 // out(c, j) = Σ_r R[r, c]·H[r, j], H int32 n × nx (d_r <= 64, nx <= 16), FP64 tensor cores
 bool rth_supported(int d_r, int nx);
 size_t rth_partials_doubles(int num_sms);
 cudaError_t launch_rth(const double* r, int64_t n, int d_r, const int32_t* h, int nx, double* out, int64_t o_rs,
+                       int64_t o_cs, double* partials, unsigned* counter, cudaStream_t st, int num_sms);
+// same, f64 weights
+cudaError_t launch_rth(const double* r, int64_t n, int d_r, const double* h, int nx, double* out, int64_t o_rs,
                        int64_t o_cs, double* partials, unsigned* counter, cudaStream_t st, int num_sms);
 size_t onehot_partials_doubles(int d, int k, int num_sms);
 cudaError_t launch_onehot_colsum(const double* s, int64_t n, int d, const int32_t* assign, int k, double* partials,

@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) kmeans_pass_kernel(KmPass p, 
           for (int mt = 0; mt < MT; ++mt) {
             const double a = on ? A[8 * mt * pitch + 4 * s] : 0.0;
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) dmma_8x8x4_sched(acc[mt][nt][0], acc[mt][nt][1], a, bf[s][nt]);
+            for (int nt = 0; nt < 2; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a, bf[s][nt]);
           }
         }
       }
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) kmeans_pass_kernel(KmPass p, 
           for (int mt2 = 0; mt2 < 2; ++mt2) {
             const double a = ar == g + 8 * mt2 ? 1.0 : 0.0;
 #pragma unroll
-            for (int nt = 0; nt < NT2; ++nt) dmma_8x8x4_sched(sta[mt2][nt][0], sta[mt2][nt][1], a, b[nt]);
+            for (int nt = 0; nt < NT2; ++nt) dmma_8x8x4(sta[mt2][nt][0], sta[mt2][nt][1], a, b[nt]);
           }
         }
       }
@@ -354,9 +354,9 @@ cudaError_t launch_kmeans_pass(const KmPass& p, cudaStream_t st, int num_sms) {
 size_t rth_partials_doubles(int num_sms) { return static_cast<size_t>(num_sms) * kConsumerWarps * 64 * 16; }
 bool rth_supported(int d_r, int nx) { return d_r >= 1 && d_r <= 64 && nx >= 1 && nx <= 16; }
 
-template <int MTR, int RPW>
+template <int MTR, int RPW, typename WT>
 __global__ void __launch_bounds__(kRingThreads, 1) rth_kernel(const double* __restrict__ rr, int64_t n, int d_r,
-                                                          const int32_t* __restrict__ h, int nx, double* out,
+                                                          const WT* __restrict__ h, int nx, double* out,
                                                           int64_t o_rs, int64_t o_cs, double* partials,
                                                           StreamSet ss, int stages, int tile_rows) {
   extern __shared__ __align__(128) char smem[];
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) rth_kernel(const double* __re
     const int cur = ring.acquire(ss, kt);
     const int rows = ring.rows_of(ring.tile_begin + kt);
     const double* R = reinterpret_cast<const double*>(ring.stage_ptr(cur, ss, 0));
-    const int32_t* H = reinterpret_cast<const int32_t*>(ring.stage_ptr(cur, ss, 1));
+    const WT* H = reinterpret_cast<const WT*>(ring.stage_ptr(cur, ss, 1));
     __syncwarp();
     if (wrow < rows) {
       const bool full = wrow + RPW <= rows;
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) rth_kernel(const double* __re
         for (int mt = 0; mt < MTR; ++mt) {
           const double a = live ? R[rl * d_r + 8 * mt + g] : 0.0;  // columns >= d_r only feed discarded rows
 #pragma unroll
-          for (int nt = 0; nt < 2; ++nt) dmma_8x8x4_sched(acc[mt][nt][0], acc[mt][nt][1], a, b[nt]);
+          for (int nt = 0; nt < 2; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a, b[nt]);
         }
       }
     }
@@ -432,8 +432,8 @@ __global__ void rth_reduce_kernel(const double* __restrict__ partials, int nb, i
   if ((threadIdx.x & 31) == 0) out[c * o_rs + j * o_cs] = v;
 }
 
-template <int MTR, int RPW>
-static cudaError_t launch_rth_rpw(const double* r, int64_t n, int d_r, const int32_t* h, int nx, double* out,
+template <int MTR, int RPW, typename WT>
+static cudaError_t launch_rth_rpw(const double* r, int64_t n, int d_r, const WT* h, int nx, double* out,
                                  int64_t o_rs, int64_t o_cs, double* partials, unsigned* counter, cudaStream_t st,
                                  int num_sms) {
   const int tile_rows = kConsumerWarps * RPW;
@@ -442,14 +442,14 @@ static cudaError_t launch_rth_rpw(const double* r, int64_t n, int d_r, const int
   ss.base[0] = reinterpret_cast<const char*>(r);
   ss.row_bytes[0] = ss.pitch[0] = static_cast<uint32_t>(d_r) * 8u;
   ss.base[1] = reinterpret_cast<const char*>(h);
-  ss.row_bytes[1] = ss.pitch[1] = static_cast<uint32_t>(nx) * 4u;
+  ss.row_bytes[1] = ss.pitch[1] = static_cast<uint32_t>(nx * sizeof(WT));
   stream_layout(ss, tile_rows, n);
   const size_t budget = 200 * 1024;
   int stages = static_cast<int>((budget - kRingHeader) / ss.stage_bytes);
   if (stages > 8) stages = 8;
   if (stages < 2) return cudaErrorNotSupported;
   const size_t smem = kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes;
-  auto kern = rth_kernel<MTR, RPW>;
+  auto kern = rth_kernel<MTR, RPW, WT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   (void)counter;
@@ -466,17 +466,18 @@ static cudaError_t launch_rth_rpw(const double* r, int64_t n, int d_r, const int
 }
 
 // 32 rows per warp while a 256-row stage stays <= 64 KB (three stages in flight), else 16
-template <int MTR>
-static cudaError_t launch_rth_mt(const double* r, int64_t n, int d_r, const int32_t* h, int nx, double* out,
+template <int MTR, typename WT>
+static cudaError_t launch_rth_mt(const double* r, int64_t n, int d_r, const WT* h, int nx, double* out,
                                  int64_t o_rs, int64_t o_cs, double* partials, unsigned* counter, cudaStream_t st,
                                  int num_sms) {
-  if (256 * (8 * d_r + 4 * nx) <= 64 * 1024)
-    return launch_rth_rpw<MTR, 32>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
-  return launch_rth_rpw<MTR, 16>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
+  if (256 * (8 * d_r + static_cast<int>(sizeof(WT)) * nx) <= 64 * 1024)
+    return launch_rth_rpw<MTR, 32, WT>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
+  return launch_rth_rpw<MTR, 16, WT>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
 }
 
-cudaError_t launch_rth(const double* r, int64_t n, int d_r, const int32_t* h, int nx, double* out, int64_t o_rs,
-                       int64_t o_cs, double* partials, unsigned* counter, cudaStream_t st, int num_sms) {
+template <typename WT>
+static cudaError_t launch_rth_t(const double* r, int64_t n, int d_r, const WT* h, int nx, double* out, int64_t o_rs,
+                                int64_t o_cs, double* partials, unsigned* counter, cudaStream_t st, int num_sms) {
   if (!rth_supported(d_r, nx)) return cudaErrorNotSupported;
   if (n <= 0) {
     for (int c = 0; c < d_r; ++c)
@@ -487,16 +488,26 @@ cudaError_t launch_rth(const double* r, int64_t n, int d_r, const int32_t* h, in
     return cudaSuccess;
   }
   switch ((d_r + 7) / 8) {
-    case 1: return launch_rth_mt<1>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
-    case 2: return launch_rth_mt<2>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
-    case 3: return launch_rth_mt<3>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
-    case 4: return launch_rth_mt<4>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
-    case 5: return launch_rth_mt<5>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
-    case 6: return launch_rth_mt<6>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
-    case 7: return launch_rth_mt<7>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
-    case 8: return launch_rth_mt<8>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
+    case 1: return launch_rth_mt<1, WT>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
+    case 2: return launch_rth_mt<2, WT>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
+    case 3: return launch_rth_mt<3, WT>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
+    case 4: return launch_rth_mt<4, WT>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
+    case 5: return launch_rth_mt<5, WT>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
+    case 6: return launch_rth_mt<6, WT>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
+    case 7: return launch_rth_mt<7, WT>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
+    case 8: return launch_rth_mt<8, WT>(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
     default: return cudaErrorNotSupported;
   }
+}
+
+cudaError_t launch_rth(const double* r, int64_t n, int d_r, const int32_t* h, int nx, double* out, int64_t o_rs,
+                       int64_t o_cs, double* partials, unsigned* counter, cudaStream_t st, int num_sms) {
+  return launch_rth_t(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
+}
+
+cudaError_t launch_rth(const double* r, int64_t n, int d_r, const double* h, int nx, double* out, int64_t o_rs,
+                       int64_t o_cs, double* partials, unsigned* counter, cudaStream_t st, int num_sms) {
+  return launch_rth_t(r, n, d_r, h, nx, out, o_rs, o_cs, partials, counter, st, num_sms);
 }
 
 }  // namespace fb

@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_dmma_zinit_kernel(LmmArgs
         for (int mt = 0; mt < MT; ++mt) {
           const double a = on ? A[8 * mt * pitch + 4 * s] : 0.0;
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma_8x8x4_sched(acc[mt][nt][0], acc[mt][nt][1], a, bf[s][nt]);
+          for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a, bf[s][nt]);
         }
       }
       double* o = p.out + (tile * tile_rows + wrow + g) * p.ldo + 2 * t;

@@ -29,10 +29,10 @@ elif which == "c4":
     nm = fb.build_star(s, [(k1, r1), (k2, r2)])
     fn = lambda: fb.kmeans(nm, fb.TrainConfig(iterations=5, k=10))
 elif which == "c5":
-    n_s, n_r = 5_000_000, 50_000
-    s = torch.rand(n_s, 10, dtype=torch.float64, device=dev, generator=g)
-    r = torch.rand(n_r, 40, dtype=torch.float64, device=dev, generator=g)
-    nm = fb.build_pkfk(s, bench.zipf_keys_dev(n_s, n_r, 1.2, g, dev), r)
+    import workloads as W
+    gg = W.generate("c5")  # the seeded NumPy c5 inputs (Zipf(1.2) keys)
+    (fk, r), = W.keys_1based(gg["parts"])
+    nm = fb.build_pkfk(torch.from_numpy(gg["s"]).to(dev), torch.from_numpy(fk).to(dev), torch.from_numpy(r).to(dev))
     fn = lambda: fb.gnmf(nm, fb.TrainConfig(iterations=5, r=5))
 else:
     rng = np.random.default_rng(1)
