@@ -259,6 +259,34 @@ int fb_scalar_map(const double* in, double* out, int64_t n, int32_t op, double x
                   fb_stream_t stream);
 int fb_unary_map(const double* in, double* out, int64_t n, int32_t fn, fb_stream_t stream);
 
+/* ---- dense / sparse pieces of the rest of the operator surface ---- */
+/* C[m x n] (+)= op(A)·op(B) on the FP64 tensor cores, row-major; op(A)[i][k] = ta ? A[k*lda+i]
+ * : A[i*lda+k], op(B)[k][j] = tb ? B[j*ldb+k] : B[k*ldb+j]. The block products of
+ * gram_transposed / dmm / dmm_gram (rewrite.py:301-446; kernel.py:110-121 dense @). */
+int fb_dense_mm(int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, int32_t ta, const double* b,
+                int64_t ldb, int32_t tb, double* c, int64_t ldc, int32_t accumulate, fb_stream_t stream);
+/* c[i, j] += mat[ra[i], cb ? cb[j] : j]: the two-sided indicator expansion E_a M E_b^T of a block
+ * product (rewrite.py:308-313, 436-444). */
+int fb_gather2_add(int64_t m, int64_t n, const double* mat, int64_t ldm, const int32_t* ra, const int32_t* cb,
+                   double* c, int64_t ldc, fb_stream_t stream);
+/* out[tgt[i], :] += a[i, :] (out: out_rows x d, zeroed here): E^T a (indicator.py:107-118). */
+int fb_scatter_rows(int64_t n, int32_t d, const int32_t* tgt, const double* a, int64_t lda, double* out,
+                    int64_t out_rows, fb_stream_t stream);
+/* E_a^T E_b as CSR counts (indicator.py:144-162): indptr[rows_a + 1], col / val with capacity n,
+ * *nnz (device int64) = stored entries, columns ascending within a row. */
+size_t fb_pair_counts_workspace_bytes(int64_t n);
+int fb_pair_counts(int64_t n, const int32_t* ta, const int32_t* tb, int64_t rows_a, int64_t cols_b, int64_t* indptr,
+                   int64_t* col, double* val, int64_t* nnz, void* ws, size_t ws_bytes, fb_stream_t stream);
+/* y (+)= P·x for a CSR P (rows x ?, int64 indptr, int32 or int64 column indices, f64 values):
+ * scipy's csr @ dense (kernel.py:110-121, the sparse factor products). */
+int fb_csr_spmm(int64_t rows, const int64_t* indptr, const void* col, int32_t col_is64, const double* val,
+                const double* x, int64_t ldx, int32_t k, double* y, int64_t ldy, int32_t accumulate,
+                fb_stream_t stream);
+/* y = P^T·x for a CSR P (rows x cols): y is cols x k, zeroed here (kernel.py:141-148 csr.T @). */
+int fb_csr_spmm_t(int64_t rows, int64_t cols, const int64_t* indptr, const void* col, int32_t col_is64,
+                  const double* val, const double* x, int64_t ldx, int32_t k, double* y, int64_t ldy,
+                  fb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -109,6 +109,13 @@ _SIGS = {
     "fb_small_gram": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "fb_nmf_objective": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp]),
     "fb_mirror_upper": (c_i32, [c_vp, c_i64, c_vp]),
+    "fb_dense_mm": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp]),
+    "fb_gather2_add": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "fb_scatter_rows": (c_i32, [c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
+    "fb_pair_counts_workspace_bytes": (c_size, [c_i64]),
+    "fb_pair_counts": (c_i32, [c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "fb_csr_spmm": (c_i32, [c_i64, c_vp, c_vp, c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp]),
+    "fb_csr_spmm_t": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),
     "fb_scalar_map": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_f64, c_vp]),
     "fb_unary_map": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp]),
 }

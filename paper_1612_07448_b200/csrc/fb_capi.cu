@@ -1179,4 +1179,58 @@ int fb_unary_map(const double* in, double* out, int64_t n, int32_t fn, fb_stream
   return cuda_status(fb::launch_unary_map(in, out, n, fn, cs(stream), g_num_sms), "unary_map");
 }
 
+// ------------------------------------------------------------------ dense / sparse pieces (fb_dense.cu)
+int fb_dense_mm(int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, int32_t ta, const double* b,
+                int64_t ldb, int32_t tb, double* c, int64_t ldc, int32_t accumulate, fb_stream_t stream) {
+  if (m < 0 || n < 0 || k < 0 || ldc < n) return fail(FB_ERR_SHAPE, "dense_mm: bad shape");
+  if ((m > 0 && n > 0) && (!c || (k > 0 && (!a || !b)))) return fail(FB_ERR_ARG, "dense_mm: NULL pointer");
+  return cuda_status(fb::launch_dense_mm(m, n, k, a, lda, ta, b, ldb, tb, c, ldc, accumulate, cs(stream)), "dense_mm");
+}
+
+int fb_gather2_add(int64_t m, int64_t n, const double* mat, int64_t ldm, const int32_t* ra, const int32_t* cb,
+                   double* c, int64_t ldc, fb_stream_t stream) {
+  if (m < 0 || n < 0 || ldc < n) return fail(FB_ERR_SHAPE, "gather2_add: bad shape");
+  if (m > 0 && n > 0 && (!mat || !ra || !c)) return fail(FB_ERR_ARG, "gather2_add: NULL pointer");
+  return cuda_status(fb::launch_gather2_add(m, n, mat, ldm, ra, cb, c, ldc, cs(stream), g_num_sms), "gather2_add");
+}
+
+int fb_scatter_rows(int64_t n, int32_t d, const int32_t* tgt, const double* a, int64_t lda, double* out,
+                    int64_t out_rows, fb_stream_t stream) {
+  if (n < 0 || d < 0 || out_rows < 0) return fail(FB_ERR_SHAPE, "scatter_rows: bad shape");
+  if ((n > 0 && d > 0 && (!tgt || !a)) || (out_rows > 0 && d > 0 && !out)) return fail(FB_ERR_ARG, "scatter_rows: NULL pointer");
+  return cuda_status(fb::launch_scatter_rows(n, d, tgt, a, lda, out, out_rows, cs(stream), g_num_sms), "scatter_rows");
+}
+
+size_t fb_pair_counts_workspace_bytes(int64_t n) { return fb::pair_counts_workspace_bytes(n); }
+
+int fb_pair_counts(int64_t n, const int32_t* ta, const int32_t* tb, int64_t rows_a, int64_t cols_b, int64_t* indptr,
+                   int64_t* col, double* val, int64_t* nnz, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  if (n < 0 || rows_a < 0 || cols_b < 0) return fail(FB_ERR_SHAPE, "pair_counts: bad shape");
+  if (!indptr || !nnz || (n > 0 && (!ta || !tb || !col || !val))) return fail(FB_ERR_ARG, "pair_counts: NULL pointer");
+  if (ws_bytes < fb::pair_counts_workspace_bytes(n)) return fail(FB_ERR_ARG, "pair_counts: workspace too small");
+  return cuda_status(fb::launch_pair_counts(n, ta, tb, rows_a, cols_b, indptr, col, val, nnz, ws, ws_bytes, cs(stream),
+                                            g_num_sms),
+                     "pair_counts");
+}
+
+int fb_csr_spmm(int64_t rows, const int64_t* indptr, const void* col, int32_t col_is64, const double* val,
+                const double* x, int64_t ldx, int32_t k, double* y, int64_t ldy, int32_t accumulate,
+                fb_stream_t stream) {
+  if (rows < 0 || k < 0 || ldy < k) return fail(FB_ERR_SHAPE, "csr_spmm: bad shape");
+  if (rows > 0 && k > 0 && (!indptr || !y)) return fail(FB_ERR_ARG, "csr_spmm: NULL pointer");
+  return cuda_status(fb::launch_csr_spmm(rows, indptr, col, col_is64, val, x, ldx, k, y, ldy, accumulate, cs(stream),
+                                         g_num_sms),
+                     "csr_spmm");
+}
+
+int fb_csr_spmm_t(int64_t rows, int64_t cols, const int64_t* indptr, const void* col, int32_t col_is64,
+                  const double* val, const double* x, int64_t ldx, int32_t k, double* y, int64_t ldy,
+                  fb_stream_t stream) {
+  if (rows < 0 || cols < 0 || k < 0 || ldy < k) return fail(FB_ERR_SHAPE, "csr_spmm_t: bad shape");
+  if (cols > 0 && k > 0 && !y) return fail(FB_ERR_ARG, "csr_spmm_t: NULL pointer");
+  return cuda_status(fb::launch_csr_spmm_t(rows, cols, indptr, col, col_is64, val, x, ldx, k, y, ldy, cs(stream),
+                                           g_num_sms),
+                     "csr_spmm_t");
+}
+
 }  // extern "C"

@@ -236,4 +236,22 @@ cudaError_t launch_nmf_objective(const double* sum_t2, const double* ttw, const 
                                  const double* cpw, const double* cph, int rr, double* trace, int it,
                                  cudaStream_t st);
 
+// fb_dense.cu -----------------------------------------------------------------------
+cudaError_t launch_dense_mm(int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, int ta, const double* b,
+                            int64_t ldb, int tb, double* c, int64_t ldc, int accumulate, cudaStream_t st);
+cudaError_t launch_gather2_add(int64_t m, int64_t n, const double* mat, int64_t ldm, const int32_t* ra,
+                               const int32_t* cb, double* c, int64_t ldc, cudaStream_t st, int num_sms);
+cudaError_t launch_scatter_rows(int64_t n, int d, const int32_t* tgt, const double* a, int64_t lda, double* out,
+                                int64_t out_rows, cudaStream_t st, int num_sms);
+size_t pair_counts_workspace_bytes(int64_t n);
+cudaError_t launch_pair_counts(int64_t n, const int32_t* ta, const int32_t* tb, int64_t rows_a, int64_t cols_b,
+                               int64_t* indptr, int64_t* col, double* val, int64_t* nnz, void* ws, size_t ws_bytes,
+                               cudaStream_t st, int num_sms);
+cudaError_t launch_csr_spmm(int64_t rows, const int64_t* indptr, const void* col, int col_is64, const double* val,
+                            const double* x, int64_t ldx, int k, double* y, int64_t ldy, int accumulate,
+                            cudaStream_t st, int num_sms);
+cudaError_t launch_csr_spmm_t(int64_t rows, int64_t cols, const int64_t* indptr, const void* col, int col_is64,
+                              const double* val, const double* x, int64_t ldx, int k, double* y, int64_t ldy,
+                              cudaStream_t st, int num_sms);
+
 }  // namespace fb

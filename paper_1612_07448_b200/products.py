@@ -1,29 +1,34 @@
 """Row-Gram, pseudo-inverse, double multiplication and non-factorizable element-wise ops.
 
 The rest of the reference's operator surface (rewrite.py:301-470, indicator.py:144-162;
-SURVEY §8(f) row 3), on the device:
+SURVEY §8(f) row 3), on the library's own sm_100a kernels (fb_dense.cu + the factorized
+operators):
 
 ==========================  =====================================  ==========================
 operator                    reference                              device composition
 ==========================  =====================================  ==========================
-``gram_transposed``         rewrite.py:301-315                     per block F·Fᵀ (DGEMM) +
-                                                                   two-sided row gather
+``gram_transposed``         rewrite.py:301-315                     per block F·Fᵀ (fb_dense_mm,
+                                                                   DMMA) + two-sided row
+                                                                   gather (fb_gather2_add)
 ``ginv``                    rewrite.py:318-333                     crossprod / gram_transposed,
                                                                    host SVD pinv of the small
                                                                    Gram, then rmm / lmm
 ``dmm``                     rewrite.py:349-389                     A·B = lmm(A, B materialised):
                                                                    B has only d_A rows
-``dmm_gram``                rewrite.py:392-446                     block products (DGEMM) +
-                                                                   keyed scatters / gathers
+``dmm_gram``                rewrite.py:392-446                     block products (fb_dense_mm)
+                                                                   + Eᵀa scatters
+                                                                   (fb_scatter_rows), the pair
+                                                                   counts · R (fb_csr_spmm)
 ``elementwise_matrix_op``   rewrite.py:449-470                     materialise + map (warns)
-``pair_product``            indicator.py:144-162                   2-D target histogram (CSR)
+``pair_product``            indicator.py:144-162                   2-D target histogram: radix
+                                                                   sort + run-length encode of
+                                                                   the combined keys → CSR
+                                                                   (fb_pair_counts)
 ==========================  =====================================  ==========================
 
 These sit beside the hot path (their outputs are n×n or n×m dense, or they run once per
-model), so they are composed from the library's LMM/RMM/crossprod kernels plus cuBLAS
-DGEMMs and torch gathers/scatters on device tensors; nothing runs on the host except the
-reference's own LAPACK SVD of a d×d Gram. ``counter=`` gets the reference's tallies
-(counting rules kernel.py:7-18) reproduced step by step.
+model). Nothing runs on the host except the reference's own LAPACK SVD of a d×d Gram;
+``counter=`` gets the reference's tallies (counting rules kernel.py:7-18) step by step.
 """
 
 import warnings
@@ -66,6 +71,21 @@ def _tally_gram(counter, n, d):
         counter.tally(d * n * (n + 1) // 2, max(d - 1, 0) * n * (n + 1) // 2)
 
 
+def _dmm(m, n, k, a, lda, ta, b, ldb, tb, c, ldc, accumulate=False, a_off=0, b_off=0, c_off=0):
+    """C (+)= op(A)·op(B) on the FP64 tensor cores (fb_dense_mm); offsets in elements."""
+    so = _lib.lib()
+    _lib.check(so.fb_dense_mm(m, n, k, D.ptr(a) + 8 * a_off, lda, int(ta), D.ptr(b) + 8 * b_off, ldb, int(tb),
+                              D.ptr(c) + 8 * c_off, ldc, int(accumulate), D.stream_handle()))
+
+
+def _gather2_add(c, mat, ra, cb=None):
+    """c += mat[ra][:, cb] (cb None: all columns) — fb_gather2_add."""
+    so = _lib.lib()
+    m, n = c.shape
+    _lib.check(so.fb_gather2_add(m, n, D.ptr(mat), mat.shape[1], D.ptr(ra), D.ptr(cb) if cb is not None else 0,
+                                 D.ptr(c), n, D.stream_handle()))
+
+
 def gram_transposed(nm, counter=None):
     """``T Tᵀ`` (the Gram matrix over rows) per column block: E_i (F_i F_iᵀ) E_iᵀ (rewrite.py:301-315).
 
@@ -73,18 +93,30 @@ def gram_transposed(nm, counter=None):
     symmetric; host operands give a NumPy result.
     """
     base = nm.untransposed()
+    n = base.shape[0]
     out = None
     for e, f in base.blocks:
-        g = _mirror(torch.mm(f, f.t()))  # cuBLAS DGEMM on the (small) factor
-        _tally_gram(counter, f.shape[0], f.shape[1])
-        if e is not None:
-            t = e.target.to(torch.int64)
-            g = g.index_select(0, t).index_select(1, t)
-        if out is None:
-            out = g
-        else:
+        f = f.contiguous()
+        nf, d = f.shape
+        _tally_gram(counter, nf, d)
+        g = torch.empty((nf, nf), dtype=torch.float64, device=f.device)
+        _dmm(nf, nf, d, f, d, False, f, d, True, g, nf)  # F·Fᵀ on the tensor cores
+        g = _mirror(g)
+        if e is None:
+            if out is None:
+                out = g
+                continue
             out = out + g
-            K.tally_accumulate(counter, out.numel())
+        else:
+            if out is None:
+                out = torch.zeros((n, n), dtype=torch.float64, device=f.device)
+                first = True
+            else:
+                first = False
+            _gather2_add(out, g, e.target, e.target)  # out += g[t][:, t]
+            if first:
+                continue
+        K.tally_accumulate(counter, out.numel())
     return D.to_like(out, nm.host_io)
 
 
@@ -180,9 +212,24 @@ def _as_dev(x):
 
 
 def _compress(e, a):
-    """Eᵀ a: scatter-add rows of a into the target buckets (indicator.py:107-118)."""
-    out = torch.zeros((e.cols, a.shape[1]), dtype=torch.float64, device=a.device)
-    return out.index_add_(0, e.target.to(torch.int64), a)
+    """Eᵀ a: scatter-add rows of a into the target buckets (indicator.py:107-118) — fb_scatter_rows."""
+    so = _lib.lib()
+    a = a.contiguous()
+    out = torch.empty((e.cols, a.shape[1]), dtype=torch.float64, device=a.device)
+    _lib.check(so.fb_scatter_rows(a.shape[0], a.shape[1], D.ptr(e.target), D.ptr(a), a.shape[1], D.ptr(out), e.cols,
+                                  D.stream_handle()))
+    return out
+
+
+def _spmm(p, x):
+    """P·x for the device CSR counts of :func:`pair_product` (fb_csr_spmm)."""
+    so = _lib.lib()
+    x = x.contiguous()
+    rows = p.shape[0]
+    y = torch.empty((rows, x.shape[1]), dtype=torch.float64, device=x.device)
+    _lib.check(so.fb_csr_spmm(rows, D.ptr(p.crow_indices()), D.ptr(p.col_indices()), 1, D.ptr(p.values()), D.ptr(x),
+                              x.shape[1], x.shape[1], D.ptr(y), x.shape[1], 0, D.stream_handle()))
+    return y
 
 
 def dmm_gram(a, b, form, counter=None):
@@ -192,75 +239,84 @@ def dmm_gram(a, b, form, counter=None):
     if a.transposed or b.transposed:
         raise ShapeError("dmm_gram operands carry no transpose flag; the form selects it")
     host = a.host_io
-    s_a, k_a, r_a = a.s, a.k, a.r
-    s_b, k_b, r_b = b.s, b.k, b.r
+    s_a, k_a, r_a = a.s.contiguous(), a.k, a.r.contiguous()
+    s_b, k_b, r_b = b.s.contiguous(), b.k, b.r.contiguous()
     d_sa, d_sb = s_a.shape[1], s_b.shape[1]
+    d_ra, d_rb = r_a.shape[1], r_b.shape[1]
+    dev = s_a.device
     if form == "atb":
         if a.shape[0] != b.shape[0]:
             raise ShapeError(f"dmm_gram A'B: row counts differ ({a.shape[0]} vs {b.shape[0]})")
         n = a.shape[0]
-        p = pair_product(k_a, k_b, counter)  # E_Aᵀ E_B, sparse CSR on the device
-        top_left = s_a.t() @ s_b
+        p = pair_product(k_a, k_b, counter)  # E_Aᵀ E_B, CSR counts on the device
+        out = torch.empty((d_sa + d_ra, d_sb + d_rb), dtype=torch.float64, device=dev)
+        ld = d_sb + d_rb
+        _dmm(d_sa, d_sb, n, s_a, d_sa, True, s_b, d_sb, False, out, ld)  # top left: S_Aᵀ S_B
         _tally_mm(counter, d_sa, n, d_sb)
         cb = _compress(k_b, s_a)
         if counter is not None:
             counter.tally(0, n * d_sa)
-        top_right = cb.t() @ r_b
-        _tally_mm(counter, d_sa, k_b.cols, r_b.shape[1])
+        _dmm(d_sa, d_rb, k_b.cols, cb, d_sa, True, r_b, d_rb, False, out, ld, c_off=d_sb)  # (E_Bᵀ S_A)ᵀ R_B
+        _tally_mm(counter, d_sa, k_b.cols, d_rb)
         ca = _compress(k_a, s_b)
         if counter is not None:
             counter.tally(0, n * d_sb)
-        bot_left = r_a.t() @ ca
-        _tally_mm(counter, r_a.shape[1], k_a.cols, d_sb)
-        mid = torch.sparse.mm(p, r_b)
+        _dmm(d_ra, d_sb, k_a.cols, r_a, d_ra, True, ca, d_sb, False, out, ld, c_off=d_sa * ld)  # R_Aᵀ (E_Aᵀ S_B)
+        _tally_mm(counter, d_ra, k_a.cols, d_sb)
+        mid = _spmm(p, r_b)
         if counter is not None:
             nnz = p._nnz()
-            counter.tally(nnz * r_b.shape[1], max(nnz - k_a.cols, 0) * r_b.shape[1])
-        bot_right = r_a.t() @ mid
-        _tally_mm(counter, r_a.shape[1], k_a.cols, r_b.shape[1])
-        out = torch.cat([torch.cat([top_left, top_right], 1), torch.cat([bot_left, bot_right], 1)], 0)
-        return D.to_like(out.contiguous(), host)
+            counter.tally(nnz * d_rb, max(nnz - k_a.cols, 0) * d_rb)
+        _dmm(d_ra, d_rb, k_a.cols, r_a, d_ra, True, mid, d_rb, False, out, ld, c_off=d_sa * ld + d_sb)
+        _tally_mm(counter, d_ra, k_a.cols, d_rb)
+        return D.to_like(out, host)
     if form == "abt":
         if a.shape[1] != b.shape[1]:
             raise ShapeError(f"dmm_gram AB': column counts differ ({a.shape[1]} vs {b.shape[1]})")
         if d_sa > d_sb:
             out = _as_dev(dmm_gram(b.device_view(), a.device_view(), "abt", counter)).t().contiguous()
             return D.to_like(out, host)
-        ta = k_a.target.to(torch.int64)
-        tb = k_b.target.to(torch.int64)
-        if d_sa == d_sb:
-            out = s_a @ s_b.t()
-            _tally_mm(counter, s_a.shape[0], d_sa, s_b.shape[0])
-            mid = r_a @ r_b.t()
-            _tally_mm(counter, r_a.shape[0], r_a.shape[1], r_b.shape[0])
-            return D.to_like((out + mid.index_select(0, ta).index_select(1, tb)).contiguous(), host)
+        n_a, n_b = s_a.shape[0], s_b.shape[0]
+        n_ra, n_rb = r_a.shape[0], r_b.shape[0]
+        out = torch.empty((n_a, n_b), dtype=torch.float64, device=dev)
+        _dmm(n_a, n_b, d_sa, s_a, d_sa, False, s_b, d_sb, True, out, n_b)  # S_A S_B1ᵀ
+        _tally_mm(counter, n_a, d_sa, n_b)
         cut = d_sb - d_sa  # S_B and R_A overlap on the middle columns
-        s_b1, s_b2 = s_b[:, :d_sa], s_b[:, d_sa:]
-        r_a1, r_a2 = r_a[:, :cut], r_a[:, cut:]
-        out = s_a @ s_b1.t()
-        _tally_mm(counter, s_a.shape[0], d_sa, s_b.shape[0])
-        x = r_a1 @ s_b2.t()
-        _tally_mm(counter, r_a.shape[0], cut, s_b.shape[0])
-        out = out + x.index_select(0, ta)
-        mid = r_a2 @ r_b.t()
-        _tally_mm(counter, r_a.shape[0], r_a2.shape[1], r_b.shape[0])
-        return D.to_like((out + mid.index_select(0, ta).index_select(1, tb)).contiguous(), host)
+        if cut:
+            x = torch.empty((n_ra, n_b), dtype=torch.float64, device=dev)
+            _dmm(n_ra, n_b, cut, r_a, d_ra, False, s_b, d_sb, True, x, n_b, b_off=d_sa)  # R_A1 S_B2ᵀ
+            _tally_mm(counter, n_ra, cut, n_b)
+            _gather2_add(out, x, k_a.target)
+        mid = torch.empty((n_ra, n_rb), dtype=torch.float64, device=dev)
+        _dmm(n_ra, n_rb, d_ra - cut, r_a, d_ra, False, r_b, d_rb, True, mid, n_rb, a_off=cut)  # R_A2 R_Bᵀ
+        _tally_mm(counter, n_ra, d_ra - cut, n_rb)
+        _gather2_add(out, mid, k_a.target, k_b.target)
+        return D.to_like(out, host)
     raise ValueError(f"unknown dmm_gram form {form!r} (expected 'atb' or 'abt')")
 
 
 def pair_product(ind_a, ind_b, counter=None):
-    """``E_aᵀ E_b`` as a sparse counts matrix (indicator.py:144-162): a CSR tensor on the device."""
+    """``E_aᵀ E_b`` as a sparse counts matrix (indicator.py:144-162): a CSR tensor on the device.
+
+    The combined keys t_a·n_b + t_b are radix-sorted and run-length encoded on the device
+    (fb_pair_counts); the CSR arrays are wrapped in a torch sparse tensor (a container).
+    """
     if ind_a.rows != ind_b.rows:
         raise ShapeError(f"pair_product: row counts differ ({ind_a.rows} vs {ind_b.rows})")
-    key = ind_a.target.to(torch.int64) * ind_b.cols + ind_b.target.to(torch.int64)
-    uniq, cnt = torch.unique(key, sorted=True, return_counts=True)
-    rows = uniq // ind_b.cols
-    cols = uniq % ind_b.cols
-    crow = torch.zeros(ind_a.cols + 1, dtype=torch.int64, device=key.device)
-    crow[1:] = torch.cumsum(torch.bincount(rows, minlength=ind_a.cols), 0)
+    so = _lib.lib()
+    n = ind_a.rows
+    dev = ind_a.target.device
+    indptr = torch.empty(ind_a.cols + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    val = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    nnz = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(so.fb_pair_counts_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    _lib.check(so.fb_pair_counts(n, D.ptr(ind_a.target), D.ptr(ind_b.target), ind_a.cols, ind_b.cols, D.ptr(indptr),
+                                 D.ptr(col), D.ptr(val), D.ptr(nnz), ws.data_ptr(), ws.numel(), D.stream_handle()))
     if counter is not None:
         counter.tally(0, ind_a.rows)
-    return torch.sparse_csr_tensor(crow, cols, cnt.to(torch.float64), size=(ind_a.cols, ind_b.cols))
+    k = int(nnz.item())
+    return torch.sparse_csr_tensor(indptr, col[:k].clone(), val[:k].clone(), size=(ind_a.cols, ind_b.cols))
 
 
 # ---------------------------------------------------------------------------

@@ -132,3 +132,72 @@ def test_device_drivers_on_transposed_matrix():
     _close(out.objective, G["ut_gnmf_obj"])
     with pytest.raises(fb.ShapeError):
         fb.kmeans(u.T, fb.TrainConfig(iterations=1, k=2))
+
+
+@pytest.mark.gpu
+def test_dense_sparse_primitives_vs_numpy():
+    """fb_dense_mm (all transposes, ragged sizes), fb_gather2_add, fb_scatter_rows, fb_pair_counts
+    (exact counts / CSR order), fb_csr_spmm and fb_csr_spmm_t against NumPy / SciPy."""
+    import scipy.sparse as sp
+    import torch
+
+    from paper_1612_07448_b200 import _device as D
+    from paper_1612_07448_b200 import _lib
+
+    so = _lib.lib()
+    st = D.stream_handle()
+    rng = np.random.default_rng(11)
+    dev = torch.device("cuda")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    for m, n, k in ((1, 1, 1), (37, 45, 13), (70, 9, 130), (33, 64, 4)):
+        for ta in (0, 1):
+            for tb in (0, 1):
+                a = rng.standard_normal((k, m) if ta else (m, k))
+                b = rng.standard_normal((n, k) if tb else (k, n))
+                want = (a.T if ta else a) @ (b.T if tb else b)
+                c = torch.full((m, n), 2.0, dtype=torch.float64, device=dev)
+                _lib.check(so.fb_dense_mm(m, n, k, D.ptr(T(a)), a.shape[1], ta, D.ptr(T(b)), b.shape[1], tb, D.ptr(c), n,
+                                          1, st))
+                np.testing.assert_allclose(c.cpu().numpy(), want + 2.0, rtol=1e-12, atol=1e-12)
+    mat = rng.standard_normal((17, 23))
+    ra = rng.integers(0, 17, 41).astype(np.int32)
+    cb = rng.integers(0, 23, 29).astype(np.int32)
+    c = torch.ones((41, 29), dtype=torch.float64, device=dev)
+    _lib.check(so.fb_gather2_add(41, 29, D.ptr(T(mat)), 23, D.ptr(T(ra)), D.ptr(T(cb)), D.ptr(c), 29, st))
+    np.testing.assert_array_equal(c.cpu().numpy(), 1.0 + mat[ra][:, cb])
+    a = rng.standard_normal((500, 7))
+    tgt = rng.integers(0, 31, 500).astype(np.int32)
+    out = torch.empty((31, 7), dtype=torch.float64, device=dev)
+    _lib.check(so.fb_scatter_rows(500, 7, D.ptr(T(tgt)), D.ptr(T(a)), 7, D.ptr(out), 31, st))
+    want = np.zeros((31, 7))
+    np.add.at(want, tgt, a)
+    np.testing.assert_allclose(out.cpu().numpy(), want, rtol=1e-12, atol=1e-12)
+    for n_rows, ca, cbn in ((1, 1, 1), (5000, 40, 17), (20000, 3, 900)):
+        t1 = rng.integers(0, ca, n_rows).astype(np.int32)
+        t2 = rng.integers(0, cbn, n_rows).astype(np.int32)
+        want = sp.csr_matrix((np.ones(n_rows), (t1, t2)), shape=(ca, cbn))
+        want.sum_duplicates()
+        want.sort_indices()
+        indptr = torch.empty(ca + 1, dtype=torch.int64, device=dev)
+        col = torch.empty(n_rows, dtype=torch.int64, device=dev)
+        val = torch.empty(n_rows, dtype=torch.float64, device=dev)
+        nnz = torch.zeros(1, dtype=torch.int64, device=dev)
+        ws = torch.empty(so.fb_pair_counts_workspace_bytes(n_rows), dtype=torch.uint8, device=dev)
+        _lib.check(so.fb_pair_counts(n_rows, D.ptr(T(t1)), D.ptr(T(t2)), ca, cbn, D.ptr(indptr), D.ptr(col), D.ptr(val),
+                                     D.ptr(nnz), ws.data_ptr(), ws.numel(), st))
+        k = int(nnz.item())
+        assert k == want.nnz
+        np.testing.assert_array_equal(indptr.cpu().numpy(), want.indptr)
+        np.testing.assert_array_equal(col[:k].cpu().numpy(), want.indices)
+        np.testing.assert_array_equal(val[:k].cpu().numpy(), want.data)
+    p = sp.random(300, 50, density=0.05, random_state=3, format="csr")
+    x = rng.standard_normal((50, 37))
+    y = torch.empty((300, 37), dtype=torch.float64, device=dev)
+    _lib.check(so.fb_csr_spmm(300, D.ptr(T(p.indptr.astype(np.int64))), D.ptr(T(p.indices.astype(np.int32))), 0,
+                              D.ptr(T(p.data)), D.ptr(T(x)), 37, 37, D.ptr(y), 37, 0, st))
+    np.testing.assert_allclose(y.cpu().numpy(), p @ x, rtol=1e-12, atol=1e-12)
+    xt = rng.standard_normal((300, 5))
+    yt = torch.empty((50, 5), dtype=torch.float64, device=dev)
+    _lib.check(so.fb_csr_spmm_t(300, 50, D.ptr(T(p.indptr.astype(np.int64))), D.ptr(T(p.indices.astype(np.int64))), 1,
+                                D.ptr(T(p.data)), D.ptr(T(xt)), 5, 5, D.ptr(yt), 5, st))
+    np.testing.assert_allclose(yt.cpu().numpy(), p.T @ xt, rtol=1e-12, atol=1e-12)
