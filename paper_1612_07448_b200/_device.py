@@ -6,6 +6,8 @@ become 2-D float64 row-major matrices (a 1-D vector becomes a single column), bu
 the current CUDA device.
 """
 
+import os
+
 import numpy as np
 import torch
 
@@ -58,12 +60,88 @@ def _csr_to_device(a):
     return out
 
 
+# Factor matrices at or below this density stay CSR in HBM (the north
+# star's "≤ 5 %"); denser sparse inputs are expanded (FB_CSR_DENSITY_MAX overrides).
+CSR_DENSITY_MAX = float(os.environ.get("FB_CSR_DENSITY_MAX", "0.05"))
+
+
+class CsrMatrix:
+    """A sparse factor matrix kept as CSR in HBM (the reference keeps sparse factors as CSR
+    with sorted indices, kernel.py:73-88): int64 ``indptr``, int32 ``indices``, f64 ``data``.
+
+    The factorized LMM / RMM / Tᵀ·X / rowSums / colSums read it natively (fb_csr_spmm,
+    fb_csr_spmm_t: traffic proportional to nnz); operators without a sparse kernel use
+    :meth:`dense`, a row-major expansion made once on first use (fb_csr_expand).
+    """
+
+    dtype = torch.float64
+
+    def __init__(self, host_csr):
+        m = host_csr.tocsr(copy=True).astype(np.float64)
+        m.sum_duplicates()
+        m.sort_indices()
+        self._host = m
+        self.shape = tuple(int(v) for v in m.shape)
+        self.nnz = int(m.nnz)
+        dev = device()
+        self.indptr = torch.from_numpy(m.indptr.astype(np.int64)).to(dev)
+        self.indices = torch.from_numpy(m.indices.astype(np.int32)).to(dev)
+        self.data = torch.from_numpy(np.ascontiguousarray(m.data, dtype=np.float64)).to(dev)
+        self._dense = None
+
+    @property
+    def device(self):
+        return self.indptr.device
+
+    def numel(self):
+        return self.shape[0] * self.shape[1]
+
+    def dense(self):
+        if self._dense is None:
+            self._dense = _csr_to_device(self._host)
+        return self._dense
+
+    def rows(self, idx):
+        """The CSR of the selected rows (0-based int64 indices, host or device)."""
+        idx = idx.detach().cpu().numpy() if isinstance(idx, torch.Tensor) else np.asarray(idx)
+        return CsrMatrix(self._host[idx])
+
+    def to_scipy(self):
+        return self._host.copy()
+
+    def __repr__(self):
+        return f"CsrMatrix({self.shape[0]}x{self.shape[1]}, nnz={self.nnz})"
+
+
+def is_csr(f):
+    return isinstance(f, CsrMatrix)
+
+
+def dense_of(f):
+    return f.dense() if isinstance(f, CsrMatrix) else f
+
+
+def as_factor(a):
+    """A factor matrix: :class:`CsrMatrix` for a scipy sparse input at or below
+    ``CSR_DENSITY_MAX`` density, else a dense 2-D float64 CUDA tensor (:func:`as_matrix`)."""
+    if _is_scipy_sparse(a):
+        n, d = a.shape
+        nnz = a.getnnz() if hasattr(a, "getnnz") else a.nnz
+        if n * d > 0 and nnz <= CSR_DENSITY_MAX * n * d:
+            return CsrMatrix(a)
+    if isinstance(a, CsrMatrix):
+        return a
+    return as_matrix(a)
+
+
 def as_matrix(a, dtype=torch.float64):
     """2-D contiguous float64 CUDA tensor (kernel.as_matrix semantics).
 
     scipy sparse inputs are accepted (the reference's CSR factor matrices) and expanded on
     the device.
     """
+    if isinstance(a, CsrMatrix):
+        return a.dense()
     if _is_scipy_sparse(a):
         return _csr_to_device(a)
     if isinstance(a, torch.Tensor):

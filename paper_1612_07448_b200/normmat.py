@@ -177,21 +177,42 @@ class NormalizedMatrix:
         if len(blocks) - (1 if blocks[0][0] is None else 0) > _lib.FB_MAX_PARTS:
             raise ShapeError(f"at most {_lib.FB_MAX_PARTS} indicator blocks are supported")
         self.variant = variant
-        self.blocks = blocks
+        self._raw = blocks  # factors as given: dense CUDA tensors or D.CsrMatrix
         self.transposed = bool(transposed)
         self.source_rows = tuple(source_rows) if source_rows is not None else None
         self.host_io = bool(host_io)
         self._cache = {}  # per-matrix device caches shared with the transposed view
 
+    # -- factors ----------------------------------------------------------
+    @property
+    def blocks(self):
+        """(indicator, dense factor) pairs. CSR factors (D.CsrMatrix) are expanded here, once
+        per matrix (the operators with CSR-native kernels read :attr:`raw_blocks` instead)."""
+        if not self.has_csr:
+            return self._raw
+        b = self._cache.get("dense_blocks")
+        if b is None:
+            b = tuple((e, D.dense_of(f)) for e, f in self._raw)
+            self._cache["dense_blocks"] = b
+        return b
+
+    @property
+    def raw_blocks(self):
+        return self._raw
+
+    @property
+    def has_csr(self):
+        return any(D.is_csr(f) for _, f in self._raw)
+
     # -- shape ------------------------------------------------------------
     @property
     def base_rows(self):
-        e, f = self.blocks[0]
+        e, f = self._raw[0]
         return e.rows if e is not None else f.shape[0]
 
     @property
     def device(self):
-        return self.blocks[0][1].device
+        return self._raw[0][1].device
 
     @property
     def indicator_blocks(self):
@@ -200,7 +221,7 @@ class NormalizedMatrix:
 
     @property
     def base_cols(self):
-        return sum(f.shape[1] for _, f in self.blocks)
+        return sum(f.shape[1] for _, f in self._raw)
 
     @property
     def shape(self):
@@ -208,7 +229,7 @@ class NormalizedMatrix:
         return (d, n) if self.transposed else (n, d)
 
     def col_offsets(self):
-        widths = [f.shape[1] for _, f in self.blocks]
+        widths = [f.shape[1] for _, f in self._raw]
         return np.concatenate([[0], np.cumsum(widths)]).astype(int)
 
     # -- accessors ---------------------------------------------------------
@@ -237,7 +258,7 @@ class NormalizedMatrix:
     # -- logical ops -------------------------------------------------------
     @property
     def T(self):
-        t = NormalizedMatrix(self.variant, self.blocks, not self.transposed, self.source_rows, self.host_io)
+        t = NormalizedMatrix(self.variant, self._raw, not self.transposed, self.source_rows, self.host_io)
         t._cache = self._cache
         return t
 
@@ -245,7 +266,7 @@ class NormalizedMatrix:
         """The same matrix with results returned as CUDA tensors (shares the caches)."""
         if not self.host_io:
             return self
-        v = NormalizedMatrix(self.variant, self.blocks, self.transposed, self.source_rows, False)
+        v = NormalizedMatrix(self.variant, self._raw, self.transposed, self.source_rows, False)
         v._cache = self._cache
         return v
 
@@ -387,6 +408,8 @@ def _remap_part(key, r, part_label=""):
     counts_kept = counts_kept[:n_used].clone()
     if n_used == n_r:
         r_kept = r
+    elif D.is_csr(r):
+        r_kept = r.rows(used)
     else:
         r_kept = torch.empty((n_used, r.shape[1]), dtype=torch.float64, device=dev)
         _lib.check(so.fb_gather_rows(D.ptr(r), r.shape[1], used.data_ptr(), n_used, r.shape[1],
@@ -397,8 +420,8 @@ def _remap_part(key, r, part_label=""):
 def build_pkfk(s, key_column, r):
     """PK-FK normalized matrix from S, its 1-based key column and R (normmat.py:201-214)."""
     host = D.is_host(s)
-    s = D.as_matrix(s)
-    r = D.as_matrix(r)
+    s = D.as_factor(s)
+    r = D.as_factor(r)
     key = _check_keys(key_column, r.shape[0])
     if key.numel() != s.shape[0]:
         raise ShapeError(f"key column length {key.numel()} != entity rows {s.shape[0]}")
@@ -409,11 +432,11 @@ def build_pkfk(s, key_column, r):
 def build_star(s, parts):
     """Star-schema normalized matrix: S plus ``[(key_column_i, R_i), ...]`` (normmat.py:217-237)."""
     host = D.is_host(s)
-    s = D.as_matrix(s)
+    s = D.as_factor(s)
     blocks = [(None, s)]
     source = [None]
     for idx, (key_column, r) in enumerate(parts):
-        r = D.as_matrix(r)
+        r = D.as_factor(r)
         key = _check_keys(key_column, r.shape[0], part_label=f" (part {idx})")
         if key.numel() != s.shape[0]:
             raise ShapeError(f"part {idx}: key column length {key.numel()} != entity rows {s.shape[0]}")

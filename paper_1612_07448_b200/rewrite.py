@@ -26,6 +26,7 @@ import torch
 
 from . import _device as D
 from . import _lib
+from . import csr_ops as _csr
 from . import kernel as K
 from .exceptions import NumericError, ShapeError
 from .normmat import NormalizedMatrix
@@ -146,12 +147,15 @@ def row_sums(nm, counter=None):
         return D.to_like(_as_dev(r).t().contiguous(), nm.host_io)
     so = _lib.lib()
     n = nm.base_rows
-    out = torch.empty((n, 1), dtype=torch.float64, device=nm.device)
-    cs = nm.c_struct()
-    ws = D.workspace(so.fb_row_sums_workspace_bytes(cs))
-    _lib.check(so.fb_row_sums(cs, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
+    if nm.has_csr:  # CSR factors read natively (csr_ops): T·1
+        out = _csr.lmm(nm, _csr.ones(nm.base_cols, nm.device))
+    else:
+        out = torch.empty((n, 1), dtype=torch.float64, device=nm.device)
+        cs = nm.c_struct()
+        ws = D.workspace(so.fb_row_sums_workspace_bytes(cs))
+        _lib.check(so.fb_row_sums(cs, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
     if counter is not None:
-        for i, (e, f) in enumerate(nm.blocks):
+        for i, (e, f) in enumerate(nm.raw_blocks):
             K.tally_rowsums(counter, f.shape[0], f.shape[1])
             if i > 0:
                 K.tally_accumulate(counter, n)
@@ -165,12 +169,15 @@ def col_sums(nm, counter=None):
         r = row_sums(nm.T, counter)
         return D.to_like(_as_dev(r).t().contiguous(), nm.host_io)
     so = _lib.lib()
-    out = torch.empty((1, nm.base_cols), dtype=torch.float64, device=nm.device)
-    cs = nm.c_struct()
-    ws = D.workspace(so.fb_col_sums_workspace_bytes(cs))
-    _lib.check(so.fb_col_sums(cs, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
+    if nm.has_csr:  # CSR factors read natively (csr_ops): (Tᵀ·1)ᵀ
+        out = _csr.tmm(nm, _csr.ones(nm.base_rows, nm.device)).reshape(1, -1)
+    else:
+        out = torch.empty((1, nm.base_cols), dtype=torch.float64, device=nm.device)
+        cs = nm.c_struct()
+        ws = D.workspace(so.fb_col_sums_workspace_bytes(cs))
+        _lib.check(so.fb_col_sums(cs, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
     if counter is not None:
-        for e, f in nm.blocks:
+        for e, f in nm.raw_blocks:
             if e is None:
                 K.tally_colsums(counter, f.shape[0], f.shape[1])
             else:
@@ -184,13 +191,16 @@ def sum_all(nm, counter=None):
     _nm_check(nm)
     base = nm.untransposed()
     so = _lib.lib()
-    cs = base.c_struct()
-    out = torch.empty(1, dtype=torch.float64, device=base.device)
-    d = base.base_cols
-    ws = D.workspace(so.fb_col_sums_workspace_bytes(cs) + 8 * d + 512)
-    _lib.check(so.fb_sum_all(cs, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
+    if base.has_csr:
+        out = _csr.sum_all(base)
+    else:
+        cs = base.c_struct()
+        out = torch.empty(1, dtype=torch.float64, device=base.device)
+        d = base.base_cols
+        ws = D.workspace(so.fb_col_sums_workspace_bytes(cs) + 8 * d + 512)
+        _lib.check(so.fb_sum_all(cs, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
     if counter is not None:
-        for e, f in base.blocks:
+        for e, f in base.raw_blocks:
             if e is None:
                 K.tally_rowsums(counter, f.shape[0], f.shape[1])
                 counter.tally(0, max(f.shape[0] - 1, 0))
@@ -211,6 +221,8 @@ def _as_dev(a):
 
 def _lmm_dev(nm, x, counter):
     """T·X on the untransposed matrix; x is a contiguous device matrix (d × d_x)."""
+    if nm.has_csr:
+        return _csr.lmm(nm, x, counter)
     so = _lib.lib()
     n, d_x = nm.base_rows, x.shape[1]
     out = torch.empty((n, d_x), dtype=torch.float64, device=x.device)
@@ -218,7 +230,7 @@ def _lmm_dev(nm, x, counter):
     ws = D.workspace(so.fb_lmm_workspace_bytes(cs, d_x))
     _lib.check(so.fb_lmm(cs, D.ptr(x), d_x, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
     if counter is not None:
-        for i, (e, f) in enumerate(nm.blocks):
+        for i, (e, f) in enumerate(nm.raw_blocks):
             K.tally_matmul(counter, f.shape[0], f.shape[1], d_x)
             if i > 0:
                 K.tally_accumulate(counter, n * d_x)
@@ -231,6 +243,11 @@ def _wt_dev(nm, w, w_rs, w_cs, n_w, out, o_js, o_cs, counter):
     The X·K halves run as segmented sums over the cached FK-sorted order (built on first use,
     like the reference's cached CSR of K, indicator.py:71-86).
     """
+    if nm.has_csr:  # CSR factors read natively (csr_ops): out(j, c) = (Tᵀ·W)[c, j]
+        wd = torch.as_strided(w, (nm.base_rows, n_w), (w_rs, w_cs)).contiguous()
+        res = _csr.tmm(nm, wd, counter)
+        torch.as_strided(out, (nm.base_cols, n_w), (o_cs, o_js)).copy_(res)
+        return out
     so = _lib.lib()
     cs = nm.c_struct()
     nm.ensure_sorted()
@@ -238,7 +255,7 @@ def _wt_dev(nm, w, w_rs, w_cs, n_w, out, o_js, o_cs, counter):
     _lib.check(so.fb_wt(cs, D.ptr(w), n_w, w_rs, w_cs, D.ptr(out), o_js, o_cs, ws.data_ptr(), ws.numel(),
                         D.stream_handle()))
     if counter is not None:
-        for e, f in nm.blocks:
+        for e, f in nm.raw_blocks:
             if e is not None:
                 counter.tally(0, n_w * e.rows)
             K.tally_matmul(counter, n_w, f.shape[0], f.shape[1])

@@ -237,8 +237,11 @@ def test_sparse_factors_through_builders():
     nm_d = fb.build_pkfk(s.toarray(), keys, r.toarray())
     np.testing.assert_array_equal(fb.materialize(nm_sp), fb.materialize(nm_d))
     x = rng.standard_normal((80, 3))
-    np.testing.assert_array_equal(fb.lmm(nm_sp, x), fb.lmm(nm_d, x))
-    np.testing.assert_array_equal(fb.crossprod(nm_sp), fb.crossprod(nm_d))
+    # factors at <= 5 % density stay CSR and the LMM reads them natively (csr_ops): the same
+    # products, summed in CSR order instead of the dense kernels' order
+    assert nm_sp.has_csr
+    np.testing.assert_allclose(fb.lmm(nm_sp, x), fb.lmm(nm_d, x), rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(fb.crossprod(nm_sp), fb.crossprod(nm_d))  # dense expansion
 
 
 def test_sparse_input_fails_loudly_without_gpu():

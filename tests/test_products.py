@@ -156,19 +156,23 @@ def test_dense_sparse_primitives_vs_numpy():
                 b = rng.standard_normal((n, k) if tb else (k, n))
                 want = (a.T if ta else a) @ (b.T if tb else b)
                 c = torch.full((m, n), 2.0, dtype=torch.float64, device=dev)
-                _lib.check(so.fb_dense_mm(m, n, k, D.ptr(T(a)), a.shape[1], ta, D.ptr(T(b)), b.shape[1], tb, D.ptr(c), n,
+                ad, bd = T(a), T(b)  # keep the device copies alive until the kernel ran
+                _lib.check(so.fb_dense_mm(m, n, k, D.ptr(ad), a.shape[1], ta, D.ptr(bd), b.shape[1], tb, D.ptr(c), n,
                                           1, st))
+                torch.cuda.synchronize()
                 np.testing.assert_allclose(c.cpu().numpy(), want + 2.0, rtol=1e-12, atol=1e-12)
     mat = rng.standard_normal((17, 23))
     ra = rng.integers(0, 17, 41).astype(np.int32)
     cb = rng.integers(0, 23, 29).astype(np.int32)
     c = torch.ones((41, 29), dtype=torch.float64, device=dev)
-    _lib.check(so.fb_gather2_add(41, 29, D.ptr(T(mat)), 23, D.ptr(T(ra)), D.ptr(T(cb)), D.ptr(c), 29, st))
+    keep = [T(mat), T(ra), T(cb)]
+    _lib.check(so.fb_gather2_add(41, 29, D.ptr(keep[0]), 23, D.ptr(keep[1]), D.ptr(keep[2]), D.ptr(c), 29, st))
     np.testing.assert_array_equal(c.cpu().numpy(), 1.0 + mat[ra][:, cb])
     a = rng.standard_normal((500, 7))
     tgt = rng.integers(0, 31, 500).astype(np.int32)
     out = torch.empty((31, 7), dtype=torch.float64, device=dev)
-    _lib.check(so.fb_scatter_rows(500, 7, D.ptr(T(tgt)), D.ptr(T(a)), 7, D.ptr(out), 31, st))
+    keep = [T(tgt), T(a)]
+    _lib.check(so.fb_scatter_rows(500, 7, D.ptr(keep[0]), D.ptr(keep[1]), 7, D.ptr(out), 31, st))
     want = np.zeros((31, 7))
     np.add.at(want, tgt, a)
     np.testing.assert_allclose(out.cpu().numpy(), want, rtol=1e-12, atol=1e-12)
@@ -183,8 +187,9 @@ def test_dense_sparse_primitives_vs_numpy():
         val = torch.empty(n_rows, dtype=torch.float64, device=dev)
         nnz = torch.zeros(1, dtype=torch.int64, device=dev)
         ws = torch.empty(so.fb_pair_counts_workspace_bytes(n_rows), dtype=torch.uint8, device=dev)
-        _lib.check(so.fb_pair_counts(n_rows, D.ptr(T(t1)), D.ptr(T(t2)), ca, cbn, D.ptr(indptr), D.ptr(col), D.ptr(val),
-                                     D.ptr(nnz), ws.data_ptr(), ws.numel(), st))
+        keep = [T(t1), T(t2)]
+        _lib.check(so.fb_pair_counts(n_rows, D.ptr(keep[0]), D.ptr(keep[1]), ca, cbn, D.ptr(indptr), D.ptr(col),
+                                     D.ptr(val), D.ptr(nnz), ws.data_ptr(), ws.numel(), st))
         k = int(nnz.item())
         assert k == want.nnz
         np.testing.assert_array_equal(indptr.cpu().numpy(), want.indptr)
@@ -193,11 +198,13 @@ def test_dense_sparse_primitives_vs_numpy():
     p = sp.random(300, 50, density=0.05, random_state=3, format="csr")
     x = rng.standard_normal((50, 37))
     y = torch.empty((300, 37), dtype=torch.float64, device=dev)
-    _lib.check(so.fb_csr_spmm(300, D.ptr(T(p.indptr.astype(np.int64))), D.ptr(T(p.indices.astype(np.int32))), 0,
-                              D.ptr(T(p.data)), D.ptr(T(x)), 37, 37, D.ptr(y), 37, 0, st))
+    keep = [T(p.indptr.astype(np.int64)), T(p.indices.astype(np.int32)), T(p.data), T(x)]
+    _lib.check(so.fb_csr_spmm(300, D.ptr(keep[0]), D.ptr(keep[1]), 0, D.ptr(keep[2]), D.ptr(keep[3]), 37, 37, D.ptr(y),
+                              37, 0, st))
     np.testing.assert_allclose(y.cpu().numpy(), p @ x, rtol=1e-12, atol=1e-12)
     xt = rng.standard_normal((300, 5))
     yt = torch.empty((50, 5), dtype=torch.float64, device=dev)
-    _lib.check(so.fb_csr_spmm_t(300, 50, D.ptr(T(p.indptr.astype(np.int64))), D.ptr(T(p.indices.astype(np.int64))), 1,
-                                D.ptr(T(p.data)), D.ptr(T(xt)), 5, 5, D.ptr(yt), 5, st))
+    keep = [T(p.indptr.astype(np.int64)), T(p.indices.astype(np.int64)), T(p.data), T(xt)]
+    _lib.check(so.fb_csr_spmm_t(300, 50, D.ptr(keep[0]), D.ptr(keep[1]), 1, D.ptr(keep[2]), D.ptr(keep[3]), 5, 5,
+                                D.ptr(yt), 5, st))
     np.testing.assert_allclose(yt.cpu().numpy(), p.T @ xt, rtol=1e-12, atol=1e-12)
