@@ -16,7 +16,9 @@ read it natively — traffic proportional to nnz instead of the dense n × d:
 * rowSums / colSums / sumAll (rewrite.py:118-165) as T·1, 1ᵀ·T and 1ᵀ·T·1.
 
 Every other operator (crossprod, the fused drivers, element-wise maps, M:N) reads the dense
-expansion the matrix makes once (``NormalizedMatrix.blocks``). Op tallies follow the
+expansion the matrix makes once (``NormalizedMatrix.blocks``). The same block-by-block route
+serves dense factors wider than the streaming kernels' 256 columns
+(``NormalizedMatrix.block_path``). Op tallies follow the
 reference's storage-aware rule for a sparse left operand (kernel.py:115-117: nnz·n
 multiplies, (nnz − m)·n additions).
 """

@@ -204,6 +204,16 @@ class NormalizedMatrix:
     def has_csr(self):
         return any(D.is_csr(f) for _, f in self._raw)
 
+    # widest factor the streaming kernels take (a factor row is staged in shared memory)
+    MAX_RING_WIDTH = 256
+
+    @property
+    def block_path(self):
+        """LMM / Tᵀ·X / row and column sums go block by block (csr_ops: CSR SpMM, DMMA block
+        products, keyed gathers / scatters) instead of through the fused streaming kernels:
+        CSR factors, or a factor wider than the streaming kernels' 256 columns."""
+        return self.has_csr or max(f.shape[1] for _, f in self._raw) > self.MAX_RING_WIDTH
+
     # -- shape ------------------------------------------------------------
     @property
     def base_rows(self):

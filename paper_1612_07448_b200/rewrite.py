@@ -147,7 +147,7 @@ def row_sums(nm, counter=None):
         return D.to_like(_as_dev(r).t().contiguous(), nm.host_io)
     so = _lib.lib()
     n = nm.base_rows
-    if nm.has_csr:  # CSR factors read natively (csr_ops): T·1
+    if nm.block_path:  # CSR factors read natively / wide factors (csr_ops): T·1
         out = _csr.lmm(nm, _csr.ones(nm.base_cols, nm.device))
     else:
         out = torch.empty((n, 1), dtype=torch.float64, device=nm.device)
@@ -169,7 +169,7 @@ def col_sums(nm, counter=None):
         r = row_sums(nm.T, counter)
         return D.to_like(_as_dev(r).t().contiguous(), nm.host_io)
     so = _lib.lib()
-    if nm.has_csr:  # CSR factors read natively (csr_ops): (Tᵀ·1)ᵀ
+    if nm.block_path:  # CSR factors read natively / wide factors (csr_ops): (Tᵀ·1)ᵀ
         out = _csr.tmm(nm, _csr.ones(nm.base_rows, nm.device)).reshape(1, -1)
     else:
         out = torch.empty((1, nm.base_cols), dtype=torch.float64, device=nm.device)
@@ -191,7 +191,7 @@ def sum_all(nm, counter=None):
     _nm_check(nm)
     base = nm.untransposed()
     so = _lib.lib()
-    if base.has_csr:
+    if base.block_path:
         out = _csr.sum_all(base)
     else:
         cs = base.c_struct()
@@ -221,7 +221,7 @@ def _as_dev(a):
 
 def _lmm_dev(nm, x, counter):
     """T·X on the untransposed matrix; x is a contiguous device matrix (d × d_x)."""
-    if nm.has_csr:
+    if nm.block_path:
         return _csr.lmm(nm, x, counter)
     so = _lib.lib()
     n, d_x = nm.base_rows, x.shape[1]
@@ -243,7 +243,7 @@ def _wt_dev(nm, w, w_rs, w_cs, n_w, out, o_js, o_cs, counter):
     The X·K halves run as segmented sums over the cached FK-sorted order (built on first use,
     like the reference's cached CSR of K, indicator.py:71-86).
     """
-    if nm.has_csr:  # CSR factors read natively (csr_ops): out(j, c) = (Tᵀ·W)[c, j]
+    if nm.block_path:  # CSR factors read natively / wide factors (csr_ops): out(j, c) = (Tᵀ·W)[c, j]
         wd = torch.as_strided(w, (nm.base_rows, n_w), (w_rs, w_cs)).contiguous()
         res = _csr.tmm(nm, wd, counter)
         torch.as_strided(out, (nm.base_cols, n_w), (o_cs, o_js)).copy_(res)

@@ -102,3 +102,27 @@ def test_csr_unreferenced_rows_dropped_and_drivers():
     w_ref, _ = O.logistic_gd(ref, y, 3, 1e-3)
     got = fb.logistic_gd(nm, y, fb.TrainConfig(iterations=3, step_size=1e-3)).weights
     assert _dev(got, w_ref) <= TOL
+
+
+@pytest.mark.gpu
+def test_wide_dense_factors_take_the_block_path():
+    """Factors wider than the streaming kernels' 256 columns: T·X, Tᵀ·X, row / column sums."""
+    import paper_1612_07448_b200 as fb
+
+    rng = np.random.default_rng(24)
+    s = rng.standard_normal((3_000, 300))
+    r = rng.standard_normal((200, 270))
+    keys = rng.integers(1, 201, size=3_000)
+    nm = fb.build_pkfk(s, keys, r)
+    ref = O.build_pkfk(s, keys, r)
+    assert nm.block_path and not nm.has_csr
+    x = rng.standard_normal((570, 3))
+    p = rng.standard_normal((3_000, 2))
+    for got, want in (
+        (fb.lmm(nm, x), O.lmm(ref, x)),
+        (fb.lmm(nm.T, p), O.lmm(ref.T, p)),
+        (fb.rmm(p.T.copy(), nm), O.rmm(p.T, ref)),
+        (fb.row_sums(nm), O.row_sums(ref)),
+        (fb.col_sums(nm), O.col_sums(ref)),
+    ):
+        assert _dev(got, want) <= TOL
