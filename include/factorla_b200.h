@@ -112,6 +112,26 @@ size_t fb_lmm_workspace_bytes(const fb_normalized* nm, int32_t d_x);
 int fb_lmm(const fb_normalized* nm, const double* x, int32_t d_x, double* out, void* ws,
            size_t ws_bytes, fb_stream_t stream);
 
+/* FK-band layout of a PK-FK matrix: a cached copy of S and of the FK column with the rows grouped
+ * into n_bands contiguous key ranges (band of row i = fk[i]·n_bands / n_r; storage order kept
+ * inside a band — a stable sort), plus the permutation back to storage order. The device
+ * analogue of the reference's cached derived layouts of K (indicator.py:71-86): built once per
+ * matrix, it lets the wide-X LMM S pass gather z = R·X from one L2-resident slice at a time when
+ * the whole z table is larger than L2 (c2: 128 MB). */
+typedef struct fb_band_layout {
+  int32_t n_bands;
+  const int32_t* perm; /* n_s: storage row of band position i */
+  const int32_t* fk;   /* n_s: part[0].fk in band order */
+  const double* s;     /* n_s x d_s: S rows in band order */
+} fb_band_layout;
+size_t fb_band_build_workspace_bytes(int64_t n);
+int fb_band_build(const fb_normalized* nm, int32_t n_bands, int32_t* perm, int32_t* fk_band,
+                  double* s_band, void* ws, size_t ws_bytes, fb_stream_t stream);
+/* fb_lmm with the S pass reading the band layout (q = 1, d_s <= 32, column chunks of 8 or 16;
+ * other shapes run fb_lmm's storage-order pass). Results are bitwise equal to fb_lmm's. */
+int fb_lmm_banded(const fb_normalized* nm, const fb_band_layout* band, const double* x, int32_t d_x,
+                  double* out, void* ws, size_t ws_bytes, fb_stream_t stream);
+
 /* rowSums(T) (rewrite.py:118-128): out n_s x 1. */
 size_t fb_row_sums_workspace_bytes(const fb_normalized* nm);
 int fb_row_sums(const fb_normalized* nm, double* out, void* ws, size_t ws_bytes,

@@ -30,7 +30,7 @@ from .normmat import (
     stats,
     transpose,
 )
-from .rewrite import col_sums, crossprod, lmm, rmm, row_sums, scalar_fn, scalar_op, sum_all
+from .rewrite import HostCallableWarning, col_sums, crossprod, lmm, rmm, row_sums, scalar_fn, scalar_op, sum_all
 from .products import (
     MaterializationWarning,
     dmm,
@@ -82,6 +82,7 @@ __all__ = [
     "elementwise_matrix_op",
     "pair_product",
     "MaterializationWarning",
+    "HostCallableWarning",
     "launch_count",
     "costmodel",
     "auto_dispatch",

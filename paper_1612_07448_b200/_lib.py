@@ -54,7 +54,17 @@ class FbNormalized(ctypes.Structure):
     ]
 
 
+class FbBandLayout(ctypes.Structure):
+    _fields_ = [
+        ("n_bands", c_i32),
+        ("perm", c_vp),
+        ("fk", c_vp),
+        ("s", c_vp),
+    ]
+
+
 _P = ctypes.POINTER(FbNormalized)
+_PB = ctypes.POINTER(FbBandLayout)
 
 # name -> (restype, argtypes)
 _SIGS = {
@@ -72,6 +82,9 @@ _SIGS = {
     "fb_i32_to_f64": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "fb_lmm_workspace_bytes": (c_size, [_P, c_i32]),
     "fb_lmm": (c_i32, [_P, c_vp, c_i32, c_vp, c_vp, c_size, c_vp]),
+    "fb_band_build_workspace_bytes": (c_size, [c_i64]),
+    "fb_band_build": (c_i32, [_P, c_i32, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "fb_lmm_banded": (c_i32, [_P, _PB, c_vp, c_i32, c_vp, c_vp, c_size, c_vp]),
     "fb_row_sums_workspace_bytes": (c_size, [_P]),
     "fb_row_sums": (c_i32, [_P, c_vp, c_vp, c_size, c_vp]),
     "fb_wt_workspace_bytes": (c_size, [_P, c_i32]),

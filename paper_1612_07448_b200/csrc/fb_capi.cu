@@ -162,6 +162,16 @@ __global__ void fill_kernel(double* p, int64_t n, double v) {
     p[i] = v;
 }
 
+__global__ void band_id_kernel(const int32_t* fk, int64_t n, int64_t n_r, int64_t n_bands, int32_t* band) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    band[i] = static_cast<int32_t>(static_cast<int64_t>(fk[i]) * n_bands / n_r);
+}
+
+__global__ void gather_i32_kernel(const int32_t* in, const int32_t* idx, int64_t n, int32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[idx[i]];
+}
+
 __global__ void mirror_upper_kernel(double* a, int64_t d) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (e >= d * d) return;
@@ -288,6 +298,78 @@ int fb_lmm(const fb_normalized* nm, const double* x, int32_t d_x, double* out, v
     cudaError_t e = fb::launch_lmm_rows(nm->s, nm->n_s, nm->d_s, x + c0, w, d_x, nm->q, fks, zs,
                                         fb::z_stride(w), out + c0, d_x, cs(stream), g_num_sms, zrows);
     if (e != cudaSuccess) return cuda_status(e, "lmm(S)");
+    c0 += w;
+  }
+  return FB_OK;
+}
+
+// ------------------------------------------------------------------ FK-band layout
+size_t fb_band_build_workspace_bytes(int64_t n) {
+  return fb::fk_sort_workspace_bytes(n) + 2 * align256(static_cast<size_t>(n > 0 ? n : 1) * 4) + 256;
+}
+
+int fb_band_build(const fb_normalized* nm, int32_t n_bands, int32_t* perm, int32_t* fk_band, double* s_band,
+                  void* ws, size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (nm->q != 1) return fail(FB_ERR_ARG, "band_build: needs exactly one attribute table (q=%d)", nm->q);
+  if (n_bands < 1 || n_bands > 4096) return fail(FB_ERR_ARG, "band_build: n_bands=%d outside [1, 4096]", n_bands);
+  const int64_t n = nm->n_s;
+  if (n == 0) return FB_OK;
+  if (!perm || !fk_band || (!s_band && nm->d_s > 0) || !ws) return fail(FB_ERR_ARG, "band_build: NULL pointer");
+  if (ws_bytes < fb_band_build_workspace_bytes(n)) return fail(FB_ERR_ARG, "band_build: workspace too small");
+  const fb_part& p = nm->part[0];
+  const size_t ib = align256(static_cast<size_t>(n) * 4);
+  int32_t* band = static_cast<int32_t*>(ws);
+  int32_t* band_sorted = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + ib);
+  void* sort_ws = static_cast<char*>(ws) + 2 * ib;
+  band_id_kernel<<<g_num_sms * 8, 256, 0, cs(stream)>>>(p.fk, n, p.n_r, n_bands, band);
+  FB_LAUNCHED();
+  // stable sort by band: storage order survives inside a band
+  cudaError_t e = fb::launch_fk_sort(band, n, n_bands, perm, band_sorted, sort_ws, ws_bytes - 2 * ib, cs(stream),
+                                     g_num_sms);
+  if (e != cudaSuccess) return cuda_status(e, "band_build(sort)");
+  gather_i32_kernel<<<g_num_sms * 8, 256, 0, cs(stream)>>>(p.fk, perm, n, fk_band);
+  FB_LAUNCHED();
+  if (nm->d_s > 0) {
+    e = fb::launch_gather_rows(nm->s, nm->d_s, nullptr, perm, n, nm->d_s, s_band, nm->d_s, cs(stream), g_num_sms);
+    if (e != cudaSuccess) return cuda_status(e, "band_build(gather)");
+  }
+  return cuda_status(cudaGetLastError(), "band_build");
+}
+
+int fb_lmm_banded(const fb_normalized* nm, const fb_band_layout* band, const double* x, int32_t d_x, double* out,
+                  void* ws, size_t ws_bytes, fb_stream_t stream) {
+  int st = check_nm(nm);
+  if (st) return st;
+  if (!band || nm->q != 1 || nm->d_s < 1 || nm->d_s > 32 || nm->n_s == 0 || !band->perm || !band->fk || !band->s)
+    return fb_lmm(nm, x, d_x, out, ws, ws_bytes, stream);
+  if (d_x < 1) return fail(FB_ERR_SHAPE, "lmm: d_x=%d", d_x);
+  if (!x || !out) return fail(FB_ERR_ARG, "lmm: NULL pointer");
+  if (ws_bytes < fb_lmm_workspace_bytes(nm, d_x)) return fail(FB_ERR_ARG, "lmm: workspace too small");
+  if (max_width(nm) > 256) return fail(FB_ERR_ARG, "lmm: factor widths above 256 are not supported");
+  const fb_part& p = nm->part[0];
+  for (int c0 = 0; c0 < d_x;) {
+    const int w = chunk_width(d_x - c0);
+    const int zst = fb::z_stride(w);
+    Carver cv{static_cast<char*>(ws), ws_bytes};
+    double* z = cv.take<double>(static_cast<size_t>(p.n_r) * zst);
+    // z = R · X[d_s:, c0:c0+w]   (rewrite.py:187)
+    cudaError_t e = fb::launch_lmm_rows(p.r, p.n_r, p.d_r, x + static_cast<int64_t>(nm->d_s) * d_x + c0, w, d_x, 0,
+                                        nullptr, nullptr, 0, z, zst, cs(stream), g_num_sms);
+    if (e != cudaSuccess) return cuda_status(e, "lmm(z)");
+    // out = S · X[0:d_s, c0:c0+w] + z[fk]   (rewrite.py:186-190), rows visited band by band
+    if (fb::lmm_band_supported(nm->d_s, w, d_x, out + c0)) {
+      e = fb::launch_lmm_band(band->s, band->fk, band->perm, nm->n_s, nm->d_s, x + c0, w, d_x, z, zst, p.n_r,
+                              out + c0, d_x, cs(stream), g_num_sms);
+    } else {
+      const int32_t* fks[1] = {p.fk};
+      const double* zs[1] = {z};
+      const int64_t zrows[1] = {p.n_r};
+      e = fb::launch_lmm_rows(nm->s, nm->n_s, nm->d_s, x + c0, w, d_x, 1, fks, zs, zst, out + c0, d_x, cs(stream),
+                              g_num_sms, zrows);
+    }
+    if (e != cudaSuccess) return cuda_status(e, "lmm(S, banded)");
     c0 += w;
   }
   return FB_OK;
@@ -887,7 +969,9 @@ static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const
                                double* tta_out, int32_t* sizes_out, void* ws, size_t ws_bytes, fb_stream_t stream) {
   int st = check_nm(nm);
   if (st) return st;
-  if (k < 1 || k > 16) return fail(FB_ERR_ARG, "kmeans: k=%d outside [1, 16]", k);
+  // k <= 16: one fused pass over S (fb_kmeans.cu); 17..64: T·(2C) in 16-column chunks, then the
+  // assign / one-hot passes and column-chunked R passes
+  if (k < 1 || k > 64) return fail(FB_ERR_ARG, "kmeans: k=%d outside [1, 64]", k);
   if (!d_t || !c || !cc || !trace || !assign || !nan_row) return fail(FB_ERR_ARG, "kmeans: NULL pointer");
   if (max_width(nm) > 256) return fail(FB_ERR_ARG, "kmeans: factor widths above 256 are not supported");
   if (ws_bytes < fb_kmeans_workspace_bytes(nm, k)) return fail(FB_ERR_ARG, "kmeans: workspace too small");
@@ -993,21 +1077,25 @@ static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const
       off += p.d_r;
       continue;
     }
-    fb::ColReduce r{};
-    r.a = p.r;
-    r.n = p.n_r;
-    r.d = p.d_r;
-    r.nx = k;
-    r.w = fbins[i];
-    r.w_rs = k;
-    r.w_cs = 1;
-    r.out = tta + off * k;
-    r.o_js = 1;
-    r.o_cs = k;
-    r.partials = cpart;
-    r.counter = cnt2;
-    e = fb::launch_colreduce(r, s, g_num_sms);
-    if (e != cudaSuccess) return cuda_status(e, "kmeans(R pass)");
+    for (int c0 = 0; c0 < k;) {  // column chunks of the widths the reduction is instantiated for
+      const int w = chunk_width(k - c0);
+      fb::ColReduce r{};
+      r.a = p.r;
+      r.n = p.n_r;
+      r.d = p.d_r;
+      r.nx = w;
+      r.w = fbins[i] + c0;
+      r.w_rs = k;
+      r.w_cs = 1;
+      r.out = tta + off * k + c0;
+      r.o_js = 1;
+      r.o_cs = k;
+      r.partials = cpart;
+      r.counter = cnt2;
+      e = fb::launch_colreduce(r, s, g_num_sms);
+      if (e != cudaSuccess) return cuda_status(e, "kmeans(R pass)");
+      c0 += w;
+    }
     off += p.d_r;
   }
   return FB_OK;
@@ -1030,7 +1118,8 @@ int fb_gnmf_step(const fb_normalized* nm, double* w, double* h, double* ttw, dou
                  int32_t r, int32_t it, double* trace, void* ws, size_t ws_bytes, fb_stream_t stream) {
   int st = check_nm(nm);
   if (st) return st;
-  if (r < 1 || r > 16) return fail(FB_ERR_ARG, "gnmf: r=%d outside [1, 16]", r);
+  // r <= 16: one fused pass over S per W step (fb_gnmf.cu); 17..64: the operator-by-operator step
+  if (r < 1 || r > 64) return fail(FB_ERR_ARG, "gnmf: r=%d outside [1, 64]", r);
   if (!w || !h || !ttw || !cpw || !sum_t2 || !trace) return fail(FB_ERR_ARG, "gnmf: NULL pointer");
   if (ws_bytes < fb_gnmf_workspace_bytes(nm, r)) return fail(FB_ERR_ARG, "gnmf: workspace too small");
   cudaStream_t s = cs(stream);
@@ -1140,7 +1229,7 @@ int fb_glm_update(double* w, const double* g, int64_t d, double alpha, const dou
 }
 
 int fb_nmf_update(double* f, const double* num, const double* g, int64_t rows, int32_t r, fb_stream_t stream) {
-  if (!f || !num || !g || r < 1 || r > 16 || rows < 0) return fail(FB_ERR_ARG, "nmf_update: bad argument");
+  if (!f || !num || !g || r < 1 || r > 64 || rows < 0) return fail(FB_ERR_ARG, "nmf_update: bad argument");
   return cuda_status(fb::launch_nmf_update(f, num, g, rows, r, 1e-12, cs(stream), g_num_sms), "nmf_update");
 }
 

@@ -14,6 +14,12 @@ cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, 
                             int nfk, const int32_t* const* fk, const double* const* z, int zstride, double* out,
                             int64_t ldo, cudaStream_t st, int num_sms, const int64_t* z_rows = nullptr);
 
+// S pass over an FK-band layout (fb_band_layout): rows of a_band / fk_band / perm in band order.
+bool lmm_band_supported(int d, int dx, int64_t ldo, const double* out);
+cudaError_t launch_lmm_band(const double* a_band, const int32_t* fk_band, const int32_t* perm, int64_t n, int d,
+                            const double* x, int dx, int64_t ldx, const double* z, int zstride, int64_t z_rows,
+                            double* out, int64_t ldo, cudaStream_t st, int num_sms);
+
 // fb_reduce.cu ---------------------------------------------------------------------
 struct ColReduce {
   const double* a;  // rows streamed: n × d row-major

@@ -612,9 +612,39 @@ __global__ void nmf_update_kernel(double* __restrict__ f, const double* __restri
   }
 }
 
+// 16 < r <= 64: a warp per row, lane s owning columns s and s + 32; the old row is broadcast by
+// shuffles, the denominators accumulate over t in ascending order exactly as above.
+__global__ void nmf_update_wide_kernel(double* __restrict__ f, const double* __restrict__ num,
+                                       const double* __restrict__ g, int64_t rows, int r, double eps) {
+  extern __shared__ double gw[];  // r × r
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) gw[e] = g[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const bool on0 = lane < r, on1 = lane + 32 < r;
+  for (int64_t i = warp; i < rows; i += nwarps) {
+    const double f0 = on0 ? f[i * r + lane] : 0.0, f1 = on1 ? f[i * r + lane + 32] : 0.0;
+    double den0 = 0.0, den1 = 0.0;
+    for (int t = 0; t < r; ++t) {
+      const double ft = __shfl_sync(0xffffffffu, t < 32 ? f0 : f1, t & 31);
+      if (on0) den0 = fma(ft, gw[t * r + lane], den0);
+      if (on1) den1 = fma(ft, gw[t * r + lane + 32], den1);
+    }
+    if (on0) f[i * r + lane] = f0 * num[i * r + lane] / (den0 + eps);
+    if (on1) f[i * r + lane + 32] = f1 * num[i * r + lane + 32] / (den1 + eps);
+  }
+}
+
 cudaError_t launch_nmf_update(double* f, const double* num, const double* g, int64_t rows, int r, double eps,
                               cudaStream_t st, int num_sms) {
   const int grid = grid_for(rows, 256, 8, num_sms);
+  if (r > 16 && r <= 64) {
+    nmf_update_wide_kernel<<<grid_for(rows, 8, 8, num_sms), 256, static_cast<size_t>(r) * r * 8, st>>>(f, num, g, rows,
+                                                                                                   r, eps);
+    FB_LAUNCHED();
+    return cudaGetLastError();
+  }
   switch (r) {
 #define FB_R_CASE(R)                                                     \
   case R:                                                                \

@@ -128,7 +128,12 @@ FB_DEV bool is_gather_warp() { return threadIdx.x >= 32 && threadIdx.x < 32 * kS
 FB_DEV int consumer_tid() { return static_cast<int>(threadIdx.x) - 32 * kServiceWarps; }
 FB_DEV int consumer_warp() { return (static_cast<int>(threadIdx.x) >> 5) - kServiceWarps; }
 
-struct TileRing {
+// RR = false: each CTA takes one contiguous range of tiles. RR = true: tiles dealt round-robin
+// (CTA c takes tiles c, c + grid, ...), so all CTAs sweep the matrix front to back together —
+// for passes whose rows are laid out in FK bands, every CTA then gathers from the same
+// L2-resident slice of the lookup table at any moment (the banded LMM S pass, fb_lmm.cu).
+template <bool RR>
+struct TileRingT {
   char* buf;        // stages * stage_bytes
   uint64_t* full;   // stages mbarriers (producer -> consumers, gatherer)
   uint64_t* empty;  // stages mbarriers (consumers -> producer)
@@ -137,7 +142,8 @@ struct TileRing {
   int tile_rows;
   int64_t n_rows;
   int64_t ntiles;                // tiles over the whole matrix
-  int64_t tile_begin, tile_end;  // this CTA's contiguous tile range
+  int64_t tile_begin, tile_end;  // this CTA's contiguous tile range (RR: first tile, ntiles)
+  int64_t tile_step;             // RR: grid size
   uint64_t policy;
   bool gathers;
   // consumer iteration state: the next stage to wait on, and the oldest stage still held
@@ -156,13 +162,29 @@ struct TileRing {
     n_rows = n_rows_;
     ntiles = (n_rows_ + tile_rows_ - 1) / tile_rows_;
     const int64_t g = gridDim.x, c = blockIdx.x;
-    tile_begin = ntiles * c / g;
-    tile_end = ntiles * (c + 1) / g;
+    if constexpr (RR) {
+      tile_begin = c;
+      tile_end = ntiles;
+      tile_step = g;
+    } else {
+      tile_begin = ntiles * c / g;
+      tile_end = ntiles * (c + 1) / g;
+      tile_step = 1;
+    }
     policy = policy_evict_first();
     gathers = false;
   }
 
-  FB_DEV int64_t count() const { return tile_end - tile_begin; }
+  FB_DEV int64_t count() const {
+    if constexpr (RR) return tile_end > tile_begin ? (tile_end - tile_begin + tile_step - 1) / tile_step : 0;
+    return tile_end - tile_begin;
+  }
+
+  // global tile index of this CTA's k-th tile
+  FB_DEV int64_t tile_of(int64_t k) const {
+    if constexpr (RR) return tile_begin + k * tile_step;
+    return tile_begin + k;
+  }
 
   FB_DEV char* stage_ptr(int st, const StreamSet& s, int stream) const {
     return buf + static_cast<uint32_t>(st) * s.stage_bytes + s.smem_off[stream];
@@ -235,7 +257,7 @@ struct TileRing {
     uint32_t ph = 0;
     const int64_t n = count();
     for (int64_t k = 0; k < n; ++k) {
-      const int64_t tile = tile_begin + k;
+      const int64_t tile = tile_of(k);
       if (k >= stages) mbar_wait(&empty[st], ph ^ 1u);
       const int rows = rows_of(tile);
       if (bulk_ok(s, tile)) {
@@ -317,9 +339,9 @@ struct TileRing {
       const int v1 = __shfl_sync(0xffffffffu, kc[g][1], ri & 31);
       return ri < 32 ? v0 : v1;
     };
-    if (n > 0) load_keys(tile_begin);
+    if (n > 0) load_keys(tile_of(0));
     for (int64_t k = 0; k < n; ++k) {
-      const int64_t tile = tile_begin + k;
+      const int64_t tile = tile_of(k);
       const int rows = rows_of(tile);
       const int rows_w = rows > gw ? (rows - gw + kGatherWarps - 1) / kGatherWarps : 0;  // rows of this warp
 #pragma unroll
@@ -327,7 +349,7 @@ struct TileRing {
         kc[g][0] = kn[g][0];
         kc[g][1] = kn[g][1];
       }
-      if (k + 1 < n) load_keys(tile + 1);  // latency overlaps this stage's wait and copies
+      if (k + 1 < n) load_keys(tile_of(k + 1));  // latency overlaps this stage's wait and copies
       if (k >= stages) mbar_wait(&empty[st], ph ^ 1u);  // the stage is free again
       if (GIDX_BULK && s.gidx && s.gidx_bulk && bulk_ok(s, tile)) {
         // one bulk copy per row, lane i moving the warp's row i (its own gidx register): the
@@ -443,7 +465,7 @@ struct TileRing {
   FB_DEV int acquire(const StreamSet& s, int64_t k) {
     const int st = stage;
     mbar_wait(&full[st], phase);
-    const int64_t tile = tile_begin + k;
+    const int64_t tile = tile_of(k);
     if (!bulk_ok(s, tile)) {
       consumer_sync();  // everyone is past the wait before the stage is overwritten
       manual_fill(s, tile, st);
@@ -464,5 +486,7 @@ struct TileRing {
     if (++rstage == stages) rstage = 0;
   }
 };
+
+using TileRing = TileRingT<false>;
 
 }  // namespace fb

@@ -435,8 +435,8 @@ def kmeans(m, cfg):
     k = cfg.k
     if k > n:
         raise DataError(f"k={k} exceeds the number of data rows ({n})")
-    if k > 16:
-        raise NotImplementedError("the device K-Means step supports k <= 16")
+    if k > 64:
+        raise NotImplementedError("the device K-Means step supports k <= 64")
     so = _lib.lib()
     st = D.stream_handle()
     cs = nm.c_struct()
@@ -496,8 +496,8 @@ def gnmf(m, cfg):
     nm = _matrix(m)
     n, d = nm.shape
     r = cfg.r
-    if r > 16:
-        raise NotImplementedError("the device GNMF step supports r <= 16")
+    if r > 64:
+        raise NotImplementedError("the device GNMF step supports r <= 64")
     if _min_value(nm) < 0:
         warnings.warn("input has negative entries; GNMF semantics assume non-negative data")
     so = _lib.lib()

@@ -19,6 +19,7 @@ d_s = 0), so every operator and driver runs unchanged on the same gathers/scatte
 """
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -328,6 +329,45 @@ class NormalizedMatrix:
             perm, fks = e.sorted_order()
             if st is not None:
                 st.part[i].perm, st.part[i].fk_sorted = D.ptr(perm), D.ptr(fks)
+
+    # FK-band layout for wide-X LMMs: off by default (0). Measured at c2 (profiles/
+    # r02_lmm16_experiments.txt): DRAM traffic of the S pass drops 7.6 -> 6.1 GB, but the permuted
+    # 128-byte output rows cost the DRAM what the z misses did (op 1.45 -> 1.42 ms) for one more
+    # copy of S in HBM. FB_LMM_BAND_MIN_MB=<MB> enables it for z = R·X tables above that size.
+    BAND_MIN_BYTES = int(float(os.environ.get("FB_LMM_BAND_MIN_MB", "0")) * (1 << 20))
+    BAND_BYTES = int(float(os.environ.get("FB_LMM_BAND_MB", "16")) * (1 << 20))
+
+    def band_layout(self, d_x):
+        """``fb_band_layout`` for a wide-X LMM, or None when the pass should stay in storage order.
+
+        Built once (cached, like the FK-sorted order): PK-FK matrices with d_S <= 32 whose
+        z = R·X table (n_R × 16 doubles) exceeds ``BAND_MIN_BYTES``, for X widths the band body
+        covers (multiples of 8). Costs one extra copy of S and of the FK column in HBM.
+        """
+        if self.variant != PKFK or self.transposed or self.has_csr or self.blocks[0][0] is not None or len(self.indicator_blocks) != 1:
+            return None
+        if d_x < 8 or d_x % 8 or not self.BAND_MIN_BYTES:
+            return None
+        s = self.blocks[0][1]
+        e, r = self.indicator_blocks[0]
+        n, d = s.shape
+        zbytes = r.shape[0] * 128
+        if not (1 <= d <= 32) or n == 0 or zbytes < self.BAND_MIN_BYTES:
+            return None
+        band = self._cache.get("band")
+        if band is None:
+            so = _lib.lib()
+            n_bands = max(2, min(4096, -(-zbytes // self.BAND_BYTES)))
+            perm = torch.empty(n, dtype=torch.int32, device=s.device)
+            fkb = torch.empty(n, dtype=torch.int32, device=s.device)
+            sb = torch.empty_like(s)
+            ws = D.workspace(so.fb_band_build_workspace_bytes(n))
+            _lib.check(so.fb_band_build(self.c_struct(), n_bands, D.ptr(perm), D.ptr(fkb), D.ptr(sb),
+                                        ws.data_ptr(), ws.numel(), D.stream_handle()))
+            st = _lib.FbBandLayout(n_bands, D.ptr(perm), D.ptr(fkb), D.ptr(sb))
+            band = (st, perm, fkb, sb)
+            self._cache["band"] = band
+        return ctypes.byref(band[0])
 
     def __repr__(self):
         n, d = self.shape

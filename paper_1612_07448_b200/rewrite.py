@@ -21,6 +21,8 @@ Operands may be NumPy arrays (results come back as NumPy, like the reference) or
 CUDA tensors (results stay on the device).
 """
 
+import warnings
+
 import numpy as np
 import torch
 
@@ -46,6 +48,7 @@ __all__ = [
     "dmm_gram",
     "elementwise_matrix_op",
     "MaterializationWarning",
+    "HostCallableWarning",
 ]
 
 _SCALAR_OPS = {"add": 0, "radd": 1, "sub": 2, "rsub": 3, "mul": 4, "rmul": 5, "div": 6, "rdiv": 7, "pow": 8, "rpow": 9}
@@ -114,21 +117,64 @@ def scalar_op(nm, x, op, counter=None):
     return out
 
 
+class HostCallableWarning(UserWarning):
+    """``scalar_fn`` received a callable that only accepts NumPy arrays: the factor matrices
+    make one round trip through host memory so the caller's own function can run on them."""
+
+
+def _apply_callable(f, fm):
+    """``f`` applied element-wise to one dense device factor matrix.
+
+    The reference hands ``f`` the factor as an ndarray (kernel.py:280-300). Here the factor is a
+    CUDA tensor: array-polymorphic callables (arithmetic lambdas, torch functions) run on it in
+    place on the device; a callable that needs an ndarray gets a host copy and its result is
+    uploaded again (warned once per call — the function is the caller's host code, not an
+    operator of this library).
+    """
+    try:
+        with torch.no_grad():
+            out = f(fm)
+        if isinstance(out, torch.Tensor) and out.shape == fm.shape and out.device == fm.device:
+            return out.to(torch.float64).contiguous(), False
+    except Exception:  # noqa: BLE001 — any failure on a tensor argument means "wants an ndarray"
+        pass
+    with np.errstate(over="ignore", divide="ignore", invalid="ignore"):
+        host = np.asarray(f(fm.cpu().numpy()), dtype=np.float64)
+    if host.shape != tuple(fm.shape):
+        raise ShapeError(f"scalar_fn: the function returned shape {host.shape} for a {tuple(fm.shape)} factor")
+    return torch.from_numpy(np.ascontiguousarray(host)).to(fm.device), True
+
+
 def scalar_fn(nm, f, counter=None):
     """Element-wise ``f(T)`` = (f(S), K, f(R)) (rewrite.py:89-99).
 
-    ``f`` is a NumPy ufunc from the supported set (exp, log, square, sqrt, abs,
-    negative, log1p, expm1, sin, cos, tanh, reciprocal) or one of those names
-    (plus "sigmoid"/"identity"). Arbitrary Python callables cannot run on the device
-    and raise ``NotImplementedError``.
+    NumPy ufuncs of the built-in set (exp, log, square, sqrt, abs, negative, log1p, expm1, sin,
+    cos, tanh, reciprocal) and those names (plus "sigmoid"/"identity") run in the library's
+    element-wise kernel (``fb_unary_map``). Any other callable is applied to each factor matrix as
+    the reference applies it (``_apply_callable``): on the device tensor when it accepts one, else
+    on a host copy with a :class:`HostCallableWarning`.
     """
     _nm_check(nm)
-    code = _UNARY.get(f) if not isinstance(f, str) else _UNARY_NAMES.get(f)
-    if code is None:
-        raise NotImplementedError(
-            f"scalar_fn: {getattr(f, '__name__', f)!r} has no device kernel; supported: {sorted(_UNARY_NAMES)}"
-        )
-    out = _map_factors(nm, lambda so, fm, o, st: so.fb_unary_map(D.ptr(fm), D.ptr(o), fm.numel(), code, st))
+    if isinstance(f, str):
+        code = _UNARY_NAMES.get(f)
+        if code is None:
+            raise ValueError(f"scalar_fn: unknown function name {f!r}; known: {sorted(_UNARY_NAMES)}")
+    else:
+        code = _UNARY.get(f) if isinstance(f, np.ufunc) else None
+        if code is None and not callable(f):
+            raise TypeError(f"scalar_fn: expected a callable or a function name, got {type(f).__name__}")
+    if code is not None:
+        out = _map_factors(nm, lambda so, fm, o, st: so.fb_unary_map(D.ptr(fm), D.ptr(o), fm.numel(), code, st))
+    else:
+        new, via_host = [], False
+        for _, fm in nm.blocks:
+            o, h = _apply_callable(f, fm)
+            new.append(o)
+            via_host |= h
+        if via_host:
+            warnings.warn(f"scalar_fn: {getattr(f, '__name__', f)!r} ran on host copies of the factor matrices",
+                          HostCallableWarning, stacklevel=2)
+        out = nm.with_factors(new)
     if counter is not None:
         for _, fm in nm.blocks:
             counter.tally(fm.numel(), 0)
@@ -228,7 +274,12 @@ def _lmm_dev(nm, x, counter):
     out = torch.empty((n, d_x), dtype=torch.float64, device=x.device)
     cs = nm.c_struct()
     ws = D.workspace(so.fb_lmm_workspace_bytes(cs, d_x))
-    _lib.check(so.fb_lmm(cs, D.ptr(x), d_x, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
+    band = nm.band_layout(d_x)  # cached FK-band copy of S when z = R·X would not stay in L2
+    if band is not None:
+        _lib.check(so.fb_lmm_banded(cs, band, D.ptr(x), d_x, D.ptr(out), ws.data_ptr(), ws.numel(),
+                                    D.stream_handle()))
+    else:
+        _lib.check(so.fb_lmm(cs, D.ptr(x), d_x, D.ptr(out), ws.data_ptr(), ws.numel(), D.stream_handle()))
     if counter is not None:
         for i, (e, f) in enumerate(nm.raw_blocks):
             K.tally_matmul(counter, f.shape[0], f.shape[1], d_x)

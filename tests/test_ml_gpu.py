@@ -233,3 +233,34 @@ def test_glm_host_inputs_do_not_pin_device_memory():
     torch.cuda.synchronize()
     assert torch.cuda.memory_allocated() <= base + (1 << 20)
     assert O.max_rel_deviation(out.weights, first.weights) <= 1e-12  # Kᵀp scatter order (REDs) varies
+
+
+@pytest.mark.parametrize("k", [17, 33, 64])
+def test_kmeans_wide_k_vs_oracle(k):
+    """k above the fused pass's 16 columns: chunked T·(2C), assign, one-hot and chunked R passes."""
+    fb = _fb()
+    rng, s, parts = _c1_like(31 + k, n_s=40_000, d_s=6, n_r=1500, d_r=5, star=True)
+    nm, ref = _both(s, parts)
+    out = fb.kmeans(nm, fb.TrainConfig(iterations=4, k=k, rng_seed=5))
+    c, obj, _ = O.kmeans(ref, k, 4, 5)
+    _close(out.centroids, c)
+    _close(out.objective, obj)
+    with pytest.raises(NotImplementedError):
+        fb.kmeans(nm, fb.TrainConfig(iterations=1, k=65))
+
+
+@pytest.mark.parametrize("r", [17, 40])
+def test_gnmf_wide_r_vs_oracle(r):
+    """r above the fused pass's 16 columns: the operator-by-operator step (LMM, Tᵀ·W, WᵀW)."""
+    fb = _fb()
+    rng = np.random.default_rng(40 + r)
+    n_s, n_r = 30_000, 400
+    key = rng.integers(1, n_r + 1, size=n_s)
+    s = rng.random((n_s, 10))
+    rr = rng.random((n_r, 24))
+    nm, ref = _both(s, [(key, rr)])
+    out = fb.gnmf(nm, fb.TrainConfig(iterations=4, r=r, rng_seed=2))
+    w, h, obj = O.gnmf(ref, r, 4, 2)
+    _close(out.factors[0], w)
+    _close(out.factors[1], h)
+    _close(out.objective, obj)

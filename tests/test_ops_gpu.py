@@ -321,3 +321,80 @@ def test_crossprod_fused_and_unfused_s_pass_agree(monkeypatch):
     monkeypatch.setenv("FB_CP_NO_NARROW", "1")
     dmma = fb.crossprod(fb.as_normalized(w))
     _close(narrow, dmma.cpu().numpy(), 1e-13)
+
+
+@pytest.mark.parametrize("n_s,d_s,n_r,d_r,d_x,zipf", [
+    (100_003, 20, 5_000, 12, 16, False),   # partial last tile (rows*4 not a multiple of 16)
+    (65_536, 20, 3_001, 8, 8, False),      # whole tiles only
+    (40_000, 7, 2_000, 5, 16, True),       # ragged k-step, skewed keys (uneven bands)
+    (30_000, 32, 1_000, 3, 40, False),     # d_x = 16 + 16 + 8 column chunks
+    (257, 4, 9, 2, 16, False),             # two tiles, more bands than CTAs have rows
+])
+def test_lmm_band_layout_bitwise_equal(monkeypatch, n_s, d_s, n_r, d_r, d_x, zipf):
+    """The FK-band S pass (fb_lmm_banded: cached band copy of S, round-robin tiles, permuted
+    stores) gives the same bits as the storage-order pass and matches the oracle."""
+    fb = _fb()
+    from paper_1612_07448_b200.normmat import NormalizedMatrix
+
+    rng = np.random.default_rng(n_s + d_x)
+    s = rng.standard_normal((n_s, d_s))
+    r = rng.standard_normal((n_r, d_r))
+    if zipf:
+        key = np.minimum(rng.zipf(1.3, size=n_s), n_r)
+    else:
+        key = rng.integers(1, n_r + 1, size=n_s)
+    x = rng.standard_normal((d_s + d_r, d_x))
+    monkeypatch.setattr(NormalizedMatrix, "BAND_MIN_BYTES", 0)
+    nm0 = fb.build_pkfk(s, key, r)
+    plain = fb.lmm(nm0, x)
+    assert "band" not in nm0._cache
+    monkeypatch.setattr(NormalizedMatrix, "BAND_MIN_BYTES", 1)
+    monkeypatch.setattr(NormalizedMatrix, "BAND_BYTES", 128 * max(1, nm0.parts[0][1].shape[0] // 7))
+    nm = fb.build_pkfk(s, key, r)
+    banded = fb.lmm(nm, x)
+    assert "band" in nm._cache
+    st, perm, fkb, sb = nm._cache["band"]
+    assert st.n_bands >= 2
+    p = perm.cpu().numpy()
+    tgt = nm.k.target_numpy()
+    band = tgt * st.n_bands // nm.parts[0][1].shape[0]
+    np.testing.assert_array_equal(p, np.argsort(band, kind="stable"))
+    np.testing.assert_array_equal(fkb.cpu().numpy(), tgt[p])
+    np.testing.assert_array_equal(sb.cpu().numpy(), s[p])
+    np.testing.assert_array_equal(banded, plain)
+    again = fb.lmm(nm, x)  # cached layout reused
+    np.testing.assert_array_equal(again, plain)
+    _close(banded, O.lmm(O.build_pkfk(s, key, r), x))
+
+
+def test_scalar_fn_arbitrary_callables():
+    """scalar_fn on callables outside the built-in ufunc set (rewrite.py:89-99 takes any f)."""
+    import warnings
+
+    fb = _fb()
+    g = golden_io.load(golden_io.names()[0])
+    nm = _build_gpu(g)
+    ref = O.build_pkfk(g["s"], golden_io.parts(g)[0][0], golden_io.parts(g)[0][1]) if len(golden_io.parts(g)) == 1 \
+        else O.build_star(g["s"], golden_io.parts(g))
+
+    def poly(a):  # array-polymorphic: runs on the device tensors
+        return a * a * 0.5 + 1.0
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        out = fb.scalar_fn(nm, poly)
+    _close(fb.materialize(out), O.materialize(O.scalar_fn(ref, poly)))
+
+    def host_only(a):  # needs an ndarray (np.where on a CUDA tensor raises)
+        return np.where(np.asarray(a) > 0.0, np.arctan(a), -1.0)
+
+    with pytest.warns(fb.HostCallableWarning):
+        out = fb.scalar_fn(nm, host_only)
+    _close(fb.materialize(out), O.materialize(O.scalar_fn(ref, host_only)))
+    c = fb.OpCounter()
+    fb.scalar_fn(nm, poly, c)  # one multiply per stored factor element (kernel.py:296-298)
+    assert (c.multiplies, c.additions) == (sum(f.numel() for _, f in nm.blocks), 0)
+    with pytest.raises(ValueError):
+        fb.scalar_fn(nm, "no_such_function")
+    with pytest.raises(fb.ShapeError):
+        fb.scalar_fn(nm, lambda a: np.asarray(a).sum(axis=0))

@@ -1,8 +1,8 @@
-"""c2 LMM X100x16 through an FK-band order (fb_normalized.band_*), CUDA events, median of 10.
+"""c2 LMM X100xDX with and without the FK-band layout (fb_lmm_banded), CUDA events, median of 10.
 
-env: BAND (bands, 0 = off), COPY (1: resident band-ordered S copy, 0: rows gathered via band_perm).
+env: NR, DX, FB_LMM_BAND_MB (z bytes per band), FB_LMM_BAND_MIN_MB (0 = storage-order pass only).
 """
-import os, sys
+import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1612_07448_b200 as fb
@@ -13,23 +13,11 @@ r = torch.randn(n_r, 80, dtype=torch.float64, device="cuda", generator=g)
 k = torch.randint(1, n_r + 1, (n_s,), device="cuda", generator=g)
 nm = fb.build_pkfk(s, k, r)
 x = torch.randn(100, dx, dtype=torch.float64, device="cuda", generator=g)
-ref = fb.lmm(nm, x).clone()
-B = int(os.environ.get("BAND", "0"))
-keep = []
-if B:
-    nm.c_struct()
-    st = nm._cache["c_struct"]
-    tgt = nm.indicator_blocks[0][0].target
-    band = tgt.long() * B // n_r
-    perm = torch.argsort(band, stable=True).to(torch.int32)
-    bfk = tgt[perm.long()].contiguous()
-    keep += [perm, bfk]
-    st.band_perm = perm.data_ptr()
-    st.band_fk[0] = bfk.data_ptr()
-    if os.environ.get("COPY", "0") == "1":
-        sb = s[perm.long()].contiguous()
-        keep.append(sb)
-        st.band_s = sb.data_ptr()
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+band = nm.band_layout(dx)
+torch.cuda.synchronize()
+build_ms = (time.perf_counter() - t0) * 1e3
 for _ in range(3):
     fb.lmm(nm, x)
 ts = []
@@ -39,5 +27,6 @@ for _ in range(10):
     ts.append(a.elapsed_time(e))
 ts.sort()
 nb = 8 * (n_s * 20 + n_r * 80) + 4 * n_s + 8 * (100 * dx + n_s * dx)
-print(f"NR={n_r} DX={dx} BAND={B} COPY={os.environ.get('COPY', '0')} ms={ts[5]:.4f} GBps={nb / ts[5] / 1e6:.0f} "
-      f"maxdiff={float((out - ref).abs().max()):.3g}", flush=True)
+nbands = nm._cache["band"][0].n_bands if band is not None else 0
+print(f"NR={n_r} DX={dx} bands={nbands} build_ms={build_ms:.1f} ms={ts[5]:.4f} GBps={nb / ts[5] / 1e6:.0f} "
+      f"frac={nb / ts[5] / 1e6 / 6542.1:.3f}", flush=True)
