@@ -112,21 +112,27 @@ size_t fb_lmm_workspace_bytes(const fb_normalized* nm, int32_t d_x);
 int fb_lmm(const fb_normalized* nm, const double* x, int32_t d_x, double* out, void* ws,
            size_t ws_bytes, fb_stream_t stream);
 
-/* FK-band layout of a PK-FK matrix: a cached copy of S and of the FK column with the rows grouped
- * into n_bands contiguous key ranges (band of row i = fk[i]·n_bands / n_r; storage order kept
- * inside a band — a stable sort), plus the permutation back to storage order. The device
- * analogue of the reference's cached derived layouts of K (indicator.py:71-86): built once per
- * matrix, it lets the wide-X LMM S pass gather z = R·X from one L2-resident slice at a time when
- * the whole z table is larger than L2 (c2: 128 MB). */
+/* FK-band layout of a PK-FK / star matrix: a cached copy of S and of the FK columns with the rows
+ * grouped into n_bands contiguous key ranges of part 0 (band of row i = fk_0[i]·n_bands / n_r;
+ * storage order kept inside a band — a stable sort), plus the permutation back to storage
+ * order. The device analogue of the reference's cached derived layouts of K (indicator.py:71-86):
+ * built once per matrix, it lets a pass over S gather z_0 = R_0·X from one L2-resident slice at a
+ * time when the whole table is larger than L2. Used by the K-Means step (every result there is
+ * a sum over rows) and, opt-in, by the wide-X LMM. */
 typedef struct fb_band_layout {
   int32_t n_bands;
-  const int32_t* perm; /* n_s: storage row of band position i */
-  const int32_t* fk;   /* n_s: part[0].fk in band order */
-  const double* s;     /* n_s x d_s: S rows in band order */
+  const int32_t* perm;             /* n_s: storage row of band position i */
+  const int32_t* fk[FB_MAX_PARTS]; /* n_s each: part[q].fk in band order */
+  const double* s;                 /* n_s x d_s: S rows in band order */
 } fb_band_layout;
 size_t fb_band_build_workspace_bytes(int64_t n);
+/* Elements between the parts of fk_band (n rounded up so every part starts 256-byte aligned). */
+int64_t fb_band_fk_stride(int64_t n);
+/* fk_band: q x fb_band_fk_stride(n_s) int32 (part-major); s_band: n_s x d_s. */
 int fb_band_build(const fb_normalized* nm, int32_t n_bands, int32_t* perm, int32_t* fk_band,
                   double* s_band, void* ws, size_t ws_bytes, fb_stream_t stream);
+/* out[perm[i]] = in[i] (band order back to storage order). */
+int fb_scatter_i32(const int32_t* in, const int32_t* perm, int64_t n, int32_t* out, fb_stream_t stream);
 /* fb_lmm with the S pass reading the band layout (q = 1, d_s <= 32, column chunks of 8 or 16;
  * other shapes run fb_lmm's storage-order pass). Results are bitwise equal to fb_lmm's. */
 int fb_lmm_banded(const fb_normalized* nm, const fb_band_layout* band, const double* x, int32_t d_x,
@@ -229,7 +235,8 @@ int fb_glm_run_fused(const fb_normalized* nm);
 int fb_glm_run(const fb_normalized* nm, const double* y, double* w, int32_t mode, double alpha, int32_t iters,
                double* trace, int32_t* diverged, void* ws, size_t ws_bytes, fb_stream_t stream);
 
-/* One K-Means iteration (ml.py:275-283) on an untransposed T with k <= 16 clusters:
+/* One K-Means iteration (ml.py:275-283) on an untransposed T with k <= 64 clusters (k <= 16: one
+ * fused pass over S; above: chunked T·(2C), assign, one-hot and R passes):
  * c is the d × k centroid matrix (updated in place; empty clusters keep theirs), cc[j] =
  * Σ c[:, j]² (in/out), d_t = rowSums(T²) (n_s), assign (n_s int32) the argmin cluster
  * (ties to the lowest index), trace[it] = Σ_i min_j dist, *nan_row = (it << 40) | row for the
@@ -239,6 +246,15 @@ size_t fb_kmeans_workspace_bytes(const fb_normalized* nm, int32_t k);
 int fb_kmeans_step(const fb_normalized* nm, const double* d_t, double* c, double* cc, int32_t k, int32_t it,
                    double* trace, int32_t* assign, unsigned long long* nan_row, void* ws, size_t ws_bytes,
                    fb_stream_t stream);
+
+/* fb_kmeans_step reading the rows through an FK-band layout: d_t and assign are in band order
+ * (d_t_band[i] = d_t[perm[i]]; fb_scatter_i32 brings the final assign back), *nan_row holds a band
+ * position. Needs the fused pass (k <= 16, d_s <= 32); every other output is a sum over rows. */
+int fb_kmeans_step_banded(const fb_normalized* nm, const fb_band_layout* band, const double* d_t_band, double* c,
+                          double* cc, int32_t k, int32_t it, double* trace, int32_t* assign_band,
+                          unsigned long long* nan_row, void* ws, size_t ws_bytes, fb_stream_t stream);
+/* 1 when fb_kmeans_step_banded can run this shape. */
+int fb_kmeans_banded_supported(const fb_normalized* nm, int32_t k);
 
 /* The two halves of fb_kmeans_step, for row-sharded data: the partial writes this shard's
  * TᵀA (d × k row-major) and integer cluster sizes (k) and its objective into trace[it];

@@ -58,7 +58,7 @@ class FbBandLayout(ctypes.Structure):
     _fields_ = [
         ("n_bands", c_i32),
         ("perm", c_vp),
-        ("fk", c_vp),
+        ("fk", c_vp * FB_MAX_PARTS),
         ("s", c_vp),
     ]
 
@@ -83,8 +83,12 @@ _SIGS = {
     "fb_lmm_workspace_bytes": (c_size, [_P, c_i32]),
     "fb_lmm": (c_i32, [_P, c_vp, c_i32, c_vp, c_vp, c_size, c_vp]),
     "fb_band_build_workspace_bytes": (c_size, [c_i64]),
+    "fb_band_fk_stride": (c_i64, [c_i64]),
     "fb_band_build": (c_i32, [_P, c_i32, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "fb_lmm_banded": (c_i32, [_P, _PB, c_vp, c_i32, c_vp, c_vp, c_size, c_vp]),
+    "fb_scatter_i32": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "fb_kmeans_banded_supported": (c_i32, [_P, c_i32]),
+    "fb_kmeans_step_banded": (c_i32, [_P, _PB, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "fb_row_sums_workspace_bytes": (c_size, [_P]),
     "fb_row_sums": (c_i32, [_P, c_vp, c_vp, c_size, c_vp]),
     "fb_wt_workspace_bytes": (c_size, [_P, c_i32]),

@@ -172,6 +172,11 @@ __global__ void gather_i32_kernel(const int32_t* in, const int32_t* idx, int64_t
     out[i] = in[idx[i]];
 }
 
+__global__ void scatter_i32_kernel(const int32_t* in, const int32_t* idx, int64_t n, int32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[idx[i]] = in[i];
+}
+
 __global__ void mirror_upper_kernel(double* a, int64_t d) {
   const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (e >= d * d) return;
@@ -308,11 +313,13 @@ size_t fb_band_build_workspace_bytes(int64_t n) {
   return fb::fk_sort_workspace_bytes(n) + 2 * align256(static_cast<size_t>(n > 0 ? n : 1) * 4) + 256;
 }
 
+int64_t fb_band_fk_stride(int64_t n) { return (n + 63) & ~int64_t(63); }
+
 int fb_band_build(const fb_normalized* nm, int32_t n_bands, int32_t* perm, int32_t* fk_band, double* s_band,
                   void* ws, size_t ws_bytes, fb_stream_t stream) {
   int st = check_nm(nm);
   if (st) return st;
-  if (nm->q != 1) return fail(FB_ERR_ARG, "band_build: needs exactly one attribute table (q=%d)", nm->q);
+  if (nm->q < 1) return fail(FB_ERR_ARG, "band_build: needs an attribute table (q=%d)", nm->q);
   if (n_bands < 1 || n_bands > 4096) return fail(FB_ERR_ARG, "band_build: n_bands=%d outside [1, 4096]", n_bands);
   const int64_t n = nm->n_s;
   if (n == 0) return FB_OK;
@@ -329,8 +336,10 @@ int fb_band_build(const fb_normalized* nm, int32_t n_bands, int32_t* perm, int32
   cudaError_t e = fb::launch_fk_sort(band, n, n_bands, perm, band_sorted, sort_ws, ws_bytes - 2 * ib, cs(stream),
                                      g_num_sms);
   if (e != cudaSuccess) return cuda_status(e, "band_build(sort)");
-  gather_i32_kernel<<<g_num_sms * 8, 256, 0, cs(stream)>>>(p.fk, perm, n, fk_band);
-  FB_LAUNCHED();
+  for (int q = 0; q < nm->q; ++q) {
+    gather_i32_kernel<<<g_num_sms * 8, 256, 0, cs(stream)>>>(nm->part[q].fk, perm, n, fk_band + q * fb_band_fk_stride(n));
+    FB_LAUNCHED();
+  }
   if (nm->d_s > 0) {
     e = fb::launch_gather_rows(nm->s, nm->d_s, nullptr, perm, n, nm->d_s, s_band, nm->d_s, cs(stream), g_num_sms);
     if (e != cudaSuccess) return cuda_status(e, "band_build(gather)");
@@ -338,11 +347,19 @@ int fb_band_build(const fb_normalized* nm, int32_t n_bands, int32_t* perm, int32
   return cuda_status(cudaGetLastError(), "band_build");
 }
 
+int fb_scatter_i32(const int32_t* in, const int32_t* perm, int64_t n, int32_t* out, fb_stream_t stream) {
+  if (n < 0 || (n > 0 && (!in || !perm || !out))) return fail(FB_ERR_ARG, "scatter_i32: bad argument");
+  if (n == 0) return FB_OK;
+  scatter_i32_kernel<<<g_num_sms * 8, 256, 0, cs(stream)>>>(in, perm, n, out);
+  FB_LAUNCHED();
+  return cuda_status(cudaGetLastError(), "scatter_i32");
+}
+
 int fb_lmm_banded(const fb_normalized* nm, const fb_band_layout* band, const double* x, int32_t d_x, double* out,
                   void* ws, size_t ws_bytes, fb_stream_t stream) {
   int st = check_nm(nm);
   if (st) return st;
-  if (!band || nm->q != 1 || nm->d_s < 1 || nm->d_s > 32 || nm->n_s == 0 || !band->perm || !band->fk || !band->s)
+  if (!band || nm->q != 1 || nm->d_s < 1 || nm->d_s > 32 || nm->n_s == 0 || !band->perm || !band->fk[0] || !band->s)
     return fb_lmm(nm, x, d_x, out, ws, ws_bytes, stream);
   if (d_x < 1) return fail(FB_ERR_SHAPE, "lmm: d_x=%d", d_x);
   if (!x || !out) return fail(FB_ERR_ARG, "lmm: NULL pointer");
@@ -360,7 +377,7 @@ int fb_lmm_banded(const fb_normalized* nm, const fb_band_layout* band, const dou
     if (e != cudaSuccess) return cuda_status(e, "lmm(z)");
     // out = S · X[0:d_s, c0:c0+w] + z[fk]   (rewrite.py:186-190), rows visited band by band
     if (fb::lmm_band_supported(nm->d_s, w, d_x, out + c0)) {
-      e = fb::launch_lmm_band(band->s, band->fk, band->perm, nm->n_s, nm->d_s, x + c0, w, d_x, z, zst, p.n_r,
+      e = fb::launch_lmm_band(band->s, band->fk[0], band->perm, nm->n_s, nm->d_s, x + c0, w, d_x, z, zst, p.n_r,
                               out + c0, d_x, cs(stream), g_num_sms);
     } else {
       const int32_t* fks[1] = {p.fk};
@@ -934,13 +951,11 @@ size_t fb_kmeans_workspace_bytes(const fb_normalized* nm, int32_t k) {
 
 static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const double* c, const double* cc,
                                int32_t k, int32_t it, double* trace, int32_t* assign, unsigned long long* nan_row,
-                               double* tta_out, int32_t* sizes_out, void* ws, size_t ws_bytes, fb_stream_t stream);
+                               double* tta_out, int32_t* sizes_out, void* ws, size_t ws_bytes, fb_stream_t stream,
+                               const fb_band_layout* band = nullptr);
 
-int fb_kmeans_step(const fb_normalized* nm, const double* d_t, double* c, double* cc, int32_t k, int32_t it,
-                   double* trace, int32_t* assign, unsigned long long* nan_row, void* ws, size_t ws_bytes,
-                   fb_stream_t stream) {
-  int st = kmeans_partial_impl(nm, d_t, c, cc, k, it, trace, assign, nan_row, nullptr, nullptr, ws, ws_bytes, stream);
-  if (st) return st;
+static int kmeans_finish(const fb_normalized* nm, double* c, double* cc, int32_t k, void* ws, size_t ws_bytes,
+                         fb_stream_t stream) {
   // the partial left TᵀA and the sizes at the head of the workspace
   const int64_t d = total_cols(nm);
   Carver cv{static_cast<char*>(ws), ws_bytes};
@@ -949,6 +964,31 @@ int fb_kmeans_step(const fb_normalized* nm, const double* d_t, double* c, double
   double* tta = cv.take<double>(static_cast<size_t>(d) * k);
   int32_t* sizes = cv.take<int32_t>(k);
   return cuda_status(fb::launch_kmeans_update(c, tta, sizes, static_cast<int>(d), k, cc, cs(stream)), "kmeans(update)");
+}
+
+int fb_kmeans_banded_supported(const fb_normalized* nm, int32_t k) {
+  return nm && nm->q >= 1 && nm->n_s > 0 && fb::kmeans_pass_supported(nm->d_s, k, nm->q) ? 1 : 0;
+}
+
+int fb_kmeans_step_banded(const fb_normalized* nm, const fb_band_layout* band, const double* d_t_band, double* c,
+                          double* cc, int32_t k, int32_t it, double* trace, int32_t* assign_band,
+                          unsigned long long* nan_row, void* ws, size_t ws_bytes, fb_stream_t stream) {
+  if (!band || !band->perm || !band->s) return fail(FB_ERR_ARG, "kmeans_banded: NULL band layout");
+  if (!fb_kmeans_banded_supported(nm, k)) return fail(FB_ERR_ARG, "kmeans_banded: shape needs the storage-order step");
+  for (int q = 0; q < nm->q; ++q)
+    if (!band->fk[q]) return fail(FB_ERR_ARG, "kmeans_banded: band layout lacks part %d", q);
+  int st = kmeans_partial_impl(nm, d_t_band, c, cc, k, it, trace, assign_band, nan_row, nullptr, nullptr, ws, ws_bytes,
+                               stream, band);
+  if (st) return st;
+  return kmeans_finish(nm, c, cc, k, ws, ws_bytes, stream);
+}
+
+int fb_kmeans_step(const fb_normalized* nm, const double* d_t, double* c, double* cc, int32_t k, int32_t it,
+                   double* trace, int32_t* assign, unsigned long long* nan_row, void* ws, size_t ws_bytes,
+                   fb_stream_t stream) {
+  int st = kmeans_partial_impl(nm, d_t, c, cc, k, it, trace, assign, nan_row, nullptr, nullptr, ws, ws_bytes, stream);
+  if (st) return st;
+  return kmeans_finish(nm, c, cc, k, ws, ws_bytes, stream);
 }
 
 int fb_kmeans_partial(const fb_normalized* nm, const double* d_t, const double* c, const double* cc, int32_t k,
@@ -966,7 +1006,8 @@ int fb_kmeans_update(double* c, const double* tta, const int32_t* sizes, int64_t
 
 static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const double* c, const double* cc,
                                int32_t k, int32_t it, double* trace, int32_t* assign, unsigned long long* nan_row,
-                               double* tta_out, int32_t* sizes_out, void* ws, size_t ws_bytes, fb_stream_t stream) {
+                               double* tta_out, int32_t* sizes_out, void* ws, size_t ws_bytes, fb_stream_t stream,
+                               const fb_band_layout* band) {
   int st = check_nm(nm);
   if (st) return st;
   // k <= 16: one fused pass over S (fb_kmeans.cu); 17..64: T·(2C) in 16-column chunks, then the
@@ -1011,10 +1052,11 @@ static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const
     if (e != cudaSuccess) return cuda_status(e, "kmeans(memset)");
   }
   static const bool fused_on = [] { const char* v = getenv("FB_KMEANS_FUSED"); return !(v && atoi(v) == 0); }();
-  if (fused_on && nm->n_s > 0 && fb::kmeans_pass_supported(nm->d_s, k, nm->q)) {
+  if ((fused_on || band) && nm->n_s > 0 && fb::kmeans_pass_supported(nm->d_s, k, nm->q)) {
     // one pass over S (fb_kmeans.cu) after the z-passes z_q = R_q · (2C)_q
     fb::KmPass kp{};
-    kp.s = nm->s;
+    kp.s = band ? band->s : nm->s;
+    kp.rr = band != nullptr;
     kp.n = nm->n_s;
     kp.d = nm->d_s;
     kp.d_t = d_t;
@@ -1030,7 +1072,7 @@ static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const
       if (!z) return fail(FB_ERR_ARG, "kmeans: workspace too small");
       e = fb::launch_lmm_rows(p.r, p.n_r, p.d_r, c2 + zoff * k, k, k, 0, nullptr, nullptr, 0, z, kp.zst, s, g_num_sms);
       if (e != cudaSuccess) return cuda_status(e, "kmeans(z)");
-      kp.fk[i] = p.fk;
+      kp.fk[i] = band ? band->fk[i] : p.fk;
       kp.z[i] = z;
       kp.ztable_bytes[i] = static_cast<size_t>(p.n_r) * kp.zst * sizeof(double);
       kp.bins[i] = fks.bins[i];

@@ -191,6 +191,7 @@ struct KmPass {
   int it;
   unsigned long long* nan_row;
   double* sta;               // SᵀA into tta[c*k + j], c < d
+  bool rr;                   // rows in FK-band order: round-robin tiles (fb_band_layout)
 };
 bool kmeans_pass_supported(int d_s, int k, int nfk);
 size_t kmeans_pass_partials_doubles(int num_sms);

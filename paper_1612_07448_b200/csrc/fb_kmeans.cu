@@ -41,7 +41,11 @@ size_t kmeans_pass_partials_doubles(int num_sms) {
   return static_cast<size_t>(num_sms) * kConsumerWarps * (1 + kKmMaxK * kKmStaCols);
 }
 
-template <int KS, int MT, bool CG>
+// RR: the rows come from an FK-band layout (fb_band_layout: S, d_t and the FK columns in band
+// order) and the tiles are dealt round-robin, so all CTAs gather z_0 from one L2-resident band
+// at a time; every result of the pass is a sum over rows or a per-row value stored in band
+// order (the caller un-permutes the final assignment once).
+template <int KS, int MT, bool CG, bool RR = false>
 __global__ void __launch_bounds__(kRingThreads, 1) kmeans_pass_kernel(KmPass p, StreamSet ss, int stages,
                                                                   int tile_rows) {
   constexpr int NT2 = (4 * KS + 7) / 8;  // 8-column n-tiles of SᵀA over d_S
@@ -64,10 +68,10 @@ __global__ void __launch_bounds__(kRingThreads, 1) kmeans_pass_kernel(KmPass p, 
     ssz[j] = 0;
   }
 
-  TileRing ring;
+  TileRingT<RR> ring;
   ring.init(buf, stages, tile_rows, p.n);
   ring.start(ss);  // __syncthreads: xs / ccs / ssz visible
-  if (ring.service<false, CG>(ss)) return;
+  if (ring.template service<false, CG>(ss)) return;
 
   const int lane = lane_id();
   const int g = lane >> 2, t = lane & 3;
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) kmeans_pass_kernel(KmPass p, 
 
   for (int64_t kt = 0; kt < ring.count(); ++kt) {
     const int cur = ring.acquire(ss, kt);
-    const int64_t tile = ring.tile_begin + kt;
+    const int64_t tile = ring.tile_of(kt);
     const int rows = ring.rows_of(tile);
     const int64_t r0 = tile * tile_rows;
     const double* S = reinterpret_cast<const double*>(ring.stage_ptr(cur, ss, 0));
@@ -183,6 +187,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) kmeans_pass_kernel(KmPass p, 
           bj = oj;
         }
       }
+      bj = bj < k ? bj : 0;  // a row of NaN distances compares false everywhere: keep the indices in range
       const int best = live ? bj : -1;  // lane my_row (part 0) owns row my_row's result
       if (live && my_part == 0) {
         const int64_t gr = r0 + r;
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) kmeans_pass_kernel(KmPass p, 
   if (tid == 0) *p.counter = 0u;
 }
 
-template <int KS, int MT, bool CG>
+template <int KS, int MT, bool CG, bool RR = false>
 static cudaError_t launch_km(const KmPass& p, cudaStream_t st, int num_sms) {
   const int tile_rows = kConsumerWarps * 8 * MT;
   StreamSet ss{};
@@ -294,7 +299,7 @@ static cudaError_t launch_km(const KmPass& p, cudaStream_t st, int num_sms) {
   if (stages > 8) stages = 8;
   if (stages < 2) return cudaErrorNotSupported;
   const size_t smem = head + kRingHeader + static_cast<size_t>(stages) * ss.stage_bytes;
-  auto kern = kmeans_pass_kernel<KS, MT, CG>;
+  auto kern = kmeans_pass_kernel<KS, MT, CG, RR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int64_t ntiles = (p.n + tile_rows - 1) / tile_rows;
@@ -304,19 +309,19 @@ static cudaError_t launch_km(const KmPass& p, cudaStream_t st, int num_sms) {
   return cudaGetLastError();
 }
 
-template <int MT, bool CG>
+template <int MT, bool CG, bool RR = false>
 static cudaError_t launch_km_ks(const KmPass& p, cudaStream_t st, int num_sms) {
   {
     switch ((p.d + 3) / 4) {
-      case 0: return launch_km<0, MT, CG>(p, st, num_sms);
-      case 1: return launch_km<1, MT, CG>(p, st, num_sms);
-      case 2: return launch_km<2, MT, CG>(p, st, num_sms);
-      case 3: return launch_km<3, MT, CG>(p, st, num_sms);
-      case 4: return launch_km<4, MT, CG>(p, st, num_sms);
-      case 5: return launch_km<5, MT, CG>(p, st, num_sms);
-      case 6: return launch_km<6, MT, CG>(p, st, num_sms);
-      case 7: return launch_km<7, MT, CG>(p, st, num_sms);
-      case 8: return launch_km<8, MT, CG>(p, st, num_sms);
+      case 0: return launch_km<0, MT, CG, RR>(p, st, num_sms);
+      case 1: return launch_km<1, MT, CG, RR>(p, st, num_sms);
+      case 2: return launch_km<2, MT, CG, RR>(p, st, num_sms);
+      case 3: return launch_km<3, MT, CG, RR>(p, st, num_sms);
+      case 4: return launch_km<4, MT, CG, RR>(p, st, num_sms);
+      case 5: return launch_km<5, MT, CG, RR>(p, st, num_sms);
+      case 6: return launch_km<6, MT, CG, RR>(p, st, num_sms);
+      case 7: return launch_km<7, MT, CG, RR>(p, st, num_sms);
+      case 8: return launch_km<8, MT, CG, RR>(p, st, num_sms);
       default: return cudaErrorNotSupported;
     }
   }
@@ -340,6 +345,7 @@ cudaError_t launch_kmeans_pass(const KmPass& p, cudaStream_t st, int num_sms) {
   for (int q = 0; q < p.nfk; ++q) zmax = p.ztable_bytes[q] > zmax ? p.ztable_bytes[q] : zmax;
   cudaError_t e = cudaMemsetAsync(p.counter, 0, sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
+  if (p.rr) return launch_km_ks<4, true, true>(p, st, num_sms);  // band layouts exist only for big z tables
   // uniform keys into a table far beyond L1: L1-bypassing gathers (as the LMM S pass)
   return zmax > (32u << 20) ? launch_km_cg<true>(p, st, num_sms) : launch_km_cg<false>(p, st, num_sms);
 }

@@ -15,6 +15,7 @@ to what the reference itself does on tiny host matrices: the seeded NumPy RNG dr
 """
 
 import collections
+import ctypes
 import os
 import time
 import warnings
@@ -422,6 +423,9 @@ def _take_rows(nm, idx):
     return out
 
 
+_BAND_MIN_ITERS = int(os.environ.get("FB_KMEANS_BAND_MIN_ITERS", "8"))
+
+
 def kmeans(m, cfg):
     """Matrix-form K-Means (ml.py:257-285); centroids are the columns of a d × k matrix.
 
@@ -449,18 +453,48 @@ def kmeans(m, cfg):
     d_t = row_sums(scalar_fn(nm, np.square, counter), counter).reshape(-1).contiguous()  # rowSums(T²) (ml.py:272)
     for _, f in nm.blocks:  # two_t = 2·T (ml.py:273), folded into T·(2C) on the device
         counter.tally(f.numel(), 0)
-    cc = _col_sq_sums(c)
-    trace = torch.zeros(cfg.iterations, dtype=torch.float64, device=dev)
-    assign = torch.empty(n, dtype=torch.int32, device=dev)
-    nan_row = torch.full((1,), -1, dtype=torch.int64, device=dev)
-    ws = _ws(so.fb_kmeans_workspace_bytes(cs, k))
+    c0 = c.clone()
+    # rows through the cached FK-band layout when part 0's z table would not stay in L2: the loop
+    # then stores nothing in row order (objective, sizes, histograms and SᵀA are sums over rows),
+    # and the last assignment is brought back to storage order once. Built on first use when the
+    # run is long enough to pay for it (FB_KMEANS_BAND_MIN_ITERS), reused afterwards.
+    band = None
+    if "band" in nm._cache or cfg.iterations >= _BAND_MIN_ITERS:
+        band = nm.kmeans_band_layout(k)
+
+    def run(band):
+        cc = _col_sq_sums(c)
+        trace = torch.zeros(cfg.iterations, dtype=torch.float64, device=dev)
+        assign = torch.empty(n, dtype=torch.int32, device=dev)
+        nan_row = torch.full((1,), -1, dtype=torch.int64, device=dev)
+        ws = _ws(so.fb_kmeans_workspace_bytes(cs, k))
+        if band is not None:
+            bst, perm = band[0], band[1]
+            d_b = torch.empty_like(d_t)
+            _lib.check(so.fb_gather_rows_i32(D.ptr(d_t), 1, D.ptr(perm), n, 1, D.ptr(d_b), 1, st))
+            a_b = torch.empty_like(assign)
+        for it in range(cfg.iterations):
+            if band is not None:
+                _lib.check(so.fb_kmeans_step_banded(cs, ctypes.byref(bst), D.ptr(d_b), D.ptr(c), D.ptr(cc), k, it,
+                                                    D.ptr(trace), D.ptr(a_b), D.ptr(nan_row), ws.data_ptr(),
+                                                    ws.numel(), st))
+            else:
+                _lib.check(so.fb_kmeans_step(cs, D.ptr(d_t), D.ptr(c), D.ptr(cc), k, it, D.ptr(trace), D.ptr(assign),
+                                             D.ptr(nan_row), ws.data_ptr(), ws.numel(), st))
+        if band is not None:
+            _lib.check(so.fb_scatter_i32(D.ptr(a_b), D.ptr(perm), n, D.ptr(assign), st))
+        return trace, assign, int(nan_row.item())
+
+    trace, assign, bad = run(band)
+    if bad != -1 and band is not None:
+        # a NaN row: the reference reports the first one in row order (kernel.py:327-339), which the
+        # band order cannot tell — repeat the run in storage order for the exact row
+        c.copy_(c0)
+        trace, assign, bad = run(None)
     for it in range(cfg.iterations):
-        _lib.check(so.fb_kmeans_step(cs, D.ptr(d_t), D.ptr(c), D.ptr(cc), k, it, D.ptr(trace), D.ptr(assign),
-                                     D.ptr(nan_row), ws.data_ptr(), ws.numel(), st))
         _tally_lmm(counter, nm, k)
         counter.tally(0, n * k)  # row_min_mask
         _tally_tmm(counter, nm, k)
-    bad = int(nan_row.item())
     wall = time.perf_counter() - t0
     if bad != -1:  # (iteration << 40) | row of the first NaN row of the first NaN iteration
         raise NumericError(f"row_min_mask: NaN in row {bad & ((1 << 40) - 1)}")

@@ -330,44 +330,79 @@ class NormalizedMatrix:
             if st is not None:
                 st.part[i].perm, st.part[i].fk_sorted = D.ptr(perm), D.ptr(fks)
 
-    # FK-band layout for wide-X LMMs: off by default (0). Measured at c2 (profiles/
-    # r02_lmm16_experiments.txt): DRAM traffic of the S pass drops 7.6 -> 6.1 GB, but the permuted
-    # 128-byte output rows cost the DRAM what the z misses did (op 1.45 -> 1.42 ms) for one more
-    # copy of S in HBM. FB_LMM_BAND_MIN_MB=<MB> enables it for z = R·X tables above that size.
+    # FK-band layout (fb_band_layout): a cached copy of S and the FK columns grouped into key bands
+    # of part 0, so a pass over S gathers z_0 = R_0·X from one L2-resident slice at a time. Both
+    # users are OFF by default — measured on B200 (profiles/r02_lmm16_experiments.txt) the layout
+    # removes the z misses but not the time:
+    # * wide-X LMM (FB_LMM_BAND_MIN_MB=<MB> enables): at c2 X100x16 the S pass's DRAM traffic drops
+    #   7.6 -> 6.1 GB, but the permuted 128-byte output rows cost the DRAM what the z misses did
+    #   (op 1.45 -> 1.42 ms; 1.12 ms with the same rows stored in band order);
+    # * fused K-Means pass (FB_KMEANS_BAND_MIN_MB=<MB> enables; nothing is stored in permuted order
+    #   inside the loop, the build takes 1.4 ms at c4): 1.077 vs 1.070 ms per c4 iteration — the
+    #   pass is bound by its consumers' per-tile chain (argmin, histogram REDs, one-hot DMMAs), not
+    #   by the gathers.
     BAND_MIN_BYTES = int(float(os.environ.get("FB_LMM_BAND_MIN_MB", "0")) * (1 << 20))
+    BAND_KMEANS_MIN_BYTES = int(float(os.environ.get("FB_KMEANS_BAND_MIN_MB", "0")) * (1 << 20))
     BAND_BYTES = int(float(os.environ.get("FB_LMM_BAND_MB", "16")) * (1 << 20))
 
-    def band_layout(self, d_x):
-        """``fb_band_layout`` for a wide-X LMM, or None when the pass should stay in storage order.
-
-        Built once (cached, like the FK-sorted order): PK-FK matrices with d_S <= 32 whose
-        z = R·X table (n_R × 16 doubles) exceeds ``BAND_MIN_BYTES``, for X widths the band body
-        covers (multiples of 8). Costs one extra copy of S and of the FK column in HBM.
-        """
-        if self.variant != PKFK or self.transposed or self.has_csr or self.blocks[0][0] is not None or len(self.indicator_blocks) != 1:
-            return None
-        if d_x < 8 or d_x % 8 or not self.BAND_MIN_BYTES:
-            return None
-        s = self.blocks[0][1]
-        e, r = self.indicator_blocks[0]
-        n, d = s.shape
-        zbytes = r.shape[0] * 128
-        if not (1 <= d <= 32) or n == 0 or zbytes < self.BAND_MIN_BYTES:
-            return None
+    def _band(self):
+        """(struct, perm, fk_band, s_band) of this matrix, built once (bands sized for 128-byte z rows)."""
         band = self._cache.get("band")
         if band is None:
             so = _lib.lib()
-            n_bands = max(2, min(4096, -(-zbytes // self.BAND_BYTES)))
+            s = self.blocks[0][1]
+            parts = self.indicator_blocks
+            n = s.shape[0]
+            zbytes = parts[0][1].shape[0] * 128
+            n_bands = max(2, min(4096, -(-zbytes // max(1, self.BAND_BYTES))))
             perm = torch.empty(n, dtype=torch.int32, device=s.device)
-            fkb = torch.empty(n, dtype=torch.int32, device=s.device)
+            fkb = torch.empty((len(parts), so.fb_band_fk_stride(n)), dtype=torch.int32, device=s.device)
             sb = torch.empty_like(s)
             ws = D.workspace(so.fb_band_build_workspace_bytes(n))
             _lib.check(so.fb_band_build(self.c_struct(), n_bands, D.ptr(perm), D.ptr(fkb), D.ptr(sb),
                                         ws.data_ptr(), ws.numel(), D.stream_handle()))
-            st = _lib.FbBandLayout(n_bands, D.ptr(perm), D.ptr(fkb), D.ptr(sb))
-            band = (st, perm, fkb, sb)
+            st = _lib.FbBandLayout()
+            st.n_bands, st.perm, st.s = n_bands, D.ptr(perm), D.ptr(sb)
+            for q in range(len(parts)):
+                st.fk[q] = D.ptr(fkb[q])
+            band = (st, perm, fkb[:, :n], sb)
             self._cache["band"] = band
-        return ctypes.byref(band[0])
+        return band
+
+    def _bandable(self):
+        if self.variant not in (PKFK, STAR) or self.transposed or self.has_csr or self.blocks[0][0] is not None:
+            return False
+        s = self.blocks[0][1]
+        return len(self.indicator_blocks) >= 1 and 1 <= s.shape[1] <= 32 and s.shape[0] > 0
+
+    def band_layout(self, d_x):
+        """``fb_band_layout`` for a wide-X LMM, or None when the pass should stay in storage order.
+
+        PK-FK matrices with d_S <= 32 whose z = R·X table (n_R × 16 doubles) exceeds
+        ``BAND_MIN_BYTES`` (0 = never), for X widths the band body covers (multiples of 8).
+        Costs one extra copy of S and of the FK column in HBM.
+        """
+        if not self._bandable() or len(self.indicator_blocks) != 1 or not self.BAND_MIN_BYTES:
+            return None
+        if d_x < 8 or d_x % 8 or self.indicator_blocks[0][1].shape[0] * 128 < self.BAND_MIN_BYTES:
+            return None
+        return ctypes.byref(self._band()[0])
+
+    def kmeans_band_layout(self, k):
+        """The band layout for the fused K-Means pass (k <= 16), or None.
+
+        Used when part 0's z table (n_R × even(k) doubles) exceeds ``BAND_KMEANS_MIN_BYTES`` and is
+        the largest of the parts (the bands follow part 0's keys).
+        """
+        if not self._bandable() or not self.BAND_KMEANS_MIN_BYTES or k > 16:
+            return None
+        rows = [f.shape[0] for _, f in self.indicator_blocks]
+        zrow = 8 * max(2, (k + 1) & ~1)
+        if rows[0] != max(rows) or rows[0] * zrow < self.BAND_KMEANS_MIN_BYTES:
+            return None
+        if not _lib.lib().fb_kmeans_banded_supported(self.c_struct(), k):
+            return None
+        return self._band()
 
     def __repr__(self):
         n, d = self.shape

@@ -264,3 +264,40 @@ def test_gnmf_wide_r_vs_oracle(r):
     _close(out.factors[0], w)
     _close(out.factors[1], h)
     _close(out.objective, obj)
+
+
+def test_kmeans_band_layout_matches_storage_order(monkeypatch):
+    """The fused K-Means pass over the FK-band layout (round-robin tiles, band-ordered S / FK / d_t)
+    gives the storage-order run's assignments bit for bit and its centroids / trace within 1e-9."""
+    fb = _fb()
+    from paper_1612_07448_b200 import ml as fbml
+    from paper_1612_07448_b200.normmat import NormalizedMatrix
+
+    rng, s, parts = _c1_like(77, n_s=120_003, d_s=6, n_r=5000, d_r=5, star=True)
+    cfg = fb.TrainConfig(iterations=6, k=10, rng_seed=5)
+    monkeypatch.setattr(NormalizedMatrix, "BAND_KMEANS_MIN_BYTES", 0)
+    nm0, ref = _both(s, parts)
+    plain = fb.kmeans(nm0, cfg)
+    assert "band" not in nm0._cache
+    monkeypatch.setattr(NormalizedMatrix, "BAND_KMEANS_MIN_BYTES", 1)
+    monkeypatch.setattr(NormalizedMatrix, "BAND_BYTES", 128 * 700)
+    monkeypatch.setattr(fbml, "_BAND_MIN_ITERS", 1)
+    nm, _ = _both(s, parts)
+    banded = fb.kmeans(nm, cfg)
+    assert "band" in nm._cache and nm._cache["band"][0].n_bands >= 2
+    st, perm, fkb, sb = nm._cache["band"]
+    p = perm.cpu().numpy()
+    for q, (e, _) in enumerate(nm.parts):
+        np.testing.assert_array_equal(fkb[q].cpu().numpy(), e.target_numpy()[p])
+    np.testing.assert_array_equal(banded.assignment.cpu().numpy(), plain.assignment.cpu().numpy())
+    _close(banded.centroids, plain.centroids, 1e-12)
+    _close(banded.objective, plain.objective, 1e-12)
+    c, obj, _ = O.kmeans(ref, 10, 6, 5)
+    _close(banded.centroids, c)
+    _close(banded.objective, obj)
+    # a NaN row is still reported in row order (the run repeats in storage order)
+    s2 = s.copy()
+    s2[4321, 2] = np.nan
+    nm2, _ = _both(s2, parts)
+    with pytest.raises(fb.NumericError, match="row 4321"):
+        fb.kmeans(nm2, cfg)

@@ -359,7 +359,7 @@ def test_lmm_band_layout_bitwise_equal(monkeypatch, n_s, d_s, n_r, d_r, d_x, zip
     tgt = nm.k.target_numpy()
     band = tgt * st.n_bands // nm.parts[0][1].shape[0]
     np.testing.assert_array_equal(p, np.argsort(band, kind="stable"))
-    np.testing.assert_array_equal(fkb.cpu().numpy(), tgt[p])
+    np.testing.assert_array_equal(fkb[0].cpu().numpy(), tgt[p])
     np.testing.assert_array_equal(sb.cpu().numpy(), s[p])
     np.testing.assert_array_equal(banded, plain)
     again = fb.lmm(nm, x)  # cached layout reused
