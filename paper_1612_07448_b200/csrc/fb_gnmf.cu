@@ -35,10 +35,18 @@ bool nmf_pass_supported(int d_s, int r, int nfk) {
 }
 
 // shared memory ahead of the ring: H_S, cph, the per-warp row tiles, the hot bins
-__host__ __device__ inline size_t nmf_head_bytes(int ks, int nt, int nfk) {
+// Hot bins: per-warp private copies (plain read-add-write by the key group's leader lane — no
+// two lanes of a warp hold the same key after __match_any_sync) when they fit in 48 KB, else one
+// copy per CTA updated with shared-memory atomics.
+__host__ __device__ inline int nmf_hot_copies(int r, int nfk) {
+  return static_cast<size_t>(kConsumerWarps) * nfk * kNmfHot * r * 8 <= 48 * 1024 ? kConsumerWarps : 1;
+}
+
+__host__ __device__ inline size_t nmf_head_bytes(int ks, int nt, int nfk, int r) {
   const int dpad = ks > 0 ? 4 * ks : 4;
   const size_t dbl = static_cast<size_t>(dpad) * (8 * nt + 4) + kNmfMaxR * kNmfMaxR +
-                     static_cast<size_t>(kConsumerWarps) * 32 * kNmfPitch + static_cast<size_t>(nfk) * kNmfHot * kNmfMaxR;
+                     static_cast<size_t>(kConsumerWarps) * 32 * kNmfPitch +
+                     static_cast<size_t>(nmf_hot_copies(r, nfk)) * nfk * kNmfHot * r;
   return (dbl * 8 + 127) & ~size_t(127);
 }
 
@@ -56,8 +64,10 @@ __global__ void __launch_bounds__(kRingThreads, 1) nmf_wpass_kernel(NmfPass p, S
   double* xs = reinterpret_cast<double*>(smem);  // H_S, dpad × ldxs
   double* cphs = xs + dpad * ldxs;              // cph, R × R (ld kNmfMaxR)
   double* tiles = cphs + kNmfMaxR * kNmfMaxR;   // [warp][32][kNmfPitch]
-  double* hot = tiles + kConsumerWarps * 32 * kNmfPitch;  // [part][kNmfHot][kNmfMaxR]
-  char* buf = smem + nmf_head_bytes(ks, NT, p.nfk);
+  double* hot = tiles + kConsumerWarps * 32 * kNmfPitch;  // [copy][part][kNmfHot][R]
+  const int hcopies = nmf_hot_copies(R, p.nfk);
+  const int hot_doubles = p.nfk * kNmfHot * R;  // per copy
+  char* buf = smem + nmf_head_bytes(ks, NT, p.nfk, R);
   for (int i = threadIdx.x; i < dpad * ldxs; i += blockDim.x) {
     const int k = i / ldxs, c = i % ldxs;
     xs[i] = (k < d && c < R) ? p.h[k * R + c] : 0.0;
@@ -66,7 +76,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) nmf_wpass_kernel(NmfPass p, S
     const int a = i / kNmfMaxR, b = i % kNmfMaxR;
     cphs[i] = (a < R && b < R) ? p.cph[a * R + b] : 0.0;
   }
-  for (int i = threadIdx.x; i < p.nfk * kNmfHot * kNmfMaxR; i += blockDim.x) hot[i] = 0.0;
+  for (int i = threadIdx.x; i < hcopies * hot_doubles; i += blockDim.x) hot[i] = 0.0;
 
   TileRing ring;
   ring.init(buf, stages, tile_rows, p.n);
@@ -81,6 +91,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) nmf_wpass_kernel(NmfPass p, S
   const bool ragged_k = (d & 3) != 0;
   double* tile = tiles + warp * 32 * kNmfPitch;
   double* trow = tile + lane * kNmfPitch;
+  double* myhot = hot + (hcopies > 1 ? warp : 0) * hot_doubles;
   double sw[kMaxMts][NT][2];  // SᵀW (S column m, W column n)
   double ww[NT][NT][2];       // WᵀW
 #pragma unroll
@@ -101,6 +112,18 @@ __global__ void __launch_bounds__(kRingThreads, 1) nmf_wpass_kernel(NmfPass p, S
     const double* W = reinterpret_cast<const double*>(ring.stage_ptr(cur, ss, 1));
     __syncwarp();
     if (wrow < rows) {
+      // this lane's keys and their hot slots, fetched now so the table lookup (global memory)
+      // is back long before step 4 needs it (ncu: the group leaders stalled on it there)
+      int32_t keyq[kMaxParts], slotq[kMaxParts];
+#pragma unroll
+      for (int q = 0; q < kMaxParts; ++q) {
+        keyq[q] = -1;
+        slotq[q] = -1;
+        if (q < p.nfk && wrow + lane < rows) {
+          keyq[q] = reinterpret_cast<const int32_t*>(ring.stage_ptr(cur, ss, 2 + q))[wrow + lane];
+          if (p.nhot[q] > 0) slotq[q] = __ldg(p.hot_slot[q] + keyq[q]);
+        }
+      }
       // 1. th = Σ_q z_q[fk_q] (parts in order) + S·H_S
       double acc[MT][NT][2];
 #pragma unroll
@@ -181,7 +204,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) nmf_wpass_kernel(NmfPass p, S
 #pragma unroll
       for (int q = 0; q < kMaxParts; ++q) {
         if (q >= p.nfk) break;
-        const int32_t key = live ? reinterpret_cast<const int32_t*>(ring.stage_ptr(cur, ss, 2 + q))[rl] : -1;
+        const int32_t key = keyq[q];  // -1 on dead rows
         if (p.nhot[q] == 0) {
           if (live) {
             double* dst = p.bins[q] + static_cast<int64_t>(key) * R;
@@ -200,11 +223,16 @@ __global__ void __launch_bounds__(kRingThreads, 1) nmf_wpass_kernel(NmfPass p, S
 #pragma unroll
             for (int j = 0; j < R; ++j) v[j] += pr[j];
           }
-          const int slot = p.hot_slot[q][key];
+          const int slot = slotq[q];
           if (slot >= 0) {
-            double* dst = hot + (q * kNmfHot + slot) * kNmfMaxR;
+            double* dst = myhot + (q * kNmfHot + slot) * R;
+            if (hcopies > 1) {
 #pragma unroll
-            for (int j = 0; j < R; ++j) atomicAdd(dst + j, v[j]);
+              for (int j = 0; j < R; ++j) dst[j] += v[j];
+            } else {
+#pragma unroll
+              for (int j = 0; j < R; ++j) atomicAdd(dst + j, v[j]);
+            }
           } else {
             double* dst = p.bins[q] + static_cast<int64_t>(key) * R;
 #pragma unroll
@@ -269,7 +297,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) nmf_wpass_kernel(NmfPass p, S
   for (int q = 0; q < p.nfk; ++q)
     for (int i = tid; i < p.nhot[q] * R; i += kConsumerThreads) {
       const int slot = i / R, j = i % R;
-      const double v = hot[(q * kNmfHot + slot) * kNmfMaxR + j];
+      double v = 0.0;
+      for (int c = 0; c < hcopies; ++c) v += hot[c * hot_doubles + (q * kNmfHot + slot) * R + j];  // warps in order
       if (v != 0.0) red_add(p.bins[q] + static_cast<int64_t>(p.hot_key[q][slot]) * R + j, v);
     }
 }
@@ -315,7 +344,7 @@ static cudaError_t launch_nmf_cfg(const NmfPass& p, cudaStream_t st, int num_sms
   ss.ngather = p.nfk;
   for (int i = 0; i < ss.count; ++i) ss.pitch[i] = ss.row_bytes[i];
   stream_layout(ss, tile_rows, p.n);
-  const size_t head = nmf_head_bytes((p.d + 3) / 4, NT, p.nfk);
+  const size_t head = nmf_head_bytes((p.d + 3) / 4, NT, p.nfk, R);
   const size_t budget = 224 * 1024;
   int stages = static_cast<int>((budget - head - kRingHeader) / ss.stage_bytes);
   if (stages > 8) stages = 8;

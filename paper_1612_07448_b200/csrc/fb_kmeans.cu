@@ -112,24 +112,38 @@ __global__ void __launch_bounds__(kRingThreads, 1) kmeans_pass_kernel(KmPass p, 
       // rows, with or without handing the z rows back to the gatherers early, measured 2-5%
       // slower at c4.)
       double acc[MT][2][2];
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-#pragma unroll
-      for (int q = 0; q < kMaxParts; ++q) {
-        if (q >= p.nfk) break;
-        const double* zq = reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, q)) + (wrow + g) * zst;
+      {  // part 0 initialises (0 + z_0 = z_0), the others add: every load of a part issues before its adds
+        const double* z0 = reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, 0)) + (wrow + g) * zst;
+        const bool has0 = p.nfk > 0;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
             const int c = 8 * nt + 2 * t;
-            if (c < zst) {
-              const double2 zv = *reinterpret_cast<const double2*>(zq + 8 * mt * zst + c);
-              acc[mt][nt][0] += zv.x;
-              acc[mt][nt][1] += zv.y;
-            }
+            double2 zv = make_double2(0.0, 0.0);
+            if (has0 && c < zst) zv = *reinterpret_cast<const double2*>(z0 + 8 * mt * zst + c);
+            acc[mt][nt][0] = zv.x;
+            acc[mt][nt][1] = zv.y;
+          }
+      }
+#pragma unroll
+      for (int q = 1; q < kMaxParts; ++q) {
+        if (q >= p.nfk) break;
+        const double* zq = reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, q)) + (wrow + g) * zst;
+        double2 zv[MT][2];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const int c = 8 * nt + 2 * t;
+            zv[mt][nt] = c < zst ? *reinterpret_cast<const double2*>(zq + 8 * mt * zst + c) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            acc[mt][nt][0] += zv[mt][nt].x;
+            acc[mt][nt][1] += zv[mt][nt].y;
           }
       }
       if constexpr (KS > 0) {
@@ -166,15 +180,42 @@ __global__ void __launch_bounds__(kRingThreads, 1) kmeans_pass_kernel(KmPass p, 
       double bv = __longlong_as_double(0x7ff0000000000000ll);  // +inf
       int bj = 1 << 30;
       bool nan = false;
+      if constexpr (LPR == 1) {
+        // the lane scans all k distances of its row. A running minimum is a chain of k dependent
+        // compare + select pairs (ncu source view at c4: 41% of the consumers' stall samples sat
+        // on these lines, two warps per scheduler cannot hide it): load every distance first,
+        // then a pairwise tournament of depth 4 — the left entry of a pair holds the lower
+        // indices and wins ties, so the result is np.argmin's (lowest index of the minimum)
+        double v[kKmMaxK];
+        int ix[kKmMaxK];
 #pragma unroll
-      for (int j0 = 0; j0 < kKmMaxK; j0 += LPR) {
-        const int j = j0 + my_part;
-        if (j < k) {
-          const double v = (dt + ccs[j]) - wr[j];  // (d_t + Σc²) − (2T)·C, ml.py:276
-          nan |= isnan(v);
-          if (v < bv) {  // increasing j: ties keep the lowest index (np.argmin)
-            bv = v;
-            bj = j;
+        for (int j = 0; j < kKmMaxK; ++j) {
+          const double x = (dt + ccs[j]) - wr[j];  // (d_t + Σc²) − (2T)·C, ml.py:276
+          nan |= j < k && x != x;
+          v[j] = j < k ? x : bv;
+          ix[j] = j;
+        }
+#pragma unroll
+        for (int w = 1; w < kKmMaxK; w <<= 1)
+#pragma unroll
+          for (int j = 0; j + w < kKmMaxK; j += 2 * w) {
+            const bool right = v[j + w] < v[j];
+            v[j] = right ? v[j + w] : v[j];
+            ix[j] = right ? ix[j + w] : ix[j];
+          }
+        bv = v[0];
+        bj = ix[0];
+      } else {
+#pragma unroll
+        for (int j0 = 0; j0 < kKmMaxK; j0 += LPR) {
+          const int j = j0 + my_part;
+          if (j < k) {
+            const double v = (dt + ccs[j]) - wr[j];  // (d_t + Σc²) − (2T)·C, ml.py:276
+            nan |= isnan(v);
+            if (v < bv) {  // increasing j: ties keep the lowest index (np.argmin)
+              bv = v;
+              bj = j;
+            }
           }
         }
       }

@@ -25,7 +25,7 @@ if [ "${3:-1}" = "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv $CMD > gpurun_out/${T}_ncu_launch.log 2>&1
   echo "launch list exit $?"
   full lmm16 "-k regex:lmm_ -s 2 -c 2" python tools/c2_op.py lmm_x16 2
-  full rmm "-k regex:colreduce|lmm_|rows_wt|segsum|rth -s 6 -c 6" python tools/c2_op.py rmm_x1 3
+  full rmm "-k regex:colreduce|lmm_|rows_wt|segsum|rth -s 2 -c 4" python tools/c2_op.py rmm_x1 3
   REPS=2 full c3 "-k regex:cp_ -s 4 -c 4" python tools/cp_c3.py
   full c4 "-k regex:kmeans_|rth_ -s 6 -c 6" python tools/time_kmeans.py
   full c5 "-k regex:nmf_|rth_|narrow_gram -s 10 -c 10" python tools/time_gnmf.py
