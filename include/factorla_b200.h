@@ -171,8 +171,9 @@ int fb_fk_sort(const int32_t* fk, int64_t n, int64_t n_r, int32_t* perm, int32_t
  * d × d row-major. q = 0 (plain SᵀS) or q = 1 with perm/fk_sorted from fb_fk_sort and
  * part[0].counts set. For an even d_s <= 128 the S side is one pass over S in FK-sorted order
  * (SᵀS on the FP64 tensor cores and KᵀS as a segmented sum from the same tiles); the R side
- * is a second pass over R with B = KᵀS. Star (q >= 2) and M:N matrices go through fb_wt per
- * block column (crossprod_impl.py). */
+ * is a second pass over R with B = KᵀS. A star schema (q >= 2) is composed from one call per
+ * part on [S, K_i R_i] plus pair-count cross blocks (fb_pair_counts, fb_csr_spmm, fb_rows_wt);
+ * odd / wider S and M:N matrices go through fb_wt per block column (crossprod_impl.py). */
 size_t fb_crossprod_workspace_bytes(const fb_normalized* nm);
 int fb_crossprod(const fb_normalized* nm, const int32_t* perm, const int32_t* fk_sorted, double* out, void* ws,
                  size_t ws_bytes, fb_stream_t stream);

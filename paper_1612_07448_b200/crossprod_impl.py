@@ -81,10 +81,76 @@ def crossprod(nm, method="efficient", counter=None):
             perm, fks = fk_sorted_order(nm.blocks[1][0])
         ws = D.workspace(so.fb_crossprod_workspace_bytes(cs))
         _lib.check(so.fb_crossprod(cs, D.ptr(perm), D.ptr(fks), D.ptr(out), ws.data_ptr(), ws.numel(), st))
+    elif 2 <= nm.blocks[0][1].shape[1] <= 128 and nm.blocks[0][1].shape[1] % 2 == 0 and nm.base_rows > 0:
+        _star_crossprod_fused(nm, out, so, st)
     else:
         _star_crossprod(nm, out, so, st)
     _tally(nm, counter)
     return D.to_like(out, nm.host_io)
+
+
+def _star_crossprod_fused(nm, out, so, st):
+    """Star schema (q >= 2) on the fused two-pass kernels, the reference's efficient plan
+    (rewrite.py:263-298) block by block:
+
+    * per part i, ``fb_crossprod`` of the PK-FK sub-matrix [S, K_i R_i] gives SᵀS, Sᵀ(K_i R_i) =
+      (K_iᵀS)ᵀR_i and R_iᵀ diag(c_i) R_i (one fused pass over S in FK_i-sorted order + one pass
+      over R_i; SᵀS is recomputed per part on the tensor cores and taken from the first);
+    * per pair i < j, the cross block R_iᵀ (K_iᵀK_j) R_j through the pair counts
+      (indicator.py:144-162): ``fb_pair_counts`` → CSR P, M = P·R_j (``fb_csr_spmm``), R_iᵀ·M
+      (``fb_dense_mm``);
+    * the lower triangle is the exact mirror of the upper.
+    """
+    import ctypes
+
+    nm.ensure_sorted()
+    nm.c_struct()
+    full = nm._cache["c_struct"]
+    d = nm.base_cols
+    dev = nm.device
+    offs = [int(o) for o in nm.col_offsets()]
+    d_s = offs[1]
+    parts = nm.indicator_blocks
+    n = nm.base_rows
+    out.zero_()
+    for i, (e, f) in enumerate(parts):
+        sub = _lib.FbNormalized()
+        sub.s, sub.n_s, sub.d_s, sub.q = full.s, full.n_s, full.d_s, 1
+        sub.part[0] = full.part[i]
+        di = f.shape[1]
+        g = torch.empty((d_s + di, d_s + di), dtype=torch.float64, device=dev)
+        perm, fks = fk_sorted_order(e)
+        ws = D.workspace(so.fb_crossprod_workspace_bytes(ctypes.byref(sub)))
+        _lib.check(so.fb_crossprod(ctypes.byref(sub), D.ptr(perm), D.ptr(fks), D.ptr(g), ws.data_ptr(), ws.numel(), st))
+        c0 = offs[i + 1]
+        if i == 0:
+            out[:d_s, :d_s] = g[:d_s, :d_s]
+        out[:d_s, c0:c0 + di] = g[:d_s, d_s:]
+        out[c0:c0 + di, c0:c0 + di] = g[d_s:, d_s:]
+    for i, (ei, fi) in enumerate(parts):
+        for j in range(i + 1, len(parts)):
+            ej, fj = parts[j]
+            # rows of the pair-count matrix = the smaller table: P = K_aᵀK_b, M = P·R_b, block = R_aᵀ·M
+            flip = fj.shape[0] < fi.shape[0]
+            (ea, fa), (eb, fb_) = ((ej, fj), (ei, fi)) if flip else ((ei, fi), (ej, fj))
+            da, db = fa.shape[1], fb_.shape[1]
+            indptr = torch.empty(ea.cols + 1, dtype=torch.int64, device=dev)
+            col = torch.empty(n, dtype=torch.int64, device=dev)
+            val = torch.empty(n, dtype=torch.float64, device=dev)
+            nnz = torch.zeros(1, dtype=torch.int64, device=dev)
+            ws = D.workspace(so.fb_pair_counts_workspace_bytes(n))
+            _lib.check(so.fb_pair_counts(n, D.ptr(ea.target), D.ptr(eb.target), ea.cols, eb.cols, D.ptr(indptr),
+                                         D.ptr(col), D.ptr(val), D.ptr(nnz), ws.data_ptr(), ws.numel(), st))
+            m = torch.empty((ea.cols, db), dtype=torch.float64, device=dev)
+            _lib.check(so.fb_csr_spmm(ea.cols, D.ptr(indptr), D.ptr(col), 1, D.ptr(val), D.ptr(fb_), db, db, D.ptr(m), db,
+                                      0, st))
+            # out[off_i + c_i, off_j + c_j]: fb_rows_wt writes (weight column, table column) through strides
+            base = out.data_ptr() + 8 * (offs[i + 1] * d + offs[j + 1])
+            o_js, o_cs = (d, 1) if flip else (1, d)
+            ws = D.workspace(so.fb_rows_wt_workspace_bytes(da, db))
+            _lib.check(so.fb_rows_wt(D.ptr(fa), ea.cols, da, D.ptr(m), db, db, 1, base, o_js, o_cs, ws.data_ptr(),
+                                     ws.numel(), st))
+    _lib.check(so.fb_mirror_upper(D.ptr(out), d, st))
 
 
 def _star_crossprod(nm, out, so, st):

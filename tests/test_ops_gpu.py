@@ -223,6 +223,9 @@ CP_CASES = [
     (30_001, 72, [(2000, 16)], "uniform", 9),   # fused S pass, 3 columns per walker lane
     (20_000, 100, [(500, 10)], "zipf", 10),     # fused S pass, 4 columns per walker lane
     (10_000, 130, [(100, 4)], "uniform", 11),   # d_S > 128: the block-column path
+    (60_001, 20, [(4000, 40), (300, 60)], "uniform", 12),          # star, fused passes + pair-count cross block
+    (50_000, 6, [(200, 5), (7000, 9), (31, 3)], "zipf", 13),      # three parts: both pair orientations
+    (33_333, 8, [(1500, 16), (1500, 4)], "uniform", 14),          # equal table sizes
 ]
 
 
