@@ -604,6 +604,12 @@ def run_extras(dev, ref, parity):
                         "s_total_20_iters": round(res.wall_time_s, 4),
                         "timing": "per iteration = median over 3 trials of (wall(20 iters) - wall(1 iter)) / 19; "
                                   "total incl. seeding and rowSums(T²)"}
+    # the same star schema's crossprod (d = 120): per-part fused passes + pair-count cross blocks
+    for _ in range(2):
+        fb.crossprod(nm)
+    ms_cp4 = _events_ms(lambda: fb.crossprod(nm), 5)
+    cp4 = fb.crossprod(nm).cpu().numpy()
+    out["c4_star_crossprod"] = {"ms": round(ms_cp4, 3), "d": int(cp4.shape[0])}
     if cpu:
         it_c = 3
         gpu3 = fb.kmeans(nm, fb.TrainConfig(iterations=it_c, k=k, rng_seed=seed))
@@ -615,6 +621,10 @@ def run_extras(dev, ref, parity):
         out["c4_kmeans"]["cpu_timing"] = f"(wall({it_c} iters) - wall(1 iter)) / {it_c - 1}"
         parity["c4"] = {f"centroids_{it_c}_iters": max_rel_deviation(gpu3.centroids, c_ref),
                         f"objective_{it_c}_iters": max_rel_deviation(gpu3.objective, tr_ref)}
+        cp4_ref, t_cp4 = timed(lambda: ref.op("crossprod", rn))
+        out["c4_star_crossprod"]["cpu_ms"] = round(1e3 * t_cp4, 1)
+        parity["c4"]["star_crossprod"] = max_rel_deviation(cp4, cp4_ref)
+        parity["c4"]["star_crossprod_symmetric"] = bool(np.array_equal(cp4, cp4.T))
         del rn
     del nm, g
     torch.cuda.empty_cache()
