@@ -324,6 +324,17 @@ int fb_csr_spmm_t(int64_t rows, int64_t cols, const int64_t* indptr, const void*
                   const double* val, const double* x, int64_t ldx, int32_t k, double* y, int64_t ldy,
                   fb_stream_t stream);
 
+/* Point-wise halves of the GD loops on a transposed matrix (ml.py:207-213, 247-252 with T = M^T,
+ * where T·w and T^T·p come from fb_wt / fb_lmm): p and the summed loss from tw = T·w and y
+ * (mode 0 logistic: p = y / (1 + exp(tw)), the stable log-loss; mode 1: p = tw - y, Σp²) into
+ * trace[it]; and w += alpha·g with *diverged (start at -1) latching the first iteration that
+ * left a non-finite weight. */
+size_t fb_glm_pointwise_workspace_bytes(void);
+int fb_glm_pointwise(const double* tw, const double* y, int64_t n, int32_t mode, double* p, double* trace,
+                     int32_t it, void* ws, size_t ws_bytes, fb_stream_t stream);
+int fb_axpy_check(double alpha, const double* x, double* y, int64_t n, int32_t it, int32_t* diverged,
+                  fb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -135,6 +135,9 @@ _SIGS = {
     "fb_csr_spmm_t": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_i32, c_vp, c_vp, c_i64, c_i32, c_vp, c_i64, c_vp]),
     "fb_scalar_map": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_f64, c_vp]),
     "fb_unary_map": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp]),
+    "fb_glm_pointwise_workspace_bytes": (c_size, []),
+    "fb_glm_pointwise": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32, c_vp, c_size, c_vp]),
+    "fb_axpy_check": (c_i32, [c_f64, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
 }
 
 _lock = threading.Lock()

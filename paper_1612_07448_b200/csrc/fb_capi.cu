@@ -1310,6 +1310,22 @@ int fb_unary_map(const double* in, double* out, int64_t n, int32_t fn, fb_stream
   return cuda_status(fb::launch_unary_map(in, out, n, fn, cs(stream), g_num_sms), "unary_map");
 }
 
+size_t fb_glm_pointwise_workspace_bytes(void) { return fb::glm_pointwise_workspace_bytes(g_num_sms); }
+
+int fb_glm_pointwise(const double* tw, const double* y, int64_t n, int32_t mode, double* p, double* trace, int32_t it,
+                     void* ws, size_t ws_bytes, fb_stream_t stream) {
+  if (n < 0 || (mode != 0 && mode != 1) || it < 0) return fail(FB_ERR_ARG, "glm_pointwise: bad argument");
+  if ((n > 0 && (!tw || !y || !p)) || !trace || !ws) return fail(FB_ERR_ARG, "glm_pointwise: NULL pointer");
+  if (ws_bytes < fb_glm_pointwise_workspace_bytes()) return fail(FB_ERR_ARG, "glm_pointwise: workspace too small");
+  return cuda_status(fb::launch_glm_pointwise(tw, y, n, mode, p, trace, it, ws, cs(stream), g_num_sms), "glm_pointwise");
+}
+
+int fb_axpy_check(double alpha, const double* x, double* y, int64_t n, int32_t it, int32_t* diverged,
+                  fb_stream_t stream) {
+  if (n < 0 || (n > 0 && (!x || !y)) || !diverged) return fail(FB_ERR_ARG, "axpy_check: bad argument");
+  return cuda_status(fb::launch_axpy_check(alpha, x, y, n, it, diverged, cs(stream), g_num_sms), "axpy_check");
+}
+
 // ------------------------------------------------------------------ dense / sparse pieces (fb_dense.cu)
 int fb_dense_mm(int64_t m, int64_t n, int64_t k, const double* a, int64_t lda, int32_t ta, const double* b,
                 int64_t ldb, int32_t tb, double* c, int64_t ldc, int32_t accumulate, fb_stream_t stream) {

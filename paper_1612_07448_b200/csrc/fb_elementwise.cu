@@ -121,4 +121,88 @@ cudaError_t launch_unary_map(const double* in, double* out, int64_t n, int fn, c
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ GLM point-wise pieces
+// The drivers on a transposed normalized matrix (ml.py:199-254 with T = Mᵀ) get T·w and Tᵀ·p from
+// the factorized operators; what is left per iteration is point-wise over the n-long vectors:
+//   mode 0 (logistic): p = y / (1 + exp(tw)), loss_i = log1p(exp(-|y·tw|)) + max(-y·tw, 0)  (ml.py:207-211)
+//   mode 1 (least squares): p = tw - y, loss_i = p²                                       (ml.py:247-249)
+// Block partials of the loss are written per CTA and summed in CTA order by the last CTA
+// (deterministic); trace[it] gets the sum.
+__global__ void __launch_bounds__(256) glm_pointwise_kernel(const double* __restrict__ tw,
+                                                            const double* __restrict__ y, int64_t n, int mode,
+                                                            double* __restrict__ p, double* partials,
+                                                            unsigned* counter, double* trace, int it) {
+  __shared__ double red[256];
+  __shared__ bool last;
+  double loss = 0.0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double t = tw[i], yy = y[i];
+    if (mode == 0) {
+      p[i] = yy / (1.0 + exp(t));
+      const double m = yy * t;
+      loss += log1p(exp(-fabs(m))) + fmax(-m, 0.0);
+    } else {
+      const double r = t - yy;
+      p[i] = r;
+      loss += r * r;
+    }
+  }
+  red[threadIdx.x] = loss;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = red[0];
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += partials[b];
+    trace[it] = s;
+    *counter = 0u;
+  }
+}
+
+size_t glm_pointwise_workspace_bytes(int num_sms) { return static_cast<size_t>(num_sms) * 4 * 8 + 256; }
+
+cudaError_t launch_glm_pointwise(const double* tw, const double* y, int64_t n, int mode, double* p, double* trace,
+                                 int it, void* ws, cudaStream_t st, int num_sms) {
+  const int grid = num_sms * 4;
+  double* partials = static_cast<double*>(ws);
+  unsigned* counter = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + static_cast<size_t>(grid) * 8);
+  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  glm_pointwise_kernel<<<grid, 256, 0, st>>>(tw, y, n, mode, p, partials, counter, trace, it);
+  FB_LAUNCHED();
+  return cudaGetLastError();
+}
+
+// y += alpha·x; *diverged (start at -1) latches the first iteration whose y holds a non-finite value
+// (the reference checks np.isfinite(w).all() after every update, ml.py:213, 252).
+__global__ void __launch_bounds__(256) axpy_check_kernel(double alpha, const double* __restrict__ x,
+                                                         double* __restrict__ y, int64_t n, int it, int* diverged) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = y[i] + alpha * x[i];
+    y[i] = v;
+    bad |= !isfinite(v);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicCAS(diverged, -1, it);
+}
+
+cudaError_t launch_axpy_check(double alpha, const double* x, double* y, int64_t n, int it, int* diverged,
+                              cudaStream_t st, int num_sms) {
+  if (n <= 0) return cudaSuccess;
+  axpy_check_kernel<<<grid_for(n, 256 * 4, 8, num_sms), 256, 0, st>>>(alpha, x, y, n, it, diverged);
+  FB_LAUNCHED();
+  return cudaGetLastError();
+}
+
 }  // namespace fb

@@ -57,6 +57,11 @@ enum UnaryFn : int {
 };
 cudaError_t launch_scalar_map(const double* in, double* out, int64_t n, int op, double x,
                               cudaStream_t st, int num_sms);
+size_t glm_pointwise_workspace_bytes(int num_sms);
+cudaError_t launch_glm_pointwise(const double* tw, const double* y, int64_t n, int mode, double* p, double* trace,
+                                 int it, void* ws, cudaStream_t st, int num_sms);
+cudaError_t launch_axpy_check(double alpha, const double* x, double* y, int64_t n, int it, int* diverged,
+                              cudaStream_t st, int num_sms);
 cudaError_t launch_unary_map(const double* in, double* out, int64_t n, int fn, cudaStream_t st,
                              int num_sms);
 

@@ -132,24 +132,29 @@ def _t_glm(m, y, cfg, mode, name):
     n, d = mt.shape
     yd = _column(y, n)
     counter = OpCounter()
-    w = torch.zeros((d, 1), dtype=torch.float64, device=yd.device)
-    trace = []
+    so = _lib.lib()
+    st = D.stream_handle()
+    dev = yd.device
+    w = torch.zeros((d, 1), dtype=torch.float64, device=dev)
+    p = torch.empty((n, 1), dtype=torch.float64, device=dev)
+    trace = torch.zeros(cfg.iterations, dtype=torch.float64, device=dev)
+    diverged = torch.full((1,), -1, dtype=torch.int32, device=dev)
+    ws = torch.empty(max(int(so.fb_glm_pointwise_workspace_bytes()), 256), dtype=torch.uint8, device=dev)
+    alpha = cfg.step_size if mode == 0 else -cfg.step_size  # ml.py:212 / ml.py:251
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for it in range(cfg.iterations):
-        tw = lmm(mt, w, counter)
-        if mode == 0:
-            p = yd / (1.0 + torch.exp(tw))
-            trace.append(float(torch.sum(torch.log1p(torch.exp(-torch.abs(yd * tw))) + torch.clamp(-yd * tw, min=0.0))))
-            w = w + cfg.step_size * lmm(mt.T, p, counter)
-        else:
-            resid = tw - yd
-            trace.append(float(torch.sum(resid**2)))
-            w = w - cfg.step_size * lmm(mt.T, resid, counter)
-        if not bool(torch.isfinite(w).all()):
-            raise DivergenceError(it)
+        tw = lmm(mt, w, counter)  # T·w: the Wᵀ·T scatter path of the untransposed factors
+        # p = y / (1 + exp(tw)) and the stable log-loss, or the residual and its square sum
+        _lib.check(so.fb_glm_pointwise(D.ptr(tw), D.ptr(yd), n, mode, D.ptr(p), D.ptr(trace), it, ws.data_ptr(),
+                                       ws.numel(), st))
+        g = lmm(mt.T, p, counter)  # Tᵀ·p: an LMM gather pass
+        _lib.check(so.fb_axpy_check(alpha, D.ptr(g), D.ptr(w), d, it, D.ptr(diverged), st))
+    bad = int(diverged.item())
     wall = time.perf_counter() - t0
-    return ModelOutput(name, (n, d), cfg, trace, weights=_np(w), wall_time_s=wall, counts=counter)
+    if bad >= 0:
+        raise DivergenceError(bad)
+    return ModelOutput(name, (n, d), cfg, _np(trace).tolist(), weights=_np(w), wall_time_s=wall, counts=counter)
 
 
 def _t_linreg_normal(m, y):
@@ -166,9 +171,15 @@ def _t_linreg_normal(m, y):
     tty = _np(lmm(mt.T, yd, counter))
     w = _pinv_dense(g, counter) @ tty
     K.tally_matmul(counter, d, d, 1)
-    resid = lmm(mt, torch.from_numpy(w).to(yd.device), counter) - yd
+    so = _lib.lib()
+    tw = lmm(mt, torch.from_numpy(w).to(yd.device), counter)
+    resid = torch.empty_like(yd)
+    obj = torch.zeros(1, dtype=torch.float64, device=yd.device)
+    ws = torch.empty(max(int(so.fb_glm_pointwise_workspace_bytes()), 256), dtype=torch.uint8, device=yd.device)
+    _lib.check(so.fb_glm_pointwise(D.ptr(tw), D.ptr(yd), n, 1, D.ptr(resid), D.ptr(obj), 0, ws.data_ptr(), ws.numel(),
+                                   D.stream_handle()))  # Σ (T·w − y)²
     wall = time.perf_counter() - t0
-    out = ModelOutput("linreg_normal", (n, d), None, [float(torch.sum(resid**2))], weights=w)
+    out = ModelOutput("linreg_normal", (n, d), None, [float(obj.item())], weights=w)
     out.wall_time_s = wall
     out.counts = counter
     return out
@@ -186,32 +197,36 @@ def _t_gnmf(m, cfg):
     dev = mt.device
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    w = torch.from_numpy(1.0 - rng.random((n, cfg.r))).to(dev)
-    h = torch.from_numpy(1.0 - rng.random((d, cfg.r))).to(dev)
-    sum_t2 = sum_all(scalar_fn(mt, np.square, counter), counter)
-    eps = 1e-12
-    trace = []
+    r = cfg.r
+    if r > 64:
+        raise NotImplementedError("the device GNMF step supports r <= 64")
+    so = _lib.lib()
+    st = D.stream_handle()
+    w = torch.from_numpy(1.0 - rng.random((n, r))).to(dev)
+    h = torch.from_numpy(1.0 - rng.random((d, r))).to(dev)
+    sum_t2 = torch.tensor([sum_all(scalar_fn(mt, np.square, counter), counter)], dtype=torch.float64, device=dev)
+    trace = torch.zeros(cfg.iterations, dtype=torch.float64, device=dev)
     cpw = _mirror_gram(w, counter)
-    for _ in range(cfg.iterations):
-        ttw = lmm(mt.T, w, counter)
-        h = h * ttw / (h @ cpw + eps)
+    for it in range(cfg.iterations):
+        ttw = lmm(mt.T, w, counter).contiguous()
+        # h ← h ∘ ttw / (h·cpw + eps), w ← w ∘ th / (w·cph + eps): fb_nmf_update, in place (ml.py:308-312)
+        _lib.check(so.fb_nmf_update(D.ptr(h), D.ptr(ttw), D.ptr(cpw), d, r, st))
         cph = _mirror_gram(h, counter)
-        th = lmm(mt, h, counter)
-        w = w * th / (w @ cph + eps)
-        ttw_now = lmm(mt.T, w, counter)
+        th = lmm(mt, h, counter).contiguous()
+        _lib.check(so.fb_nmf_update(D.ptr(w), D.ptr(th), D.ptr(cph), n, r, st))
+        ttw_now = lmm(mt.T, w, counter).contiguous()
         cpw = _mirror_gram(w, counter)
-        sq = sum_t2 - 2.0 * float(torch.sum(ttw_now * h)) + float(torch.sum(cpw * cph))
-        trace.append(float(np.sqrt(max(sq, 0.0))))
+        # ‖T − W Hᵀ‖ = sqrt(max(ΣT² − 2 Σ(TᵀW ∘ H) + Σ(WᵀW ∘ HᵀH), 0))  (ml.py:314-315)
+        _lib.check(so.fb_nmf_objective(D.ptr(sum_t2), D.ptr(ttw_now), D.ptr(h), d * r, D.ptr(cpw), D.ptr(cph), r * r,
+                                       D.ptr(trace), it, st))
+    trace = _np(trace).tolist()
     wall = time.perf_counter() - t0
     return ModelOutput("gnmf", (n, d), cfg, trace, factors=(_np(w), _np(h)), wall_time_s=wall, counts=counter)
 
 
 def _mirror_gram(f, counter):
     """kernel.crossprod of a small dense factor: fᵀf with the upper triangle mirrored (kernel.py:138-154)."""
-    g = f.t() @ f
-    g = torch.triu(g) + torch.triu(g, 1).t()
-    K.tally_crossprod(counter, f.shape[0], f.shape[1])
-    return g
+    return _crossprod_nm(as_normalized(f.contiguous()), counter=counter).contiguous()  # DMMA / narrow Gram, exact mirror
 
 
 def _column(y, n, what="y"):
