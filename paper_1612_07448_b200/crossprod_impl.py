@@ -72,7 +72,9 @@ def crossprod(nm, method="efficient", counter=None):
     q = len(nm.blocks) - 1
     cs = nm.c_struct()
     if nm.blocks[0][0] is not None:
-        _star_crossprod(nm, out, so, st)  # M:N: every block gathered (the fused passes need S = block 0)
+        # M:N / multi-table M:N: every block keyed — the same plan with a zero-width S
+        # (R_iᵀ diag(c_i) R_i per table, pair-count cross blocks)
+        _star_crossprod_fused(nm, out, so, st) if nm.base_rows > 0 else _star_crossprod(nm, out, so, st)
     elif q == 1 and nm.blocks[0][1].shape[1] > 128:
         _star_crossprod(nm, out, so, st)  # the fused segmented KᵀS covers d_S <= 128
     elif q <= 1:
@@ -118,8 +120,10 @@ def _star_crossprod_fused(nm, out, so, st):
     d = nm.base_cols
     dev = nm.device
     offs = [int(o) for o in nm.col_offsets()]
-    d_s = offs[1]
     parts = nm.indicator_blocks
+    d_s = int(full.d_s)  # 0 for M:N matrices (every block is a keyed part)
+    if nm.blocks[0][0] is None:
+        offs = offs[1:]  # offs[i] = first column of part i
     n = nm.base_rows
     out.zero_()
     for i, (e, f) in enumerate(parts):
@@ -131,10 +135,11 @@ def _star_crossprod_fused(nm, out, so, st):
         perm, fks = fk_sorted_order(e)
         ws = D.workspace(so.fb_crossprod_workspace_bytes(ctypes.byref(sub)))
         _lib.check(so.fb_crossprod(ctypes.byref(sub), D.ptr(perm), D.ptr(fks), D.ptr(g), ws.data_ptr(), ws.numel(), st))
-        c0 = offs[i + 1]
-        if i == 0:
+        c0 = offs[i]
+        if i == 0 and d_s:
             out[:d_s, :d_s] = g[:d_s, :d_s]
-        out[:d_s, c0:c0 + di] = g[:d_s, d_s:]
+        if d_s:
+            out[:d_s, c0:c0 + di] = g[:d_s, d_s:]
         out[c0:c0 + di, c0:c0 + di] = g[d_s:, d_s:]
     for i, (ei, fi) in enumerate(parts):
         for j in range(i + 1, len(parts)):
@@ -155,7 +160,7 @@ def _star_crossprod_fused(nm, out, so, st):
             # column chunks of R_b in the widths the column reduction is instantiated for: each chunk's
             # M = P·R_b[:, c0:c0+w] is its own contiguous n_a × w matrix, so the reduction streams its
             # weights row-aligned with R_a (interleaved mode) instead of reading them strided
-            base = out.data_ptr() + 8 * (offs[i + 1] * d + offs[j + 1])
+            base = out.data_ptr() + 8 * (offs[i] * d + offs[j])
             o_js, o_cs = (d, 1) if flip else (1, d)
             c0 = 0
             while c0 < db:
