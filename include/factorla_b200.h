@@ -236,7 +236,7 @@ int fb_glm_run_fused(const fb_normalized* nm);
 int fb_glm_run(const fb_normalized* nm, const double* y, double* w, int32_t mode, double alpha, int32_t iters,
                double* trace, int32_t* diverged, void* ws, size_t ws_bytes, fb_stream_t stream);
 
-/* One K-Means iteration (ml.py:275-283) on an untransposed T with k <= 64 clusters (k <= 16: one
+/* One K-Means iteration (ml.py:275-283) on an untransposed T with k <= 4096 clusters (k <= 16: one
  * fused pass over S; above: chunked T·(2C), assign, one-hot and R passes):
  * c is the d × k centroid matrix (updated in place; empty clusters keep theirs), cc[j] =
  * Σ c[:, j]² (in/out), d_t = rowSums(T²) (n_s), assign (n_s int32) the argmin cluster

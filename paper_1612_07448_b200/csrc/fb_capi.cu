@@ -1010,9 +1010,9 @@ static int kmeans_partial_impl(const fb_normalized* nm, const double* d_t, const
                                const fb_band_layout* band) {
   int st = check_nm(nm);
   if (st) return st;
-  // k <= 16: one fused pass over S (fb_kmeans.cu); 17..64: T·(2C) in 16-column chunks, then the
-  // assign / one-hot passes and column-chunked R passes
-  if (k < 1 || k > 64) return fail(FB_ERR_ARG, "kmeans: k=%d outside [1, 64]", k);
+  // k <= 16: one fused pass over S (fb_kmeans.cu); wider: T·(2C) in 16-column chunks, then the
+  // assign pass, one-hot passes over windows of 64 clusters and column-chunked R passes
+  if (k < 1 || k > fb::kKmeansMaxK) return fail(FB_ERR_ARG, "kmeans: k=%d outside [1, %d]", k, fb::kKmeansMaxK);
   if (!d_t || !c || !cc || !trace || !assign || !nan_row) return fail(FB_ERR_ARG, "kmeans: NULL pointer");
   if (max_width(nm) > 256) return fail(FB_ERR_ARG, "kmeans: factor widths above 256 are not supported");
   if (ws_bytes < fb_kmeans_workspace_bytes(nm, k)) return fail(FB_ERR_ARG, "kmeans: workspace too small");
@@ -1160,8 +1160,8 @@ int fb_gnmf_step(const fb_normalized* nm, double* w, double* h, double* ttw, dou
                  int32_t r, int32_t it, double* trace, void* ws, size_t ws_bytes, fb_stream_t stream) {
   int st = check_nm(nm);
   if (st) return st;
-  // r <= 16: one fused pass over S per W step (fb_gnmf.cu); 17..64: the operator-by-operator step
-  if (r < 1 || r > 64) return fail(FB_ERR_ARG, "gnmf: r=%d outside [1, 64]", r);
+  // r <= 16: one fused pass over S per W step (fb_gnmf.cu); wider: the operator-by-operator step
+  if (r < 1 || r > fb::kNmfStepMaxR) return fail(FB_ERR_ARG, "gnmf: r=%d outside [1, %d]", r, fb::kNmfStepMaxR);
   if (!w || !h || !ttw || !cpw || !sum_t2 || !trace) return fail(FB_ERR_ARG, "gnmf: NULL pointer");
   if (ws_bytes < fb_gnmf_workspace_bytes(nm, r)) return fail(FB_ERR_ARG, "gnmf: workspace too small");
   cudaStream_t s = cs(stream);
@@ -1271,7 +1271,7 @@ int fb_glm_update(double* w, const double* g, int64_t d, double alpha, const dou
 }
 
 int fb_nmf_update(double* f, const double* num, const double* g, int64_t rows, int32_t r, fb_stream_t stream) {
-  if (!f || !num || !g || r < 1 || r > 64 || rows < 0) return fail(FB_ERR_ARG, "nmf_update: bad argument");
+  if (!f || !num || !g || r < 1 || r > fb::kNmfStepMaxR || rows < 0) return fail(FB_ERR_ARG, "nmf_update: bad argument");
   return cuda_status(fb::launch_nmf_update(f, num, g, rows, r, 1e-12, cs(stream), g_num_sms), "nmf_update");
 }
 

@@ -32,7 +32,8 @@ constexpr int kNB = 4;          // block tiles one warp may touch (BS = 2: 4 × 
 constexpr int kMaxGroups = 16;  // gridDim.y job groups
 constexpr int kMaxBT = 256;     // block tiles per pass
 constexpr int kWalkers = 3;     // KᵀS walker warps of the fused S pass (416 + 96 threads: 128 registers each;
-                                // a fourth walker caps registers at 96 and the consumers spill)
+                                // a fourth walker caps registers at 96 and the consumers spill; a gatherer
+                                // warp traded for a fourth walker (512 threads kept): no gain, round 2)
 constexpr int kWalkNB = kNB;    // block tiles per consumer warp in the fused pass
 
 // block tile code: bits 0-5 A block bi, bits 6-11 W block bj, bit 12 W from region 1.
@@ -675,7 +676,7 @@ int gram_tile_rows(uint32_t row_bytes, bool gather) {
 
 // Launch one pass; *gridx = CTAs per group (each wrote kConsumerWarps partial slots).
 cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_rows, cudaStream_t st, int num_sms,
-                     int* gridx, int bs, int walk_cj = 0) {
+                     int* gridx, int bs, int walk_cj = 0, int walk_nb = kWalkNB) {
   stream_layout(ss, tile_rows, a.n);
   int stages = static_cast<int>((200 * 1024 - kRingHeader - 256) / ss.stage_bytes);
   if (stages > 6) stages = 6;
@@ -697,7 +698,7 @@ cudaError_t run_gram(const BlockJobs& J, GramArgs& a, StreamSet& ss, int tile_ro
   cudaError_t e;
 #define FB_WALK_CASE(S, CJ)                                                                                     \
   if (bs == S && walk_cj == CJ) {                                                                               \
-    auto kern = cp_gram_kernel<S, false, kWalkers, CJ, kWalkNB>;                                                \
+    auto kern = walk_nb == 2 ? cp_gram_kernel<S, false, kWalkers, CJ, 2> : cp_gram_kernel<S, false, kWalkers, CJ, kWalkNB>; \
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));        \
     if (e != cudaSuccess) return e;                                                                             \
     kern<<<gdim, kRingThreads + 32 * kWalkers, smem, st>>>(J, a, ss, stages, tile_rows);                         \
@@ -998,8 +999,25 @@ cudaError_t launch_crossprod(const CrossArgs& c, void* ws, size_t ws_bytes, cuda
     ReduceArgs r{sp, 0, a.ra, a.cw, a.w1_col0, c.d_s, 0, 0, 0, c.out, d, 8 * bs_s, t2s, 0, {}};
     BlockJobs JS;
     if (!build_block_jobs(t2s, 0, tr / 4, 0, JS, r.wmask, false, kWalkNB)) return cudaErrorNotSupported;
+    // Opt-in (FB_CP_NB2=1, measurement): when no warp's range touches more than two block tiles
+    // (c3: 10 block tiles over 8 warps), the two-tile instantiation halves the accumulator
+    // registers and the freed registers keep each range's bounds and offsets live across tiles
+    // instead of re-deriving them from the constant bank at every range (an S2R -> LDC -> LDC ->
+    // LDS chain per range per tile). The consumers alone get faster (c3 op 2.79 -> 2.61 ms with the
+    // walkers idle), but the walkers' DADDs share the FP64 datapath with the DMMAs and then cost
+    // what the idle slots used to hide: 3.00 vs 2.93 ms with everything on, so it is not the default.
+    int walk_nb = kWalkNB;
+    {
+      BlockJobs J2;
+      uint8_t wm2[kMaxBT];
+      if (getenv("FB_CP_NB2") && build_block_jobs(t2s, 0, tr / 4, 0, J2, wm2, false, 2) && J2.ngroups == JS.ngroups) {
+        JS = J2;
+        std::copy(wm2, wm2 + kMaxBT, r.wmask);
+        walk_nb = 2;
+      }
+    }
     int gridx = 0;
-    e = run_gram(JS, a, ss, tr, st, num_sms, &gridx, bs_s, (c.d_s + 31) / 32);
+    e = run_gram(JS, a, ss, tr, st, num_sms, &gridx, bs_s, (c.d_s + 31) / 32, walk_nb);
     if (e != cudaSuccess) return e;
     r.gridx = gridx;
     launch_reduce(r, st);

@@ -164,6 +164,12 @@ cudaError_t launch_glm_spass(const GlmArgs& g, cudaStream_t st, int num_sms);
 cudaError_t launch_glm_update(double* w, const double* g, int d, double alpha, const double* loss, double* trace,
                               int it, int* diverged, cudaStream_t st);
 
+// Widest K-Means / GNMF problems of the operator-by-operator steps (k, r <= 16 take the fused passes):
+// the assign pass keeps cc[k] and k size counters in shared memory, the NMF update an r-wide row
+// per warp; the gram of W is a q = 0 crossprod (d <= 256).
+constexpr int kKmeansMaxK = 4096;
+constexpr int kNmfStepMaxR = 256;
+
 struct KmFk {
   int nfk;
   const int32_t* fk[kMaxParts];

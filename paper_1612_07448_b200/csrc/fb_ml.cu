@@ -252,8 +252,9 @@ __global__ void kmeans_assign_kernel(const double* __restrict__ tc, const double
                                      int32_t* __restrict__ assign, int32_t* __restrict__ sizes,
                                      double* __restrict__ partials, unsigned* counter, double* trace, int it,
                                      unsigned long long* nan_row) {
-  __shared__ double ccs[64];
-  __shared__ int32_t ssz[64];
+  extern __shared__ double km_assign_smem[];  // cc[k], then the CTA's k size counters
+  double* ccs = km_assign_smem;
+  int32_t* ssz = reinterpret_cast<int32_t*>(km_assign_smem + k);
   __shared__ double wsum[32];
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     ccs[j] = cc[j];
@@ -314,25 +315,29 @@ __global__ void kmeans_assign_kernel(const double* __restrict__ tc, const double
 cudaError_t launch_kmeans_assign(const double* tc, const double* d_t, const double* cc, int64_t n, int k,
                                  const KmFk& fks, int32_t* assign, int32_t* sizes, double* partials, unsigned* counter,
                                  double* trace, int it, unsigned long long* nan_row, cudaStream_t st, int num_sms) {
-  if (k < 1 || k > 64) return cudaErrorNotSupported;
+  if (k < 1 || k > kKmeansMaxK) return cudaErrorNotSupported;
   cudaError_t e = cudaMemsetAsync(sizes, 0, sizeof(int32_t) * k, st);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
   const int grid = grid_for(n, 256, 4, num_sms);
-  kmeans_assign_kernel<<<grid, 256, 0, st>>>(tc, d_t, cc, n, k, fks, assign, sizes, partials, counter, trace, it,
-                                             nan_row);
+  kmeans_assign_kernel<<<grid, 256, static_cast<size_t>(k) * 12, st>>>(tc, d_t, cc, n, k, fks, assign, sizes, partials,
+                                                                       counter, trace, it, nan_row);
   FB_LAUNCHED();
   return cudaGetLastError();
 }
 
 // out[c*k + j] = Σ_{i: assign[i] = j} S[i, c]: per-thread private accumulators in shared
 // memory (stride k+1 doubles: conflict-free), per-CTA partials summed in CTA order.
+// Clusters [j0, j0 + kc) of k per launch (kc <= 64: the shared accumulators of wider k do not fit):
+// rows of other clusters fall into the spare slot kc, so every cluster's rows are summed in the
+// order one unwindowed launch would use.
 __global__ void onehot_colsum_kernel(const double* __restrict__ s, int64_t n, int d, const int32_t* __restrict__ assign,
-                                     int k, double* partials, unsigned* counter, double* out) {
-  extern __shared__ double accs[];  // [blockDim.x][k + 1]
+                                     int k, int j0, int kc, double* partials, unsigned* counter, double* out) {
+  extern __shared__ double accs[];  // [blockDim.x][kc + 1]
   const int tid = threadIdx.x;
-  const int ks = k + 1;
+  const int ks = kc + 1;
+  auto slot = [&](int a) { return static_cast<unsigned>(a - j0) < static_cast<unsigned>(kc) ? a - j0 : kc; };
   for (int j = 0; j < ks; ++j) accs[tid * ks + j] = 0.0;
   const int groups = blockDim.x / d;
   const int col = tid % d, grp = tid / d;
@@ -349,15 +354,15 @@ __global__ void onehot_colsum_kernel(const double* __restrict__ s, int64_t n, in
         v[u] = __ldg(s + (r + u * step) * d + col);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) accs[tid * ks + a[u]] += v[u];
+      for (int u = 0; u < 8; ++u) accs[tid * ks + slot(a[u])] += v[u];
     }
-    for (; r < n; r += step) accs[tid * ks + assign[r]] += s[r * d + col];
+    for (; r < n; r += step) accs[tid * ks + slot(assign[r])] += s[r * d + col];
   }
   __syncthreads();
-  // fold groups -> per-CTA partial [d][k]
-  double* part = partials + static_cast<size_t>(blockIdx.x) * d * k;
-  for (int e = tid; e < d * k; e += blockDim.x) {
-    const int c = e / k, j = e % k;
+  // fold groups -> per-CTA partial [d][kc]
+  double* part = partials + static_cast<size_t>(blockIdx.x) * d * kc;
+  for (int e = tid; e < d * kc; e += blockDim.x) {
+    const int c = e / kc, j = e % kc;
     double v = 0.0;
     for (int gI = 0; gI < groups; ++gI) v += accs[(gI * d + c) * ks + j];
     part[e] = v;
@@ -369,9 +374,9 @@ __global__ void onehot_colsum_kernel(const double* __restrict__ s, int64_t n, in
   __syncthreads();
   if (ticket != gridDim.x - 1) return;
   __threadfence();
-  for (int e = tid >> 5; e < d * k; e += blockDim.x >> 5) {  // one warp per output
-    const double v = warp_sum_strided(partials + e, gridDim.x, static_cast<size_t>(d) * k);
-    if ((tid & 31) == 0) out[e] = v;
+  for (int e = tid >> 5; e < d * kc; e += blockDim.x >> 5) {  // one warp per output
+    const double v = warp_sum_strided(partials + e, gridDim.x, static_cast<size_t>(d) * kc);
+    if ((tid & 31) == 0) out[(e / kc) * k + j0 + e % kc] = v;
   }
   if (tid == 0) *counter = 0u;
 }
@@ -548,9 +553,10 @@ cudaError_t launch_onehot_colsum(const double* s, int64_t n, int d, const int32_
     FB_LAUNCHED();
     return cudaGetLastError();
   }
-  if (d > 256 || k > 64) return cudaErrorNotSupported;
+  if (d > 256 || k > kKmeansMaxK) return cudaErrorNotSupported;
   int threads = 256;
-  const size_t smem = static_cast<size_t>(threads) * (k + 1) * 8;
+  const int kc_max = k < 64 ? k : 64;
+  const size_t smem = static_cast<size_t>(threads) * (kc_max + 1) * 8;
   cudaError_t e = cudaFuncSetAttribute(onehot_colsum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -558,8 +564,11 @@ cudaError_t launch_onehot_colsum(const double* s, int64_t n, int d, const int32_
   if (e != cudaSuccess) return e;
   const int groups = threads / d;
   const int grid = grid_for(n, groups * 16, 2, num_sms);
-  onehot_colsum_kernel<<<grid, threads, smem, st>>>(s, n, d, assign, k, partials, counter, out);
-  FB_LAUNCHED();
+  for (int j0 = 0; j0 < k; j0 += kc_max) {  // one pass over S per window of 64 clusters
+    const int kc = k - j0 < kc_max ? k - j0 : kc_max;
+    onehot_colsum_kernel<<<grid, threads, smem, st>>>(s, n, d, assign, k, j0, kc, partials, counter, out);
+    FB_LAUNCHED();
+  }
   return cudaGetLastError();
 }
 
@@ -636,9 +645,37 @@ __global__ void nmf_update_wide_kernel(double* __restrict__ f, const double* __r
   }
 }
 
+// r > 64: a warp per row with the old row staged in the warp's shared slice; lane s owns columns
+// s, s + 32, ...; g is read through L1 (r² doubles: up to 512 KB); denominators accumulate over t in
+// ascending order exactly as above.
+__global__ void nmf_update_any_kernel(double* __restrict__ f, const double* __restrict__ num,
+                                      const double* __restrict__ g, int64_t rows, int r, double eps) {
+  extern __shared__ double frow[];  // [warps][r]
+  const int lane = threadIdx.x & 31;
+  double* fs = frow + (threadIdx.x >> 5) * r;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = warp; i < rows; i += nwarps) {
+    for (int c = lane; c < r; c += 32) fs[c] = f[i * r + c];
+    __syncwarp();
+    for (int c = lane; c < r; c += 32) {
+      double den = 0.0;
+      for (int t = 0; t < r; ++t) den = fma(fs[t], __ldg(g + t * r + c), den);
+      f[i * r + c] = fs[c] * num[i * r + c] / (den + eps);
+    }
+    __syncwarp();
+  }
+}
+
 cudaError_t launch_nmf_update(double* f, const double* num, const double* g, int64_t rows, int r, double eps,
                               cudaStream_t st, int num_sms) {
   const int grid = grid_for(rows, 256, 8, num_sms);
+  if (r > 64 && r <= kNmfStepMaxR) {
+    nmf_update_any_kernel<<<grid_for(rows, 8, 8, num_sms), 256, static_cast<size_t>(8) * r * 8, st>>>(f, num, g, rows,
+                                                                                                   r, eps);
+    FB_LAUNCHED();
+    return cudaGetLastError();
+  }
   if (r > 16 && r <= 64) {
     nmf_update_wide_kernel<<<grid_for(rows, 8, 8, num_sms), 256, static_cast<size_t>(r) * r * 8, st>>>(f, num, g, rows,
                                                                                                    r, eps);

@@ -198,8 +198,8 @@ def _t_gnmf(m, cfg):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     r = cfg.r
-    if r > 64:
-        raise NotImplementedError("the device GNMF step supports r <= 64")
+    if r > _MAX_R:
+        raise NotImplementedError(f"the device GNMF step supports r <= {_MAX_R}")
     so = _lib.lib()
     st = D.stream_handle()
     w = torch.from_numpy(1.0 - rng.random((n, r))).to(dev)
@@ -438,6 +438,10 @@ def _take_rows(nm, idx):
     return out
 
 
+# widest problems of the operator-by-operator steps (fb_kernels.cuh kKmeansMaxK / kNmfStepMaxR)
+_MAX_K = 4096
+_MAX_R = 256
+
 _BAND_MIN_ITERS = int(os.environ.get("FB_KMEANS_BAND_MIN_ITERS", "8"))
 
 
@@ -454,8 +458,8 @@ def kmeans(m, cfg):
     k = cfg.k
     if k > n:
         raise DataError(f"k={k} exceeds the number of data rows ({n})")
-    if k > 64:
-        raise NotImplementedError("the device K-Means step supports k <= 64")
+    if k > _MAX_K:
+        raise NotImplementedError(f"the device K-Means step supports k <= {_MAX_K}")
     so = _lib.lib()
     st = D.stream_handle()
     cs = nm.c_struct()
@@ -545,8 +549,8 @@ def gnmf(m, cfg):
     nm = _matrix(m)
     n, d = nm.shape
     r = cfg.r
-    if r > 64:
-        raise NotImplementedError("the device GNMF step supports r <= 64")
+    if r > _MAX_R:
+        raise NotImplementedError(f"the device GNMF step supports r <= {_MAX_R}")
     if _min_value(nm) < 0:
         warnings.warn("input has negative entries; GNMF semantics assume non-negative data")
     so = _lib.lib()

@@ -235,9 +235,10 @@ def test_glm_host_inputs_do_not_pin_device_memory():
     assert O.max_rel_deviation(out.weights, first.weights) <= 1e-12  # Kᵀp scatter order (REDs) varies
 
 
-@pytest.mark.parametrize("k", [17, 33, 64])
+@pytest.mark.parametrize("k", [17, 33, 64, 100, 150])
 def test_kmeans_wide_k_vs_oracle(k):
-    """k above the fused pass's 16 columns: chunked T·(2C), assign, one-hot and chunked R passes."""
+    """k above the fused pass's 16 columns: chunked T·(2C), assign, one-hot and chunked R passes
+    (k = 150: the one-hot sums go window by window of 64 clusters)."""
     fb = _fb()
     rng, s, parts = _c1_like(31 + k, n_s=40_000, d_s=6, n_r=1500, d_r=5, star=True)
     nm, ref = _both(s, parts)
@@ -246,10 +247,10 @@ def test_kmeans_wide_k_vs_oracle(k):
     _close(out.centroids, c)
     _close(out.objective, obj)
     with pytest.raises(NotImplementedError):
-        fb.kmeans(nm, fb.TrainConfig(iterations=1, k=65))
+        fb.kmeans(nm, fb.TrainConfig(iterations=1, k=4097))
 
 
-@pytest.mark.parametrize("r", [17, 40])
+@pytest.mark.parametrize("r", [17, 40, 70, 130])
 def test_gnmf_wide_r_vs_oracle(r):
     """r above the fused pass's 16 columns: the operator-by-operator step (LMM, Tᵀ·W, WᵀW)."""
     fb = _fb()
