@@ -267,7 +267,8 @@ int fb_kmeans_partial(const fb_normalized* nm, const double* d_t, const double* 
 int fb_kmeans_update(double* c, const double* tta, const int32_t* sizes, int64_t d, int32_t k, double* cc,
                      fb_stream_t stream);
 
-/* One GNMF multiplicative-update iteration (ml.py:306-315), r <= 16: w (n_s × r), h (d × r),
+/* One GNMF multiplicative-update iteration (ml.py:306-315), r <= 256 (r <= 16: one fused pass over S per
+ * W step; wider r: operator by operator): w (n_s × r), h (d × r),
  * ttw = Tᵀw (d × r, in: for the current w, out: for the updated w), cpw = wᵀw (r × r,
  * in/out), sum_t2 = Σ T² (device scalar), trace[it] = Frobenius objective. */
 size_t fb_gnmf_workspace_bytes(const fb_normalized* nm, int32_t r);
