@@ -83,7 +83,9 @@ def crossprod(nm, method="efficient", counter=None):
             perm, fks = fk_sorted_order(nm.blocks[1][0])
         ws = D.workspace(so.fb_crossprod_workspace_bytes(cs))
         _lib.check(so.fb_crossprod(cs, D.ptr(perm), D.ptr(fks), D.ptr(out), ws.data_ptr(), ws.numel(), st))
-    elif 2 <= nm.blocks[0][1].shape[1] <= 128 and nm.blocks[0][1].shape[1] % 2 == 0 and nm.base_rows > 0:
+    elif nm.blocks[0][1].shape[1] <= 128 and nm.base_rows > 0:
+        # odd d_S included: fb_crossprod then runs its unfused S pass (SᵀS in storage order + the
+        # segmented KᵀS walk) per part, still far from the block-column path's cost
         _star_crossprod_fused(nm, out, so, st)
     else:
         _star_crossprod(nm, out, so, st)

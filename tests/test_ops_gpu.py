@@ -218,7 +218,7 @@ CP_CASES = [
     (50_001, 7, [(997, 5)], "uniform", 4),     # odd widths: non-bulk gather fill
     (20_000, 64, [(3, 8)], "uniform", 5),      # huge runs, tiny R
     (12_345, 0, [(300, 9)], "uniform", 6),     # no entity features
-    (40_001, 5, [(97, 6), (1000, 3)], "uniform", 7),  # star: block-column path
+    (40_001, 5, [(97, 6), (1000, 3)], "uniform", 7),  # star, odd d_S: per-part unfused S pass + cross block
     (1, 3, [(1, 2)], "uniform", 8),
     (30_001, 72, [(2000, 16)], "uniform", 9),   # fused S pass, 3 columns per walker lane
     (20_000, 100, [(500, 10)], "zipf", 10),     # fused S pass, 4 columns per walker lane
@@ -226,6 +226,9 @@ CP_CASES = [
     (60_001, 20, [(4000, 40), (300, 60)], "uniform", 12),          # star, fused passes + pair-count cross block
     (50_000, 6, [(200, 5), (7000, 9), (31, 3)], "zipf", 13),      # three parts: both pair orientations
     (33_333, 8, [(1500, 16), (1500, 4)], "uniform", 14),          # equal table sizes
+    (45_001, 19, [(3000, 7), (200, 12)], "zipf", 15),              # star, odd d_S, skewed keys
+    (25_000, 1, [(100, 3), (50, 2)], "uniform", 16),               # star, one entity column
+    (25_000, 0, [(100, 3), (50, 2)], "uniform", 17),               # star without entity features
 ]
 
 

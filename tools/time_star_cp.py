@@ -8,7 +8,8 @@ from paper_1612_07448_b200 import crossprod_impl as CI
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(7)
 n_s = 10_000_000
-s = torch.rand(n_s, 20, dtype=torch.float64, device=dev, generator=g)
+d_s = int(os.environ.get("D_S", "20"))
+s = torch.rand(n_s, d_s, dtype=torch.float64, device=dev, generator=g)
 r1 = torch.rand(1_000_000, 40, dtype=torch.float64, device=dev, generator=g)
 r2 = torch.rand(100_000, 60, dtype=torch.float64, device=dev, generator=g)
 k1 = torch.randint(1, 1_000_001, (n_s,), device=dev, generator=g)
