@@ -500,13 +500,15 @@ def dgemm_peak_tflops():
     return 2 * n**3 / (best * 1e-3) / 1e12
 
 
-def _slope(run, n1=1, n2=20, trials=3):
-    """Per-iteration wall time of a driver: median over trials of (wall(n2) - wall(n1)) / (n2 - n1)."""
+def _loop_ms_per_iter(run, iters=20, trials=3):
+    """Per-iteration device time of a driver's iteration loop: median over trials of the CUDA-event span the
+    driver records around its loop (`ModelOutput.loop_ms`) / iterations. (Until the last session of round 2 this was
+    a wall-clock slope, (wall(20) - wall(1)) / 19, whose two ~0.1 s host-side seeding / RNG terms made it jitter by
+    +-0.2 ms per iteration between boxes.)"""
     pers, last = [], None
     for _ in range(trials):
-        r1 = run(n1)
-        last = run(n2)
-        pers.append((last.wall_time_s - r1.wall_time_s) / (n2 - n1))
+        last = run(iters)
+        pers.append(last.loop_ms * 1e-3 / iters)
     pers.sort()
     return pers[len(pers) // 2], last
 
@@ -599,11 +601,11 @@ def run_extras(dev, ref, parity):
     nm = _build_gpu(fb, g, dev)
     k, seed = g["k"], g["kmeans_seed"]
     fb.kmeans(nm, fb.TrainConfig(iterations=2, k=k, rng_seed=seed))  # warm: workspaces, kernel attributes
-    per, res = _slope(lambda it: fb.kmeans(nm, fb.TrainConfig(iterations=it, k=k, rng_seed=seed)))
+    per, res = _loop_ms_per_iter(lambda it: fb.kmeans(nm, fb.TrainConfig(iterations=it, k=k, rng_seed=seed)))
     out["c4_kmeans"] = {"iter_per_s": round(1 / per, 1), "ms_per_iter": round(1e3 * per, 3),
                         "s_total_20_iters": round(res.wall_time_s, 4),
-                        "timing": "per iteration = median over 3 trials of (wall(20 iters) - wall(1 iter)) / 19; "
-                                  "total incl. seeding and rowSums(T²)"}
+                        "timing": "per iteration = median over 3 trials of the 20-iteration loop's CUDA-event span "
+                                  "/ 20 (ModelOutput.loop_ms); total = wall clock incl. seeding and rowSums(T²)"}
     # the same star schema's crossprod (d = 120): per-part fused passes + pair-count cross blocks
     for _ in range(2):
         fb.crossprod(nm)
@@ -633,11 +635,12 @@ def run_extras(dev, ref, parity):
     nm = _build_gpu(fb, g, dev)
     rr, seed = g["r"], g["gnmf_seed"]
     fb.gnmf(nm, fb.TrainConfig(iterations=2, r=rr, rng_seed=seed))  # warm: workspaces, sorted order, attributes
-    per, res = _slope(lambda it: fb.gnmf(nm, fb.TrainConfig(iterations=it, r=rr, rng_seed=seed)))
+    per, res = _loop_ms_per_iter(lambda it: fb.gnmf(nm, fb.TrainConfig(iterations=it, r=rr, rng_seed=seed)))
     out["c5_gnmf"] = {"iter_per_s": round(1 / per, 1), "ms_per_iter": round(1e3 * per, 3),
                       "s_total_20_iters": round(res.wall_time_s, 4), "kept_r_rows": int(nm.r.shape[0]),
-                      "timing": "per iteration = median over 3 trials of (wall(20 iters) - wall(1 iter)) / 19; total "
-                                "incl. the host RNG draw of W (5M×5, the reference's default_rng call) and its upload"}
+                      "timing": "per iteration = median over 3 trials of the 20-iteration loop's CUDA-event span / 20 "
+                                "(ModelOutput.loop_ms); total = wall clock incl. the host RNG draw of W (5M×5, the "
+                                "reference's default_rng call) and its upload"}
     if cpu:
         rn = ref.build(g)
         ref.prepare(rn)

@@ -492,6 +492,8 @@ def kmeans(m, cfg):
             d_b = torch.empty_like(d_t)
             _lib.check(so.fb_gather_rows_i32(D.ptr(d_t), 1, D.ptr(perm), n, 1, D.ptr(d_b), 1, st))
             a_b = torch.empty_like(assign)
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
         for it in range(cfg.iterations):
             if band is not None:
                 _lib.check(so.fb_kmeans_step_banded(cs, ctypes.byref(bst), D.ptr(d_b), D.ptr(c), D.ptr(cc), k, it,
@@ -500,16 +502,18 @@ def kmeans(m, cfg):
             else:
                 _lib.check(so.fb_kmeans_step(cs, D.ptr(d_t), D.ptr(c), D.ptr(cc), k, it, D.ptr(trace), D.ptr(assign),
                                              D.ptr(nan_row), ws.data_ptr(), ws.numel(), st))
+        ev[1].record()
         if band is not None:
             _lib.check(so.fb_scatter_i32(D.ptr(a_b), D.ptr(perm), n, D.ptr(assign), st))
-        return trace, assign, int(nan_row.item())
+        bad = int(nan_row.item())  # synchronizes
+        return trace, assign, bad, ev[0].elapsed_time(ev[1])
 
-    trace, assign, bad = run(band)
+    trace, assign, bad, loop_ms = run(band)
     if bad != -1 and band is not None:
         # a NaN row: the reference reports the first one in row order (kernel.py:327-339), which the
         # band order cannot tell — repeat the run in storage order for the exact row
         c.copy_(c0)
-        trace, assign, bad = run(None)
+        trace, assign, bad, loop_ms = run(None)
     for it in range(cfg.iterations):
         _tally_lmm(counter, nm, k)
         counter.tally(0, n * k)  # row_min_mask
@@ -519,6 +523,7 @@ def kmeans(m, cfg):
         raise NumericError(f"row_min_mask: NaN in row {bad & ((1 << 40) - 1)}")
     out = ModelOutput("kmeans", (n, d), cfg, _np(trace).tolist(), centroids=_np(c), wall_time_s=wall, counts=counter)
     out.assignment = assign  # last iteration's argmin cluster per row (int32, device): parity checks
+    out.loop_ms = loop_ms  # the iteration loop alone on the device timeline (CUDA events)
     return out
 
 
@@ -571,6 +576,8 @@ def gnmf(m, cfg):
     _lib.check(so.fb_wt(cs, D.ptr(w), r, r, 1, D.ptr(ttw), 1, r, wsz.data_ptr(), wsz.numel(), st))
     trace = torch.zeros(cfg.iterations, dtype=torch.float64, device=dev)
     ws = _ws(so.fb_gnmf_workspace_bytes(cs, r))
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ev[0].record()
     for it in range(cfg.iterations):
         _lib.check(so.fb_gnmf_step(cs, D.ptr(w), D.ptr(h), D.ptr(ttw), D.ptr(cpw), D.ptr(sum_t2), r, it,
                                    D.ptr(trace), ws.data_ptr(), ws.numel(), st))
@@ -579,6 +586,9 @@ def gnmf(m, cfg):
         _tally_lmm(counter, nm, r)
         _tally_tmm(counter, nm, r)
         K.tally_crossprod(counter, n, r)
-    objective = _np(trace).tolist()
+    ev[1].record()
+    objective = _np(trace).tolist()  # synchronizes
     wall = time.perf_counter() - t0
-    return ModelOutput("gnmf", (n, d), cfg, objective, factors=(_np(w), _np(h)), wall_time_s=wall, counts=counter)
+    out = ModelOutput("gnmf", (n, d), cfg, objective, factors=(_np(w), _np(h)), wall_time_s=wall, counts=counter)
+    out.loop_ms = ev[0].elapsed_time(ev[1])  # the iteration loop alone on the device timeline (CUDA events)
+    return out
