@@ -448,6 +448,10 @@ static cudaError_t launch_rowdot(LmmArgs p, cudaStream_t st, int num_sms) {
   // rows per warp per tile: 32, fewer for wide rows (stage <= ~44 KB)
   int rw = 32;
   while (rw > 4 && static_cast<size_t>(row_bytes) * rw * kConsumerWarps > 48 * 1024) rw >>= 1;
+  // a lane group takes at most 8 interleaved rows per tile (the widest instantiation below): widths
+  // 16 and 32 (L = 16 / 32 with rows short enough for rw = 32) would need 16 / 32 — their rows past
+  // the eighth were never computed (found by tests/test_fuzz_gpu.py, round 2)
+  while (rw > 1 && rw * L > 8 * 32) rw >>= 1;
   StreamSet ss;
   fill_streams(p, ss, p.d);
   const size_t fixed = (static_cast<size_t>(p.d > 0 ? p.d : 1) * NX * 8 + 127) & ~size_t(127);

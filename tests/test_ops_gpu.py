@@ -249,6 +249,25 @@ def test_crossprod_seeded_vs_oracle(case):
     np.testing.assert_array_equal(cp, cp.T)
 
 
+@pytest.mark.parametrize("d_s,d_r", [(16, 16), (32, 20), (20, 32), (16, 32), (48, 64)])
+@pytest.mark.parametrize("d_x", [1, 2, 3, 4, 17])
+def test_lmm_rowdot_widths_16_32(d_s, d_r, d_x):
+    """Factor widths whose lane groups span 16 / 32 lanes (rowdot kernel, d_x <= 4 and the remainder chunk of
+    d_x = 17): every row of a tile must be computed (a lane group handles at most 8 rows per tile)."""
+    fb = _fb()
+    rng = np.random.default_rng(100 * d_s + d_r + d_x)
+    n_s, n_r = 5003, 152
+    s = rng.standard_normal((n_s, d_s))
+    r = rng.standard_normal((n_r, d_r))
+    key = rng.integers(1, n_r + 1, size=n_s)
+    nm, ref = fb.build_pkfk(s, key, r), O.build_pkfk(s, key, r)
+    x = rng.standard_normal((d_s + d_r, d_x))
+    _close(fb.lmm(nm, x), O.lmm(ref, x))
+    if d_x == 1:
+        _close(fb.row_sums(nm), O.row_sums(ref))
+        _close(fb.row_sums(fb.scalar_fn(nm, np.square)), O.row_sums(O.scalar_fn(ref, np.square)))
+
+
 def test_fk_sorted_order_is_stable_argsort():
     fb = _fb()
     from paper_1612_07448_b200.crossprod_impl import fk_sorted_order
