@@ -559,7 +559,10 @@ FB_DEV bool reduce_coords(const ReduceArgs& r, int64_t e, int& i, int& pc, int& 
 __global__ void cp_reduce_kernel(ReduceArgs r) {
   const int64_t e = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (e >= static_cast<int64_t>(r.da) * (r.da + r.db)) return;
+  // r1only passes (launch_rtx) have da·db elements: the gram bound let the last CTA's spare warps
+  // reduce and store up to 7 elements of a row past the block (found by tests/test_fuzz_gpu.py:
+  // K-Means with an even k > 16 not a multiple of 8 had its first cluster sizes overwritten)
+  if (e >= static_cast<int64_t>(r.da) * ((r.r1only ? 0 : r.da) + r.db)) return;
   int i, pc, orow, ocol;
   if (!reduce_coords(r, e, i, pc, orow, ocol)) return;
   const uint32_t mask = tile_writers(r, i, pc);

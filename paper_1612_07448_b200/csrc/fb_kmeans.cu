@@ -376,8 +376,27 @@ static cudaError_t launch_km_cg(const KmPass& p, cudaStream_t st, int num_sms) {
   return launch_km_ks<4, CG>(p, st, num_sms);
 }
 
+// Shape limits of the fused pass and room for two ring stages of 256 rows (S, d_t, the FK columns and
+// the gathered z rows of every part): wide stars (three parts at k > 8, two parts with a wide S)
+// do not fit and take the operator-by-operator step. (Until the randomised-fixture suite of round 2
+// this tested the shape limits only and the launch then failed with "unsupported size".)
 bool kmeans_pass_supported(int d_s, int k, int nfk) {
-  return k >= 1 && k <= kKmMaxK && d_s >= 0 && d_s <= kKmStaCols && nfk >= 0 && nfk <= kMaxParts;
+  if (!(k >= 1 && k <= kKmMaxK && d_s >= 0 && d_s <= kKmStaCols && nfk >= 0 && nfk <= kMaxParts)) return false;
+  constexpr int MT = 4;
+  StreamSet ss{};
+  ss.count = 2 + nfk;
+  ss.row_bytes[0] = static_cast<uint32_t>(d_s) * 8u;
+  ss.row_bytes[1] = 8u;
+  for (int q = 0; q < nfk; ++q) {
+    ss.row_bytes[2 + q] = 4u;
+    ss.grow_bytes[q] = static_cast<uint32_t>(z_stride(k)) * 8u;
+  }
+  ss.ngather = nfk;
+  for (int i = 0; i < ss.count; ++i) ss.pitch[i] = ss.row_bytes[i];
+  stream_layout(ss, kConsumerWarps * 8 * MT, kConsumerWarps * 8 * MT);
+  const size_t head = km_head_bytes((d_s + 3) / 4, MT);
+  const size_t budget = 224 * 1024;
+  return ss.stage_bytes > 0 && head + kRingHeader + 2 * static_cast<size_t>(ss.stage_bytes) <= budget;
 }
 
 cudaError_t launch_kmeans_pass(const KmPass& p, cudaStream_t st, int num_sms) {

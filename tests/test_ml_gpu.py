@@ -235,7 +235,7 @@ def test_glm_host_inputs_do_not_pin_device_memory():
     assert O.max_rel_deviation(out.weights, first.weights) <= 1e-12  # Kᵀp scatter order (REDs) varies
 
 
-@pytest.mark.parametrize("k", [17, 33, 64, 100, 150])
+@pytest.mark.parametrize("k", [17, 18, 20, 28, 33, 64, 100, 150])
 def test_kmeans_wide_k_vs_oracle(k):
     """k above the fused pass's 16 columns: chunked T·(2C), assign, one-hot and chunked R passes
     (k = 150: the one-hot sums go window by window of 64 clusters)."""
