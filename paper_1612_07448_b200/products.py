@@ -74,6 +74,12 @@ def _tally_gram(counter, n, d):
 def _dmm(m, n, k, a, lda, ta, b, ldb, tb, c, ldc, accumulate=False, a_off=0, b_off=0, c_off=0):
     """C (+)= op(A)·op(B) on the FP64 tensor cores (fb_dense_mm); offsets in elements."""
     so = _lib.lib()
+    if m == 0 or n == 0:
+        return
+    if k == 0:  # an empty contraction (a zero-width S): the product is the zero block
+        if not accumulate:
+            torch.as_strided(c.reshape(-1), (m, n), (ldc, 1), c_off).zero_()
+        return
     _lib.check(so.fb_dense_mm(m, n, k, D.ptr(a) + 8 * a_off, lda, int(ta), D.ptr(b) + 8 * b_off, ldb, int(tb),
                               D.ptr(c) + 8 * c_off, ldc, int(accumulate), D.stream_handle()))
 

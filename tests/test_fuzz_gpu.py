@@ -198,3 +198,110 @@ def test_random_fixtures_drivers_vs_oracle(batch):
                 _one_driver_fixture(fb, 50_000 + seed)
         except Exception as e:
             raise AssertionError(f"driver fixture seed {50_000 + seed}: {type(e).__name__}: {e}") from e
+
+
+# --------------------------------------------------------------------------- larger shapes, products, CSR inputs
+N_MEDIUM = int(os.environ.get("FB_FUZZ_MEDIUM", "60"))
+
+
+def _one_medium_fixture(fb, seed):
+    """Shapes that span many tiles and CTAs (up to 300k rows), wider operands, scipy CSR factors,
+    T·Tᵀ (small n only), and the normal equations."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(seed)
+    q = int(rng.integers(1, 4))
+    n = int(rng.integers(4_000, 300_000))
+    d_s = int(rng.integers(0, 70))
+    s = rng.standard_normal((n, d_s))
+    parts = []
+    for _ in range(q):
+        n_r = int(rng.integers(1, 20_000))
+        parts.append((_draw_keys(rng, n, n_r), rng.standard_normal((n_r, int(rng.integers(1, 90))))))
+    csr = rng.integers(0, 4) == 0  # a quarter of the fixtures hand the attribute tables over as scipy CSR
+    if csr:
+        dev_parts = []
+        for k, r in parts:
+            r = r * (rng.random(r.shape) < 0.04)
+            dev_parts.append((k, r))
+        parts = dev_parts
+        gpu_parts = [(k, sp.csr_matrix(r)) for k, r in parts]
+    else:
+        gpu_parts = parts
+    if q == 1:
+        nm, ref = fb.build_pkfk(s, gpu_parts[0][0], gpu_parts[0][1]), O.build_pkfk(s, parts[0][0], parts[0][1])
+    else:
+        nm, ref = fb.build_star(s, gpu_parts), O.build_star(s, parts)
+    d = ref.d
+    dx, dp = int(rng.integers(1, 40)), int(rng.integers(1, 40))
+    x = rng.standard_normal((d, dx))
+    p = rng.standard_normal((n, dp))
+    _check("lmm", fb.lmm(nm, x), O.lmm(ref, x))
+    _check("tmm", fb.lmm(nm.T, p), O.lmm(ref.T, p))
+    _check("rmm", fb.rmm(np.ascontiguousarray(p.T), nm), O.rmm(p.T, ref))
+    _check("row_sums", fb.row_sums(nm), O.row_sums(ref))
+    _check("col_sums", fb.col_sums(nm), O.col_sums(ref))
+    cp = _np(fb.crossprod(nm))
+    _check("crossprod", cp, O.crossprod(ref))
+    np.testing.assert_array_equal(cp, cp.T)
+    if not csr:
+        y = O.lmm(ref, rng.standard_normal((d, 1))) + 0.01 * rng.standard_normal((n, 1))
+        out = fb.linreg_normal(nm, y)
+        w, obj = O.linreg_normal(ref, y)
+        _check("linreg_normal_obj", out.objective, obj, 1e-7)  # pinv of a d × d Gram on both sides (SURVEY N15)
+
+
+@pytest.mark.parametrize("batch", range((N_MEDIUM + 9) // 10))
+def test_random_medium_fixtures_vs_oracle(batch):
+    import warnings
+
+    import paper_1612_07448_b200 as fb
+
+    for seed in range(batch * 10, min((batch + 1) * 10, N_MEDIUM)):
+        try:
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                _one_medium_fixture(fb, 90_000 + seed)
+        except Exception as e:
+            raise AssertionError(f"medium fixture seed {90_000 + seed}: {type(e).__name__}: {e}") from e
+
+
+N_PRODUCT = int(os.environ.get("FB_FUZZ_PRODUCTS", "150"))
+
+
+def _one_product_fixture(fb, seed):
+    """T·Tᵀ, the pseudo-inverse through the small Gram and the pair-count product on small schemas."""
+    kind, rng, data = _draw(seed)
+    if kind == "mn":
+        return
+    s, parts = data
+    n = min(s.shape[0], 300)  # T·Tᵀ is n × n
+    s, parts = s[:n], [(k[:n], r) for k, r in parts]
+    nm, ref = _build(fb, kind, (s, parts))
+    g = _np(fb.gram_transposed(nm))
+    _check("gram_transposed", g, O.gram_transposed(ref))
+    np.testing.assert_array_equal(g, g.T)
+    t_ref = O.materialize(ref)
+    if kind == "pkfk":  # double multiplication takes PK-FK operands only, as in the reference (rewrite.py:349-389)
+        _check("dmm_a_at", fb.dmm(nm, nm.T), t_ref @ t_ref.T)
+        _check("dmm_at_a", fb.dmm(nm.T, nm), t_ref.T @ t_ref)
+    if len(parts) >= 2:
+        (ea, _), (eb, _) = nm.indicator_blocks[:2]
+        (ta, ra), (tb, rb) = ref.parts[:2]
+        pp = fb.pair_product(ea, eb)
+        np.testing.assert_array_equal(pp.to_dense().cpu().numpy(), O.pair_product(ta, ra.shape[0], tb, rb.shape[0]))
+
+
+@pytest.mark.parametrize("batch", range((N_PRODUCT + BATCH - 1) // BATCH))
+def test_random_fixtures_products_vs_oracle(batch):
+    import warnings
+
+    import paper_1612_07448_b200 as fb
+
+    for seed in range(batch * BATCH, min((batch + 1) * BATCH, N_PRODUCT)):
+        try:
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                _one_product_fixture(fb, 70_000 + seed)
+        except Exception as e:
+            raise AssertionError(f"product fixture seed {70_000 + seed}: {type(e).__name__}: {e}") from e
