@@ -141,8 +141,20 @@ N_DRIVER = int(os.environ.get("FB_FUZZ_DRIVERS", "400"))
 DTOL = 1e-9  # drivers: the north star's bar (iterated sums; K-Means ties would show as O(1) deviations)
 
 
-def _one_driver_fixture(fb, seed):
-    kind, rng, data = _draw(seed)
+def _draw_medium(seed):
+    """PK-FK / star schemas whose passes span many tiles and CTAs (4k-150k rows)."""
+    rng = np.random.default_rng(seed)
+    q = int(rng.integers(1, 4))
+    n = int(rng.integers(4_000, 150_000))
+    parts = []
+    for _ in range(q):
+        n_r = int(rng.integers(1, 5_000))
+        parts.append((_draw_keys(rng, n, n_r), rng.standard_normal((n_r, int(rng.integers(1, 41))))))
+    return ("pkfk" if q == 1 else "star"), rng, (rng.standard_normal((n, int(rng.integers(0, 41)))), parts)
+
+
+def _one_driver_fixture(fb, seed, draw=None):
+    kind, rng, data = (draw or _draw)(seed)
     if kind != "mn":  # non-negative data so GNMF runs on the same fixture
         s, parts = data
         data = (np.abs(s), [(k, np.abs(r)) for k, r in parts])
@@ -264,6 +276,24 @@ def test_random_medium_fixtures_vs_oracle(batch):
                 _one_medium_fixture(fb, 90_000 + seed)
         except Exception as e:
             raise AssertionError(f"medium fixture seed {90_000 + seed}: {type(e).__name__}: {e}") from e
+
+
+N_MEDIUM_DRIVER = int(os.environ.get("FB_FUZZ_MEDIUM_DRIVERS", "40"))
+
+
+@pytest.mark.parametrize("batch", range((N_MEDIUM_DRIVER + 9) // 10))
+def test_random_medium_fixtures_drivers_vs_oracle(batch):
+    import warnings
+
+    import paper_1612_07448_b200 as fb
+
+    for seed in range(batch * 10, min((batch + 1) * 10, N_MEDIUM_DRIVER)):
+        try:
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                _one_driver_fixture(fb, 110_000 + seed, _draw_medium)
+        except Exception as e:
+            raise AssertionError(f"medium driver fixture seed {110_000 + seed}: {type(e).__name__}: {e}") from e
 
 
 N_PRODUCT = int(os.environ.get("FB_FUZZ_PRODUCTS", "150"))
