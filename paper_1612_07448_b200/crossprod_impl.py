@@ -82,11 +82,23 @@ def crossprod(nm, method="efficient", counter=None):
         if q == 1:
             perm, fks = fk_sorted_order(nm.blocks[1][0])
         ws = D.workspace(so.fb_crossprod_workspace_bytes(cs))
-        _lib.check(so.fb_crossprod(cs, D.ptr(perm), D.ptr(fks), D.ptr(out), ws.data_ptr(), ws.numel(), st))
+        try:
+            _lib.check(so.fb_crossprod(cs, D.ptr(perm), D.ptr(fks), D.ptr(out), ws.data_ptr(), ws.numel(), st))
+        except ValueError as e:
+            # a shape the two-pass kernels' job tables cannot hold (e.g. d_S = 125 beside a 250-wide R:
+            # more than 256 block tiles in the R pass): the block-column path, exact but slower
+            if q != 1 or "unsupported size" not in str(e):
+                raise
+            _star_crossprod(nm, out, so, st)
     elif nm.blocks[0][1].shape[1] <= 128 and nm.base_rows > 0:
         # odd d_S included: fb_crossprod then runs its unfused S pass (SᵀS in storage order + the
         # segmented KᵀS walk) per part, still far from the block-column path's cost
-        _star_crossprod_fused(nm, out, so, st)
+        try:
+            _star_crossprod_fused(nm, out, so, st)
+        except ValueError as e:
+            if "unsupported size" not in str(e):
+                raise
+            _star_crossprod(nm, out, so, st)
     else:
         _star_crossprod(nm, out, so, st)
     _tally(nm, counter)

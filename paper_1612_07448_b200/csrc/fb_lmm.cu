@@ -43,6 +43,7 @@ struct LmmArgs {
   int cols;                    // rowdot: columns per lane (d / lanes)
   float zfrac;                 // z-pass (nfk == 0): evict_last fraction of the stored z rows
   int debug;                   // FB_LMM_DEBUG (measurement only): 1 skip stores, 4 plain stores
+  int zcol0;                   // rowdot: first column of the gathered z rows this launch adds (sub-chunks)
   size_t ztable_bytes[kMaxParts];  // bytes of each z table (host side: gather cache choice)
 };
 
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) lmm_rowdot_kernel(LmmArgs p, 
       for (int q = 0; q < p.nfk; ++q) {
         const double* zr = reinterpret_cast<const double*>(ring.gather_ptr(cur, ss, q)) + r * p.zstride;
 #pragma unroll
-        for (int j = 0; j < NX; ++j) res[j] += zr[j];
+        for (int j = 0; j < NX; ++j) res[j] += zr[p.zcol0 + j];
       }
       double* o = p.out + (r0 + r) * p.ldo;
 #pragma unroll
@@ -559,8 +560,26 @@ cudaError_t launch_lmm_rows(const double* a, int64_t n, int d, const double* x, 
     default:
       break;
   }
-  if (dx <= 8) return launch_dmma<1>(p, st, num_sms);
-  return launch_dmma<2>(p, st, num_sms);
+  cudaError_t e = dx <= 8 ? launch_dmma<1>(p, st, num_sms) : launch_dmma<2>(p, st, num_sms);
+  if (e != cudaErrorNotSupported) return e;
+  // Two 64-row DMMA stages of a wide factor (d above ~170, less with gathered z rows) do not fit
+  // the ring: the same product in column sub-chunks of <= 4 on the rowdot kernel, whose tiles
+  // shrink to 4 rows per warp (found by the wide fixtures of tests/test_fuzz_gpu.py)
+  for (int c0 = 0; c0 < dx; c0 += 4) {
+    LmmArgs q = p;
+    q.x = p.x + c0;
+    q.out = p.out + c0;
+    q.dx = dx - c0 < 4 ? dx - c0 : 4;
+    q.zcol0 = c0;
+    switch (q.dx) {
+      case 1: e = launch_rowdot<1>(q, st, num_sms); break;
+      case 2: e = launch_rowdot<2>(q, st, num_sms); break;
+      case 3: e = launch_rowdot<3>(q, st, num_sms); break;
+      default: e = launch_rowdot<4>(q, st, num_sms); break;
+    }
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace fb

@@ -183,12 +183,12 @@ def _one_driver_fixture(fb, seed, draw=None):
     _check("linreg_w", out.weights, w, DTOL)
     _check("linreg_obj", out.objective, obj, DTOL)
     # K-Means (k <= n) and GNMF
-    k = int(rng.integers(1, min(n, 20) + 1))
+    k = int(rng.integers(1, min(n, 40) + 1))
     out = fb.kmeans(nm, fb.TrainConfig(iterations=it, k=k, rng_seed=seed))
     c, obj, _ = O.kmeans(ref, k, it, seed)
     _check("kmeans_c", out.centroids, c, DTOL)
     _check_scaled("kmeans_obj", out.objective, obj, float((t_ref * t_ref).sum()), DTOL)
-    r = int(rng.integers(1, 20))
+    r = int(rng.integers(1, 40))
     out = fb.gnmf(nm, fb.TrainConfig(iterations=it, r=r, rng_seed=seed))
     w, h, obj = O.gnmf(ref, r, it, seed)
     _check("gnmf_w", out.factors[0], w, DTOL)
@@ -335,3 +335,53 @@ def test_random_fixtures_products_vs_oracle(batch):
                 _one_product_fixture(fb, 70_000 + seed)
         except Exception as e:
             raise AssertionError(f"product fixture seed {70_000 + seed}: {type(e).__name__}: {e}") from e
+
+
+N_WIDE = int(os.environ.get("FB_FUZZ_WIDE", "40"))
+
+
+def _one_wide_fixture(fb, seed):
+    """Wide factor matrices (60-300 columns: past the streaming kernels' 128 / 256-column paths)."""
+    rng = np.random.default_rng(seed)
+    q = int(rng.integers(1, 3))
+    n = int(rng.integers(500, 20_000))
+    s = rng.standard_normal((n, int(rng.integers(60, 301))))
+    parts = []
+    for _ in range(q):
+        n_r = int(rng.integers(1, 2_000))
+        parts.append((_draw_keys(rng, n, n_r), rng.standard_normal((n_r, int(rng.integers(60, 301))))))
+    if q == 1:
+        nm, ref = fb.build_pkfk(s, parts[0][0], parts[0][1]), O.build_pkfk(s, parts[0][0], parts[0][1])
+    else:
+        nm, ref = fb.build_star(s, parts), O.build_star(s, parts)
+    d = ref.d
+    x = rng.standard_normal((d, int(rng.integers(1, 40))))
+    p = rng.standard_normal((n, int(rng.integers(1, 40))))
+    _check("lmm", fb.lmm(nm, x), O.lmm(ref, x))
+    _check("tmm", fb.lmm(nm.T, p), O.lmm(ref.T, p))
+    _check("rmm", fb.rmm(np.ascontiguousarray(p.T), nm), O.rmm(p.T, ref))
+    _check("row_sums", fb.row_sums(nm), O.row_sums(ref))
+    _check("col_sums", fb.col_sums(nm), O.col_sums(ref))
+    _check("sum_all", np.asarray(fb.sum_all(nm)), np.asarray(O.sum_all(ref)), 1e-9)
+    if max([s.shape[1]] + [r.shape[1] for _, r in parts]) <= 256:
+        cp = _np(fb.crossprod(nm))
+        _check("crossprod", cp, O.crossprod(ref))
+        np.testing.assert_array_equal(cp, cp.T)
+    else:  # the documented limit of the crossprod kernels (DESIGN.md §7): a clear error, not a wrong answer
+        with pytest.raises(ValueError, match="widths above 256"):
+            fb.crossprod(nm)
+
+
+@pytest.mark.parametrize("batch", range((N_WIDE + 9) // 10))
+def test_random_wide_fixtures_vs_oracle(batch):
+    import warnings
+
+    import paper_1612_07448_b200 as fb
+
+    for seed in range(batch * 10, min((batch + 1) * 10, N_WIDE)):
+        try:
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                _one_wide_fixture(fb, 130_000 + seed)
+        except Exception as e:
+            raise AssertionError(f"wide fixture seed {130_000 + seed}: {type(e).__name__}: {e}") from e
