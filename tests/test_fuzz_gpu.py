@@ -2,7 +2,7 @@
 
 The reference's spec names an "oracle suite of 1000 random fixtures, rel 1e-10" as an acceptance
 criterion it never shipped. This is that suite for the hot path: every fixture draws
-a schema (PK-FK, star with 2-3 attribute tables, or M:N), its shapes — including single rows, d_S = 0,
+a schema (PK-FK, star with 2-3 attribute tables, M:N or multi-table M:N), its shapes — including single rows, d_S = 0,
 odd widths, attribute rows no key references, keys that repeat one value — and its operands from one
 seed, builds it on the device and in the oracle, checks the construction bit for bit and every
 operator at normwise rel 1e-10 (bench.py:38-43's metric). FB_FUZZ_N sets the fixture count
@@ -67,6 +67,11 @@ def _draw(seed):
     kind = ("pkfk", "pkfk", "star", "star", "mn")[rng.integers(0, 5)]
     small = rng.integers(0, 4) == 0
     n = int(rng.integers(1, 40)) if small else int(rng.integers(40, 4000))
+    if kind == "mn" and rng.integers(0, 2):  # half of the M:N fixtures: multi-table, explicit 0-based row map
+        q = int(rng.integers(2, 5))
+        tables = [rng.standard_normal((int(rng.integers(1, 80)), int(rng.integers(1, 12)))) for _ in range(q)]
+        row_map = np.stack([rng.integers(0, t.shape[0], size=n) for t in tables], axis=1)
+        return "multimn", rng, (row_map, tables)
     if kind == "mn":
         n_s, n_r = int(rng.integers(1, 60)), int(rng.integers(1, 60))
         dom = int(rng.integers(1, 8))
@@ -88,6 +93,8 @@ def _draw(seed):
 def _build(fb, kind, data):
     if kind == "mn":
         return fb.build_mn(*data), O.build_mn(*data)
+    if kind == "multimn":
+        return fb.build_multimn(*data), O.build_multimn(*data)
     s, parts = data
     if kind == "pkfk":
         return fb.build_pkfk(s, parts[0][0], parts[0][1]), O.build_pkfk(s, parts[0][0], parts[0][1])
@@ -155,7 +162,9 @@ def _draw_medium(seed):
 
 def _one_driver_fixture(fb, seed, draw=None):
     kind, rng, data = (draw or _draw)(seed)
-    if kind != "mn":  # non-negative data so GNMF runs on the same fixture
+    if kind == "multimn":
+        data = (data[0], [np.abs(t) for t in data[1]])
+    elif kind != "mn":  # non-negative data so GNMF runs on the same fixture
         s, parts = data
         data = (np.abs(s), [(k, np.abs(r)) for k, r in parts])
     else:
@@ -302,7 +311,7 @@ N_PRODUCT = int(os.environ.get("FB_FUZZ_PRODUCTS", "150"))
 def _one_product_fixture(fb, seed):
     """T·Tᵀ, the pseudo-inverse through the small Gram and the pair-count product on small schemas."""
     kind, rng, data = _draw(seed)
-    if kind == "mn":
+    if kind in ("mn", "multimn"):
         return
     s, parts = data
     n = min(s.shape[0], 300)  # T·Tᵀ is n × n

@@ -14,6 +14,6 @@ for seed in range(n):
     except Exception as e:
         bad += 1
         kind, rng, data = F._draw(50_000 + seed)
-        shape = (data[0].shape, [(k.shape[0], r.shape) for k, r in data[1]]) if kind != "mn" else (data[0].shape, data[2].shape)
+        shape = kind if kind in ("mn", "multimn") else (data[0].shape, [(k.shape[0], r.shape) for k, r in data[1]])
         print(f"seed {50_000 + seed} {kind} {shape}: {type(e).__name__}: {str(e)[:160]}", flush=True)
 print("failures", bad, "of", n)
